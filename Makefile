@@ -1,0 +1,25 @@
+# Builds the C-ABI shared library of the B200 Lloyd hot path (sm_100a only).
+NVCC      ?= nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+SRC_DIR   := paper_2501_05587_b200/csrc
+OUT_DIR   := paper_2501_05587_b200/lib
+SRCS      := $(wildcard $(SRC_DIR)/*.cu)
+OBJS      := $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
+HDRS      := $(wildcard $(SRC_DIR)/*.cuh) include/popcorn_b200.h
+LIB       := $(OUT_DIR)/libpopcorn_b200.so
+
+all: $(LIB)
+
+build/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	@mkdir -p $(OUT_DIR)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean

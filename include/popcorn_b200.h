@@ -1,0 +1,153 @@
+/*
+ * popcorn_b200 — C ABI of the B200-native Lloyd hot path.
+ *
+ * This is the drop-in boundary below the reference's Python driver
+ * `run_lloyd` (/root/reference/pkg/src/popcorn/clustering.py:291-325), which is
+ * reached through the estimator plugin registry `_ALGORITHMS`
+ * (estimator.py:18).  The reference binds nothing natively (it is pure
+ * numpy); these are the entry points a ctypes binding of that driver calls
+ * (see INTEGRATION.md).  Every function:
+ *   - takes plain pointers (device pointers unless named *_host) and sizes,
+ *   - takes the CUDA stream as `void*` (a cudaStream_t; NULL = legacy stream),
+ *   - is asynchronous with respect to the host unless stated otherwise,
+ *   - returns 0 on success, a positive cudaError_t value on a CUDA error, or a
+ *     negative PCB_E* code on bad arguments (pcb_error_string() describes it).
+ *
+ * Per-iteration kernels read a device "state" block (int64 words: iterations
+ * recorded, stop flag, converged flag, repairs of the current iteration) and
+ * return immediately once the stop flag is set, so a whole max_iters loop can
+ * be enqueued (or captured in a CUDA graph) with no host synchronisation —
+ * the convergence test of clustering.py:322-324 runs on the device.
+ *
+ * Fused accumulator `acc` (f64, the buffer all-reduced across ranks):
+ *   [ sums k*d | counts k | objective | changed ]   (k*d + k + 2 words)
+ */
+#ifndef POPCORN_B200_H
+#define POPCORN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCB_ABI_VERSION 1
+
+#define PCB_EINVAL   (-1)   /* bad size / pointer argument            */
+#define PCB_EUNSUP   (-2)   /* unsupported shape for this kernel        */
+#define PCB_ENODEV   (-3)   /* no sm_100 device                          */
+
+/* Assignment kernel variants (`variant` argument of pcb_assign_*). */
+#define PCB_ASSIGN_AUTO      0  /* library picks            */
+#define PCB_ASSIGN_ROWREG    1  /* FFMA, one point per thread (d <= 32)     */
+#define PCB_ASSIGN_TILED     2  /* FFMA, register-tiled SIMT GEMM (any d)   */
+#define PCB_ASSIGN_TC3XTF32  3  /* tcgen05 3xTF32, TMEM accumulators (f32)  */
+#define PCB_ASSIGN_DELTA     4  /* delta-chunked P.C.P^T ablation (f32)     */
+
+int         pcb_abi_version(void);
+const char* pcb_error_string(int code);
+/* sm count / compute capability of `device`; returns PCB_ENODEV if not sm_100. */
+int pcb_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- one-time point preparation (clustering.py:302: point_norms) ---------- */
+int pcb_point_norms_f32(const float* P, int64_t n, int d, float* pnorm, void* stream);
+int pcb_point_norms_f64(const double* P, int64_t n, int d, double* pnorm, void* stream);
+
+/* Split X (rows x d, row stride d) into TF32 hi = rna_tf32(X) and lo = X - hi,
+ * written with row stride `ld` (>= d, zero padded), for the 3xTF32 kernel. */
+int pcb_split_tf32(const float* X, int64_t rows, int d, int ld, float* hi, float* lo, void* stream);
+
+/* ---- assignment: distance stage + row argmin (clustering.py:310-311,
+ *      dense.py:56-68) fused with the bookkeeping of _assignment_step
+ *      (clustering.py:147-149): per-cluster counts, objective, changed.
+ *   labels[i] = argmin_j D[i,j] (lowest j on ties), mind[i] = D[i,labels[i]]
+ *   where D[i,j] = pnorm[i] + (cnorm[j] - 2 <p_i, c_j>).
+ *   labels_prev / acc / state may be NULL (predict mode: estimator.py:131-136).
+ *   C, cnorm: centroids k x d and their squared norms.
+ *   For PCB_ASSIGN_TC3XTF32 the caller passes the split operands through
+ *   pcb_assign_tc_f32 instead.                                              */
+int pcb_assign_f32(const float* P, const float* pnorm, int64_t n, int d,
+                   const float* C, const float* cnorm, int k,
+                   const int32_t* labels_prev, int32_t* labels, float* mind,
+                   double* acc, const long long* state, int variant, void* stream);
+int pcb_assign_f64(const double* P, const double* pnorm, int64_t n, int d,
+                   const double* C, const double* cnorm, int k,
+                   const int32_t* labels_prev, int32_t* labels, double* mind,
+                   double* acc, const long long* state, int variant, void* stream);
+
+/* ---- centroid update (clustering.py:282-288): counting sort of point ids by
+ *      label, then a segmented f64 sum of point rows per cluster into acc.  */
+/* counts: the counts block of acc (acc + k*d).  offsets: k+1 segment starts. */
+int pcb_sort_by_label(const int32_t* labels, int64_t n, int k, const double* counts,
+                      int32_t* offsets /* k+1 */, int32_t* cursor /* k */, int32_t* perm,
+                      const long long* state, void* stream);
+/* Adds the per-cluster row sums into acc[0 : k*d) (RED.ADD.F64). */
+int pcb_segment_sums_f32(const float* P, int64_t n, int d, const int32_t* perm,
+                         const int32_t* offsets, int k, double* acc,
+                         const long long* state, void* stream);
+int pcb_segment_sums_f64(const double* P, int64_t n, int d, const int32_t* perm,
+                         const int32_t* offsets, int k, double* acc,
+                         const long long* state, void* stream);
+
+/* ---- empty-cluster repair (clustering.py:111-139), single-rank, on device.
+ *   For each empty cluster j ascending: the not-yet-moved point with the
+ *   largest own distance (lowest index on ties) moves to j; repeated while any
+ *   cluster is empty.  Adjusts acc (sums, counts, objective, changed) and
+ *   state[3] (repairs).  No-op when no cluster is empty.                    */
+int64_t pcb_repair_scratch_bytes(int k);   /* device scratch the caller provides */
+int pcb_repair_f32(const float* P, const float* pnorm, int64_t n, int d,
+                   const float* C, const float* cnorm, int k,
+                   const int32_t* labels_prev, int32_t* labels, float* mind,
+                   double* acc, long long* state, void* scratch, int64_t scratch_bytes,
+                   void* stream);
+int pcb_repair_f64(const double* P, const double* pnorm, int64_t n, int d,
+                   const double* C, const double* cnorm, int k,
+                   const int32_t* labels_prev, int32_t* labels, double* mind,
+                   double* acc, long long* state, void* scratch, int64_t scratch_bytes,
+                   void* stream);
+
+/* Multi-rank repair (host-orchestrated).  argmax_own writes
+ * [own distance, global index] of this rank's best unmoved point (ties ->
+ * lowest index).  repair_apply moves the donor on its owner rank and writes a
+ * delta record (f64, d+4 words: p_donor | old label | d_objective |
+ * d_changed | valid=1); non-owners zero it; after an all-reduce SUM every rank
+ * calls repair_commit to patch its accumulator identically.                */
+int pcb_argmax_own_f32(const float* mind, int64_t n, int64_t offset, double* out2, void* stream);
+int pcb_argmax_own_f64(const double* mind, int64_t n, int64_t offset, double* out2, void* stream);
+int pcb_repair_apply_f32(const float* P, const float* pnorm, int d, const float* C,
+                         const float* cnorm, const int32_t* labels_prev, int32_t* labels,
+                         float* mind, int64_t donor_local, int j, double* delta, void* stream);
+int pcb_repair_apply_f64(const double* P, const double* pnorm, int d, const double* C,
+                         const double* cnorm, const int32_t* labels_prev, int32_t* labels,
+                         double* mind, int64_t donor_local, int j, double* delta, void* stream);
+int pcb_repair_commit(double* acc, int k, int d, int j, const double* delta, long long* state,
+                      void* stream);
+
+/* ---- finalize: c_j = sums_j / counts_j (empty -> 0, clustering.py:286-287),
+ *      cnorm, optional TF32 hi/lo split of C (row stride ld), history
+ *      recording and the convergence test (clustering.py:319-324).
+ *      n_total: global point count (all ranks).                            */
+int pcb_finalize_f32(const double* acc, int k, int d, int64_t n_total,
+                     float* C, float* cnorm, float* c_hi, float* c_lo, int ld,
+                     double* objective_hist, long long* repairs_hist,
+                     long long* state, int check_convergence, double tol, void* stream);
+int pcb_finalize_f64(const double* acc, int k, int d, int64_t n_total,
+                     double* C, double* cnorm,
+                     double* objective_hist, long long* repairs_hist,
+                     long long* state, int check_convergence, double tol, void* stream);
+
+/* Initial centroids from labels (clustering.py:298-300) without touching the
+ * state: acc must hold sums+counts (sort + segment sums); writes C, cnorm. */
+int pcb_centroids_from_acc_f32(const double* acc, int k, int d, float* C, float* cnorm,
+                               float* c_hi, float* c_lo, int ld, void* stream);
+int pcb_centroids_from_acc_f64(const double* acc, int k, int d, double* C, double* cnorm,
+                               void* stream);
+/* cnorm for externally supplied centroids (fixed init). */
+int pcb_centroid_norms_f32(const float* C, int k, int d, float* cnorm,
+                           float* c_hi, float* c_lo, int ld, void* stream);
+int pcb_centroid_norms_f64(const double* C, int k, int d, double* cnorm, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POPCORN_B200_H */

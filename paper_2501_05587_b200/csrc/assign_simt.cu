@@ -1,0 +1,325 @@
+// FFMA (CUDA-core) assignment kernels: distance + row argmin + bookkeeping.
+//
+// Replaces, for one Lloyd iteration, the reference's
+//   D = pn[:,None] - 2.0*(P @ C.T) + cn[None,:]        clustering.py:310-311
+//   raw = row_argmin(D)                                dense.py:56-68
+//   counts / objective / changed bookkeeping           clustering.py:146-149
+// without ever materialising the n x k matrix D.
+//
+// Distances are ranked on s_ij = cnorm_j - 2 <p_i, c_j> (the per-row constant
+// pnorm_i does not change the argmin, dense.py's row-shift invariance), and the
+// own distance mind_i = pnorm_i + s_i,label is what the objective sums.
+// Ties break to the lowest centroid index (strict '<' in ascending j, and
+// (v, j) lexicographic merges across threads).
+//
+// Two variants:
+//  * assign_rowreg<T, DP, PPT>: one point per thread (PPT points), point held in
+//    registers (d <= DP <= 32), centroids broadcast from shared memory.  This is
+//    the small-d path of the north star (C1 d=2, C2 d=16).
+//  * assign_tiled<T>: register-tiled SIMT GEMM (64x64x16 tiles, 4x4 per thread)
+//    with the argmin fused in the epilogue; any d.  Used for f64 and as the
+//    non-tensor-core fallback for large d.
+#include "pcb_common.cuh"
+#include "pcb_launch.cuh"
+
+namespace pcb {
+
+constexpr int kHistMax = 12288;  // per-block smem histogram (48 KB of int)
+
+// Per-block bookkeeping shared by all assignment kernels: counts histogram,
+// objective (sum of own distances, f64), changed (labels != previous labels).
+struct BlockBook {
+  int* hist;        // smem, k ints, or nullptr -> direct global REDs
+  double obj;       // thread-local partials
+  long long changed;
+};
+
+__device__ __forceinline__ void book_point(BlockBook& b, double* acc, const AccLayout& L,
+                                           int lab, double own, const int32_t* labels_prev, int64_t i) {
+  b.obj += own;
+  if (labels_prev != nullptr) b.changed += (labels_prev[i] != lab);
+  if (b.hist != nullptr) atomicAdd(&b.hist[lab], 1);
+  else atomicAdd(&acc[L.counts() + lab], 1.0);
+}
+
+__device__ void book_flush(BlockBook& b, double* acc, const AccLayout& L, int k) {
+  __shared__ double s_obj[32];
+  __shared__ long long s_chg[32];
+  double o = warp_sum(b.obj);
+  long long c = warp_sum(b.changed);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { s_obj[w] = o; s_chg[w] = c; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    o = lane < nw ? s_obj[lane] : 0.0;
+    c = lane < nw ? s_chg[lane] : 0;
+    o = warp_sum(o);
+    c = warp_sum(c);
+    if (lane == 0) {
+      atomicAdd(&acc[L.objective()], o);
+      atomicAdd(&acc[L.changed()], (double)c);
+    }
+  }
+  if (b.hist != nullptr) {
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      int h = b.hist[j];
+      if (h) atomicAdd(&acc[L.counts() + j], (double)h);
+    }
+  }
+}
+
+__device__ __forceinline__ void flag_nonfinite(const long long* state, double v) {
+  if (state != nullptr && !isfinite(v)) atomicExch((unsigned long long*)&state[kNanFlag], 1ull);
+}
+
+// ---------------------------------------------------------------------------
+// Small-d: one point per thread, centroids in shared memory.
+// ---------------------------------------------------------------------------
+template <typename T, int DP, int PPT>
+__global__ void __launch_bounds__(256)
+assign_rowreg(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, int d,
+              const T* __restrict__ C, const T* __restrict__ cnorm, int k, int kc,
+              const int32_t* __restrict__ labels_prev, int32_t* __restrict__ labels,
+              T* __restrict__ mind, double* __restrict__ acc, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sC = reinterpret_cast<T*>(smem_raw);          // [kc][DP]
+  T* sN = sC + (size_t)kc * DP;                     // [kc]
+  int* hist = reinterpret_cast<int*>(sN + kc);      // [k] (optional)
+  const AccLayout L{k, d};
+  BlockBook book{(acc != nullptr && k <= kHistMax) ? hist : nullptr, 0.0, 0};
+  if (book.hist) for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
+
+  auto load_chunk = [&](int c0) {
+    const int cnt = min(kc, k - c0);
+    for (int e = threadIdx.x; e < cnt * DP; e += blockDim.x) {
+      const int jj = e / DP, t = e - jj * DP;
+      sC[e] = t < d ? C[(int64_t)(c0 + jj) * d + t] : T(0);
+    }
+    for (int jj = threadIdx.x; jj < cnt; jj += blockDim.x) sN[jj] = cnorm[c0 + jj];
+  };
+  const bool single_chunk = (k <= kc);
+  if (single_chunk) load_chunk(0);
+  __syncthreads();
+
+  const int64_t group = (int64_t)blockDim.x * PPT;
+  for (int64_t base = (int64_t)blockIdx.x * group; base < n; base += (int64_t)gridDim.x * group) {
+    T p[PPT][DP];
+    int64_t idx[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+      idx[r] = base + threadIdx.x + (int64_t)r * blockDim.x;
+      const int64_t ii = idx[r] < n ? idx[r] : (n - 1);
+#pragma unroll
+      for (int t = 0; t < DP; ++t) p[r][t] = t < d ? P[ii * d + t] : T(0);
+    }
+    T bv[PPT];
+    int bj[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) { bv[r] = T(INFINITY); bj[r] = 0; }
+
+    for (int c0 = 0; c0 < k; c0 += kc) {
+      if (!single_chunk) { __syncthreads(); load_chunk(c0); __syncthreads(); }
+      const int cnt = min(kc, k - c0);
+      for (int jj = 0; jj < cnt; ++jj) {
+        T c[DP];
+#pragma unroll
+        for (int t = 0; t < DP; ++t) c[t] = sC[jj * DP + t];
+        const T cn = sN[jj];
+#pragma unroll
+        for (int r = 0; r < PPT; ++r) {
+          T dot = T(0);
+#pragma unroll
+          for (int t = 0; t < DP; ++t) dot = fma(p[r][t], c[t], dot);
+          const T s = fma(T(-2), dot, cn);
+          if (s < bv[r]) { bv[r] = s; bj[r] = c0 + jj; }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+      if (idx[r] < n) {
+        const T own = pnorm[idx[r]] + bv[r];
+        labels[idx[r]] = bj[r];
+        if (mind) mind[idx[r]] = own;
+        if (acc) book_point(book, acc, L, bj[r], (double)own, labels_prev, idx[r]);
+        flag_nonfinite(state, (double)own);
+      }
+    }
+  }
+  if (acc) {
+    __syncthreads();
+    book_flush(book, acc, L, k);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Any d: register-tiled SIMT GEMM with fused argmin.  Block tile 64 points x
+// 64 centroids x 16 dims, 256 threads, each thread a 4x4 micro-tile with rows
+// ty+16r and columns tx+16c.  Every CTA walks all k centroids for its row
+// tile, keeping a per-row running (value, index) minimum in registers.
+// ---------------------------------------------------------------------------
+constexpr int TBM = 64, TBN = 64, TBK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+assign_tiled(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, int d,
+             const T* __restrict__ C, const T* __restrict__ cnorm, int k,
+             const int32_t* __restrict__ labels_prev, int32_t* __restrict__ labels,
+             T* __restrict__ mind, double* __restrict__ acc, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  __shared__ T As[TBK][TBM + 1];
+  __shared__ T Bs[TBK][TBN + 1];
+  __shared__ T sN[TBN];
+  __shared__ int hist_s[kHistMax > 4096 ? 4096 : kHistMax];
+  const AccLayout L{k, d};
+  BlockBook book{(acc != nullptr && k <= 4096) ? hist_s : nullptr, 0.0, 0};
+  if (book.hist) for (int j = threadIdx.x; j < k; j += blockDim.x) hist_s[j] = 0;
+  __syncthreads();
+
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t mtiles = (n + TBM - 1) / TBM;
+  for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+    const int64_t row0 = mt * TBM;
+    T bv[4];
+    int bj[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) { bv[r] = T(INFINITY); bj[r] = 0; }
+    for (int col0 = 0; col0 < k; col0 += TBN) {
+      T accm[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) accm[r][c] = T(0);
+      for (int k0 = 0; k0 < d; k0 += TBK) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < TBM * TBK; e += blockDim.x) {
+          const int m = e / TBK, kk = e - m * TBK;
+          const int64_t row = row0 + m;
+          As[kk][m] = (row < n && k0 + kk < d) ? P[row * d + k0 + kk] : T(0);
+          const int j = col0 + m;   // TBN == TBM
+          Bs[kk][m] = (j < k && k0 + kk < d) ? C[(int64_t)j * d + k0 + kk] : T(0);
+        }
+        if (threadIdx.x < TBN) sN[threadIdx.x] = (col0 + threadIdx.x < k) ? cnorm[col0 + threadIdx.x] : T(0);
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < TBK; ++kk) {
+          T a[4], b[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) accm[r][c] = fma(a[r], b[c], accm[r][c]);
+        }
+      }
+      // epilogue for this centroid tile: columns ascending within the thread
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = col0 + tx + 16 * c;
+        if (j < k) {
+          const T cn = sN[tx + 16 * c];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const T s = fma(T(-2), accm[r][c], cn);
+            argmin_merge(bv[r], bj[r], s, j);
+          }
+        }
+      }
+    }
+    // merge across the 16 threads (tx) that share these rows
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        T v2 = __shfl_xor_sync(0xffffffffu, bv[r], o);
+        int j2 = __shfl_xor_sync(0xffffffffu, bj[r], o);
+        argmin_merge(bv[r], bj[r], v2, j2);
+      }
+      const int64_t row = row0 + ty + 16 * r;
+      if (tx == 0 && row < n) {
+        const T own = pnorm[row] + bv[r];
+        labels[row] = bj[r];
+        if (mind) mind[row] = own;
+        if (acc) book_point(book, acc, L, bj[r], (double)own, labels_prev, row);
+        flag_nonfinite(state, (double)own);
+      }
+    }
+  }
+  if (acc) {
+    __syncthreads();
+    book_flush(book, acc, L, k);
+  }
+}
+
+template <typename T, int DP, int PPT>
+static int launch_rowreg(const T* P, const T* pnorm, int64_t n, int d, const T* C, const T* cnorm,
+                         int k, const int32_t* lp, int32_t* lab, T* mind, double* acc,
+                         const long long* state, cudaStream_t st) {
+  const int per = (DP + 1) * (int)sizeof(T);
+  int kc = 32768 / per;
+  if (kc > k) kc = k;
+  size_t smem = (size_t)kc * per + ((acc != nullptr && k <= kHistMax) ? (size_t)k * sizeof(int) : 0);
+  auto kern = assign_rowreg<T, DP, PPT>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  const int64_t groups = (n + 256 * PPT - 1) / (256 * PPT);
+  const int grid = (int)std::min<int64_t>(groups, (int64_t)persistent_grid(kern, 256, smem));
+  kern<<<grid, 256, smem, st>>>(P, pnorm, n, d, C, cnorm, k, kc, lp, lab, mind, acc, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename T>
+static int assign_dispatch(const T* P, const T* pnorm, int64_t n, int d, const T* C, const T* cnorm,
+                           int k, const int32_t* lp, int32_t* lab, T* mind, double* acc,
+                           const long long* state, int variant, cudaStream_t st) {
+  if (n < 1 || d < 1 || k < 1 || !P || !pnorm || !C || !cnorm || !lab) return PCB_EINVAL;
+  if (variant == PCB_ASSIGN_AUTO) variant = (d <= 32) ? PCB_ASSIGN_ROWREG : PCB_ASSIGN_TILED;
+  if (variant == PCB_ASSIGN_ROWREG) {
+    if (d <= 1) return launch_rowreg<T, 1, 4>(P, pnorm, n, d, C, cnorm, k, lp, lab, mind, acc, state, st);
+    if (d <= 2) return launch_rowreg<T, 2, 4>(P, pnorm, n, d, C, cnorm, k, lp, lab, mind, acc, state, st);
+    if (d <= 4) return launch_rowreg<T, 4, 4>(P, pnorm, n, d, C, cnorm, k, lp, lab, mind, acc, state, st);
+    if (d <= 8) return launch_rowreg<T, 8, 2>(P, pnorm, n, d, C, cnorm, k, lp, lab, mind, acc, state, st);
+    if (d <= 16) return launch_rowreg<T, 16, 2>(P, pnorm, n, d, C, cnorm, k, lp, lab, mind, acc, state, st);
+    if (d <= 32) return launch_rowreg<T, 32, 1>(P, pnorm, n, d, C, cnorm, k, lp, lab, mind, acc, state, st);
+    return PCB_EUNSUP;
+  }
+  if (variant == PCB_ASSIGN_TILED) {
+    auto kern = assign_tiled<T>;
+    const int64_t mtiles = (n + TBM - 1) / TBM;
+    const int grid = (int)std::min<int64_t>(mtiles, (int64_t)persistent_grid(kern, 256, 0));
+    kern<<<grid, 256, 0, st>>>(P, pnorm, n, d, C, cnorm, k, lp, lab, mind, acc, state);
+    PCB_CHECK_LAUNCH();
+    return 0;
+  }
+  return PCB_EUNSUP;
+}
+
+}  // namespace pcb
+
+extern "C" int pcb_assign_f32(const float* P, const float* pnorm, int64_t n, int d,
+                              const float* C, const float* cnorm, int k,
+                              const int32_t* labels_prev, int32_t* labels, float* mind,
+                              double* acc, const long long* state, int variant, void* stream) {
+  if (variant == PCB_ASSIGN_TC3XTF32) return PCB_EUNSUP;  // use pcb_assign_tc_f32
+  if (variant == PCB_ASSIGN_DELTA)
+    return pcb::assign_delta_f32(P, pnorm, n, d, C, cnorm, k, labels_prev, labels, mind, acc, state,
+                                 (cudaStream_t)stream);
+  return pcb::assign_dispatch<float>(P, pnorm, n, d, C, cnorm, k, labels_prev, labels, mind, acc,
+                                     state, variant, (cudaStream_t)stream);
+}
+
+extern "C" int pcb_assign_f64(const double* P, const double* pnorm, int64_t n, int d,
+                              const double* C, const double* cnorm, int k,
+                              const int32_t* labels_prev, int32_t* labels, double* mind,
+                              double* acc, const long long* state, int variant, void* stream) {
+  if (variant == PCB_ASSIGN_TC3XTF32 || variant == PCB_ASSIGN_DELTA) return PCB_EUNSUP;
+  return pcb::assign_dispatch<double>(P, pnorm, n, d, C, cnorm, k, labels_prev, labels, mind, acc,
+                                      state, variant, (cudaStream_t)stream);
+}

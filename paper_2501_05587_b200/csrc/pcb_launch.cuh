@@ -1,0 +1,26 @@
+// Host-side launch helpers shared by the kernel translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <stdint.h>
+
+namespace pcb {
+
+// SM count of the current device (cached per device).
+int sm_count();
+
+// Grid for a persistent kernel: SMs x resident blocks per SM.
+template <typename K>
+inline int persistent_grid(K kernel, int block, size_t smem) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  return per_sm * sm_count();
+}
+
+int assign_delta_f32(const float* P, const float* pnorm, int64_t n, int d, const float* C,
+                     const float* cnorm, int k, const int32_t* labels_prev, int32_t* labels,
+                     float* mind, double* acc, const long long* state, cudaStream_t st);
+
+}  // namespace pcb

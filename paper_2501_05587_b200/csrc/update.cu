@@ -1,0 +1,255 @@
+// Centroid update: per-cluster sums of point rows (clustering.py:282-288).
+//
+// The reference computes, for every cluster j, P[flatnonzero(labels==j)].mean(0)
+// (k passes over the labels, f32 accumulation).  Here:
+//   1. scan_counts:  exclusive scan of the cluster counts (already produced by
+//                    the assignment kernel) -> segment offsets;
+//   2. scatter:      counting sort of point ids by label; a warp aggregates
+//                    equal labels with __match_any_sync so one atomic claims a
+//                    run of slots per label and warp;
+//   3. segment sums: a fixed partition of the sorted ids into slices; each
+//                    slice walks its ids in order, gathering full point rows
+//                    (coalesced, one row per warp step for large d) and
+//                    accumulating in f64 registers; a label boundary flushes
+//                    the partial with one RED.ADD.F64 per dimension.
+// Every point row is read exactly once from HBM (n*d*sizeof(T) bytes), rows
+// are contiguous, and no shared-memory atomics are needed (on sm_100 f32/f64
+// shared atomics are CAS loops).  Sums are f64, so the f32 centroid
+// sum/count is correctly rounded up to the ~1e-16 summation error.
+#include "pcb_common.cuh"
+#include "pcb_launch.cuh"
+
+namespace pcb {
+
+__global__ void __launch_bounds__(1024)
+scan_counts(const double* __restrict__ counts, int k, int32_t* __restrict__ offsets,
+            int32_t* __restrict__ cursor, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  __shared__ int warp_tot[32];
+  __shared__ int carry_s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = 0; base < k; base += blockDim.x) {
+    const int j = base + threadIdx.x;
+    const int c = j < k ? (int)counts[j] : 0;
+    int x = c;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int t = warp_tot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const int carry = carry_s;
+    const int excl = carry + (w > 0 ? warp_tot[w - 1] : 0) + x - c;
+    if (j < k) { offsets[j] = excl; cursor[j] = excl; }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_s = excl + c;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) offsets[k] = carry_s;
+}
+
+__global__ void __launch_bounds__(256)
+scatter_by_label(const int32_t* __restrict__ labels, int64_t n, int32_t* __restrict__ cursor,
+                 int32_t* __restrict__ perm, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool live = i < n;
+    const unsigned act = __ballot_sync(0xffffffffu, live);
+    if (!live) continue;
+    const int j = labels[i];
+    const unsigned peers = __match_any_sync(act, j);
+    const int leader = __ffs(peers) - 1;
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    int slot = 0;
+    if (lane == leader) slot = atomicAdd(&cursor[j], __popc(peers));
+    slot = __shfl_sync(peers, slot, leader);
+    perm[slot + rank] = (int32_t)i;
+  }
+}
+
+// Largest j with offsets[j] <= s (segments may be empty: offsets non-decreasing).
+__device__ __forceinline__ int segment_of(const int32_t* offsets, int k, int64_t s) {
+  int lo = 0, hi = k - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (offsets[mid] <= s) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Large d: one warp per slice, lanes across a 32*VEC-wide chunk of dimensions.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256)
+segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict__ perm,
+            const int32_t* __restrict__ offsets, int k, int64_t slice, double* __restrict__ acc,
+            const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nslices = (n + slice - 1) / slice;
+  const int chunk = 32 * VEC;
+  for (int64_t sl = warp; sl < nslices; sl += nwarps) {
+    const int64_t s0 = sl * slice, s1 = min(n, s0 + slice);
+    const int j0 = segment_of(offsets, k, s0);
+    for (int t0 = 0; t0 < d; t0 += chunk) {
+      const int tb = t0 + lane * VEC;
+      double a[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) a[v] = 0.0;
+      int j = j0;
+      int64_t jend = offsets[j + 1];
+      int64_t s = s0;
+      auto flush = [&](int jj) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          if (tb + v < d) atomicAdd(&acc[(int64_t)jj * d + tb + v], a[v]);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) a[v] = 0.0;
+      };
+      while (s < s1) {
+        while (s >= jend) {  // crossed into a later segment
+          flush(j);
+          ++j;
+          jend = offsets[j + 1];
+        }
+        const int64_t e = min(s1, jend);
+        // unrolled gather of up to 4 rows at a time
+        for (; s + 4 <= e; s += 4) {
+          T r[4][VEC];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t i = perm[s + u];
+            const T* row = P + i * d;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) r[u][v] = (tb + v < d) ? row[tb + v] : T(0);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) a[v] += (double)r[u][v];
+        }
+        for (; s < e; ++s) {
+          const int64_t i = perm[s];
+          const T* row = P + i * d;
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) a[v] += (tb + v < d) ? (double)row[tb + v] : 0.0;
+        }
+      }
+      flush(j);
+    }
+  }
+}
+
+// Small d (<= DP <= 16): one thread per slice, the whole row in registers.
+template <typename T, int DP>
+__global__ void __launch_bounds__(256)
+segsum_thread(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict__ perm,
+              const int32_t* __restrict__ offsets, int k, int64_t slice, double* __restrict__ acc,
+              const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nslices = (n + slice - 1) / slice;
+  for (int64_t sl = tid; sl < nslices; sl += nth) {
+    const int64_t s0 = sl * slice, s1 = min(n, s0 + slice);
+    int j = segment_of(offsets, k, s0);
+    int64_t jend = offsets[j + 1];
+    double a[DP];
+#pragma unroll
+    for (int t = 0; t < DP; ++t) a[t] = 0.0;
+    for (int64_t s = s0; s < s1; ++s) {
+      while (s >= jend) {
+#pragma unroll
+        for (int t = 0; t < DP; ++t) {
+          if (t < d && a[t] != 0.0) atomicAdd(&acc[(int64_t)j * d + t], a[t]);
+          a[t] = 0.0;
+        }
+        ++j;
+        jend = offsets[j + 1];
+      }
+      const T* row = P + (int64_t)perm[s] * d;
+#pragma unroll
+      for (int t = 0; t < DP; ++t) if (t < d) a[t] += (double)row[t];
+    }
+#pragma unroll
+    for (int t = 0; t < DP; ++t)
+      if (t < d && a[t] != 0.0) atomicAdd(&acc[(int64_t)j * d + t], a[t]);
+  }
+}
+
+template <typename T>
+static int segment_sums(const T* P, int64_t n, int d, const int32_t* perm, const int32_t* offsets,
+                        int k, double* acc, const long long* state, cudaStream_t st) {
+  if (n < 1 || d < 1 || k < 1 || !P || !perm || !offsets || !acc) return PCB_EINVAL;
+  const int sms = sm_count();
+  if (d <= 16) {
+    // ~8 slices per thread-wave keeps every SM busy; min 16 rows per slice
+    const int64_t threads = (int64_t)sms * 2048;
+    int64_t slice = std::max<int64_t>(16, (n + threads - 1) / threads);
+    const int64_t nsl = (n + slice - 1) / slice;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 255) / 256, (int64_t)sms * 8));
+#define PCB_SEG_T(DPV) segsum_thread<T, DPV><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, slice, acc, state)
+    if (d <= 2) PCB_SEG_T(2);
+    else if (d <= 4) PCB_SEG_T(4);
+    else if (d <= 8) PCB_SEG_T(8);
+    else PCB_SEG_T(16);
+#undef PCB_SEG_T
+  } else {
+    const int64_t warps = (int64_t)sms * 64;
+    int64_t slice = std::max<int64_t>(64, (n + warps - 1) / warps);
+    const int64_t nsl = (n + slice - 1) / slice;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl * 32 + 255) / 256, (int64_t)sms * 8));
+    if (d <= 64)
+      segsum_warp<T, 2><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, slice, acc, state);
+    else
+      segsum_warp<T, 4><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, slice, acc, state);
+  }
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace pcb
+
+extern "C" int pcb_sort_by_label(const int32_t* labels, int64_t n, int k, const double* counts,
+                                 int32_t* offsets, int32_t* cursor, int32_t* perm,
+                                 const long long* state, void* stream) {
+  if (n < 1 || k < 1 || !labels || !counts || !offsets || !cursor || !perm) return PCB_EINVAL;
+  if (n > INT32_MAX) return PCB_EUNSUP;
+  cudaStream_t st = (cudaStream_t)stream;
+  pcb::scan_counts<<<1, 1024, 0, st>>>(counts, k, offsets, cursor, state);
+  PCB_CHECK_LAUNCH();
+  const int sms = pcb::sm_count();
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+  pcb::scatter_by_label<<<grid, 256, 0, st>>>(labels, n, cursor, perm, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_segment_sums_f32(const float* P, int64_t n, int d, const int32_t* perm,
+                                    const int32_t* offsets, int k, double* acc,
+                                    const long long* state, void* stream) {
+  return pcb::segment_sums<float>(P, n, d, perm, offsets, k, acc, state, (cudaStream_t)stream);
+}
+
+extern "C" int pcb_segment_sums_f64(const double* P, int64_t n, int d, const int32_t* perm,
+                                    const int32_t* offsets, int k, double* acc,
+                                    const long long* state, void* stream) {
+  return pcb::segment_sums<double>(P, n, d, perm, offsets, k, acc, state, (cudaStream_t)stream);
+}

@@ -1,0 +1,141 @@
+"""Row-sharded multi-GPU Lloyd: one process per GPU, NCCL over NVLink.
+
+Points are split into contiguous row ranges (global index = rank offset +
+local index, so the reference's lowest-index tie breaks stay global).
+Centroids are replicated.  Each iteration exchanges exactly one buffer: the
+fused f64 accumulator [sums k*d | counts k | objective | changed]
+(8*(k*(d+1)+2) bytes: 1.06 MB at n=10M/d=128/k=1024) with one in-place
+``all_reduce(SUM)``; every rank then runs the identical finalize, so the
+centroids stay bitwise identical across ranks.
+
+Empty-cluster repair (clustering.py:111-139) needs global decisions; it is
+rare and host-orchestrated: one host read of the global counts per iteration
+decides whether it runs; per donor, each rank's best unmoved point
+(argmax_own) is all-gathered, the owner applies the move and publishes a
+delta that every rank commits after an all_reduce.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .clustering import ClusteringResult, KKMeansConfig, TimingBreakdown, init_assignments
+from .validation import normalize_dtype
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous, balanced row range of `rank` (first n % world ranks get one more)."""
+    base, rem = divmod(n, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+class Comm:
+    """torch.distributed plumbing used by the engine (NCCL on GPU, gloo in CPU tests)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world_size = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.offset = 0
+
+    def all_reduce_sum(self, t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def all_reduce_max(self, t):
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+
+    def all_gather(self, t):
+        out = [torch.empty_like(t) for _ in range(self.world_size)]
+        dist.all_gather(out, t, group=self.group)
+        return out
+
+    def barrier(self):
+        dist.barrier(group=self.group)
+
+    # -- global empty-cluster repair ------------------------------------------------
+    def repair(self, eng, prev, new) -> None:
+        k, d = eng.k, eng.d
+        kd = k * d
+        counts = eng.acc[kd:kd + k]
+        if eng.state[1].item() != 0:           # stopped: nothing to do
+            return
+        if not bool((counts == 0).any().item()):
+            return
+        sfx = eng.sfx
+        key = torch.empty(2, dtype=torch.float64, device=eng.dev)
+        delta = torch.empty(d + 4, dtype=torch.float64, device=eng.dev)
+        while True:
+            empties = torch.nonzero(counts == 0).flatten().tolist()
+            if not empties:
+                return
+            for j in empties:
+                L.call(f"pcb_argmax_own_{sfx}", _p(eng.mind), eng.n, self.offset, _p(key), _stream())
+                keys = torch.stack(self.all_gather(key)).cpu().numpy()
+                # max own distance, lowest global index on ties (clustering.py:135-137)
+                order = np.lexsort((keys[:, 1], -keys[:, 0]))
+                donor = int(keys[order[0], 1])
+                delta.zero_()
+                local = donor - self.offset
+                if 0 <= local < eng.n:
+                    L.call(f"pcb_repair_apply_{sfx}", _p(eng.P), _p(eng.pnorm), d, _p(eng.C),
+                           _p(eng.cnorm), _p(prev), _p(new), _p(eng.mind), local, int(j),
+                           _p(delta), _stream())
+                self.all_reduce_sum(delta)
+                L.call("pcb_repair_commit", _p(eng.acc), k, d, int(j), _p(delta), _p(eng.state),
+                       _stream())
+
+
+def run_lloyd_sharded(points_local, cfg: KKMeansConfig, n_total: int, offset: int,
+                      comm: Comm | None = None) -> ClusteringResult:
+    """Lloyd over a row shard; every rank returns the same global history/centroids
+    and its own shard's labels.  Init labels are the reference's global
+    PCG64 stream (clustering.py:91-108), sliced to the shard."""
+    from .engine import LloydEngine
+
+    comm = comm or Comm()
+    comm.offset = offset
+    cfg.validate_for(n_total)
+    dtype = normalize_dtype(cfg.dtype)
+    labels0 = init_assignments(n_total, cfg.k, cfg.seed)
+    n_local = int(points_local.shape[0])
+    eng = LloydEngine(points_local, cfg.k, dtype=dtype, device=cfg.device, variant=cfg.variant,
+                      comm=comm, n_total=n_total, max_iters=cfg.max_iters)
+    if cfg.init is None:
+        eng.init_centroids_from_labels(labels0[offset:offset + n_local])
+    else:
+        eng.set_labels(labels0[offset:offset + n_local])
+        eng.set_centroids(np.asarray(cfg.init))
+    out = eng.run(cfg.max_iters, cfg.tol, cfg.check_convergence,
+                  record_history=cfg.record_label_history)
+    return ClusteringResult(labels=out.labels, iterations_run=out.iterations_run,
+                            objective_history=out.objective_history, converged=out.converged,
+                            timings=TimingBreakdown(0.0, out.distance_seconds, out.update_seconds),
+                            label_history=out.label_history, repairs=out.repairs,
+                            centroids=out.centroids)
+
+
+def init_from_env(backend: str = "nccl"):
+    """Initialise torch.distributed from torchrun's env (127.0.0.1 rendezvous)."""
+    if dist.is_initialized():
+        return
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if backend == "nccl":
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group(backend=backend, rank=rank, world_size=world)

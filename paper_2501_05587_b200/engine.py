@@ -1,0 +1,292 @@
+"""Device-resident Lloyd engine: buffers, kernel sequencing, collectives.
+
+One ``LloydEngine`` owns one rank's row shard of the points for one fit.
+Per iteration it enqueues, on the current CUDA stream and with no host
+synchronisation:
+
+    acc <- 0                                   fused f64 accumulator
+    assign      (labels, mind, counts, objective, changed)   clustering.py:310-311, 146-149
+    sort_by_label + segment_sums (per-cluster f64 row sums)  clustering.py:282-288
+    [all_reduce(acc) over NCCL when world_size > 1]
+    repair      (empty clusters, on device; no-op normally)  clustering.py:111-139
+    finalize    (centroids, cnorm, history, convergence)     clustering.py:316-324
+
+Every kernel checks the device stop flag, so ``check_convergence`` costs no
+host round trip; the host syncs once at the end of the fit.  PyTorch is used
+only for device memory, streams, pinned host buffers and torch.distributed.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+_F32 = np.dtype(np.float32)
+_F64 = np.dtype(np.float64)
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def require_cuda(device=None) -> torch.device:
+    """The CUDA device to run on; RuntimeError if there is none (no CPU fallback)."""
+    L.load()
+    if not torch.cuda.is_available():
+        raise RuntimeError("popcorn_b200 needs a CUDA sm_100 device; none is available "
+                           "(there is no CPU fallback)")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                       torch.device(device).index or 0)
+    sm, mj, mn = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    rc = L.load().pcb_device_info(dev.index, ctypes.byref(sm), ctypes.byref(mj), ctypes.byref(mn))
+    if rc != 0:
+        raise RuntimeError(f"device {dev} is sm_{mj.value}{mn.value}; popcorn_b200 is built for sm_100a")
+    return dev
+
+
+def resolve_variant(variant: str, dtype: np.dtype, d: int) -> str:
+    if variant not in L.VARIANTS:
+        raise ValueError(f"unknown assign variant {variant!r}; expected one of {tuple(L.VARIANTS)}")
+    if variant != "auto":
+        if dtype == _F64 and variant in ("tc3xtf32", "delta"):
+            raise ValueError(f"variant {variant!r} is float32-only")
+        if variant == "rowreg" and d > 32:
+            raise ValueError("variant 'rowreg' needs d <= 32")
+        return variant
+    if d <= 32:
+        return "rowreg"
+    return "tiled"
+
+
+@dataclass
+class RunOutput:
+    iterations_run: int
+    converged: bool
+    objective_history: np.ndarray
+    repairs: np.ndarray
+    labels: np.ndarray
+    label_history: list
+    centroids: np.ndarray
+    distance_seconds: float
+    update_seconds: float
+
+
+class LloydEngine:
+    """One rank's shard: P (n_local x d) resident in HBM, centroids replicated."""
+
+    def __init__(self, points, k: int, *, dtype=np.float32, device=None, variant: str = "auto",
+                 comm=None, n_total: int | None = None, max_iters: int = 30):
+        self.dev = require_cuda(device)
+        self.dtype = np.dtype(dtype)
+        self.tdtype = torch.float32 if self.dtype == _F32 else torch.float64
+        self.sfx = "f32" if self.dtype == _F32 else "f64"
+        self.comm = comm
+        with torch.cuda.device(self.dev):
+            if isinstance(points, torch.Tensor):
+                P = points.to(device=self.dev, dtype=self.tdtype).contiguous()
+            else:
+                host = torch.from_numpy(np.ascontiguousarray(points, dtype=self.dtype))
+                P = host.pin_memory().to(self.dev, non_blocking=True)
+            self.P = P
+            self.n, self.d = int(P.shape[0]), int(P.shape[1])
+            self.k = int(k)
+            self.n_total = int(n_total if n_total is not None else self.n)
+            self.variant = resolve_variant(variant, self.dtype, self.d)
+            self.vcode = L.VARIANTS[self.variant]
+            n, d, kk = self.n, self.d, self.k
+            dev, td = self.dev, self.tdtype
+            self.pnorm = torch.empty(n, dtype=td, device=dev)
+            self.C = torch.zeros((kk, d), dtype=td, device=dev)
+            self.cnorm = torch.empty(kk, dtype=td, device=dev)
+            self.labels = [torch.zeros(n, dtype=torch.int32, device=dev) for _ in range(2)]
+            self.mind = torch.empty(n, dtype=td, device=dev)
+            self.acc_size = kk * d + kk + 2
+            self.acc = torch.zeros(self.acc_size, dtype=torch.float64, device=dev)
+            self.perm = torch.empty(n, dtype=torch.int32, device=dev)
+            self.offsets = torch.empty(kk + 1, dtype=torch.int32, device=dev)
+            self.cursor = torch.empty(kk, dtype=torch.int32, device=dev)
+            self.state = torch.zeros(L.STATE_WORDS, dtype=torch.int64, device=dev)
+            self.max_iters = max(1, int(max_iters))
+            self.obj_hist = torch.zeros(self.max_iters, dtype=torch.float64, device=dev)
+            self.rep_hist = torch.zeros(self.max_iters, dtype=torch.int64, device=dev)
+            sb = int(L.load().pcb_repair_scratch_bytes(kk))
+            self.repair_scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+            self.repair_scratch_bytes = sb
+            # split operands for the tensor-core path (allocated on demand)
+            self.ld = 0
+            self.P_hi = self.P_lo = self.C_hi = self.C_lo = None
+            L.call(f"pcb_point_norms_{self.sfx}", _p(self.P), n, d, _p(self.pnorm), _stream())
+
+    # -- centroid initialisation ------------------------------------------------
+    def set_centroids(self, C) -> None:
+        """Fixed centroids (additive `init=`), replicated on every rank."""
+        with torch.cuda.device(self.dev):
+            Ct = torch.as_tensor(np.ascontiguousarray(C, dtype=self.dtype).reshape(self.k, self.d))
+            self.C.copy_(Ct.to(self.dev))
+            self._centroid_norms()
+
+    def _centroid_norms(self) -> None:
+        if self.dtype == _F32:
+            L.call("pcb_centroid_norms_f32", _p(self.C), self.k, self.d, _p(self.cnorm),
+                   _p(self.C_hi), _p(self.C_lo), self.ld, _stream())
+        else:
+            L.call("pcb_centroid_norms_f64", _p(self.C), self.k, self.d, _p(self.cnorm), _stream())
+
+    def set_labels(self, labels_local: np.ndarray, counts_global: np.ndarray | None = None) -> None:
+        """Labels of this shard (clustering.py:298); previous labels of iteration 1."""
+        with torch.cuda.device(self.dev):
+            lab = torch.from_numpy(np.ascontiguousarray(labels_local, dtype=np.int32))
+            self.labels[0].copy_(lab.to(self.dev))
+
+    def init_centroids_from_labels(self, labels_local: np.ndarray) -> None:
+        """Initial means over the init labels (clustering.py:298-300), on device."""
+        self.set_labels(labels_local)
+        with torch.cuda.device(self.dev):
+            counts = np.bincount(np.asarray(labels_local), minlength=self.k).astype(np.float64)
+            self.acc.zero_()
+            self.acc[self.k * self.d:self.k * self.d + self.k].copy_(torch.from_numpy(counts).to(self.dev))
+            self._sort_and_sum(self.labels[0], None)
+            self._allreduce(self.acc)
+            if self.dtype == _F32:
+                L.call("pcb_centroids_from_acc_f32", _p(self.acc), self.k, self.d, _p(self.C),
+                       _p(self.cnorm), _p(self.C_hi), _p(self.C_lo), self.ld, _stream())
+            else:
+                L.call("pcb_centroids_from_acc_f64", _p(self.acc), self.k, self.d, _p(self.C),
+                       _p(self.cnorm), _stream())
+
+    # -- building blocks ---------------------------------------------------------
+    def _allreduce(self, t) -> None:
+        if self.comm is not None and self.comm.world_size > 1:
+            self.comm.all_reduce_sum(t)
+
+    def _sort_and_sum(self, labels, state) -> None:
+        counts = self.acc[self.k * self.d:]
+        L.call("pcb_sort_by_label", _p(labels), self.n, self.k, _p(counts), _p(self.offsets),
+               _p(self.cursor), _p(self.perm), _p(state), _stream())
+        L.call(f"pcb_segment_sums_{self.sfx}", _p(self.P), self.n, self.d, _p(self.perm),
+               _p(self.offsets), self.k, _p(self.acc), _p(state), _stream())
+
+    def _assign(self, prev, new, acc, state) -> None:
+        L.call(f"pcb_assign_{self.sfx}", _p(self.P), _p(self.pnorm), self.n, self.d, _p(self.C),
+               _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
+               self.vcode, _stream())
+
+    def _repair(self, prev, new) -> None:
+        if self.comm is not None and self.comm.world_size > 1:
+            self.comm.repair(self, prev, new)
+            return
+        L.call(f"pcb_repair_{self.sfx}", _p(self.P), _p(self.pnorm), self.n, self.d, _p(self.C),
+               _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(self.acc),
+               _p(self.state), _p(self.repair_scratch), self.repair_scratch_bytes, _stream())
+
+    def _finalize(self, check_convergence: bool, tol: float) -> None:
+        if self.dtype == _F32:
+            L.call("pcb_finalize_f32", _p(self.acc), self.k, self.d, self.n_total, _p(self.C),
+                   _p(self.cnorm), _p(self.C_hi), _p(self.C_lo), self.ld, _p(self.obj_hist),
+                   _p(self.rep_hist), _p(self.state), int(check_convergence), float(tol), _stream())
+        else:
+            L.call("pcb_finalize_f64", _p(self.acc), self.k, self.d, self.n_total, _p(self.C),
+                   _p(self.cnorm), _p(self.obj_hist), _p(self.rep_hist), _p(self.state),
+                   int(check_convergence), float(tol), _stream())
+
+    def iteration(self, t: int, check_convergence: bool = False, tol: float = 0.0,
+                  events=None) -> None:
+        """Enqueue Lloyd iteration t (reads labels[t%2], writes labels[(t+1)%2])."""
+        prev, new = self.labels[t % 2], self.labels[(t + 1) % 2]
+        self.acc.zero_()
+        if events is not None:
+            events[0].record()
+        self._assign(prev, new, self.acc, self.state)
+        if events is not None:
+            events[1].record()
+        self._sort_and_sum(new, self.state)
+        self._allreduce(self.acc)
+        self._repair(prev, new)
+        self._finalize(check_convergence, tol)
+        if events is not None:
+            events[2].record()
+
+    # -- whole fit -----------------------------------------------------------------
+    def run(self, max_iters: int, tol: float = 0.0, check_convergence: bool = False,
+            record_history: bool = True, timing: bool = True) -> RunOutput:
+        if max_iters > self.max_iters:
+            raise ValueError("max_iters exceeds the engine's history capacity")
+        with torch.cuda.device(self.dev):
+            self.state.zero_()
+            hist = None
+            if record_history:
+                hist = torch.empty((max_iters, self.n), dtype=torch.int32, pin_memory=True)
+            evs = []
+            for t in range(max_iters):
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
+                self.iteration(t, check_convergence, tol, ev)
+                if ev is not None:
+                    evs.append(ev)
+                if hist is not None:
+                    hist[t].copy_(self.labels[(t + 1) % 2], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return self.collect(hist, evs)
+
+    def collect(self, hist=None, evs=()) -> RunOutput:
+        st = self.state.cpu().numpy()
+        if st[5] != 0:
+            raise ValueError("row_argmin: matrix contains NaN")  # dense.py:66-67 semantics
+        iters = int(st[0])
+        labels = self.labels[iters % 2].cpu().numpy()
+        dist_s = upd_s = 0.0
+        for ev in list(evs)[:iters]:
+            dist_s += ev[0].elapsed_time(ev[1]) / 1e3
+            upd_s += ev[1].elapsed_time(ev[2]) / 1e3
+        return RunOutput(
+            iterations_run=iters, converged=bool(st[2]),
+            objective_history=self.obj_hist[:iters].cpu().numpy().astype(np.float64),
+            repairs=self.rep_hist[:iters].cpu().numpy().astype(np.int64),
+            labels=labels,
+            label_history=[hist[t].numpy().copy() for t in range(iters)] if hist is not None else [],
+            centroids=self.C.cpu().numpy(), distance_seconds=dist_s, update_seconds=upd_s)
+
+    # -- lockstep / predict -----------------------------------------------------------
+    def step_from(self, centroids, labels_prev) -> dict:
+        """One iteration from given centroids and previous labels (parity harness)."""
+        self.set_centroids(centroids)
+        self.set_labels(labels_prev)
+        with torch.cuda.device(self.dev):
+            self.state.zero_()
+            self.iteration(0)
+            torch.cuda.current_stream().synchronize()
+            acc = self.acc.cpu().numpy()
+            st = self.state.cpu().numpy()
+            kd = self.k * self.d
+            return {
+                "labels": self.labels[1].cpu().numpy(),
+                "mind": self.mind.cpu().numpy(),
+                "objective": float(self.obj_hist[0].item()),
+                "changed": float(acc[kd + self.k + 1]) / self.n_total,
+                "moved": int(self.rep_hist[0].item()),
+                "centroids": self.C.cpu().numpy(),
+                "counts": acc[kd:kd + self.k].copy(),
+                "nan": bool(st[5]),
+            }
+
+    def predict(self, X) -> np.ndarray:
+        """Nearest centroid for new points (estimator.py:131-136) — the same
+        assignment kernel with the bookkeeping disabled."""
+        with torch.cuda.device(self.dev):
+            Xt = (X.to(self.dev, self.tdtype) if isinstance(X, torch.Tensor) else
+                  torch.from_numpy(np.ascontiguousarray(X, dtype=self.dtype)).to(self.dev))
+            m = int(Xt.shape[0])
+            xn = torch.empty(m, dtype=self.tdtype, device=self.dev)
+            out = torch.empty(m, dtype=torch.int32, device=self.dev)
+            L.call(f"pcb_point_norms_{self.sfx}", _p(Xt), m, self.d, _p(xn), _stream())
+            L.call(f"pcb_assign_{self.sfx}", _p(Xt), _p(xn), m, self.d, _p(self.C), _p(self.cnorm),
+                   self.k, None, _p(out), None, None, None, self.vcode if self.variant != "delta" else 0,
+                   _stream())
+            return out.cpu().numpy()

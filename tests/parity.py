@@ -1,0 +1,62 @@
+"""Lockstep parity checker (SURVEY.md Appendix B / BASELINE.json north_star).
+
+Given the reference step (oracle, same inputs) and the GPU step, assert:
+
+* labels identical except rows whose f64 top-2 relative gap (d2-d1)/|d1|
+  at the step's input centroids is below GAP_EXEMPT = 1e-5;
+* objective within OBJ_RTOL = 1e-6 relative of the reference, plus an f32
+  rounding allowance for the reference's own expansion
+  (2^-22 * sum_i (pn_i + cn_label_i)), which only matters when the
+  objective is tiny compared with the norms (cancellation);
+* centroids within CEN_RTOL = 1e-5 (per centroid, inf-norm relative) of the
+  f64 means over the GPU's own labels, and of the reference's centroids
+  whenever the labels agree;
+* moved (repairs) and changed identical whenever the labels agree.
+"""
+import numpy as np
+
+import oracle
+
+GAP_EXEMPT = 1e-5
+OBJ_RTOL = 1e-6
+CEN_RTOL = 1e-5
+
+
+def centroid_rel_err(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    num = np.abs(a - b).max(axis=1)
+    den = np.maximum(np.abs(b).max(axis=1), 1e-30)
+    return float((num / den).max())
+
+
+def check_step(P, C_in, labels_prev, k, gpu, ref=None, *, dtype=np.float32, what=""):
+    """Compare one GPU step (dict from LloydEngine.step_from) with the oracle."""
+    Pd = np.ascontiguousarray(P, dtype=dtype)
+    Cd = np.ascontiguousarray(C_in, dtype=dtype)
+    if ref is None:
+        ref = oracle.lloyd_step(Pd, oracle.point_norms(Pd), Cd, labels_prev, k)
+    _, gap = oracle.top2_gap_f64(Pd, Cd)
+    diff = gpu["labels"] != ref.labels
+    # a repaired row can legitimately differ only through a different donor,
+    # which itself requires a near-tie; treat donors like exempt rows
+    exempt = gap < GAP_EXEMPT
+    bad = diff & ~exempt
+    assert not bad.any(), (f"{what}: {int(bad.sum())} non-exempt label mismatches "
+                           f"(first rows {np.flatnonzero(bad)[:8].tolist()}, gaps {gap[bad][:8]})")
+    pn = oracle.point_norms(Pd.astype(np.float64))
+    cn = (Cd.astype(np.float64) ** 2).sum(1)
+    allowance = 2.0 ** -22 * float((pn + cn[ref.labels]).sum())
+    dobj = abs(gpu["objective"] - ref.objective)
+    assert dobj <= OBJ_RTOL * abs(ref.objective) + allowance, (
+        f"{what}: objective {gpu['objective']!r} vs ref {ref.objective!r} (|d|={dobj:.3e})")
+    exact = oracle.mean_centroids_f64(Pd, gpu["labels"], k)
+    err = centroid_rel_err(gpu["centroids"], exact)
+    assert err <= CEN_RTOL, f"{what}: centroids vs f64 means rel err {err:.3e}"
+    if not diff.any():
+        assert gpu["moved"] == ref.moved, f"{what}: moved {gpu['moved']} vs {ref.moved}"
+        assert abs(gpu["changed"] - ref.changed) <= 1e-12, f"{what}: changed"
+        err_ref = centroid_rel_err(gpu["centroids"], ref.centroids)
+        assert err_ref <= CEN_RTOL, f"{what}: centroids vs reference rel err {err_ref:.3e}"
+    return {"mismatches": int(diff.sum()), "exempt": int(exempt.sum()),
+            "obj_rel": dobj / max(abs(ref.objective), 1e-300), "cen_rel": err}
