@@ -59,7 +59,8 @@ int pcb_split_tf32(const float* X, int64_t rows, int d, int ld, float* hi, float
 
 /* ---- assignment: distance stage + row argmin (clustering.py:310-311,
  *      dense.py:56-68) fused with the bookkeeping of _assignment_step
- *      (clustering.py:147-149): per-cluster counts, objective, changed.
+ *      (clustering.py:146-149): per-cluster counts and changed (the objective
+ *      is summed by pcb_segment_sums_* from exact own distances).
  *   labels[i] = argmin_j D[i,j] (lowest j on ties), mind[i] = D[i,labels[i]]
  *   where D[i,j] = pnorm[i] + (cnorm[j] - 2 <p_i, c_j>).
  *   labels_prev / acc / state may be NULL (predict mode: estimator.py:131-136).
@@ -75,51 +76,61 @@ int pcb_assign_f64(const double* P, const double* pnorm, int64_t n, int d,
                    const int32_t* labels_prev, int32_t* labels, double* mind,
                    double* acc, const long long* state, int variant, void* stream);
 
+/* tcgen05 3xTF32 variant (PCB_ASSIGN_TC3XTF32): operands pre-split with
+ * pcb_split_tf32 into hi/lo matrices of row stride ld (multiple of 32, >= d);
+ * same outputs and bookkeeping as pcb_assign_f32.                          */
+int pcb_assign_tc_f32(const float* P_hi, const float* P_lo, int ld, const float* pnorm, int64_t n,
+                      int d, const float* C_hi, const float* C_lo, const float* cnorm, int k,
+                      const int32_t* labels_prev, int32_t* labels, float* mind, double* acc,
+                      const long long* state, void* stream);
+
 /* ---- centroid update (clustering.py:282-288): counting sort of point ids by
  *      label, then a segmented f64 sum of point rows per cluster into acc.  */
 /* counts: the counts block of acc (acc + k*d).  offsets: k+1 segment starts. */
 int pcb_sort_by_label(const int32_t* labels, int64_t n, int k, const double* counts,
                       int32_t* offsets /* k+1 */, int32_t* cursor /* k */, int32_t* perm,
                       const long long* state, void* stream);
-/* Adds the per-cluster row sums into acc[0 : k*d) (RED.ADD.F64). */
+/* Adds the per-cluster row sums into acc[0 : k*d) (RED.ADD.F64) and, for
+ * every sorted position s, the exact own distance own_sorted[s] =
+ * sum_t (P[perm[s]][t] - C[label][t])^2 (f64) of the new labels, whose sum goes
+ * to acc's objective word (clustering.py:148).  C: the centroids the labels
+ * were assigned against.                                                    */
 int pcb_segment_sums_f32(const float* P, int64_t n, int d, const int32_t* perm,
-                         const int32_t* offsets, int k, double* acc,
-                         const long long* state, void* stream);
+                         const int32_t* offsets, int k, const float* C, double* own_sorted,
+                         double* acc, const long long* state, void* stream);
 int pcb_segment_sums_f64(const double* P, int64_t n, int d, const int32_t* perm,
-                         const int32_t* offsets, int k, double* acc,
-                         const long long* state, void* stream);
+                         const int32_t* offsets, int k, const double* C, double* own_sorted,
+                         double* acc, const long long* state, void* stream);
 
 /* ---- empty-cluster repair (clustering.py:111-139), single-rank, on device.
  *   For each empty cluster j ascending: the not-yet-moved point with the
  *   largest own distance (lowest index on ties) moves to j; repeated while any
- *   cluster is empty.  Adjusts acc (sums, counts, objective, changed) and
- *   state[3] (repairs).  No-op when no cluster is empty.                    */
+ *   cluster is empty.  Reads own_sorted/perm from the update kernel, adjusts
+ *   acc (sums, counts, objective, changed) and state[3] (repairs).  No-op
+ *   when no cluster is empty.  One cooperative launch.                     */
 int64_t pcb_repair_scratch_bytes(int k);   /* device scratch the caller provides */
-int pcb_repair_f32(const float* P, const float* pnorm, int64_t n, int d,
-                   const float* C, const float* cnorm, int k,
-                   const int32_t* labels_prev, int32_t* labels, float* mind,
-                   double* acc, long long* state, void* scratch, int64_t scratch_bytes,
-                   void* stream);
-int pcb_repair_f64(const double* P, const double* pnorm, int64_t n, int d,
-                   const double* C, const double* cnorm, int k,
-                   const int32_t* labels_prev, int32_t* labels, double* mind,
-                   double* acc, long long* state, void* scratch, int64_t scratch_bytes,
-                   void* stream);
+int pcb_repair_f32(const float* P, int64_t n, int d, const float* C, int k, const int32_t* perm,
+                   const int32_t* labels_prev, int32_t* labels, double* own_sorted, double* acc,
+                   long long* state, void* scratch, int64_t scratch_bytes, void* stream);
+int pcb_repair_f64(const double* P, int64_t n, int d, const double* C, int k, const int32_t* perm,
+                   const int32_t* labels_prev, int32_t* labels, double* own_sorted, double* acc,
+                   long long* state, void* scratch, int64_t scratch_bytes, void* stream);
 
 /* Multi-rank repair (host-orchestrated).  argmax_own writes
- * [own distance, global index] of this rank's best unmoved point (ties ->
- * lowest index).  repair_apply moves the donor on its owner rank and writes a
- * delta record (f64, d+4 words: p_donor | old label | d_objective |
- * d_changed | valid=1); non-owners zero it; after an all-reduce SUM every rank
- * calls repair_commit to patch its accumulator identically.                */
-int pcb_argmax_own_f32(const float* mind, int64_t n, int64_t offset, double* out2, void* stream);
-int pcb_argmax_own_f64(const double* mind, int64_t n, int64_t offset, double* out2, void* stream);
-int pcb_repair_apply_f32(const float* P, const float* pnorm, int d, const float* C,
-                         const float* cnorm, const int32_t* labels_prev, int32_t* labels,
-                         float* mind, int64_t donor_local, int j, double* delta, void* stream);
-int pcb_repair_apply_f64(const double* P, const double* pnorm, int d, const double* C,
-                         const double* cnorm, const int32_t* labels_prev, int32_t* labels,
-                         double* mind, int64_t donor_local, int j, double* delta, void* stream);
+ * [own distance, global point index, local sorted position] of this rank's
+ * best unmoved point (ties -> lowest index).  repair_apply moves the donor
+ * (sorted position pos) on its owner rank and writes a delta record (f64,
+ * d+4 words: p_donor | old label | d_objective | d_changed | valid=1);
+ * non-owners zero it; after an all-reduce SUM every rank calls repair_commit
+ * to patch its (already identical) accumulator.                           */
+int pcb_argmax_own(const double* own_sorted, const int32_t* perm, int64_t n, int64_t offset,
+                   double* out3, void* stream);
+int pcb_repair_apply_f32(const float* P, int d, const float* C, const int32_t* perm,
+                         const int32_t* labels_prev, int32_t* labels, double* own_sorted,
+                         int64_t pos, int j, double* delta, void* stream);
+int pcb_repair_apply_f64(const double* P, int d, const double* C, const int32_t* perm,
+                         const int32_t* labels_prev, int32_t* labels, double* own_sorted,
+                         int64_t pos, int j, double* delta, void* stream);
 int pcb_repair_commit(double* acc, int k, int d, int j, const double* delta, long long* state,
                       void* stream);
 

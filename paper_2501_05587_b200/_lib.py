@@ -28,16 +28,16 @@ SIGNATURES = {
     "pcb_split_tf32": (I32, [P, I64, I32, I32, P, P, P]),
     "pcb_assign_f32": (I32, [P, P, I64, I32, P, P, I32, P, P, P, P, P, I32, P]),
     "pcb_assign_f64": (I32, [P, P, I64, I32, P, P, I32, P, P, P, P, P, I32, P]),
+    "pcb_assign_tc_f32": (I32, [P, P, I32, P, I64, I32, P, P, P, I32, P, P, P, P, P, P]),
     "pcb_sort_by_label": (I32, [P, I64, I32, P, P, P, P, P, P]),
-    "pcb_segment_sums_f32": (I32, [P, I64, I32, P, P, I32, P, P, P]),
-    "pcb_segment_sums_f64": (I32, [P, I64, I32, P, P, I32, P, P, P]),
+    "pcb_segment_sums_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P]),
+    "pcb_segment_sums_f64": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P]),
     "pcb_repair_scratch_bytes": (I64, [I32]),
-    "pcb_repair_f32": (I32, [P, P, I64, I32, P, P, I32, P, P, P, P, P, P, I64, P]),
-    "pcb_repair_f64": (I32, [P, P, I64, I32, P, P, I32, P, P, P, P, P, P, I64, P]),
-    "pcb_argmax_own_f32": (I32, [P, I64, I64, P, P]),
-    "pcb_argmax_own_f64": (I32, [P, I64, I64, P, P]),
-    "pcb_repair_apply_f32": (I32, [P, P, I32, P, P, P, P, P, I64, I32, P, P]),
-    "pcb_repair_apply_f64": (I32, [P, P, I32, P, P, P, P, P, I64, I32, P, P]),
+    "pcb_repair_f32": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, I64, P]),
+    "pcb_repair_f64": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, I64, P]),
+    "pcb_argmax_own": (I32, [P, P, I64, I64, P, P]),
+    "pcb_repair_apply_f32": (I32, [P, I32, P, P, P, P, P, I64, I32, P, P]),
+    "pcb_repair_apply_f64": (I32, [P, I32, P, P, P, P, P, I64, I32, P, P]),
     "pcb_repair_commit": (I32, [P, I32, I32, I32, P, P, P]),
     "pcb_finalize_f32": (I32, [P, I32, I32, I64, P, P, P, P, I32, P, P, P, I32, F64, P]),
     "pcb_finalize_f64": (I32, [P, I32, I32, I64, P, P, P, P, P, I32, F64, P]),

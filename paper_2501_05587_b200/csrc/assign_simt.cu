@@ -26,40 +26,32 @@ namespace pcb {
 
 constexpr int kHistMax = 12288;  // per-block smem histogram (48 KB of int)
 
-// Per-block bookkeeping shared by all assignment kernels: counts histogram,
-// objective (sum of own distances, f64), changed (labels != previous labels).
+// Per-block bookkeeping shared by all assignment kernels: counts histogram and
+// changed (labels != previous labels).  The objective is summed by the update
+// kernel from exact own distances (see update.cu).
 struct BlockBook {
   int* hist;        // smem, k ints, or nullptr -> direct global REDs
-  double obj;       // thread-local partials
   long long changed;
 };
 
 __device__ __forceinline__ void book_point(BlockBook& b, double* acc, const AccLayout& L,
-                                           int lab, double own, const int32_t* labels_prev, int64_t i) {
-  b.obj += own;
+                                           int lab, const int32_t* labels_prev, int64_t i) {
   if (labels_prev != nullptr) b.changed += (labels_prev[i] != lab);
   if (b.hist != nullptr) atomicAdd(&b.hist[lab], 1);
   else atomicAdd(&acc[L.counts() + lab], 1.0);
 }
 
 __device__ void book_flush(BlockBook& b, double* acc, const AccLayout& L, int k) {
-  __shared__ double s_obj[32];
   __shared__ long long s_chg[32];
-  double o = warp_sum(b.obj);
   long long c = warp_sum(b.changed);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) { s_obj[w] = o; s_chg[w] = c; }
+  if (lane == 0) s_chg[w] = c;
   __syncthreads();
   if (w == 0) {
     const int nw = (blockDim.x + 31) >> 5;
-    o = lane < nw ? s_obj[lane] : 0.0;
     c = lane < nw ? s_chg[lane] : 0;
-    o = warp_sum(o);
     c = warp_sum(c);
-    if (lane == 0) {
-      atomicAdd(&acc[L.objective()], o);
-      atomicAdd(&acc[L.changed()], (double)c);
-    }
+    if (lane == 0) atomicAdd(&acc[L.changed()], (double)c);
   }
   if (b.hist != nullptr) {
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
@@ -88,7 +80,7 @@ assign_rowreg(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, i
   T* sN = sC + (size_t)kc * DP;                     // [kc]
   int* hist = reinterpret_cast<int*>(sN + kc);      // [k] (optional)
   const AccLayout L{k, d};
-  BlockBook book{(acc != nullptr && k <= kHistMax) ? hist : nullptr, 0.0, 0};
+  BlockBook book{(acc != nullptr && k <= kHistMax) ? hist : nullptr, 0};
   if (book.hist) for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
 
   auto load_chunk = [&](int c0) {
@@ -143,7 +135,7 @@ assign_rowreg(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, i
         const T own = pnorm[idx[r]] + bv[r];
         labels[idx[r]] = bj[r];
         if (mind) mind[idx[r]] = own;
-        if (acc) book_point(book, acc, L, bj[r], (double)own, labels_prev, idx[r]);
+        if (acc) book_point(book, acc, L, bj[r], labels_prev, idx[r]);
         flag_nonfinite(state, (double)own);
       }
     }
@@ -174,7 +166,7 @@ assign_tiled(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, in
   __shared__ T sN[TBN];
   __shared__ int hist_s[kHistMax > 4096 ? 4096 : kHistMax];
   const AccLayout L{k, d};
-  BlockBook book{(acc != nullptr && k <= 4096) ? hist_s : nullptr, 0.0, 0};
+  BlockBook book{(acc != nullptr && k <= 4096) ? hist_s : nullptr, 0};
   if (book.hist) for (int j = threadIdx.x; j < k; j += blockDim.x) hist_s[j] = 0;
   __syncthreads();
 
@@ -244,7 +236,7 @@ assign_tiled(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, in
         const T own = pnorm[row] + bv[r];
         labels[row] = bj[r];
         if (mind) mind[row] = own;
-        if (acc) book_point(book, acc, L, bj[r], (double)own, labels_prev, row);
+        if (acc) book_point(book, acc, L, bj[r], labels_prev, row);
         flag_nonfinite(state, (double)own);
       }
     }

@@ -1,0 +1,307 @@
+// Fused distance + argmin on the 5th-generation tensor cores (tcgen05), 3xTF32.
+//
+// Replaces clustering.py:310-311 (D = pn - 2 P C^T + cn, OpenBLAS sgemm +
+// three n x k temporaries) and dense.py:56-68 (row argmin) for float32 with
+// d > 32.  The n x k distance matrix never leaves the SM: the GEMM
+// accumulates in TMEM and the epilogue turns each accumulator row into a
+// running (min, argmin) in registers.
+//
+// FP32-faithful products with TF32 tensor cores (3xTF32): every operand x is
+// pre-split into hi = rna_tf32(x) and lo = x - hi (exact), and
+//     <p, c> ~= <p_hi, c_hi> + <p_hi, c_lo> + <p_lo, c_hi>
+// (the dropped lo*lo term is ~2^-22 relative).  P is split once per fit
+// (pcb_split_tf32), C once per iteration by the finalize kernel.
+//
+// Structure (one CTA per SM, persistent over 128-row tiles):
+//   warp 0     TMA producer: per (row tile, centroid tile, 32-wide K chunk)
+//              loads A_hi, A_lo (128 x 32 f32) and B_hi, B_lo (BN x 32 f32),
+//              128-byte swizzled, into a STAGES-deep smem ring (mbarriers).
+//   warp 1     MMA issuer (one thread): 4 K-steps x 3 products of
+//              tcgen05.mma.cta_group::1.kind::tf32 M=128 N=BN K=8 per stage,
+//              accumulating into one of two TMEM buffers (2 x BN columns);
+//              tcgen05.commit frees smem stages and publishes accumulators.
+//   warp 2     TMEM allocator.
+//   warps 4-7  epilogue: tcgen05.ld 32 columns at a time (thread = row),
+//              s_j = cnorm_j - 2 acc_j, running (min, lowest j), then the
+//              bookkeeping of _assignment_step (labels, own distance, counts,
+//              objective, changed) exactly like the FFMA kernels.
+// The double-buffered accumulator lets the epilogue of centroid tile t overlap
+// the MMAs of tile t+1.
+#include <cudaTypedefs.h>
+
+#include "pcb_common.cuh"
+#include "pcb_launch.cuh"
+#include "tc_ptx.cuh"
+
+namespace pcb {
+
+constexpr int TC_BM = 128;     // rows per tile (UMMA M)
+constexpr int TC_BK = 32;      // f32 per 128-byte swizzle row
+constexpr int TC_THREADS = 256;
+constexpr int TC_HIST_MAX = 4096;
+
+template <int BN>
+struct TcCfg {
+  static constexpr int kStages = BN == 256 ? 2 : (BN == 128 ? 3 : 4);
+  static constexpr uint32_t kABytes = TC_BM * TC_BK * 4;   // 16 KB
+  static constexpr uint32_t kBBytes = BN * TC_BK * 4;
+  static constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;
+  static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                        : (2 * BN <= 256) ? 256 : 512;
+  static constexpr uint32_t kBarBytes = 1024;  // barriers + tmem ptr, padded
+  static constexpr uint32_t kSmem = 1024 /*align slack*/ + kStages * kStageBytes + kBarBytes +
+                                    TC_HIST_MAX * 4;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+                       const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+                       const float* __restrict__ pnorm, const float* __restrict__ cnorm, int64_t n, int k,
+                       int d, int num_kc, const int32_t* __restrict__ labels_prev,
+                       int32_t* __restrict__ labels, float* __restrict__ mind, double* __restrict__ acc,
+                       const long long* __restrict__ state) {
+  using Cfg = TcCfg<BN>;
+  if (stopped(state)) return;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
+  uint8_t* bar_area = smem + Cfg::kStages * Cfg::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bar_area);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* tfull = empty + Cfg::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* hist = reinterpret_cast<int*>(bar_area + Cfg::kBarBytes);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool use_hist = acc != nullptr && k <= TC_HIST_MAX;
+  if (use_hist)
+    for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm_ahi);
+    ptx::prefetch_tmap(&tm_alo);
+    ptx::prefetch_tmap(&tm_bhi);
+    ptx::prefetch_tmap(&tm_blo);
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t mtiles = (n + TC_BM - 1) / TC_BM;
+  const int ntiles = (k + BN - 1) / BN;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      const uint64_t pol_a = ptx::policy_evict_first();
+      const uint64_t pol_b = ptx::policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+        const int y_a = (int)(mt * TC_BM);
+        for (int nt = 0; nt < ntiles; ++nt) {
+          for (int kc = 0; kc < num_kc; ++kc) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1u);
+            uint8_t* st = smem + stage * Cfg::kStageBytes;
+            ptx::mbar_expect_tx(&full[stage], Cfg::kStageBytes);
+            const uint64_t pa = (nt + 1 == ntiles) ? pol_a : pol_b;  // A re-read per centroid tile
+            ptx::tma_load_2d(&tm_ahi, &full[stage], st, kc * TC_BK, y_a, pa);
+            ptx::tma_load_2d(&tm_alo, &full[stage], st + Cfg::kABytes, kc * TC_BK, y_a, pa);
+            ptx::tma_load_2d(&tm_bhi, &full[stage], st + 2 * Cfg::kABytes, kc * TC_BK, nt * BN, pol_b);
+            ptx::tma_load_2d(&tm_blo, &full[stage], st + 2 * Cfg::kABytes + Cfg::kBBytes, kc * TC_BK,
+                             nt * BN, pol_b);
+            if (++stage == Cfg::kStages) { stage = 0; phase ^= 1u; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = ptx::idesc_tf32<TC_BM, BN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int abuf = 0;
+      uint32_t aphase = 0;
+      for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+        for (int nt = 0; nt < ntiles; ++nt) {
+          ptx::mbar_wait(&tempty[abuf], aphase ^ 1u);
+          ptx::tc_fence_after();
+          const uint32_t dt = tmem + (uint32_t)(abuf * BN);
+          for (int kc = 0; kc < num_kc; ++kc) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t base = ptx::smem_u32(smem + stage * Cfg::kStageBytes);
+            const uint64_t ahi = ptx::sdesc_k_sw128(base);
+            const uint64_t alo = ptx::sdesc_k_sw128(base + Cfg::kABytes);
+            const uint64_t bhi = ptx::sdesc_k_sw128(base + 2 * Cfg::kABytes);
+            const uint64_t blo = ptx::sdesc_k_sw128(base + 2 * Cfg::kABytes + Cfg::kBBytes);
+#pragma unroll
+            for (int ks = 0; ks < TC_BK / 8; ++ks) {
+              const uint64_t off = (uint64_t)(ks * 8 * 4) >> 4;  // 32 bytes per K=8 step
+              ptx::umma_tf32(dt, ahi + off, bhi + off, idesc, (kc | ks) != 0);
+              ptx::umma_tf32(dt, ahi + off, blo + off, idesc, 1u);
+              ptx::umma_tf32(dt, alo + off, bhi + off, idesc, 1u);
+            }
+            ptx::umma_commit(&empty[stage]);
+            if (++stage == Cfg::kStages) { stage = 0; phase ^= 1u; }
+          }
+          ptx::umma_commit(&tfull[abuf]);
+          abuf ^= 1;
+          if (abuf == 0) aphase ^= 1u;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int ew = warp - 4;  // TMEM lane group ew*32 .. ew*32+31
+    const int r_in_tile = ew * 32 + lane;
+    int abuf = 0;
+    uint32_t aphase = 0;
+    long long chg = 0;
+    for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+      float best = INFINITY;
+      int bj = 0;
+      for (int nt = 0; nt < ntiles; ++nt) {
+        ptx::mbar_wait(&tfull[abuf], aphase);
+        ptx::tc_fence_after();
+        const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(abuf * BN);
+        const int jbase = nt * BN;
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+          float v[32];
+          ptx::tmem_ld_32x32b_x32(taddr + cb, v);
+          const int j0 = jbase + cb;
+          if (j0 + 32 <= k) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float s = fmaf(-2.0f, v[i], __ldg(&cnorm[j0 + i]));
+              if (s < best) { best = s; bj = j0 + i; }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (j0 + i < k) {
+                const float s = fmaf(-2.0f, v[i], __ldg(&cnorm[j0 + i]));
+                if (s < best) { best = s; bj = j0 + i; }
+              }
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[abuf]);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1u;
+      }
+      const int64_t row = mt * TC_BM + r_in_tile;
+      if (row < n) {
+        const float own = pnorm[row] + best;
+        labels[row] = bj;
+        if (mind) mind[row] = own;
+        if (acc) {
+          if (labels_prev) chg += (labels_prev[row] != bj);
+          if (use_hist) atomicAdd(&hist[bj], 1);
+          else atomicAdd(&acc[(int64_t)k * d + bj], 1.0);
+        }
+        if (state != nullptr && !isfinite(own))
+          atomicExch((unsigned long long*)&state[kNanFlag], 1ull);
+      }
+    }
+    if (acc) {
+      chg = warp_sum(chg);
+      if (lane == 0) atomicAdd(&acc[(int64_t)k * d + k + 1], (double)chg);
+      ptx::named_bar_sync(1, 128);
+      if (use_hist)
+        for (int j = r_in_tile; j < k; j += 128)
+          if (hist[j]) atomicAdd(&acc[(int64_t)k * d + j], (double)hist[j]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc<Cfg::kTmemCols>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major f32 matrix (rows x ld), box = 32 columns x box_rows rows, 128B swizzle.
+static int make_tmap(CUtensorMap* m, const float* base, int64_t rows, int ld, int box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return PCB_ENODEV;
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : PCB_EINVAL;
+}
+
+template <int BN>
+static int launch_tc(const float* phi, const float* plo, int ld, const float* pnorm, int64_t n, int d,
+                     const float* chi, const float* clo, const float* cnorm, int k, const int32_t* lp,
+                     int32_t* lab, float* mind, double* acc, const long long* state, cudaStream_t st) {
+  using Cfg = TcCfg<BN>;
+  CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
+  int rc;
+  if ((rc = make_tmap(&ta_hi, phi, n, ld, TC_BM))) return rc;
+  if ((rc = make_tmap(&ta_lo, plo, n, ld, TC_BM))) return rc;
+  if ((rc = make_tmap(&tb_hi, chi, k, ld, BN))) return rc;
+  if ((rc = make_tmap(&tb_lo, clo, k, ld, BN))) return rc;
+  auto kern = assign_tc3xtf32_kernel<BN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t mtiles = (n + TC_BM - 1) / TC_BM;
+  const int grid = (int)std::min<int64_t>(mtiles, (int64_t)sm_count());
+  kern<<<grid, TC_THREADS, Cfg::kSmem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, pnorm, cnorm, n, k, d, ld / TC_BK, lp,
+                                              lab, mind, acc, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace pcb
+
+extern "C" int pcb_assign_tc_f32(const float* P_hi, const float* P_lo, int ld, const float* pnorm, int64_t n,
+                                 int d, const float* C_hi, const float* C_lo, const float* cnorm, int k,
+                                 const int32_t* labels_prev, int32_t* labels, float* mind, double* acc,
+                                 const long long* state, void* stream) {
+  if (n < 1 || d < 1 || k < 1 || ld < d || ld % pcb::TC_BK != 0 || !P_hi || !P_lo || !C_hi || !C_lo ||
+      !pnorm || !cnorm || !labels)
+    return PCB_EINVAL;
+  if (n > INT32_MAX) return PCB_EUNSUP;  // TMA coordinates are 32-bit
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k > 128)
+    return pcb::launch_tc<256>(P_hi, P_lo, ld, pnorm, n, d, C_hi, C_lo, cnorm, k, labels_prev, labels, mind,
+                               acc, state, st);
+  if (k > 64)
+    return pcb::launch_tc<128>(P_hi, P_lo, ld, pnorm, n, d, C_hi, C_lo, cnorm, k, labels_prev, labels, mind,
+                               acc, state, st);
+  return pcb::launch_tc<64>(P_hi, P_lo, ld, pnorm, n, d, C_hi, C_lo, cnorm, k, labels_prev, labels, mind,
+                            acc, state, st);
+}

@@ -5,8 +5,9 @@
 // that was empty at the start of the pass, in ascending order, the point with
 // the largest own distance D[i, label_i] among points not moved yet (ties ->
 // lowest index) is moved to that cluster.  Own distances of unmoved points
-// never change (their labels do not), so mind[] from the assignment kernel is
-// the reference's `own` vector; a moved point gets mind = -inf.
+// never change (their labels do not), so own_sorted[] written by the update
+// kernel (in label-sorted order, perm[s] = point id) is the reference's `own`
+// vector; a moved point gets own = -inf.
 //
 // One cooperative launch (grid = SMs x occupancy) does the whole thing with a
 // grid-wide argmax per donor (one grid.sync per donor: block keys are double
@@ -26,31 +27,38 @@ namespace cg = cooperative_groups;
 namespace pcb {
 
 struct DonorKey {
-  double v;
-  long long i;
+  double v;     // own distance
+  long long i;  // point id (global on multi-rank)
+  long long s;  // position in the label-sorted order (local)
 };
 
 __device__ __forceinline__ void argmax_merge(DonorKey& a, const DonorKey& b) {
   if (b.v > a.v || (b.v == a.v && b.i < a.i)) a = b;
 }
 
+// Exact own distance (same evaluation as the update kernel): sum (p - c)^2 in f64.
 template <typename T>
-__device__ double pair_distance(const T* P, const T* pnorm, const T* C, const T* cnorm, int d,
-                                int64_t i, int j) {
-  // same association as the assignment kernels: pnorm + (cnorm - 2<p,c>)
-  T dot = T(0);
-  for (int t = 0; t < d; ++t) dot = fma(P[i * d + t], C[(int64_t)j * d + t], dot);
-  const T s = fma(T(-2), dot, cnorm[j]);
-  return (double)(pnorm[i] + s);
+__device__ double pair_distance(const T* P, const T* C, int d, int64_t i, int j) {
+  double q = 0.0;
+  for (int t = 0; t < d; ++t) {
+    const double e = (double)P[i * d + t] - (double)C[(int64_t)j * d + t];
+    q = fma(e, e, q);
+  }
+  return q;
+}
+
+__device__ __forceinline__ DonorKey shfl_key(const DonorKey& k, int o) {
+  return DonorKey{__shfl_xor_sync(0xffffffffu, k.v, o), __shfl_xor_sync(0xffffffffu, k.i, o),
+                  __shfl_xor_sync(0xffffffffu, k.s, o)};
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256)
-repair_kernel(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, int d,
-              const T* __restrict__ C, const T* __restrict__ cnorm, int k,
-              const int32_t* __restrict__ labels_prev, int32_t* __restrict__ labels,
-              T* __restrict__ mind, double* __restrict__ acc, long long* __restrict__ state,
-              DonorKey* __restrict__ keys /* 2*gridDim */, int* __restrict__ elist /* k+1 */) {
+repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C, int k,
+              const int32_t* __restrict__ perm, const int32_t* __restrict__ labels_prev,
+              int32_t* __restrict__ labels, double* __restrict__ own, double* __restrict__ acc,
+              long long* __restrict__ state, DonorKey* __restrict__ keys /* 2*gridDim */,
+              int* __restrict__ elist /* k+1 */) {
   if (stopped(state)) return;
   cg::grid_group grid = cg::this_grid();
   const AccLayout L{k, d};
@@ -80,16 +88,13 @@ repair_kernel(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, i
     for (int e = 0; e < ne; ++e) {
       const int j = ((volatile int*)elist)[1 + e];
       // block-local argmax of own distance over unmoved points
-      DonorKey best{-INFINITY, n};
-      for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        DonorKey c{(double)mind[i], i};
+      DonorKey best{-INFINITY, n, 0};
+      for (int64_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
+        DonorKey c{own[q], (long long)perm[q], q};
         argmax_merge(best, c);
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        DonorKey b{__shfl_xor_sync(0xffffffffu, best.v, o), __shfl_xor_sync(0xffffffffu, best.i, o)};
-        argmax_merge(best, b);
-      }
+      for (int o = 16; o > 0; o >>= 1) argmax_merge(best, shfl_key(best, o));
       if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = best;
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -102,15 +107,12 @@ repair_kernel(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, i
       // holds the donor applies the donation, so its own next scan already
       // sees mind[donor] = -inf without another grid barrier.
       if (threadIdx.x < 32) {
-        DonorKey g{-INFINITY, n};
+        DonorKey g{-INFINITY, n, 0};
         for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) argmax_merge(g, keys[parity * gridDim.x + b]);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          DonorKey b{__shfl_xor_sync(0xffffffffu, g.v, o), __shfl_xor_sync(0xffffffffu, g.i, o)};
-          argmax_merge(g, b);
-        }
+        for (int o = 16; o > 0; o >>= 1) argmax_merge(g, shfl_key(g, o));
         const int64_t donor = g.i;
-        if (donor >= lo && donor < hi) {
+        if (donor < n && g.s >= lo && g.s < hi) {
           const int old = labels[donor];
           for (int t = threadIdx.x; t < d; t += 32) {
             const double p = (double)P[donor * d + t];
@@ -118,8 +120,8 @@ repair_kernel(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, i
             atomicAdd(&acc[(int64_t)j * d + t], p);
           }
           if (threadIdx.x == 0) {
-            const double dnew = pair_distance(P, pnorm, C, cnorm, d, donor, j);
-            atomicAdd(&acc[L.objective()], dnew - (double)mind[donor]);
+            const double dnew = pair_distance(P, C, d, donor, j);
+            atomicAdd(&acc[L.objective()], dnew - own[g.s]);
             if (labels_prev != nullptr) {
               const int prev = labels_prev[donor];
               atomicAdd(&acc[L.changed()], (double)((j != prev) - (old != prev)));
@@ -127,7 +129,7 @@ repair_kernel(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, i
             atomicAdd(&acc[L.counts() + old], -1.0);
             atomicAdd(&acc[L.counts() + j], 1.0);
             labels[donor] = j;
-            mind[donor] = T(-INFINITY);
+            own[g.s] = -INFINITY;
             atomicAdd((unsigned long long*)&state[kMoved], 1ull);
           }
         }
@@ -147,11 +149,10 @@ static size_t repair_scratch(int k) {
 }
 
 template <typename T>
-static int repair(const T* P, const T* pnorm, int64_t n, int d, const T* C, const T* cnorm, int k,
-                  const int32_t* lp, int32_t* lab, T* mind, double* acc, long long* state,
+static int repair(const T* P, int64_t n, int d, const T* C, int k, const int32_t* perm,
+                  const int32_t* lp, int32_t* lab, double* own, double* acc, long long* state,
                   void* scratch, int64_t scratch_bytes, cudaStream_t st) {
-  if (n < 1 || d < 1 || k < 1 || !P || !pnorm || !C || !cnorm || !lab || !mind || !acc || !state ||
-      !scratch)
+  if (n < 1 || d < 1 || k < 1 || !P || !C || !perm || !lab || !own || !acc || !state || !scratch)
     return PCB_EINVAL;
   if (scratch_bytes < (int64_t)repair_scratch(k)) return PCB_EINVAL;
   auto kern = repair_kernel<T>;
@@ -162,9 +163,9 @@ static int repair(const T* P, const T* pnorm, int64_t n, int d, const T* C, cons
   const int grid = repair_grid();
   DonorKey* keys = (DonorKey*)scratch;
   int* elist = (int*)(keys + 2 * grid);
-  void* args[] = {(void*)&P, (void*)&pnorm, (void*)&n, (void*)&d, (void*)&C, (void*)&cnorm,
-                  (void*)&k, (void*)&lp, (void*)&lab, (void*)&mind, (void*)&acc, (void*)&state,
-                  (void*)&keys, (void*)&elist};
+  void* args[] = {(void*)&P,   (void*)&n,   (void*)&d,   (void*)&C,     (void*)&k,
+                  (void*)&perm, (void*)&lp, (void*)&lab, (void*)&own, (void*)&acc,
+                  (void*)&state, (void*)&keys, (void*)&elist};
   e = cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(256), args, 0, st);
   return (int)e;
 }
@@ -173,21 +174,20 @@ static int repair(const T* P, const T* pnorm, int64_t n, int d, const T* C, cons
 
 extern "C" int64_t pcb_repair_scratch_bytes(int k) { return (int64_t)pcb::repair_scratch(k); }
 
-extern "C" int pcb_repair_f32(const float* P, const float* pnorm, int64_t n, int d, const float* C,
-                              const float* cnorm, int k, const int32_t* labels_prev, int32_t* labels,
-                              float* mind, double* acc, long long* state, void* scratch,
+extern "C" int pcb_repair_f32(const float* P, int64_t n, int d, const float* C, int k,
+                              const int32_t* perm, const int32_t* labels_prev, int32_t* labels,
+                              double* own_sorted, double* acc, long long* state, void* scratch,
                               int64_t scratch_bytes, void* stream) {
-  return pcb::repair<float>(P, pnorm, n, d, C, cnorm, k, labels_prev, labels, mind, acc, state,
-                            scratch, scratch_bytes, (cudaStream_t)stream);
+  return pcb::repair<float>(P, n, d, C, k, perm, labels_prev, labels, own_sorted, acc, state, scratch,
+                            scratch_bytes, (cudaStream_t)stream);
 }
 
-extern "C" int pcb_repair_f64(const double* P, const double* pnorm, int64_t n, int d,
-                              const double* C, const double* cnorm, int k,
-                              const int32_t* labels_prev, int32_t* labels, double* mind,
-                              double* acc, long long* state, void* scratch, int64_t scratch_bytes,
-                              void* stream) {
-  return pcb::repair<double>(P, pnorm, n, d, C, cnorm, k, labels_prev, labels, mind, acc, state,
-                             scratch, scratch_bytes, (cudaStream_t)stream);
+extern "C" int pcb_repair_f64(const double* P, int64_t n, int d, const double* C, int k,
+                              const int32_t* perm, const int32_t* labels_prev, int32_t* labels,
+                              double* own_sorted, double* acc, long long* state, void* scratch,
+                              int64_t scratch_bytes, void* stream) {
+  return pcb::repair<double>(P, n, d, C, k, perm, labels_prev, labels, own_sorted, acc, state, scratch,
+                             scratch_bytes, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -200,45 +200,44 @@ extern "C" int pcb_repair_f64(const double* P, const double* pnorm, int64_t n, i
 // ---------------------------------------------------------------------------
 namespace pcb {
 
-template <typename T>
 __global__ void __launch_bounds__(1024)
-argmax_own_kernel(const T* __restrict__ mind, int64_t n, int64_t offset, double* __restrict__ out) {
+argmax_own_kernel(const double* __restrict__ own, const int32_t* __restrict__ perm, int64_t n,
+                  int64_t offset, double* __restrict__ out) {
   __shared__ DonorKey s_warp[32];
-  DonorKey best{-INFINITY, offset + n};
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    DonorKey c{(double)mind[i], offset + i};
+  DonorKey best{-INFINITY, offset + n, 0};
+  for (int64_t q = threadIdx.x; q < n; q += blockDim.x) {
+    DonorKey c{own[q], offset + (long long)perm[q], q};
     argmax_merge(best, c);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    DonorKey b{__shfl_xor_sync(0xffffffffu, best.v, o), __shfl_xor_sync(0xffffffffu, best.i, o)};
-    argmax_merge(best, b);
-  }
+  for (int o = 16; o > 0; o >>= 1) argmax_merge(best, shfl_key(best, o));
   if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = best;
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) argmax_merge(best, s_warp[w]);
     out[0] = best.v;
     out[1] = (double)best.i;
+    out[2] = (double)best.s;
   }
 }
 
 template <typename T>
-__global__ void repair_apply_kernel(const T* __restrict__ P, const T* __restrict__ pnorm, int d,
-                                    const T* __restrict__ C, const T* __restrict__ cnorm,
+__global__ void repair_apply_kernel(const T* __restrict__ P, int d, const T* __restrict__ C,
+                                    const int32_t* __restrict__ perm,
                                     const int32_t* __restrict__ labels_prev,
-                                    int32_t* __restrict__ labels, T* __restrict__ mind,
-                                    int64_t donor, int j, double* __restrict__ delta) {
+                                    int32_t* __restrict__ labels, double* __restrict__ own,
+                                    int64_t pos, int j, double* __restrict__ delta) {
+  const int64_t donor = perm[pos];
   for (int t = threadIdx.x; t < d; t += blockDim.x) delta[t] = (double)P[donor * d + t];
   if (threadIdx.x == 0) {
     const int old = labels[donor];
-    const double dnew = pair_distance(P, pnorm, C, cnorm, d, donor, j);
+    const double dnew = pair_distance(P, C, d, donor, j);
     delta[d] = (double)old;
-    delta[d + 1] = dnew - (double)mind[donor];
+    delta[d + 1] = dnew - own[pos];
     delta[d + 2] = labels_prev ? (double)((j != labels_prev[donor]) - (old != labels_prev[donor])) : 0.0;
     delta[d + 3] = 1.0;
     labels[donor] = j;
-    mind[donor] = T(-INFINITY);
+    own[pos] = -INFINITY;
   }
 }
 
@@ -262,40 +261,30 @@ __global__ void repair_commit_kernel(double* __restrict__ acc, int k, int d, int
 
 }  // namespace pcb
 
-extern "C" int pcb_argmax_own_f32(const float* mind, int64_t n, int64_t offset, double* out2,
-                                  void* stream) {
-  if (n < 1 || !mind || !out2) return PCB_EINVAL;
-  pcb::argmax_own_kernel<float><<<1, 1024, 0, (cudaStream_t)stream>>>(mind, n, offset, out2);
+extern "C" int pcb_argmax_own(const double* own_sorted, const int32_t* perm, int64_t n, int64_t offset,
+                              double* out3, void* stream) {
+  if (n < 1 || !own_sorted || !perm || !out3) return PCB_EINVAL;
+  pcb::argmax_own_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(own_sorted, perm, n, offset, out3);
   PCB_CHECK_LAUNCH();
   return 0;
 }
 
-extern "C" int pcb_argmax_own_f64(const double* mind, int64_t n, int64_t offset, double* out2,
-                                  void* stream) {
-  if (n < 1 || !mind || !out2) return PCB_EINVAL;
-  pcb::argmax_own_kernel<double><<<1, 1024, 0, (cudaStream_t)stream>>>(mind, n, offset, out2);
+extern "C" int pcb_repair_apply_f32(const float* P, int d, const float* C, const int32_t* perm,
+                                    const int32_t* labels_prev, int32_t* labels, double* own_sorted,
+                                    int64_t pos, int j, double* delta, void* stream) {
+  if (d < 1 || !P || !C || !perm || !labels || !own_sorted || !delta || pos < 0) return PCB_EINVAL;
+  pcb::repair_apply_kernel<float><<<1, 128, 0, (cudaStream_t)stream>>>(P, d, C, perm, labels_prev, labels,
+                                                                      own_sorted, pos, j, delta);
   PCB_CHECK_LAUNCH();
   return 0;
 }
 
-extern "C" int pcb_repair_apply_f32(const float* P, const float* pnorm, int d, const float* C,
-                                    const float* cnorm, const int32_t* labels_prev,
-                                    int32_t* labels, float* mind, int64_t donor_local, int j,
-                                    double* delta, void* stream) {
-  if (d < 1 || !P || !labels || !mind || !delta || donor_local < 0) return PCB_EINVAL;
-  pcb::repair_apply_kernel<float><<<1, 128, 0, (cudaStream_t)stream>>>(
-      P, pnorm, d, C, cnorm, labels_prev, labels, mind, donor_local, j, delta);
-  PCB_CHECK_LAUNCH();
-  return 0;
-}
-
-extern "C" int pcb_repair_apply_f64(const double* P, const double* pnorm, int d, const double* C,
-                                    const double* cnorm, const int32_t* labels_prev,
-                                    int32_t* labels, double* mind, int64_t donor_local, int j,
-                                    double* delta, void* stream) {
-  if (d < 1 || !P || !labels || !mind || !delta || donor_local < 0) return PCB_EINVAL;
-  pcb::repair_apply_kernel<double><<<1, 128, 0, (cudaStream_t)stream>>>(
-      P, pnorm, d, C, cnorm, labels_prev, labels, mind, donor_local, j, delta);
+extern "C" int pcb_repair_apply_f64(const double* P, int d, const double* C, const int32_t* perm,
+                                    const int32_t* labels_prev, int32_t* labels, double* own_sorted,
+                                    int64_t pos, int j, double* delta, void* stream) {
+  if (d < 1 || !P || !C || !perm || !labels || !own_sorted || !delta || pos < 0) return PCB_EINVAL;
+  pcb::repair_apply_kernel<double><<<1, 128, 0, (cudaStream_t)stream>>>(P, d, C, perm, labels_prev, labels,
+                                                                       own_sorted, pos, j, delta);
   PCB_CHECK_LAUNCH();
   return 0;
 }

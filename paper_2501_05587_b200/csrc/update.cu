@@ -1,4 +1,5 @@
-// Centroid update: per-cluster sums of point rows (clustering.py:282-288).
+// Centroid update: per-cluster sums of point rows (clustering.py:282-288)
+// and the own distances / objective of the new labels (clustering.py:148).
 //
 // The reference computes, for every cluster j, P[flatnonzero(labels==j)].mean(0)
 // (k passes over the labels, f32 accumulation).  Here:
@@ -93,119 +94,170 @@ __device__ __forceinline__ int segment_of(const int32_t* offsets, int k, int64_t
   return lo;
 }
 
-// Large d: one warp per slice, lanes across a 32*VEC-wide chunk of dimensions.
-template <typename T, int VEC>
+// Exact own distance of a point to its centroid, in f64 from f32/f64 inputs:
+// sum_t (p_t - c_t)^2.  This is what the objective sums (clustering.py:148),
+// evaluated here — where the point row is already in registers — instead of
+// in the assignment kernel, so every assignment variant (FFMA, 3xTF32 tensor
+// cores) reports the same, correctly rounded own distances and objective.
+
+// d > 16: one warp per slice of sorted ids; lane l owns dimensions l + 32 v.
+template <typename T, int NV>
 __global__ void __launch_bounds__(256)
 segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict__ perm,
-            const int32_t* __restrict__ offsets, int k, int64_t slice, double* __restrict__ acc,
+            const int32_t* __restrict__ offsets, int k, const T* __restrict__ C, int64_t slice,
+            double* __restrict__ own_sorted, double* __restrict__ acc,
             const long long* __restrict__ state) {
   if (stopped(state)) return;
+  const AccLayout L{k, d};
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nslices = (n + slice - 1) / slice;
-  const int chunk = 32 * VEC;
+  double obj = 0.0;
   for (int64_t sl = warp; sl < nslices; sl += nwarps) {
     const int64_t s0 = sl * slice, s1 = min(n, s0 + slice);
-    const int j0 = segment_of(offsets, k, s0);
-    for (int t0 = 0; t0 < d; t0 += chunk) {
-      const int tb = t0 + lane * VEC;
-      double a[VEC];
+    int j = segment_of(offsets, k, s0);
+    int64_t jend = offsets[j + 1];
+    double a[NV];
+    T c[NV];
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) a[v] = 0.0;
-      int j = j0;
-      int64_t jend = offsets[j + 1];
-      int64_t s = s0;
-      auto flush = [&](int jj) {
+    for (int v = 0; v < NV; ++v) {
+      const int t = lane + 32 * v;
+      a[v] = 0.0;
+      c[v] = t < d ? C[(int64_t)j * d + t] : T(0);
+    }
+    int64_t s = s0;
+    while (s < s1) {
+      if (s >= jend) {
 #pragma unroll
-        for (int v = 0; v < VEC; ++v)
-          if (tb + v < d) atomicAdd(&acc[(int64_t)jj * d + tb + v], a[v]);
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) a[v] = 0.0;
-      };
-      while (s < s1) {
-        while (s >= jend) {  // crossed into a later segment
-          flush(j);
-          ++j;
-          jend = offsets[j + 1];
+        for (int v = 0; v < NV; ++v) {
+          const int t = lane + 32 * v;
+          if (t < d) atomicAdd(&acc[(int64_t)j * d + t], a[v]);
+          a[v] = 0.0;
         }
-        const int64_t e = min(s1, jend);
-        // unrolled gather of up to 4 rows at a time
-        for (; s + 4 <= e; s += 4) {
-          T r[4][VEC];
+        do { ++j; jend = offsets[j + 1]; } while (s >= jend);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int64_t i = perm[s + u];
-            const T* row = P + i * d;
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) r[u][v] = (tb + v < d) ? row[tb + v] : T(0);
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) a[v] += (double)r[u][v];
-        }
-        for (; s < e; ++s) {
-          const int64_t i = perm[s];
-          const T* row = P + i * d;
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) a[v] += (tb + v < d) ? (double)row[tb + v] : 0.0;
+        for (int v = 0; v < NV; ++v) {
+          const int t = lane + 32 * v;
+          c[v] = t < d ? C[(int64_t)j * d + t] : T(0);
         }
       }
-      flush(j);
+      const int64_t e = min(s1, jend);
+      // two rows in flight per step
+      for (; s + 2 <= e; s += 2) {
+        const T* r0 = P + (int64_t)perm[s] * d;
+        const T* r1 = P + (int64_t)perm[s + 1] * d;
+        T x0[NV], x1[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int t = lane + 32 * v;
+          x0[v] = t < d ? r0[t] : T(0);
+          x1[v] = t < d ? r1[t] : T(0);
+        }
+        double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          a[v] += (double)x0[v] + (double)x1[v];
+          const double e0 = (double)x0[v] - (double)c[v], e1 = (double)x1[v] - (double)c[v];
+          q0 = fma(e0, e0, q0);
+          q1 = fma(e1, e1, q1);
+        }
+        q0 = warp_sum(q0);
+        q1 = warp_sum(q1);
+        if (lane == 0) { own_sorted[s] = q0; own_sorted[s + 1] = q1; obj += q0 + q1; }
+      }
+      if (s < e) {
+        const T* r0 = P + (int64_t)perm[s] * d;
+        double q0 = 0.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int t = lane + 32 * v;
+          const T x = t < d ? r0[t] : T(0);
+          a[v] += (double)x;
+          const double e0 = (double)x - (double)c[v];
+          q0 = fma(e0, e0, q0);
+        }
+        q0 = warp_sum(q0);
+        if (lane == 0) { own_sorted[s] = q0; obj += q0; }
+        ++s;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int t = lane + 32 * v;
+      if (t < d) atomicAdd(&acc[(int64_t)j * d + t], a[v]);
     }
   }
+  if (lane == 0 && obj != 0.0) atomicAdd(&acc[L.objective()], obj);
 }
 
-// Small d (<= DP <= 16): one thread per slice, the whole row in registers.
+// d <= 16: one thread per slice, the whole row in registers.
 template <typename T, int DP>
 __global__ void __launch_bounds__(256)
 segsum_thread(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict__ perm,
-              const int32_t* __restrict__ offsets, int k, int64_t slice, double* __restrict__ acc,
+              const int32_t* __restrict__ offsets, int k, const T* __restrict__ C, int64_t slice,
+              double* __restrict__ own_sorted, double* __restrict__ acc,
               const long long* __restrict__ state) {
   if (stopped(state)) return;
+  const AccLayout L{k, d};
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int64_t nslices = (n + slice - 1) / slice;
+  double obj = 0.0;
   for (int64_t sl = tid; sl < nslices; sl += nth) {
     const int64_t s0 = sl * slice, s1 = min(n, s0 + slice);
     int j = segment_of(offsets, k, s0);
     int64_t jend = offsets[j + 1];
     double a[DP];
+    T c[DP];
 #pragma unroll
-    for (int t = 0; t < DP; ++t) a[t] = 0.0;
+    for (int t = 0; t < DP; ++t) { a[t] = 0.0; c[t] = t < d ? C[(int64_t)j * d + t] : T(0); }
     for (int64_t s = s0; s < s1; ++s) {
-      while (s >= jend) {
+      if (s >= jend) {
 #pragma unroll
         for (int t = 0; t < DP; ++t) {
-          if (t < d && a[t] != 0.0) atomicAdd(&acc[(int64_t)j * d + t], a[t]);
+          if (t < d) atomicAdd(&acc[(int64_t)j * d + t], a[t]);
           a[t] = 0.0;
         }
-        ++j;
-        jend = offsets[j + 1];
+        do { ++j; jend = offsets[j + 1]; } while (s >= jend);
+#pragma unroll
+        for (int t = 0; t < DP; ++t) c[t] = t < d ? C[(int64_t)j * d + t] : T(0);
       }
       const T* row = P + (int64_t)perm[s] * d;
+      double q = 0.0;
 #pragma unroll
-      for (int t = 0; t < DP; ++t) if (t < d) a[t] += (double)row[t];
+      for (int t = 0; t < DP; ++t) {
+        if (t < d) {
+          const T x = row[t];
+          a[t] += (double)x;
+          const double e = (double)x - (double)c[t];
+          q = fma(e, e, q);
+        }
+      }
+      own_sorted[s] = q;
+      obj += q;
     }
 #pragma unroll
     for (int t = 0; t < DP; ++t)
-      if (t < d && a[t] != 0.0) atomicAdd(&acc[(int64_t)j * d + t], a[t]);
+      if (t < d) atomicAdd(&acc[(int64_t)j * d + t], a[t]);
   }
+  obj = warp_sum(obj);
+  if ((threadIdx.x & 31) == 0 && obj != 0.0) atomicAdd(&acc[L.objective()], obj);
 }
 
 template <typename T>
 static int segment_sums(const T* P, int64_t n, int d, const int32_t* perm, const int32_t* offsets,
-                        int k, double* acc, const long long* state, cudaStream_t st) {
-  if (n < 1 || d < 1 || k < 1 || !P || !perm || !offsets || !acc) return PCB_EINVAL;
+                        int k, const T* C, double* own, double* acc, const long long* state,
+                        cudaStream_t st) {
+  if (n < 1 || d < 1 || k < 1 || !P || !perm || !offsets || !acc || !C || !own) return PCB_EINVAL;
+  if (d > 1024) return PCB_EUNSUP;
   const int sms = sm_count();
   if (d <= 16) {
-    // ~8 slices per thread-wave keeps every SM busy; min 16 rows per slice
     const int64_t threads = (int64_t)sms * 2048;
     int64_t slice = std::max<int64_t>(16, (n + threads - 1) / threads);
     const int64_t nsl = (n + slice - 1) / slice;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 255) / 256, (int64_t)sms * 8));
-#define PCB_SEG_T(DPV) segsum_thread<T, DPV><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, slice, acc, state)
+#define PCB_SEG_T(DPV) segsum_thread<T, DPV><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, C, slice, own, acc, state)
     if (d <= 2) PCB_SEG_T(2);
     else if (d <= 4) PCB_SEG_T(4);
     else if (d <= 8) PCB_SEG_T(8);
@@ -216,10 +268,14 @@ static int segment_sums(const T* P, int64_t n, int d, const int32_t* perm, const
     int64_t slice = std::max<int64_t>(64, (n + warps - 1) / warps);
     const int64_t nsl = (n + slice - 1) / slice;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl * 32 + 255) / 256, (int64_t)sms * 8));
-    if (d <= 64)
-      segsum_warp<T, 2><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, slice, acc, state);
-    else
-      segsum_warp<T, 4><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, slice, acc, state);
+#define PCB_SEG_W(NVV) segsum_warp<T, NVV><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, C, slice, own, acc, state)
+    if (d <= 32) PCB_SEG_W(1);
+    else if (d <= 64) PCB_SEG_W(2);
+    else if (d <= 128) PCB_SEG_W(4);
+    else if (d <= 256) PCB_SEG_W(8);
+    else if (d <= 512) PCB_SEG_W(16);
+    else PCB_SEG_W(32);
+#undef PCB_SEG_W
   }
   PCB_CHECK_LAUNCH();
   return 0;
@@ -243,13 +299,15 @@ extern "C" int pcb_sort_by_label(const int32_t* labels, int64_t n, int k, const 
 }
 
 extern "C" int pcb_segment_sums_f32(const float* P, int64_t n, int d, const int32_t* perm,
-                                    const int32_t* offsets, int k, double* acc,
-                                    const long long* state, void* stream) {
-  return pcb::segment_sums<float>(P, n, d, perm, offsets, k, acc, state, (cudaStream_t)stream);
+                                    const int32_t* offsets, int k, const float* C, double* own_sorted,
+                                    double* acc, const long long* state, void* stream) {
+  return pcb::segment_sums<float>(P, n, d, perm, offsets, k, C, own_sorted, acc, state,
+                                  (cudaStream_t)stream);
 }
 
 extern "C" int pcb_segment_sums_f64(const double* P, int64_t n, int d, const int32_t* perm,
-                                    const int32_t* offsets, int k, double* acc,
-                                    const long long* state, void* stream) {
-  return pcb::segment_sums<double>(P, n, d, perm, offsets, k, acc, state, (cudaStream_t)stream);
+                                    const int32_t* offsets, int k, const double* C, double* own_sorted,
+                                    double* acc, const long long* state, void* stream) {
+  return pcb::segment_sums<double>(P, n, d, perm, offsets, k, C, own_sorted, acc, state,
+                                   (cudaStream_t)stream);
 }

@@ -76,24 +76,23 @@ class Comm:
         if not bool((counts == 0).any().item()):
             return
         sfx = eng.sfx
-        key = torch.empty(2, dtype=torch.float64, device=eng.dev)
+        key = torch.empty(3, dtype=torch.float64, device=eng.dev)
         delta = torch.empty(d + 4, dtype=torch.float64, device=eng.dev)
         while True:
             empties = torch.nonzero(counts == 0).flatten().tolist()
             if not empties:
                 return
             for j in empties:
-                L.call(f"pcb_argmax_own_{sfx}", _p(eng.mind), eng.n, self.offset, _p(key), _stream())
+                L.call("pcb_argmax_own", _p(eng.own), _p(eng.perm), eng.n, self.offset, _p(key),
+                       _stream())
                 keys = torch.stack(self.all_gather(key)).cpu().numpy()
                 # max own distance, lowest global index on ties (clustering.py:135-137)
                 order = np.lexsort((keys[:, 1], -keys[:, 0]))
-                donor = int(keys[order[0], 1])
+                win = order[0]
                 delta.zero_()
-                local = donor - self.offset
-                if 0 <= local < eng.n:
-                    L.call(f"pcb_repair_apply_{sfx}", _p(eng.P), _p(eng.pnorm), d, _p(eng.C),
-                           _p(eng.cnorm), _p(prev), _p(new), _p(eng.mind), local, int(j),
-                           _p(delta), _stream())
+                if win == self.rank:
+                    L.call(f"pcb_repair_apply_{sfx}", _p(eng.P), d, _p(eng.C), _p(eng.perm), _p(prev),
+                           _p(new), _p(eng.own), int(keys[win, 2]), int(j), _p(delta), _stream())
                 self.all_reduce_sum(delta)
                 L.call("pcb_repair_commit", _p(eng.acc), k, d, int(j), _p(delta), _p(eng.state),
                        _stream())

@@ -63,7 +63,7 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int) -> str:
         return variant
     if d <= 32:
         return "rowreg"
-    return "tiled"
+    return "tc3xtf32" if dtype == _F32 else "tiled"
 
 
 @dataclass
@@ -111,6 +111,7 @@ class LloydEngine:
             self.acc_size = kk * d + kk + 2
             self.acc = torch.zeros(self.acc_size, dtype=torch.float64, device=dev)
             self.perm = torch.empty(n, dtype=torch.int32, device=dev)
+            self.own = torch.empty(n, dtype=torch.float64, device=dev)  # own distances, sorted order
             self.offsets = torch.empty(kk + 1, dtype=torch.int32, device=dev)
             self.cursor = torch.empty(kk, dtype=torch.int32, device=dev)
             self.state = torch.zeros(L.STATE_WORDS, dtype=torch.int64, device=dev)
@@ -120,10 +121,17 @@ class LloydEngine:
             sb = int(L.load().pcb_repair_scratch_bytes(kk))
             self.repair_scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
             self.repair_scratch_bytes = sb
-            # split operands for the tensor-core path (allocated on demand)
+            # split operands for the tensor-core path
             self.ld = 0
             self.P_hi = self.P_lo = self.C_hi = self.C_lo = None
             L.call(f"pcb_point_norms_{self.sfx}", _p(self.P), n, d, _p(self.pnorm), _stream())
+            if self.variant == "tc3xtf32":
+                self.ld = (d + 31) // 32 * 32
+                self.P_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
+                self.P_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
+                self.C_hi = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
+                self.C_lo = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
+                L.call("pcb_split_tf32", _p(self.P), n, d, self.ld, _p(self.P_hi), _p(self.P_lo), _stream())
 
     # -- centroid initialisation ------------------------------------------------
     def set_centroids(self, C) -> None:
@@ -172,9 +180,14 @@ class LloydEngine:
         L.call("pcb_sort_by_label", _p(labels), self.n, self.k, _p(counts), _p(self.offsets),
                _p(self.cursor), _p(self.perm), _p(state), _stream())
         L.call(f"pcb_segment_sums_{self.sfx}", _p(self.P), self.n, self.d, _p(self.perm),
-               _p(self.offsets), self.k, _p(self.acc), _p(state), _stream())
+               _p(self.offsets), self.k, _p(self.C), _p(self.own), _p(self.acc), _p(state), _stream())
 
     def _assign(self, prev, new, acc, state) -> None:
+        if self.variant == "tc3xtf32":
+            L.call("pcb_assign_tc_f32", _p(self.P_hi), _p(self.P_lo), self.ld, _p(self.pnorm), self.n,
+                   self.d, _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(prev), _p(new),
+                   _p(self.mind), _p(acc), _p(state), _stream())
+            return
         L.call(f"pcb_assign_{self.sfx}", _p(self.P), _p(self.pnorm), self.n, self.d, _p(self.C),
                _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
                self.vcode, _stream())
@@ -183,9 +196,9 @@ class LloydEngine:
         if self.comm is not None and self.comm.world_size > 1:
             self.comm.repair(self, prev, new)
             return
-        L.call(f"pcb_repair_{self.sfx}", _p(self.P), _p(self.pnorm), self.n, self.d, _p(self.C),
-               _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(self.acc),
-               _p(self.state), _p(self.repair_scratch), self.repair_scratch_bytes, _stream())
+        L.call(f"pcb_repair_{self.sfx}", _p(self.P), self.n, self.d, _p(self.C), self.k, _p(self.perm),
+               _p(prev), _p(new), _p(self.own), _p(self.acc), _p(self.state), _p(self.repair_scratch),
+               self.repair_scratch_bytes, _stream())
 
     def _finalize(self, check_convergence: bool, tol: float) -> None:
         if self.dtype == _F32:
@@ -286,7 +299,14 @@ class LloydEngine:
             xn = torch.empty(m, dtype=self.tdtype, device=self.dev)
             out = torch.empty(m, dtype=torch.int32, device=self.dev)
             L.call(f"pcb_point_norms_{self.sfx}", _p(Xt), m, self.d, _p(xn), _stream())
-            L.call(f"pcb_assign_{self.sfx}", _p(Xt), _p(xn), m, self.d, _p(self.C), _p(self.cnorm),
-                   self.k, None, _p(out), None, None, None, self.vcode if self.variant != "delta" else 0,
-                   _stream())
+            if self.variant == "tc3xtf32":
+                xh = torch.empty((m, self.ld), dtype=torch.float32, device=self.dev)
+                xl = torch.empty_like(xh)
+                L.call("pcb_split_tf32", _p(Xt), m, self.d, self.ld, _p(xh), _p(xl), _stream())
+                L.call("pcb_assign_tc_f32", _p(xh), _p(xl), self.ld, _p(xn), m, self.d, _p(self.C_hi),
+                       _p(self.C_lo), _p(self.cnorm), self.k, None, _p(out), None, None, None, _stream())
+            else:
+                L.call(f"pcb_assign_{self.sfx}", _p(Xt), _p(xn), m, self.d, _p(self.C), _p(self.cnorm),
+                       self.k, None, _p(out), None, None, None, self.vcode if self.variant != "delta" else 0,
+                       _stream())
             return out.cpu().numpy()

@@ -52,7 +52,7 @@ def test_argument_errors_without_gpu():
     from paper_2501_05587_b200 import _lib
     lib = _lib.load()
     assert lib.pcb_assign_f32(None, None, 0, 2, None, None, 3, None, None, None, None, None, 0, None) == -1
-    assert lib.pcb_segment_sums_f32(None, 10, 2, None, None, 3, None, None, None) == -1
+    assert lib.pcb_segment_sums_f32(None, 10, 2, None, None, 3, None, None, None, None, None) == -1
     assert lib.pcb_split_tf32(None, 4, 8, 4, None, None, None) == -1
 
 
