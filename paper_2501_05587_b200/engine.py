@@ -211,7 +211,7 @@ class LloydEngine:
                    int(check_convergence), float(tol), _stream())
 
     def iteration(self, t: int, check_convergence: bool = False, tol: float = 0.0,
-                  events=None) -> None:
+                  events=None, raw_out=None) -> None:
         """Enqueue Lloyd iteration t (reads labels[t%2], writes labels[(t+1)%2])."""
         prev, new = self.labels[t % 2], self.labels[(t + 1) % 2]
         self.acc.zero_()
@@ -222,6 +222,8 @@ class LloydEngine:
             events[1].record()
         self._sort_and_sum(new, self.state)
         self._allreduce(self.acc)
+        if raw_out is not None:
+            raw_out.copy_(new)
         self._repair(prev, new)
         self._finalize(check_convergence, tol)
         if events is not None:
@@ -273,13 +275,15 @@ class LloydEngine:
         self.set_labels(labels_prev)
         with torch.cuda.device(self.dev):
             self.state.zero_()
-            self.iteration(0)
+            raw = torch.empty_like(self.labels[1])
+            self.iteration(0, raw_out=raw)
             torch.cuda.current_stream().synchronize()
             acc = self.acc.cpu().numpy()
             st = self.state.cpu().numpy()
             kd = self.k * self.d
             return {
                 "labels": self.labels[1].cpu().numpy(),
+                "raw_labels": raw.cpu().numpy(),
                 "mind": self.mind.cpu().numpy(),
                 "objective": float(self.obj_hist[0].item()),
                 "changed": float(acc[kd + self.k + 1]) / self.n_total,
