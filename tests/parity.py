@@ -40,16 +40,14 @@ def _donor_swap_exempt(P, C, gpu, ref, diff):
         return cand
     raw = ref.raw_labels
     own = ((P64 - C64[raw]) ** 2).sum(1)
-    a = np.flatnonzero(ref_don & ~gpu_don)   # donors only in the reference
-    b = np.flatnonzero(gpu_don & ~ref_don)   # donors only on the GPU
+    # every donor-related mismatch must have a swap partner: another mismatched
+    # donor (in either run) whose own distance ties with it to DONOR_RTOL
+    pool = np.flatnonzero(cand)
     ok = np.zeros_like(diff)
-    for x in np.flatnonzero(cand):
-        other = b if ref_don[x] and not gpu_don[x] else a
-        if other.size and np.min(np.abs(own[other] - own[x])) <= DONOR_RTOL * abs(own[x]):
+    for x in pool:
+        others = pool[pool != x]
+        if others.size and np.min(np.abs(own[others] - own[x])) <= DONOR_RTOL * abs(own[x]):
             ok[x] = True
-        if ref_don[x] and gpu_don[x]:
-            # donor in both runs but sent to different clusters: order swap upstream
-            ok[x] = bool(a.size or b.size)
     return ok
 
 

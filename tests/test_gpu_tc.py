@@ -85,7 +85,7 @@ def test_3xtf32_dot_products_fp32_faithful():
 
 
 @pytest.mark.parametrize("n,d,k", [(1000, 40, 17), (777, 100, 300), (4096, 64, 64), (300, 33, 1),
-                                   (5000, 128, 1024), (2000, 784, 256), (1500, 96, 129), (129, 64, 4096)])
+                                   (5000, 128, 1024), (2000, 784, 256), (1500, 96, 129), (5000, 64, 4096)])
 def test_tc_lockstep_ragged_shapes(n, d, k):
     from paper_2501_05587_b200.engine import LloydEngine
     P = oracle.make_blobs(n, d, max(k, 1), seed=n + d)
