@@ -43,6 +43,7 @@ extern "C" {
 #define PCB_ASSIGN_TILED     2  /* FFMA, register-tiled SIMT GEMM (any d)   */
 #define PCB_ASSIGN_TC3XTF32  3  /* tcgen05 3xTF32, TMEM accumulators (f32)  */
 #define PCB_ASSIGN_DELTA     4  /* delta-chunked P.C.P^T ablation (f32)     */
+#define PCB_ASSIGN_SCREEN    5  /* tcgen05 1xTF32 certified screening (f32) */
 
 int         pcb_abi_version(void);
 const char* pcb_error_string(int code);
@@ -83,6 +84,32 @@ int pcb_assign_tc_f32(const float* P_hi, const float* P_lo, int ld, const float*
                       int d, const float* C_hi, const float* C_lo, const float* cnorm, int k,
                       const int32_t* labels_prev, int32_t* labels, float* mind, double* acc,
                       const long long* state, void* stream);
+
+/* Certified 1xTF32 screening variant ("tc1xtf32s", see assign_screen.cu):
+ * one TF32 tensor-core pass on the raw f32 operands (d % 4 == 0) with a
+ * rigorous per-row error bound; rows whose argmin is not certified are listed
+ * in amb_list/amb_count (caller zeroes amb_count) and resolved exactly-as-3xTF32
+ * by pcb_resolve_ambiguous_f32.  Labels only: counts/changed come from
+ * pcb_count_labels.
+ *   pcb_screen_prep_points:    anorm = |trunc(p)|, danorm = |p - trunc(p)|,
+ *                              bstat[2] = OFF (once per fit)
+ *   pcb_screen_prep_centroids: bnorm, dbnorm, bstat[0..1] (after every
+ *                              centroid update)                                */
+int pcb_screen_prep_points(const float* P, int64_t n, int d, float* anorm, float* danorm,
+                           float* bstat /* 4 */, void* stream);
+int pcb_screen_prep_centroids(const float* C, int k, int d, float* bnorm, float* dbnorm,
+                              float* bstat, void* stream);
+int pcb_assign_screen_f32(const float* P, int64_t n, int d, const float* C, int k, const float* cnorm,
+                          const float* anorm, const float* danorm, const float* bstat,
+                          int32_t* labels, int* amb_list, int* amb_count, const long long* state,
+                          void* stream);
+int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_list,
+                              const int* amb_count, int ld, float* sub_hi, float* sub_lo,
+                              int32_t* sub_labels, const float* pnorm, const float* C_hi,
+                              const float* C_lo, const float* cnorm, int k, int32_t* labels,
+                              const long long* state, void* stream);
+int pcb_count_labels(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
+                     double* acc, const long long* state, void* stream);
 
 /* ---- centroid update (clustering.py:282-288): counting sort of point ids by
  *      label, then a segmented f64 sum of point rows per cluster into acc.  */

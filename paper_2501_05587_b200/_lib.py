@@ -29,6 +29,11 @@ SIGNATURES = {
     "pcb_assign_f32": (I32, [P, P, I64, I32, P, P, I32, P, P, P, P, P, I32, P]),
     "pcb_assign_f64": (I32, [P, P, I64, I32, P, P, I32, P, P, P, P, P, I32, P]),
     "pcb_assign_tc_f32": (I32, [P, P, I32, P, I64, I32, P, P, P, I32, P, P, P, P, P, P]),
+    "pcb_screen_prep_points": (I32, [P, I64, I32, P, P, P, P]),
+    "pcb_screen_prep_centroids": (I32, [P, I32, I32, P, P, P, P]),
+    "pcb_assign_screen_f32": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P]),
+    "pcb_resolve_ambiguous_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P, P, P, I32, P, P, P]),
+    "pcb_count_labels": (I32, [P, P, I64, I32, I32, P, P, P]),
     "pcb_sort_by_label": (I32, [P, I64, I32, P, P, P, P, P, P]),
     "pcb_segment_sums_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P]),
     "pcb_segment_sums_f64": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P]),
@@ -47,9 +52,9 @@ SIGNATURES = {
     "pcb_centroid_norms_f64": (I32, [P, I32, I32, P, P]),
 }
 
-ASSIGN_AUTO, ASSIGN_ROWREG, ASSIGN_TILED, ASSIGN_TC3XTF32, ASSIGN_DELTA = 0, 1, 2, 3, 4
+ASSIGN_AUTO, ASSIGN_ROWREG, ASSIGN_TILED, ASSIGN_TC3XTF32, ASSIGN_DELTA, ASSIGN_SCREEN = 0, 1, 2, 3, 4, 5
 VARIANTS = {"auto": ASSIGN_AUTO, "rowreg": ASSIGN_ROWREG, "tiled": ASSIGN_TILED,
-            "tc3xtf32": ASSIGN_TC3XTF32, "delta": ASSIGN_DELTA}
+            "tc3xtf32": ASSIGN_TC3XTF32, "delta": ASSIGN_DELTA, "tc1xtf32s": ASSIGN_SCREEN}
 STATE_WORDS = 8
 
 _lib = None

@@ -1,0 +1,458 @@
+// Certified 1xTF32 screening for the distance stage (variant "tc1xtf32s").
+//
+// The 3xTF32 kernel (assign_tc.cu) runs at 95 % of the TF32 tensor pipe, so
+// its only remaining lever is fewer tensor-core passes.  This kernel makes ONE
+// TF32 pass over the raw f32 operands (tcgen05 kind::tf32 reads an f32 word by
+// truncating it to TF32) and certifies the argmin with a rigorous error bound:
+//
+//   G  = <p, c>,  T = <trunc(p), trunc(c)> (+ TC accumulation error)
+//   |G - T| <= |da||c~| + |a~||dc| + |da||dc| + (K/8 + 1) 2^-22 |a~||c~|
+//   (Cauchy-Schwarz on the exact truncation residuals da = p - trunc(p),
+//   dc = c - trunc(c); a round-to-nearest conversion would only shrink them)
+//
+// Ranking key  key_j = (cnorm_j + OFF) - 2 T_j,  OFF > max_i |p_i|^2 so keys are
+// positive and can carry a 5-bit column index in their low mantissa bits
+// (a single LOP3), making (value, index) min a plain FMNMX.  With a per-row
+// uniform bound E_i (max over centroids of the B-side norms, plus every
+// rounding of the key arithmetic and the packing), the true argmin j* obeys
+// key_{j*} <= S1 + 2 E_i, so a row whose second-smallest key S2 exceeds
+// S1 + 2 E_i has a certified, unique argmin.  Other rows ("ambiguous") are
+// appended to a list and resolved by the 3xTF32 kernel on a compacted copy;
+// their count is data dependent (~14 % right after a random-label init, ~3 %
+// near convergence on the c3 blobs).
+//
+// Epilogue cost per accumulator element: 1 FFMA + 1 LOP3 + 2.5 FMNMX (pairs,
+// 3-input min), which keeps the ALU pipe just under the TF32 MMA rate at d=128.
+#include <cudaTypedefs.h>
+
+#include "pcb_common.cuh"
+#include "pcb_launch.cuh"
+#include "tc_ptx.cuh"
+
+namespace pcb {
+
+constexpr int SC_BM = 128;
+constexpr int SC_BK = 32;
+constexpr int SC_THREADS = 256;
+constexpr int SC_KMAX = 8192;  // smem copy of the shifted centroid norms
+
+template <int BN>
+struct ScCfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr uint32_t kABytes = SC_BM * SC_BK * 4;  // 16 KB
+  static constexpr uint32_t kBBytes = BN * SC_BK * 4;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr uint32_t kBarBytes = 1024;
+  static constexpr uint32_t kSmem = 1024 + kStages * kStageBytes + kBarBytes + SC_KMAX * 4;
+};
+
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+__device__ __forceinline__ float pack_idx(float key, uint32_t i) {
+  return __uint_as_float((__float_as_uint(key) & 0xFFFFFFE0u) | i);
+}
+
+// bstat layout (f32): [0] max_j |c~_j|, [1] max_j |dc_j|, [2] OFF, [3] spare
+template <int BN>
+__global__ void __launch_bounds__(SC_THREADS, 1)
+assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                     const float* __restrict__ anorm, const float* __restrict__ danorm,
+                     const float* __restrict__ cnorm, const float* __restrict__ bstat, int64_t n, int k,
+                     int num_kc, int32_t* __restrict__ labels, int* __restrict__ amb_list,
+                     int* __restrict__ amb_count, const long long* __restrict__ state) {
+  using Cfg = ScCfg<BN>;
+  if (stopped(state)) return;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
+  uint8_t* bar_area = smem + Cfg::kStages * Cfg::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bar_area);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* tfull = empty + Cfg::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* cprime = reinterpret_cast<float*>(bar_area + Cfg::kBarBytes);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (k + BN - 1) / BN;
+  const float OFF = bstat[2];
+  for (int j = threadIdx.x; j < ntiles * BN; j += blockDim.x)
+    cprime[j] = j < k ? cnorm[j] + OFF : 3.0e38f;
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm_a);
+    ptx::prefetch_tmap(&tm_b);
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t mtiles = (n + SC_BM - 1) / SC_BM;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_a = ptx::policy_evict_first();
+      const uint64_t pol_b = ptx::policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+        const int y_a = (int)(mt * SC_BM);
+        for (int nt = 0; nt < ntiles; ++nt) {
+          const uint64_t pa = (nt + 1 == ntiles) ? pol_a : pol_b;
+          for (int kc = 0; kc < num_kc; ++kc) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1u);
+            uint8_t* st = smem + stage * Cfg::kStageBytes;
+            ptx::mbar_expect_tx(&full[stage], Cfg::kStageBytes);
+            ptx::tma_load_2d(&tm_a, &full[stage], st, kc * SC_BK, y_a, pa);
+            ptx::tma_load_2d(&tm_b, &full[stage], st + Cfg::kABytes, kc * SC_BK, nt * BN, pol_b);
+            if (++stage == Cfg::kStages) { stage = 0; phase ^= 1u; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_tf32<SC_BM, BN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int abuf = 0;
+      uint32_t aphase = 0;
+      for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+        for (int nt = 0; nt < ntiles; ++nt) {
+          ptx::mbar_wait(&tempty[abuf], aphase ^ 1u);
+          ptx::tc_fence_after();
+          const uint32_t dt = tmem + (uint32_t)(abuf * BN);
+          for (int kc = 0; kc < num_kc; ++kc) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t base = ptx::smem_u32(smem + stage * Cfg::kStageBytes);
+            const uint64_t ad = ptx::sdesc_k_sw128(base);
+            const uint64_t bd = ptx::sdesc_k_sw128(base + Cfg::kABytes);
+#pragma unroll
+            for (int ks = 0; ks < SC_BK / 8; ++ks) {
+              const uint64_t off = (uint64_t)(ks * 8 * 4) >> 4;
+              ptx::umma_tf32(dt, ad + off, bd + off, idesc, (kc | ks) != 0);
+            }
+            ptx::umma_commit(&empty[stage]);
+            if (++stage == Cfg::kStages) { stage = 0; phase ^= 1u; }
+          }
+          ptx::umma_commit(&tfull[abuf]);
+          abuf ^= 1;
+          if (abuf == 0) aphase ^= 1u;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int r_in_tile = ew * 32 + lane;
+    const float Bmax = bstat[0], dBmax = bstat[1];
+    // TC accumulation: per K=8 MMA <= 9 terms aligned/truncated at 2^-23 of the
+    // largest partial (|partial| <= sum |a~_t c~_t| <= |a~||c~|)
+    const float acc_rel = (float)(num_kc * 4 + 2) * 9.0f * 0x1p-23f;
+    int abuf = 0;
+    uint32_t aphase = 0;
+    for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+      float R1 = 3.4e38f, R2 = 3.4e38f;
+      int r1 = 0;
+      for (int nt = 0; nt < ntiles; ++nt) {
+        ptx::mbar_wait(&tfull[abuf], aphase);
+        ptx::tc_fence_after();
+        const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(abuf * BN);
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+          float v[32];
+          ptx::tmem_ld_32x32b_x32(taddr + cb, v);
+          const float4* cp4 = reinterpret_cast<const float4*>(cprime + nt * BN + cb);
+          float S1 = 3.4e38f, S2 = 3.4e38f;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 c4 = cp4[q];
+            const float k0 = pack_idx(fmaf(-2.0f, v[4 * q + 0], c4.x), 4 * q + 0);
+            const float k1 = pack_idx(fmaf(-2.0f, v[4 * q + 1], c4.y), 4 * q + 1);
+            const float k2 = pack_idx(fmaf(-2.0f, v[4 * q + 2], c4.z), 4 * q + 2);
+            const float k3 = pack_idx(fmaf(-2.0f, v[4 * q + 3], c4.w), 4 * q + 3);
+            float lo = fminf(k0, k1), hi = fmaxf(k0, k1);
+            S2 = fmin3(S2, hi, fmaxf(S1, lo));
+            S1 = fminf(S1, lo);
+            lo = fminf(k2, k3);
+            hi = fmaxf(k2, k3);
+            S2 = fmin3(S2, hi, fmaxf(S1, lo));
+            S1 = fminf(S1, lo);
+          }
+          // merge this 32-column chunk into the row's running top-2 (lowest j on ties)
+          if (S1 < R1) {
+            R2 = fminf(R1, S2);
+            R1 = S1;
+            r1 = nt * BN + cb + (int)(__float_as_uint(S1) & 31u);
+          } else {
+            R2 = fminf(R2, S1);
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[abuf]);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1u;
+      }
+      const int64_t row = mt * SC_BM + r_in_tile;
+      bool amb = false;
+      if (row < n) {
+        labels[row] = r1;
+        const float an = anorm[row], dan = danorm[row];
+        // rigorous per-row bound on |key_j - OFF - s_j| (see header), rounded up
+        const float g = dan * Bmax + an * dBmax + dan * dBmax + acc_rel * an * Bmax;
+        const float cb = Bmax + dBmax;
+        const float kmax = OFF + 2.0f * (an + dan) * cb + cb * cb;
+        const float E = 1.0001f * (2.0f * g + 0x1p-16f * kmax);
+        amb = !(R2 > R1 + 2.0f * E);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, amb);
+      if (m) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(amb_count, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (amb) amb_list[base + __popc(m & ((1u << lane) - 1u))] = (int)row;
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc<Cfg::kTmemCols>(tmem);
+}
+
+// ---- screening prep / fallback helpers ---------------------------------------
+
+__device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__device__ __forceinline__ void atomic_max_pos(float* addr, float v) {
+  atomicMax(reinterpret_cast<unsigned int*>(addr), __float_as_uint(v));  // v >= 0
+}
+
+// Per row: |trunc(p)|, |p - trunc(p)| (rounded up), and the max point norm^2.
+__global__ void __launch_bounds__(256)
+row_trunc_norms_kernel(const float* __restrict__ X, int64_t rows, int d, float* __restrict__ an,
+                       float* __restrict__ dan, float* __restrict__ maxsq) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  float wmax = 0.0f;
+  for (int64_t i = w; i < rows; i += nw) {
+    double s_t = 0.0, s_d = 0.0, s_x = 0.0;
+    for (int t = lane; t < d; t += 32) {
+      const float x = X[i * d + t];
+      const float h = trunc_tf32(x);
+      const double dd = (double)x - (double)h;
+      s_t = fma((double)h, (double)h, s_t);
+      s_d = fma(dd, dd, s_d);
+      s_x = fma((double)x, (double)x, s_x);
+    }
+    s_t = warp_sum(s_t);
+    s_d = warp_sum(s_d);
+    s_x = warp_sum(s_x);
+    if (lane == 0) {
+      an[i] = (float)(sqrt(s_t) * (1.0 + 1e-6));
+      dan[i] = (float)(sqrt(s_d) * (1.0 + 1e-6));
+      wmax = fmaxf(wmax, (float)(s_x * (1.0 + 1e-6)));
+    }
+  }
+  if (lane == 0 && maxsq != nullptr) atomic_max_pos(maxsq, wmax);
+}
+
+__global__ void max2_kernel(const float* __restrict__ b, const float* __restrict__ db, int k,
+                            float* __restrict__ out) {
+  float m0 = 0.0f, m1 = 0.0f;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) { m0 = fmaxf(m0, b[j]); m1 = fmaxf(m1, db[j]); }
+  atomic_max_pos(&out[0], m0);
+  atomic_max_pos(&out[1], m1);
+}
+
+__global__ void screen_stats_finish(float* __restrict__ bstat, const float* __restrict__ maxsq) {
+  // OFF = 1.01 * max|p|^2 + 1 keeps every key positive
+  bstat[2] = 1.01f * (*maxsq) + 1.0f;
+}
+
+// Gather the ambiguous rows into a compact TF32 hi/lo split (row stride ld).
+__global__ void __launch_bounds__(256)
+gather_split_rows(const float* __restrict__ P, int d, const int* __restrict__ list,
+                  const int* __restrict__ count, int ld, float* __restrict__ hi, float* __restrict__ lo,
+                  const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int64_t cnt = *count;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < cnt; r += nw) {
+    const int64_t i = list[r];
+    for (int t = lane; t < ld; t += 32) {
+      const float x = t < d ? P[i * d + t] : 0.0f;
+      uint32_t h;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+      hi[r * ld + t] = __uint_as_float(h);
+      lo[r * ld + t] = x - __uint_as_float(h);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+scatter_rows_labels(const int* __restrict__ list, const int* __restrict__ count,
+                    const int32_t* __restrict__ sub, int32_t* __restrict__ labels,
+                    const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int64_t cnt = *count;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < cnt; r += (int64_t)gridDim.x * blockDim.x)
+    labels[list[r]] = sub[r];
+}
+
+// counts and changed of the final labels (clustering.py:146-149) — used by the
+// screened variant, whose assignment kernel only produces labels.
+__global__ void __launch_bounds__(256)
+count_labels_kernel(const int32_t* __restrict__ labels, const int32_t* __restrict__ prev, int64_t n, int k,
+                    int d, double* __restrict__ acc, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  extern __shared__ int hist[];
+  const AccLayout L{k, d};
+  for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
+  __syncthreads();
+  long long chg = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int l = labels[i];
+    atomicAdd(&hist[l], 1);
+    if (prev) chg += (prev[i] != l);
+  }
+  chg = warp_sum(chg);
+  if ((threadIdx.x & 31) == 0 && chg) atomicAdd(&acc[L.changed()], (double)chg);
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x)
+    if (hist[j]) atomicAdd(&acc[L.counts() + j], (double)hist[j]);
+}
+
+static int make_tmap_rows(CUtensorMap* m, const float* base, int64_t rows, int cols, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (enc == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return PCB_ENODEV;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)SC_BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : PCB_EINVAL;
+}
+
+template <int BN>
+static int launch_screen(const float* P, int64_t n, int d, const float* C, int k, const float* an,
+                         const float* dan, const float* cnorm, const float* bstat, int32_t* labels,
+                         int* amb_list, int* amb_count, const long long* state, cudaStream_t st) {
+  using Cfg = ScCfg<BN>;
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_tmap_rows(&ta, P, n, d, SC_BM))) return rc;
+  if ((rc = make_tmap_rows(&tb, C, k, d, BN))) return rc;
+  auto kern = assign_screen_kernel<BN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t mtiles = (n + SC_BM - 1) / SC_BM;
+  const int grid = (int)std::min<int64_t>(mtiles, (int64_t)sm_count());
+  kern<<<grid, SC_THREADS, Cfg::kSmem, st>>>(ta, tb, an, dan, cnorm, bstat, n, k, (d + SC_BK - 1) / SC_BK, labels,
+                                             amb_list, amb_count, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace pcb
+
+using namespace pcb;
+
+extern "C" int pcb_screen_prep_points(const float* P, int64_t n, int d, float* anorm, float* danorm,
+                                      float* bstat, void* stream) {
+  if (n < 1 || d < 1 || !P || !anorm || !danorm || !bstat) return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bstat, 0, 4 * sizeof(float), st);
+  if (e != cudaSuccess) return (int)e;
+  const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, (int64_t)sm_count() * 16);
+  row_trunc_norms_kernel<<<grid, 256, 0, st>>>(P, n, d, anorm, danorm, bstat + 3);
+  PCB_CHECK_LAUNCH();
+  screen_stats_finish<<<1, 1, 0, st>>>(bstat, bstat + 3);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_screen_prep_centroids(const float* C, int k, int d, float* bnorm, float* dbnorm,
+                                         float* bstat, void* stream) {
+  if (k < 1 || d < 1 || !C || !bnorm || !dbnorm || !bstat) return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bstat, 0, 2 * sizeof(float), st);
+  if (e != cudaSuccess) return (int)e;
+  row_trunc_norms_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(C, k, d, bnorm, dbnorm, nullptr);
+  PCB_CHECK_LAUNCH();
+  max2_kernel<<<1, 256, 0, st>>>(bnorm, dbnorm, k, bstat);  // bstat[0] = max|c~|, [1] = max|dc|
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_assign_screen_f32(const float* P, int64_t n, int d, const float* C, int k, const float* cnorm,
+                                     const float* anorm, const float* danorm, const float* bstat,
+                                     int32_t* labels, int* amb_list, int* amb_count, const long long* state,
+                                     void* stream) {
+  if (n < 1 || d < 1 || k < 1 || !P || !C || !cnorm || !anorm || !danorm || !bstat || !labels || !amb_list ||
+      !amb_count)
+    return PCB_EINVAL;
+  if (d % 4 != 0 || n > INT32_MAX) return PCB_EUNSUP;  // TMA: 16-byte row strides
+  if (k > SC_KMAX) return PCB_EUNSUP;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k > 128)
+    return launch_screen<256>(P, n, d, C, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state, st);
+  return launch_screen<128>(P, n, d, C, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state, st);
+}
+
+extern "C" int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_list,
+                                         const int* amb_count, int ld, float* sub_hi, float* sub_lo,
+                                         int32_t* sub_labels, const float* pnorm, const float* C_hi,
+                                         const float* C_lo, const float* cnorm, int k, int32_t* labels,
+                                         const long long* state, void* stream) {
+  if (n < 1 || d < 1 || k < 1 || ld < d || ld % 32 || !P || !amb_list || !amb_count || !sub_hi || !sub_lo ||
+      !sub_labels || !pnorm || !C_hi || !C_lo || !cnorm || !labels)
+    return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = sm_count() * 8;
+  gather_split_rows<<<grid, 256, 0, st>>>(P, d, amb_list, amb_count, ld, sub_hi, sub_lo, state);
+  PCB_CHECK_LAUNCH();
+  int rc = assign_tc3xtf32_devcount(sub_hi, sub_lo, ld, pnorm, n, d, C_hi, C_lo, cnorm, k, sub_labels, amb_count,
+                                    state, st);
+  if (rc) return rc;
+  scatter_rows_labels<<<grid, 256, 0, st>>>(amb_list, amb_count, sub_labels, labels, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_count_labels(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
+                                double* acc, const long long* state, void* stream) {
+  if (n < 1 || k < 1 || !labels || !acc) return PCB_EINVAL;
+  if (k > 12288) return PCB_EUNSUP;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 4);
+  count_labels_kernel<<<grid, 256, k * sizeof(int), (cudaStream_t)stream>>>(labels, labels_prev, n, k, d, acc,
+                                                                          state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}

@@ -60,9 +60,10 @@ assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_
                        const float* __restrict__ pnorm, const float* __restrict__ cnorm, int64_t n, int k,
                        int d, int num_kc, const int32_t* __restrict__ labels_prev,
                        int32_t* __restrict__ labels, float* __restrict__ mind, double* __restrict__ acc,
-                       const long long* __restrict__ state) {
+                       const long long* __restrict__ state, const int* __restrict__ n_dev) {
   using Cfg = TcCfg<BN>;
   if (stopped(state)) return;
+  if (n_dev != nullptr) n = min(n, (int64_t)*n_dev);  // row count known only on the device
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
@@ -266,7 +267,8 @@ static int make_tmap(CUtensorMap* m, const float* base, int64_t rows, int ld, in
 template <int BN>
 static int launch_tc(const float* phi, const float* plo, int ld, const float* pnorm, int64_t n, int d,
                      const float* chi, const float* clo, const float* cnorm, int k, const int32_t* lp,
-                     int32_t* lab, float* mind, double* acc, const long long* state, cudaStream_t st) {
+                     int32_t* lab, float* mind, double* acc, const long long* state, cudaStream_t st,
+                     const int* n_dev = nullptr) {
   using Cfg = TcCfg<BN>;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   int rc;
@@ -280,9 +282,24 @@ static int launch_tc(const float* phi, const float* plo, int ld, const float* pn
   const int64_t mtiles = (n + TC_BM - 1) / TC_BM;
   const int grid = (int)std::min<int64_t>(mtiles, (int64_t)sm_count());
   kern<<<grid, TC_THREADS, Cfg::kSmem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, pnorm, cnorm, n, k, d, ld / TC_BK, lp,
-                                              lab, mind, acc, state);
+                                              lab, mind, acc, state, n_dev);
   PCB_CHECK_LAUNCH();
   return 0;
+}
+
+// 3xTF32 assignment of a row subset whose count lives on the device (the
+// ambiguous rows of the screened kernel, compacted by gather_split_rows).
+int assign_tc3xtf32_devcount(const float* phi, const float* plo, int ld, const float* pnorm, int64_t cap,
+                             int d, const float* chi, const float* clo, const float* cnorm, int k,
+                             int32_t* lab, const int* n_dev, const long long* state, cudaStream_t st) {
+  if (k > 128)
+    return launch_tc<256>(phi, plo, ld, pnorm, cap, d, chi, clo, cnorm, k, nullptr, lab, nullptr, nullptr,
+                          state, st, n_dev);
+  if (k > 64)
+    return launch_tc<128>(phi, plo, ld, pnorm, cap, d, chi, clo, cnorm, k, nullptr, lab, nullptr, nullptr,
+                          state, st, n_dev);
+  return launch_tc<64>(phi, plo, ld, pnorm, cap, d, chi, clo, cnorm, k, nullptr, lab, nullptr, nullptr, state,
+                       st, n_dev);
 }
 
 }  // namespace pcb

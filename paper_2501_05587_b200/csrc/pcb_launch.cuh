@@ -23,4 +23,8 @@ int assign_delta_f32(const float* P, const float* pnorm, int64_t n, int d, const
                      const float* cnorm, int k, const int32_t* labels_prev, int32_t* labels,
                      float* mind, double* acc, const long long* state, cudaStream_t st);
 
+int assign_tc3xtf32_devcount(const float* phi, const float* plo, int ld, const float* pnorm, int64_t cap,
+                             int d, const float* chi, const float* clo, const float* cnorm, int k,
+                             int32_t* lab, const int* n_dev, const long long* state, cudaStream_t st);
+
 }  // namespace pcb

@@ -56,8 +56,10 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int) -> str:
     if variant not in L.VARIANTS:
         raise ValueError(f"unknown assign variant {variant!r}; expected one of {tuple(L.VARIANTS)}")
     if variant != "auto":
-        if dtype == _F64 and variant in ("tc3xtf32", "delta"):
+        if dtype == _F64 and variant in ("tc3xtf32", "delta", "tc1xtf32s"):
             raise ValueError(f"variant {variant!r} is float32-only")
+        if variant == "tc1xtf32s" and d % 4 != 0:
+            raise ValueError("variant 'tc1xtf32s' needs d % 4 == 0 (TMA row stride)")
         if variant == "rowreg" and d > 32:
             raise ValueError("variant 'rowreg' needs d <= 32")
         return variant
@@ -125,13 +127,29 @@ class LloydEngine:
             self.ld = 0
             self.P_hi = self.P_lo = self.C_hi = self.C_lo = None
             L.call(f"pcb_point_norms_{self.sfx}", _p(self.P), n, d, _p(self.pnorm), _stream())
-            if self.variant == "tc3xtf32":
+            if self.variant in ("tc3xtf32", "tc1xtf32s"):
                 self.ld = (d + 31) // 32 * 32
-                self.P_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
-                self.P_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.C_hi = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
                 self.C_lo = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
+            if self.variant == "tc3xtf32":
+                self.P_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
+                self.P_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 L.call("pcb_split_tf32", _p(self.P), n, d, self.ld, _p(self.P_hi), _p(self.P_lo), _stream())
+            if self.variant == "tc1xtf32s":
+                # certified screening: raw P for the TF32 pass, compact hi/lo for the
+                # ambiguous rows (capacity n), truncation norms for the error bound
+                self.anorm = torch.empty(n, dtype=torch.float32, device=dev)
+                self.danorm = torch.empty(n, dtype=torch.float32, device=dev)
+                self.bnorm = torch.empty(kk, dtype=torch.float32, device=dev)
+                self.dbnorm = torch.empty(kk, dtype=torch.float32, device=dev)
+                self.bstat = torch.zeros(4, dtype=torch.float32, device=dev)
+                self.amb_list = torch.empty(n, dtype=torch.int32, device=dev)
+                self.amb_count = torch.zeros(1, dtype=torch.int32, device=dev)
+                self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
+                self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
+                self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
+                L.call("pcb_screen_prep_points", _p(self.P), n, d, _p(self.anorm), _p(self.danorm),
+                       _p(self.bstat), _stream())
 
     # -- centroid initialisation ------------------------------------------------
     def set_centroids(self, C) -> None:
@@ -141,10 +159,16 @@ class LloydEngine:
             self.C.copy_(Ct.to(self.dev))
             self._centroid_norms()
 
+    def _screen_centroid_stats(self) -> None:
+        if self.variant == "tc1xtf32s":
+            L.call("pcb_screen_prep_centroids", _p(self.C), self.k, self.d, _p(self.bnorm),
+                   _p(self.dbnorm), _p(self.bstat), _stream())
+
     def _centroid_norms(self) -> None:
         if self.dtype == _F32:
             L.call("pcb_centroid_norms_f32", _p(self.C), self.k, self.d, _p(self.cnorm),
                    _p(self.C_hi), _p(self.C_lo), self.ld, _stream())
+            self._screen_centroid_stats()
         else:
             L.call("pcb_centroid_norms_f64", _p(self.C), self.k, self.d, _p(self.cnorm), _stream())
 
@@ -166,6 +190,7 @@ class LloydEngine:
             if self.dtype == _F32:
                 L.call("pcb_centroids_from_acc_f32", _p(self.acc), self.k, self.d, _p(self.C),
                        _p(self.cnorm), _p(self.C_hi), _p(self.C_lo), self.ld, _stream())
+                self._screen_centroid_stats()
             else:
                 L.call("pcb_centroids_from_acc_f64", _p(self.acc), self.k, self.d, _p(self.C),
                        _p(self.cnorm), _stream())
@@ -183,6 +208,19 @@ class LloydEngine:
                _p(self.offsets), self.k, _p(self.C), _p(self.own), _p(self.acc), _p(state), _stream())
 
     def _assign(self, prev, new, acc, state) -> None:
+        if self.variant == "tc1xtf32s":
+            self.amb_count.zero_()
+            L.call("pcb_assign_screen_f32", _p(self.P), self.n, self.d, _p(self.C), self.k,
+                   _p(self.cnorm), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
+                   _p(self.amb_list), _p(self.amb_count), _p(state), _stream())
+            L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.amb_list),
+                   _p(self.amb_count), self.ld, _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels),
+                   _p(self.pnorm), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(new),
+                   _p(state), _stream())
+            if acc is not None:
+                L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
+                       _stream())
+            return
         if self.variant == "tc3xtf32":
             L.call("pcb_assign_tc_f32", _p(self.P_hi), _p(self.P_lo), self.ld, _p(self.pnorm), self.n,
                    self.d, _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(prev), _p(new),
@@ -205,6 +243,7 @@ class LloydEngine:
             L.call("pcb_finalize_f32", _p(self.acc), self.k, self.d, self.n_total, _p(self.C),
                    _p(self.cnorm), _p(self.C_hi), _p(self.C_lo), self.ld, _p(self.obj_hist),
                    _p(self.rep_hist), _p(self.state), int(check_convergence), float(tol), _stream())
+            self._screen_centroid_stats()
         else:
             L.call("pcb_finalize_f64", _p(self.acc), self.k, self.d, self.n_total, _p(self.C),
                    _p(self.cnorm), _p(self.obj_hist), _p(self.rep_hist), _p(self.state),
@@ -303,7 +342,7 @@ class LloydEngine:
             xn = torch.empty(m, dtype=self.tdtype, device=self.dev)
             out = torch.empty(m, dtype=torch.int32, device=self.dev)
             L.call(f"pcb_point_norms_{self.sfx}", _p(Xt), m, self.d, _p(xn), _stream())
-            if self.variant == "tc3xtf32":
+            if self.variant in ("tc3xtf32", "tc1xtf32s"):
                 xh = torch.empty((m, self.ld), dtype=torch.float32, device=self.dev)
                 xl = torch.empty_like(xh)
                 L.call("pcb_split_tf32", _p(Xt), m, self.d, self.ld, _p(xh), _p(xl), _stream())

@@ -105,3 +105,67 @@ def test_tc_full_run_matches_ffma_run():
     for r in (a, b):
         np.testing.assert_allclose(r.objective_history, ref.objective_history, rtol=1e-6)
     np.testing.assert_array_equal(a.labels, ref.labels)
+
+
+# ---------------------------------------------------------------------------
+# certified 1xTF32 screening (variant tc1xtf32s)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,d,k", [(1000, 40, 17), (777, 100, 300), (4096, 64, 64), (300, 32, 1),
+                                   (5000, 128, 1024), (2000, 784, 256), (1500, 96, 129), (5000, 64, 4096),
+                                   (20000, 128, 1024)])
+def test_screen_lockstep_ragged_shapes(n, d, k):
+    from paper_2501_05587_b200.engine import LloydEngine
+    P = oracle.make_blobs(n, d, max(k, 1), seed=n + d)
+    lab = oracle.init_assignments(n, k, 1)
+    C = oracle.mean_centroids(P, lab, k)
+    eng = LloydEngine(P, k, variant="tc1xtf32s", max_iters=1)
+    pn = oracle.point_norms(P)
+    for t in range(3):
+        ref = oracle.lloyd_step(P, pn, C, lab, k)
+        gpu = eng.step_from(C, lab)
+        check_step(P, C, lab, k, gpu, ref=ref, what=f"screen n={n} d={d} k={k} it{t}")
+        C, lab = ref.centroids, ref.labels
+
+
+def test_screen_certified_labels_are_exact_argmin():
+    """Rows not sent to the fallback must carry the exact (f64) argmin."""
+    from paper_2501_05587_b200.engine import LloydEngine
+    rng = make_rng(11)
+    n, d, k = 6000, 128, 512
+    P = rng.normal(0, 3, size=(n, d)).astype(np.float32)
+    C = rng.normal(0, 3, size=(k, d)).astype(np.float32)
+    eng = LloydEngine(P, k, variant="tc1xtf32s", max_iters=1)
+    eng.set_centroids(C)
+    out = eng.step_from(C, np.zeros(n, dtype=np.int32))
+    amb = int(eng.amb_count.item())
+    P64, C64 = P.astype(np.float64), C.astype(np.float64)
+    D = (P64 * P64).sum(1)[:, None] - 2 * P64 @ C64.T + (C64 * C64).sum(1)[None, :]
+    exact = D.argmin(1)
+    srt = np.sort(D, 1)
+    gap = (srt[:, 1] - srt[:, 0]) / np.abs(srt[:, 0])
+    bad = (out["raw_labels"] != exact) & (gap >= 1e-5)
+    assert not bad.any(), f"{int(bad.sum())} wrong certified labels"
+    print(f"ambiguous rows: {amb}/{n}")
+    assert amb < n
+
+
+def test_screen_duplicate_centroids_tie_to_lowest_index():
+    from paper_2501_05587_b200.engine import LloydEngine
+    rng = make_rng(12)
+    n, d, k = 3000, 64, 64
+    P = rng.normal(0, 1, size=(n, d)).astype(np.float32)
+    C = rng.normal(0, 1, size=(k, d)).astype(np.float32)
+    C[40] = C[7]  # exact duplicate: every row nearest to it must pick 7
+    eng = LloydEngine(P, k, variant="tc1xtf32s", max_iters=1)
+    out = eng.step_from(C, np.zeros(n, dtype=np.int32))
+    assert not np.any(out["raw_labels"] == 40)
+    assert eng.amb_count.item() >= np.sum(out["raw_labels"] == 7)
+
+
+def test_screen_full_run_matches_reference():
+    import paper_2501_05587_b200 as pcb
+    P = oracle.make_blobs(20000, 128, 64, seed=4)
+    a = pcb.run_lloyd(P, pcb.KKMeansConfig(k=64, max_iters=8, variant="tc1xtf32s"))
+    ref = oracle.run_lloyd(P, 64, max_iters=8)
+    np.testing.assert_allclose(a.objective_history, ref.objective_history, rtol=1e-6)
+    np.testing.assert_array_equal(a.labels, ref.labels)
