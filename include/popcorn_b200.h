@@ -86,23 +86,24 @@ int pcb_assign_tc_f32(const float* P_hi, const float* P_lo, int ld, const float*
                       const long long* state, void* stream);
 
 /* Certified 1xTF32 screening variant ("tc1xtf32s", see assign_screen.cu):
- * one TF32 tensor-core pass on the raw f32 operands (d % 4 == 0) with a
- * rigorous per-row error bound; rows whose argmin is not certified are listed
- * in amb_list/amb_count (caller zeroes amb_count) and resolved exactly-as-3xTF32
- * by pcb_resolve_ambiguous_f32.  Labels only: counts/changed come from
+ * one TF32 tensor-core pass on TF32-rounded operands (P_r = rna(P), C_r =
+ * rna(C) = the finalize kernel's C_hi, row stride ld) with a rigorous per-row
+ * error bound; rows whose argmin is not certified are listed in
+ * amb_list/amb_count (caller zeroes amb_count) and resolved as 3xTF32 by
+ * pcb_resolve_ambiguous_f32.  Labels only: counts/changed come from
  * pcb_count_labels.
- *   pcb_screen_prep_points:    anorm = |trunc(p)|, danorm = |p - trunc(p)|,
+ *   pcb_screen_prep_points:    P_r, anorm = |rna(p)|, danorm = |p - rna(p)|,
  *                              bstat[2] = OFF (once per fit)
  *   pcb_screen_prep_centroids: bnorm, dbnorm, bstat[0..1] (after every
  *                              centroid update)                                */
-int pcb_screen_prep_points(const float* P, int64_t n, int d, float* anorm, float* danorm,
-                           float* bstat /* 4 */, void* stream);
+int pcb_screen_prep_points(const float* P, int64_t n, int d, int ld, float* P_r, float* anorm,
+                           float* danorm, float* bstat /* 4 */, void* stream);
 int pcb_screen_prep_centroids(const float* C, int k, int d, float* bnorm, float* dbnorm,
                               float* bstat, void* stream);
-int pcb_assign_screen_f32(const float* P, int64_t n, int d, const float* C, int k, const float* cnorm,
-                          const float* anorm, const float* danorm, const float* bstat,
-                          int32_t* labels, int* amb_list, int* amb_count, const long long* state,
-                          void* stream);
+int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const float* C_r, int k,
+                          const float* cnorm, const float* anorm, const float* danorm,
+                          const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
+                          const long long* state, void* stream);
 int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_list,
                               const int* amb_count, int ld, float* sub_hi, float* sub_lo,
                               int32_t* sub_labels, const float* pnorm, const float* C_hi,

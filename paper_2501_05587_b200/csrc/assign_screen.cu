@@ -2,13 +2,14 @@
 //
 // The 3xTF32 kernel (assign_tc.cu) runs at 95 % of the TF32 tensor pipe, so
 // its only remaining lever is fewer tensor-core passes.  This kernel makes ONE
-// TF32 pass over the raw f32 operands (tcgen05 kind::tf32 reads an f32 word by
-// truncating it to TF32) and certifies the argmin with a rigorous error bound:
+// TF32 pass over TF32-rounded operands p~ = rna(p), c~ = rna(c) (exactly
+// representable, so the tensor core's f32->tf32 conversion is exact) and
+// certifies the argmin with a rigorous error bound:
 //
-//   G  = <p, c>,  T = <trunc(p), trunc(c)> (+ TC accumulation error)
-//   |G - T| <= |da||c~| + |a~||dc| + |da||dc| + (K/8 + 1) 2^-22 |a~||c~|
-//   (Cauchy-Schwarz on the exact truncation residuals da = p - trunc(p),
-//   dc = c - trunc(c); a round-to-nearest conversion would only shrink them)
+//   G  = <p, c>,  T = <p~, c~> (+ TC accumulation error)
+//   |G - T| <= |da||c~| + |p~||dc| + |da||dc| + acc
+//   (Cauchy-Schwarz on the exact residuals da = p - p~, dc = c - c~; acc is the
+//   accumulation bound, 9 terms at 2^-23 per K=8 MMA)
 //
 // Ranking key  key_j = (cnorm_j + OFF) - 2 T_j,  OFF > max_i |p_i|^2 so keys are
 // positive and can carry a 5-bit column index in their low mantissa bits
@@ -33,7 +34,7 @@ namespace pcb {
 
 constexpr int SC_BM = 128;
 constexpr int SC_BK = 32;
-constexpr int SC_THREADS = 256;
+constexpr int SC_THREADS = 384;  // warps 0-3 control, 4-11 epilogue (2 per TMEM lane group)
 constexpr int SC_KMAX = 8192;  // smem copy of the shifted centroid norms
 
 template <int BN>
@@ -43,9 +44,13 @@ struct ScCfg {
   static constexpr uint32_t kBBytes = BN * SC_BK * 4;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr uint32_t kBarBytes = 1024;
+  static constexpr uint32_t kBarBytes = 2048;  // barriers, tmem slot, row-merge exchange (128 x 3 words)
   static constexpr uint32_t kSmem = 1024 + kStages * kStageBytes + kBarBytes + SC_KMAX * 4;
 };
+
+// chunk-local column ids; held in registers so (key & ~31) | id is a single LOP3
+__constant__ uint32_t kChunkIds[32] = {0,  1,  2,  3,  4,  5,  6,  7,  8,  9,  10, 11, 12, 13, 14, 15,
+                                       16, 17, 18, 19, 20, 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31};
 
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
   float r;
@@ -92,7 +97,7 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], 128);
+      ptx::mbar_init(&tempty[b], 256);
     }
     ptx::fence_barrier_init();
   }
@@ -157,12 +162,19 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
       }
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;
-    const int r_in_tile = ew * 32 + lane;
+    // Epilogue: warp w reads TMEM lane group (w % 4); the two warps of a group
+    // (half h = 0/1) take alternating 32-column chunks and merge per row tile.
+    const int g = warp & 3, h = (warp - 4) >> 2;
+    const int r_in_tile = g * 32 + lane;
+    float* xchg = reinterpret_cast<float*>(tmem_slot + 4);  // [128][3]
     const float Bmax = bstat[0], dBmax = bstat[1];
     // TC accumulation: per K=8 MMA <= 9 terms aligned/truncated at 2^-23 of the
     // largest partial (|partial| <= sum |a~_t c~_t| <= |a~||c~|)
     const float acc_rel = (float)(num_kc * 4 + 2) * 9.0f * 0x1p-23f;
+    // chunk-local column ids held in registers so (key & ~31) | id is one LOP3
+    uint32_t cid[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) cid[i] = kChunkIds[i];
     int abuf = 0;
     uint32_t aphase = 0;
     for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
@@ -171,29 +183,32 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
       for (int nt = 0; nt < ntiles; ++nt) {
         ptx::mbar_wait(&tfull[abuf], aphase);
         ptx::tc_fence_after();
-        const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(abuf * BN);
+        const uint32_t taddr = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)(abuf * BN);
 #pragma unroll 1
-        for (int cb = 0; cb < BN; cb += 32) {
+        for (int cb = h * 32; cb < BN; cb += 64) {
           float v[32];
           ptx::tmem_ld_32x32b_x32(taddr + cb, v);
           const float4* cp4 = reinterpret_cast<const float4*>(cprime + nt * BN + cb);
-          float S1 = 3.4e38f, S2 = 3.4e38f;
+          // two independent top-2 chains (even / odd column pairs) for ILP
+          float S1a = 3.4e38f, S2a = 3.4e38f, S1b = 3.4e38f, S2b = 3.4e38f;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float4 c4 = cp4[q];
-            const float k0 = pack_idx(fmaf(-2.0f, v[4 * q + 0], c4.x), 4 * q + 0);
-            const float k1 = pack_idx(fmaf(-2.0f, v[4 * q + 1], c4.y), 4 * q + 1);
-            const float k2 = pack_idx(fmaf(-2.0f, v[4 * q + 2], c4.z), 4 * q + 2);
-            const float k3 = pack_idx(fmaf(-2.0f, v[4 * q + 3], c4.w), 4 * q + 3);
+            const float k0 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[4 * q + 0], c4.x)) & 0xFFFFFFE0u) | cid[4 * q + 0]);
+            const float k1 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[4 * q + 1], c4.y)) & 0xFFFFFFE0u) | cid[4 * q + 1]);
+            const float k2 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[4 * q + 2], c4.z)) & 0xFFFFFFE0u) | cid[4 * q + 2]);
+            const float k3 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[4 * q + 3], c4.w)) & 0xFFFFFFE0u) | cid[4 * q + 3]);
             float lo = fminf(k0, k1), hi = fmaxf(k0, k1);
-            S2 = fmin3(S2, hi, fmaxf(S1, lo));
-            S1 = fminf(S1, lo);
+            S2a = fmin3(S2a, hi, fmaxf(S1a, lo));
+            S1a = fminf(S1a, lo);
             lo = fminf(k2, k3);
             hi = fmaxf(k2, k3);
-            S2 = fmin3(S2, hi, fmaxf(S1, lo));
-            S1 = fminf(S1, lo);
+            S2b = fmin3(S2b, hi, fmaxf(S1b, lo));
+            S1b = fminf(S1b, lo);
           }
-          // merge this 32-column chunk into the row's running top-2 (lowest j on ties)
+          const float S1 = fminf(S1a, S1b);
+          const float S2 = fmin3(S2a, S2b, fmaxf(S1a, S1b));
+          // merge the chunk into the running top-2 (earlier chunks win ties)
           if (S1 < R1) {
             R2 = fminf(R1, S2);
             R1 = S1;
@@ -207,25 +222,42 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1u;
       }
-      const int64_t row = mt * SC_BM + r_in_tile;
-      bool amb = false;
-      if (row < n) {
-        labels[row] = r1;
-        const float an = anorm[row], dan = danorm[row];
-        // rigorous per-row bound on |key_j - OFF - s_j| (see header), rounded up
-        const float g = dan * Bmax + an * dBmax + dan * dBmax + acc_rel * an * Bmax;
-        const float cb = Bmax + dBmax;
-        const float kmax = OFF + 2.0f * (an + dan) * cb + cb * cb;
-        const float E = 1.0001f * (2.0f * g + 0x1p-16f * kmax);
-        amb = !(R2 > R1 + 2.0f * E);
+      // combine the two column halves of every row
+      if (h == 1) {
+        xchg[r_in_tile * 3 + 0] = R1;
+        xchg[r_in_tile * 3 + 1] = R2;
+        xchg[r_in_tile * 3 + 2] = __int_as_float(r1);
       }
-      const unsigned m = __ballot_sync(0xffffffffu, amb);
-      if (m) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(amb_count, __popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (amb) amb_list[base + __popc(m & ((1u << lane) - 1u))] = (int)row;
+      ptx::named_bar_sync(1, 256);
+      if (h == 0) {
+        const float oR1 = xchg[r_in_tile * 3 + 0], oR2 = xchg[r_in_tile * 3 + 1];
+        const int or1 = __float_as_int(xchg[r_in_tile * 3 + 2]);
+        // min over the packed keys; exact-value ties across halves make the row
+        // ambiguous (R2 == R1) and are resolved by the fallback
+        const bool take = (oR1 < R1) || (oR1 == R1 && or1 < r1);
+        R2 = fminf(fmaxf(R1, oR1), fminf(R2, oR2));
+        if (take) { R1 = oR1; r1 = or1; }
+        const int64_t row = mt * SC_BM + r_in_tile;
+        bool amb = false;
+        if (row < n) {
+          labels[row] = r1;
+          const float an = anorm[row], dan = danorm[row];
+          // rigorous per-row bound on |key_j - OFF - s_j| (see header), rounded up
+          const float gerr = dan * Bmax + an * dBmax + dan * dBmax + acc_rel * an * Bmax;
+          const float cbn = Bmax + dBmax;
+          const float kmax = OFF + 2.0f * (an + dan) * cbn + cbn * cbn;
+          const float E = 1.0001f * (2.0f * gerr + 0x1p-16f * kmax);
+          amb = !(R2 > R1 + 2.0f * E);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, amb);
+        if (m) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(amb_count, __popc(m));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (amb) amb_list[base + __popc(m & ((1u << lane) - 1u))] = (int)row;
+        }
       }
+      ptx::named_bar_sync(1, 256);
     }
   }
   ptx::tc_fence_before();
@@ -236,25 +268,33 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
 
 // ---- screening prep / fallback helpers ---------------------------------------
 
-__device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  return __uint_as_float(h);
+}
 
 __device__ __forceinline__ void atomic_max_pos(float* addr, float v) {
   atomicMax(reinterpret_cast<unsigned int*>(addr), __float_as_uint(v));  // v >= 0
 }
 
-// Per row: |trunc(p)|, |p - trunc(p)| (rounded up), and the max point norm^2.
+// Per row of X (rows x d): |rna(x)|, |x - rna(x)| (rounded up), the max |x|^2,
+// and optionally the rounded copy Xr (row stride ld, zero padded).
 __global__ void __launch_bounds__(256)
-row_trunc_norms_kernel(const float* __restrict__ X, int64_t rows, int d, float* __restrict__ an,
-                       float* __restrict__ dan, float* __restrict__ maxsq) {
+row_tf32_norms_kernel(const float* __restrict__ X, int64_t rows, int d, float* __restrict__ an,
+                      float* __restrict__ dan, float* __restrict__ maxsq, float* __restrict__ Xr, int ld) {
   const int lane = threadIdx.x & 31;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   float wmax = 0.0f;
   for (int64_t i = w; i < rows; i += nw) {
     double s_t = 0.0, s_d = 0.0, s_x = 0.0;
+    if (Xr != nullptr)
+      for (int t = d + lane; t < ld; t += 32) Xr[i * ld + t] = 0.0f;
     for (int t = lane; t < d; t += 32) {
       const float x = X[i * d + t];
-      const float h = trunc_tf32(x);
+      const float h = rna_tf32(x);
+      if (Xr != nullptr) Xr[i * ld + t] = h;
       const double dd = (double)x - (double)h;
       s_t = fma((double)h, (double)h, s_t);
       s_d = fma(dd, dd, s_d);
@@ -361,20 +401,20 @@ static int make_tmap_rows(CUtensorMap* m, const float* base, int64_t rows, int c
 }
 
 template <int BN>
-static int launch_screen(const float* P, int64_t n, int d, const float* C, int k, const float* an,
+static int launch_screen(const float* P, int64_t n, int ld, const float* C, int k, const float* an,
                          const float* dan, const float* cnorm, const float* bstat, int32_t* labels,
                          int* amb_list, int* amb_count, const long long* state, cudaStream_t st) {
   using Cfg = ScCfg<BN>;
   CUtensorMap ta, tb;
   int rc;
-  if ((rc = make_tmap_rows(&ta, P, n, d, SC_BM))) return rc;
-  if ((rc = make_tmap_rows(&tb, C, k, d, BN))) return rc;
+  if ((rc = make_tmap_rows(&ta, P, n, ld, SC_BM))) return rc;
+  if ((rc = make_tmap_rows(&tb, C, k, ld, BN))) return rc;
   auto kern = assign_screen_kernel<BN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   if (e != cudaSuccess) return (int)e;
   const int64_t mtiles = (n + SC_BM - 1) / SC_BM;
   const int grid = (int)std::min<int64_t>(mtiles, (int64_t)sm_count());
-  kern<<<grid, SC_THREADS, Cfg::kSmem, st>>>(ta, tb, an, dan, cnorm, bstat, n, k, (d + SC_BK - 1) / SC_BK, labels,
+  kern<<<grid, SC_THREADS, Cfg::kSmem, st>>>(ta, tb, an, dan, cnorm, bstat, n, k, ld / SC_BK, labels,
                                              amb_list, amb_count, state);
   PCB_CHECK_LAUNCH();
   return 0;
@@ -384,14 +424,14 @@ static int launch_screen(const float* P, int64_t n, int d, const float* C, int k
 
 using namespace pcb;
 
-extern "C" int pcb_screen_prep_points(const float* P, int64_t n, int d, float* anorm, float* danorm,
-                                      float* bstat, void* stream) {
-  if (n < 1 || d < 1 || !P || !anorm || !danorm || !bstat) return PCB_EINVAL;
+extern "C" int pcb_screen_prep_points(const float* P, int64_t n, int d, int ld, float* P_r, float* anorm,
+                                      float* danorm, float* bstat, void* stream) {
+  if (n < 1 || d < 1 || ld < d || ld % 32 || !P || !P_r || !anorm || !danorm || !bstat) return PCB_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(bstat, 0, 4 * sizeof(float), st);
   if (e != cudaSuccess) return (int)e;
   const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, (int64_t)sm_count() * 16);
-  row_trunc_norms_kernel<<<grid, 256, 0, st>>>(P, n, d, anorm, danorm, bstat + 3);
+  row_tf32_norms_kernel<<<grid, 256, 0, st>>>(P, n, d, anorm, danorm, bstat + 3, P_r, ld);
   PCB_CHECK_LAUNCH();
   screen_stats_finish<<<1, 1, 0, st>>>(bstat, bstat + 3);
   PCB_CHECK_LAUNCH();
@@ -404,26 +444,28 @@ extern "C" int pcb_screen_prep_centroids(const float* C, int k, int d, float* bn
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(bstat, 0, 2 * sizeof(float), st);
   if (e != cudaSuccess) return (int)e;
-  row_trunc_norms_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(C, k, d, bnorm, dbnorm, nullptr);
+  row_tf32_norms_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(C, k, d, bnorm, dbnorm, nullptr, nullptr, 0);
   PCB_CHECK_LAUNCH();
   max2_kernel<<<1, 256, 0, st>>>(bnorm, dbnorm, k, bstat);  // bstat[0] = max|c~|, [1] = max|dc|
   PCB_CHECK_LAUNCH();
   return 0;
 }
 
-extern "C" int pcb_assign_screen_f32(const float* P, int64_t n, int d, const float* C, int k, const float* cnorm,
-                                     const float* anorm, const float* danorm, const float* bstat,
-                                     int32_t* labels, int* amb_list, int* amb_count, const long long* state,
-                                     void* stream) {
-  if (n < 1 || d < 1 || k < 1 || !P || !C || !cnorm || !anorm || !danorm || !bstat || !labels || !amb_list ||
-      !amb_count)
+extern "C" int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const float* C_r, int k,
+                                     const float* cnorm, const float* anorm, const float* danorm,
+                                     const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
+                                     const long long* state, void* stream) {
+  if (n < 1 || ld < 32 || ld % 32 || k < 1 || !P_r || !C_r || !cnorm || !anorm || !danorm || !bstat || !labels ||
+      !amb_list || !amb_count)
     return PCB_EINVAL;
-  if (d % 4 != 0 || n > INT32_MAX) return PCB_EUNSUP;  // TMA: 16-byte row strides
+  if (n > INT32_MAX) return PCB_EUNSUP;
   if (k > SC_KMAX) return PCB_EUNSUP;
   cudaStream_t st = (cudaStream_t)stream;
   if (k > 128)
-    return launch_screen<256>(P, n, d, C, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state, st);
-  return launch_screen<128>(P, n, d, C, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state, st);
+    return launch_screen<256>(P_r, n, ld, C_r, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state,
+                              st);
+  return launch_screen<128>(P_r, n, ld, C_r, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state,
+                            st);
 }
 
 extern "C" int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_list,

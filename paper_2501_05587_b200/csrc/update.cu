@@ -84,6 +84,47 @@ scatter_by_label(const int32_t* __restrict__ labels, int64_t n, int32_t* __restr
   }
 }
 
+// Block-aggregated counting-sort scatter: a block ranks a chunk of ids per
+// label in shared memory (native ATOMS.POPC.INC), claims one global range per
+// (chunk, label), then writes.  ~k global atomics per 4096 ids instead of one
+// per warp-label group.
+constexpr int SC_EPT = 16;
+
+__global__ void __launch_bounds__(256)
+scatter_by_label_blocked(const int32_t* __restrict__ labels, int64_t n, int k, int32_t* __restrict__ cursor,
+                         int32_t* __restrict__ perm, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  extern __shared__ int sm[];
+  int* hist = sm;
+  int* base = sm + k;
+  const int64_t chunk = (int64_t)blockDim.x * SC_EPT;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
+    __syncthreads();
+    int lab[SC_EPT], rnk[SC_EPT];
+#pragma unroll
+    for (int e = 0; e < SC_EPT; ++e) {
+      const int64_t i = c * chunk + e * blockDim.x + threadIdx.x;
+      lab[e] = i < n ? labels[i] : -1;
+    }
+#pragma unroll
+    for (int e = 0; e < SC_EPT; ++e) rnk[e] = lab[e] >= 0 ? atomicAdd(&hist[lab[e]], 1) : 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      const int h = hist[j];
+      base[j] = h ? atomicAdd(&cursor[j], h) : 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < SC_EPT; ++e) {
+      const int64_t i = c * chunk + e * blockDim.x + threadIdx.x;
+      if (lab[e] >= 0) perm[base[lab[e]] + rnk[e]] = (int32_t)i;
+    }
+    __syncthreads();
+  }
+}
+
 // Largest j with offsets[j] <= s (segments may be empty: offsets non-decreasing).
 __device__ __forceinline__ int segment_of(const int32_t* offsets, int k, int64_t s) {
   int lo = 0, hi = k - 1;
@@ -292,8 +333,14 @@ extern "C" int pcb_sort_by_label(const int32_t* labels, int64_t n, int k, const 
   pcb::scan_counts<<<1, 1024, 0, st>>>(counts, k, offsets, cursor, state);
   PCB_CHECK_LAUNCH();
   const int sms = pcb::sm_count();
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
-  pcb::scatter_by_label<<<grid, 256, 0, st>>>(labels, n, cursor, perm, state);
+  if (k <= 6144) {
+    const int64_t chunks = (n + 256 * pcb::SC_EPT - 1) / (256 * pcb::SC_EPT);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)sms * 4));
+    pcb::scatter_by_label_blocked<<<grid, 256, 2 * k * sizeof(int), st>>>(labels, n, k, cursor, perm, state);
+  } else {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+    pcb::scatter_by_label<<<grid, 256, 0, st>>>(labels, n, cursor, perm, state);
+  }
   PCB_CHECK_LAUNCH();
   return 0;
 }

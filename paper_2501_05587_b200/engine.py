@@ -58,8 +58,6 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int) -> str:
     if variant != "auto":
         if dtype == _F64 and variant in ("tc3xtf32", "delta", "tc1xtf32s"):
             raise ValueError(f"variant {variant!r} is float32-only")
-        if variant == "tc1xtf32s" and d % 4 != 0:
-            raise ValueError("variant 'tc1xtf32s' needs d % 4 == 0 (TMA row stride)")
         if variant == "rowreg" and d > 32:
             raise ValueError("variant 'rowreg' needs d <= 32")
         return variant
@@ -148,8 +146,9 @@ class LloydEngine:
                 self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
-                L.call("pcb_screen_prep_points", _p(self.P), n, d, _p(self.anorm), _p(self.danorm),
-                       _p(self.bstat), _stream())
+                self.P_r = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
+                L.call("pcb_screen_prep_points", _p(self.P), n, d, self.ld, _p(self.P_r), _p(self.anorm),
+                       _p(self.danorm), _p(self.bstat), _stream())
 
     # -- centroid initialisation ------------------------------------------------
     def set_centroids(self, C) -> None:
@@ -210,7 +209,7 @@ class LloydEngine:
     def _assign(self, prev, new, acc, state) -> None:
         if self.variant == "tc1xtf32s":
             self.amb_count.zero_()
-            L.call("pcb_assign_screen_f32", _p(self.P), self.n, self.d, _p(self.C), self.k,
+            L.call("pcb_assign_screen_f32", _p(self.P_r), self.n, self.ld, _p(self.C_hi), self.k,
                    _p(self.cnorm), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
                    _p(self.amb_list), _p(self.amb_count), _p(state), _stream())
             L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.amb_list),
