@@ -256,6 +256,7 @@ def main():
     st = eng.state.cpu().numpy()
     if st[5] != 0:
         raise SystemExit("non-finite distances during the bench")
+    amb = int(eng.amb_count.item()) if getattr(eng, "amb_count", None) is not None else None
 
     ms_per_step = ms / K
     value = 1e3 / ms_per_step  # whole-job iterations/s (all ranks, n total)
@@ -294,7 +295,8 @@ def main():
                    "l2": "inputs larger than L2" if n * d * 4 > 126e6 else "inputs fit in L2 (no flush)"},
         "dists_per_sec": n * k / (ms_per_step * 1e-3),
         "roofline": roof,
-        "gpu_launches": 6 * K,
+        "gpu_launches": (12 if eng.variant == "tc1xtf32s" else 6) * K,
+        "screen_ambiguous_rows_last_iter": amb,
         "clocks": clocks,
     }
     del eng, P

@@ -44,7 +44,7 @@ struct ScCfg {
   static constexpr uint32_t kBBytes = BN * SC_BK * 4;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr uint32_t kBarBytes = 2048;  // barriers, tmem slot, row-merge exchange (128 x 3 words)
+  static constexpr uint32_t kBarBytes = 4096;  // barriers, tmem slot, row-merge exchange (2 x 128 x 3 words)
   static constexpr uint32_t kSmem = 1024 + kStages * kStageBytes + kBarBytes + SC_KMAX * 4;
 };
 
@@ -177,6 +177,7 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
     for (int i = 0; i < 32; ++i) cid[i] = kChunkIds[i];
     int abuf = 0;
     uint32_t aphase = 0;
+    int tile_it = 0;
     for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
       float R1 = 3.4e38f, R2 = 3.4e38f;
       int r1 = 0;
@@ -189,15 +190,22 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
           float v[32];
           ptx::tmem_ld_32x32b_x32(taddr + cb, v);
           const float4* cp4 = reinterpret_cast<const float4*>(cprime + nt * BN + cb);
-          // two independent top-2 chains (even / odd column pairs) for ILP
+          // four independent top-2 chains (column pairs mod 4) for ILP
           float S1a = 3.4e38f, S2a = 3.4e38f, S1b = 3.4e38f, S2b = 3.4e38f;
+          float S1c = 3.4e38f, S2c = 3.4e38f, S1d = 3.4e38f, S2d = 3.4e38f;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 c4 = cp4[q];
-            const float k0 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[4 * q + 0], c4.x)) & 0xFFFFFFE0u) | cid[4 * q + 0]);
-            const float k1 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[4 * q + 1], c4.y)) & 0xFFFFFFE0u) | cid[4 * q + 1]);
-            const float k2 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[4 * q + 2], c4.z)) & 0xFFFFFFE0u) | cid[4 * q + 2]);
-            const float k3 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[4 * q + 3], c4.w)) & 0xFFFFFFE0u) | cid[4 * q + 3]);
+          for (int q = 0; q < 4; ++q) {
+            const float4 c4 = cp4[2 * q];
+            const float4 c5 = cp4[2 * q + 1];
+            const int b0 = 8 * q;
+            const float k0 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 0], c4.x)) & 0xFFFFFFE0u) | cid[b0 + 0]);
+            const float k1 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 1], c4.y)) & 0xFFFFFFE0u) | cid[b0 + 1]);
+            const float k2 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 2], c4.z)) & 0xFFFFFFE0u) | cid[b0 + 2]);
+            const float k3 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 3], c4.w)) & 0xFFFFFFE0u) | cid[b0 + 3]);
+            const float k4 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 4], c5.x)) & 0xFFFFFFE0u) | cid[b0 + 4]);
+            const float k5 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 5], c5.y)) & 0xFFFFFFE0u) | cid[b0 + 5]);
+            const float k6 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 6], c5.z)) & 0xFFFFFFE0u) | cid[b0 + 6]);
+            const float k7 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 7], c5.w)) & 0xFFFFFFE0u) | cid[b0 + 7]);
             float lo = fminf(k0, k1), hi = fmaxf(k0, k1);
             S2a = fmin3(S2a, hi, fmaxf(S1a, lo));
             S1a = fminf(S1a, lo);
@@ -205,7 +213,24 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
             hi = fmaxf(k2, k3);
             S2b = fmin3(S2b, hi, fmaxf(S1b, lo));
             S1b = fminf(S1b, lo);
+            lo = fminf(k4, k5);
+            hi = fmaxf(k4, k5);
+            S2c = fmin3(S2c, hi, fmaxf(S1c, lo));
+            S1c = fminf(S1c, lo);
+            lo = fminf(k6, k7);
+            hi = fmaxf(k6, k7);
+            S2d = fmin3(S2d, hi, fmaxf(S1d, lo));
+            S1d = fminf(S1d, lo);
           }
+          // merge the four chains: top-2 of {(S1a,S2a),(S1b,S2b),(S1c,S2c),(S1d,S2d)}
+          const float m_ab = fminf(S1a, S1b), M_ab = fmaxf(S1a, S1b);
+          const float m_cd = fminf(S1c, S1d), M_cd = fmaxf(S1c, S1d);
+          S2a = fmin3(M_ab, S2a, S2b);
+          S2c = fmin3(M_cd, S2c, S2d);
+          S1a = m_ab;
+          S1c = m_cd;
+          S1b = S1c;
+          S2b = S2c;
           const float S1 = fminf(S1a, S1b);
           const float S2 = fmin3(S2a, S2b, fmaxf(S1a, S1b));
           // merge the chunk into the running top-2 (earlier chunks win ties)
@@ -222,16 +247,21 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1u;
       }
-      // combine the two column halves of every row
+      // combine the two column halves of every row: h=1 publishes into a
+      // double-buffered slot (pair barrier 1+g), h=0 consumes and releases it
+      // (pair barrier 5+g); only the two warps of a lane group synchronise.
+      float* slot = xchg + (tile_it & 1) * (128 * 3);
       if (h == 1) {
-        xchg[r_in_tile * 3 + 0] = R1;
-        xchg[r_in_tile * 3 + 1] = R2;
-        xchg[r_in_tile * 3 + 2] = __int_as_float(r1);
-      }
-      ptx::named_bar_sync(1, 256);
-      if (h == 0) {
-        const float oR1 = xchg[r_in_tile * 3 + 0], oR2 = xchg[r_in_tile * 3 + 1];
-        const int or1 = __float_as_int(xchg[r_in_tile * 3 + 2]);
+        if (tile_it >= 2) ptx::named_bar_sync(5 + g, 64);
+        slot[r_in_tile * 3 + 0] = R1;
+        slot[r_in_tile * 3 + 1] = R2;
+        slot[r_in_tile * 3 + 2] = __int_as_float(r1);
+        ptx::named_bar_arrive(1 + g, 64);
+      } else {
+        ptx::named_bar_sync(1 + g, 64);
+        const float oR1 = slot[r_in_tile * 3 + 0], oR2 = slot[r_in_tile * 3 + 1];
+        const int or1 = __float_as_int(slot[r_in_tile * 3 + 2]);
+        ptx::named_bar_arrive(5 + g, 64);
         // min over the packed keys; exact-value ties across halves make the row
         // ambiguous (R2 == R1) and are resolved by the fallback
         const bool take = (oR1 < R1) || (oR1 == R1 && or1 < r1);
@@ -257,8 +287,12 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
           if (amb) amb_list[base + __popc(m & ((1u << lane) - 1u))] = (int)row;
         }
       }
-      ptx::named_bar_sync(1, 256);
+      ++tile_it;
     }
+    // balance the release barrier: h=0 arrived once per tile, h=1 synced for
+    // tiles >= 2 only
+    if (h == 1)
+      for (int t = 0; t < min(tile_it, 2); ++t) ptx::named_bar_sync(5 + g, 64);
   }
   ptx::tc_fence_before();
   __syncthreads();
