@@ -35,7 +35,7 @@ namespace pcb {
 constexpr int SC_BM = 128;
 constexpr int SC_BK = 32;
 constexpr int SC_THREADS = 384;  // warps 0-3 control, 4-11 epilogue (2 per TMEM lane group)
-constexpr int SC_KMAX = 8192;  // smem copy of the shifted centroid norms
+constexpr int SC_KMAX = 6144;  // smem copy of the shifted centroid norms (k <= 6144)
 
 template <int BN>
 struct ScCfg {
@@ -46,6 +46,7 @@ struct ScCfg {
   static constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr uint32_t kBarBytes = 4096;  // barriers, tmem slot, row-merge exchange (2 x 128 x 3 words)
   static constexpr uint32_t kSmem = 1024 + kStages * kStageBytes + kBarBytes + SC_KMAX * 4;
+  static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
 // chunk-local column ids; held in registers so (key & ~31) | id is a single LOP3

@@ -52,7 +52,7 @@ def require_cuda(device=None) -> torch.device:
     return dev
 
 
-def resolve_variant(variant: str, dtype: np.dtype, d: int) -> str:
+def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
     if variant not in L.VARIANTS:
         raise ValueError(f"unknown assign variant {variant!r}; expected one of {tuple(L.VARIANTS)}")
     if variant != "auto":
@@ -60,10 +60,15 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int) -> str:
             raise ValueError(f"variant {variant!r} is float32-only")
         if variant == "rowreg" and d > 32:
             raise ValueError("variant 'rowreg' needs d <= 32")
+        if variant == "tc1xtf32s" and k > SCREEN_KMAX:
+            raise ValueError(f"variant 'tc1xtf32s' supports k <= {SCREEN_KMAX}")
         return variant
     if d <= 32:
         return "rowreg"
     return "tc3xtf32" if dtype == _F32 else "tiled"
+
+
+SCREEN_KMAX = 6144  # assign_screen.cu SC_KMAX
 
 
 @dataclass
@@ -98,8 +103,9 @@ class LloydEngine:
             self.P = P
             self.n, self.d = int(P.shape[0]), int(P.shape[1])
             self.k = int(k)
+            assert self.k >= 1
             self.n_total = int(n_total if n_total is not None else self.n)
-            self.variant = resolve_variant(variant, self.dtype, self.d)
+            self.variant = resolve_variant(variant, self.dtype, self.d, self.k)
             self.vcode = L.VARIANTS[self.variant]
             n, d, kk = self.n, self.d, self.k
             dev, td = self.dev, self.tdtype
