@@ -81,7 +81,9 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
   uint64_t* empty = full + Cfg::kStages;
   uint64_t* tfull = empty + Cfg::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xwritten = tempty + 2;    // [4 lane groups][2 slots]: h=1 published a slot
+  uint64_t* xreleased = xwritten + 8; // [4][2]: h=0 consumed a slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xreleased + 8);
   float* cprime = reinterpret_cast<float*>(bar_area + Cfg::kBarBytes);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -99,6 +101,10 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 256);
+    }
+    for (int b = 0; b < 8; ++b) {
+      ptx::mbar_init(&xwritten[b], 32);
+      ptx::mbar_init(&xreleased[b], 32);
     }
     ptx::fence_barrier_init();
   }
@@ -167,7 +173,7 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
     // (half h = 0/1) take alternating 32-column chunks and merge per row tile.
     const int g = warp & 3, h = (warp - 4) >> 2;
     const int r_in_tile = g * 32 + lane;
-    float* xchg = reinterpret_cast<float*>(tmem_slot + 4);  // [128][3]
+    float* xchg = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][128][3]
     const float Bmax = bstat[0], dBmax = bstat[1];
     // TC accumulation: per K=8 MMA <= 9 terms aligned/truncated at 2^-23 of the
     // largest partial (|partial| <= sum |a~_t c~_t| <= |a~||c~|)
@@ -249,20 +255,23 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
         if (abuf == 0) aphase ^= 1u;
       }
       // combine the two column halves of every row: h=1 publishes into a
-      // double-buffered slot (pair barrier 1+g), h=0 consumes and releases it
-      // (pair barrier 5+g); only the two warps of a lane group synchronise.
-      float* slot = xchg + (tile_it & 1) * (128 * 3);
+      // double-buffered slot, h=0 consumes and releases it; mbarriers per lane
+      // group and slot (phase = use count of the slot), so only the two warps
+      // of a lane group ever wait on each other.
+      const int sidx = tile_it & 1;
+      const uint32_t use = (uint32_t)(tile_it >> 1);
+      float* slot = xchg + sidx * (128 * 3);
       if (h == 1) {
-        if (tile_it >= 2) ptx::named_bar_sync(5 + g, 64);
+        if (tile_it >= 2) ptx::mbar_wait(&xreleased[g * 2 + sidx], (use - 1u) & 1u);
         slot[r_in_tile * 3 + 0] = R1;
         slot[r_in_tile * 3 + 1] = R2;
         slot[r_in_tile * 3 + 2] = __int_as_float(r1);
-        ptx::named_bar_arrive(1 + g, 64);
+        ptx::mbar_arrive(&xwritten[g * 2 + sidx]);
       } else {
-        ptx::named_bar_sync(1 + g, 64);
+        ptx::mbar_wait(&xwritten[g * 2 + sidx], use & 1u);
         const float oR1 = slot[r_in_tile * 3 + 0], oR2 = slot[r_in_tile * 3 + 1];
         const int or1 = __float_as_int(slot[r_in_tile * 3 + 2]);
-        ptx::named_bar_arrive(5 + g, 64);
+        ptx::mbar_arrive(&xreleased[g * 2 + sidx]);
         // min over the packed keys; exact-value ties across halves make the row
         // ambiguous (R2 == R1) and are resolved by the fallback
         const bool take = (oR1 < R1) || (oR1 == R1 && or1 < r1);
@@ -290,10 +299,6 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
       }
       ++tile_it;
     }
-    // balance the release barrier: h=0 arrived once per tile, h=1 synced for
-    // tiles >= 2 only
-    if (h == 1)
-      for (int t = 0; t < min(tile_it, 2); ++t) ptx::named_bar_sync(5 + g, 64);
   }
   ptx::tc_fence_before();
   __syncthreads();
