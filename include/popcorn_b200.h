@@ -50,6 +50,11 @@ const char* pcb_error_string(int code);
 /* sm count / compute capability of `device`; returns PCB_ENODEV if not sm_100. */
 int pcb_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 
+/* Input validation on the device (validation.py:45-46): *out = number of
+ * non-finite entries among X[0:count]. */
+int pcb_count_nonfinite_f32(const float* X, int64_t count, unsigned long long* out, void* stream);
+int pcb_count_nonfinite_f64(const double* X, int64_t count, unsigned long long* out, void* stream);
+
 /* ---- one-time point preparation (clustering.py:302: point_norms) ---------- */
 int pcb_point_norms_f32(const float* P, int64_t n, int d, float* pnorm, void* stream);
 int pcb_point_norms_f64(const double* P, int64_t n, int d, double* pnorm, void* stream);

@@ -23,6 +23,8 @@ SIGNATURES = {
     "pcb_abi_version": (I32, []),
     "pcb_error_string": (ctypes.c_char_p, [I32]),
     "pcb_device_info": (I32, [I32, P, P, P]),
+    "pcb_count_nonfinite_f32": (I32, [P, I64, P, P]),
+    "pcb_count_nonfinite_f64": (I32, [P, I64, P, P]),
     "pcb_point_norms_f32": (I32, [P, I64, I32, P, P]),
     "pcb_point_norms_f64": (I32, [P, I64, I32, P, P]),
     "pcb_split_tf32": (I32, [P, I64, I32, I32, P, P, P]),

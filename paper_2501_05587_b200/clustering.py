@@ -120,7 +120,11 @@ def _prepare_points(points, cfg: KKMeansConfig):
             return points, int(points.shape[0]), int(points.shape[1])
     except ImportError:  # pragma: no cover
         pass
-    P = as_float_matrix(points, dtype=normalize_dtype(cfg.dtype), name="points")
+    # Small inputs are scanned for non-finite values on the host; large ones
+    # (> 16M values) on the device right after the copy (same ValueError).
+    A = np.asarray(points)
+    host_check = A.size <= (1 << 24)
+    P = as_float_matrix(points, dtype=normalize_dtype(cfg.dtype), name="points", check_finite=host_check)
     return P, P.shape[0], P.shape[1]
 
 
@@ -140,7 +144,7 @@ def run_lloyd(points, cfg: KKMeansConfig) -> ClusteringResult:
     cfg.validate_for(n)
     labels0 = init_assignments(n, cfg.k, cfg.seed)
     eng = LloydEngine(P, cfg.k, dtype=dtype, device=cfg.device, variant=cfg.variant,
-                      max_iters=cfg.max_iters)
+                      max_iters=cfg.max_iters, check_finite=isinstance(P, np.ndarray) and P.size > (1 << 24))
     if cfg.init is None:
         eng.init_centroids_from_labels(labels0)
     else:

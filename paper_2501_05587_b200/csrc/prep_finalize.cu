@@ -223,3 +223,36 @@ extern "C" int pcb_centroid_norms_f64(const double* C, int k, int d, double* cno
   PCB_CHECK_LAUNCH();
   return 0;
 }
+
+// Input validation on the device (validation.py:45-46 semantics): number of
+// non-finite entries of X, so the driver can raise ValueError without a host
+// pass over n*d values.
+template <typename T>
+__global__ void __launch_bounds__(256)
+count_nonfinite_kernel(const T* __restrict__ X, int64_t count, unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+    c += !isfinite(X[e]);
+  c = pcb::warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+extern "C" int pcb_count_nonfinite_f32(const float* X, int64_t count, unsigned long long* out, void* stream) {
+  if (count < 0 || !X || !out) return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return (int)e;
+  count_nonfinite_kernel<float><<<blocks_for(count, 1024), 256, 0, st>>>(X, count, out);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_count_nonfinite_f64(const double* X, int64_t count, unsigned long long* out, void* stream) {
+  if (count < 0 || !X || !out) return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return (int)e;
+  count_nonfinite_kernel<double><<<blocks_for(count, 1024), 256, 0, st>>>(X, count, out);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}

@@ -37,6 +37,39 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+_STAGING = {}  # device index -> (pinned buffers, events, copy stream)
+_STAGE_CHUNK = 1 << 25  # elements per pinned staging buffer (128 MiB of f32)
+
+
+def h2d_staged(host: np.ndarray, dev: torch.device) -> torch.Tensor:
+    """Host (pageable numpy) -> device copy through two reusable pinned staging
+    buffers on a side stream: the CPU memcpy of chunk i+1 overlaps the DMA of
+    chunk i, and no per-call pinned allocation of the whole array is needed."""
+    src = torch.from_numpy(host)
+    flat = src.view(-1)
+    out = torch.empty(tuple(host.shape), dtype=src.dtype, device=dev)
+    if flat.numel() <= _STAGE_CHUNK:
+        out.copy_(src)
+        return out
+    key = (dev.index, src.dtype)
+    if key not in _STAGING:
+        bufs = [torch.empty(_STAGE_CHUNK, dtype=src.dtype).pin_memory() for _ in range(2)]
+        _STAGING[key] = (bufs, [torch.cuda.Event() for _ in range(2)], torch.cuda.Stream(dev))
+    bufs, evs, cs = _STAGING[key]
+    dflat = out.view(-1)
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    for i, off in enumerate(range(0, flat.numel(), _STAGE_CHUNK)):
+        b = i & 1
+        evs[b].synchronize()            # the DMA that last read this buffer is done
+        m = min(_STAGE_CHUNK, flat.numel() - off)
+        bufs[b][:m].copy_(flat[off:off + m])
+        with torch.cuda.stream(cs):
+            dflat[off:off + m].copy_(bufs[b][:m], non_blocking=True)
+            evs[b].record(cs)
+    torch.cuda.current_stream(dev).wait_stream(cs)
+    return out
+
+
 def require_cuda(device=None) -> torch.device:
     """The CUDA device to run on; RuntimeError if there is none (no CPU fallback)."""
     L.load()
@@ -65,7 +98,9 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
         return variant
     if d <= 32:
         return "rowreg"
-    return "tc3xtf32" if dtype == _F32 else "tiled"
+    if dtype != _F32:
+        return "tiled"
+    return "tc1xtf32s" if k <= SCREEN_KMAX else "tc3xtf32"
 
 
 SCREEN_KMAX = 6144  # assign_screen.cu SC_KMAX
@@ -88,7 +123,8 @@ class LloydEngine:
     """One rank's shard: P (n_local x d) resident in HBM, centroids replicated."""
 
     def __init__(self, points, k: int, *, dtype=np.float32, device=None, variant: str = "auto",
-                 comm=None, n_total: int | None = None, max_iters: int = 30):
+                 comm=None, n_total: int | None = None, max_iters: int = 30,
+                 check_finite: bool = False):
         self.dev = require_cuda(device)
         self.dtype = np.dtype(dtype)
         self.tdtype = torch.float32 if self.dtype == _F32 else torch.float64
@@ -98,9 +134,14 @@ class LloydEngine:
             if isinstance(points, torch.Tensor):
                 P = points.to(device=self.dev, dtype=self.tdtype).contiguous()
             else:
-                host = torch.from_numpy(np.ascontiguousarray(points, dtype=self.dtype))
-                P = host.pin_memory().to(self.dev, non_blocking=True)
+                P = h2d_staged(np.ascontiguousarray(points, dtype=self.dtype), self.dev)
             self.P = P
+            if check_finite:
+                # validation.py:45-46 on the device: ValueError like the reference
+                cnt = torch.zeros(1, dtype=torch.int64, device=self.dev)
+                L.call(f"pcb_count_nonfinite_{self.sfx}", _p(P), P.numel(), _p(cnt), _stream())
+                if int(cnt.item()) != 0:
+                    raise ValueError("points contains non-finite entries")
             self.n, self.d = int(P.shape[0]), int(P.shape[1])
             self.k = int(k)
             assert self.k >= 1

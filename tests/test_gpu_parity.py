@@ -168,3 +168,12 @@ def test_repair_path_device():
     assert ref.repairs.sum() > 0
     np.testing.assert_array_equal(res.repairs, ref.repairs)
     np.testing.assert_array_equal(np.stack(res.label_history), np.stack(ref.label_history))
+
+
+def test_device_side_finiteness_check():
+    """Large inputs are validated on the device after the copy: same ValueError."""
+    import paper_2501_05587_b200 as pcb
+    P = np.zeros((1 << 19, 33), dtype=np.float32)  # > 16M values
+    P[12345, 7] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        pcb.run_lloyd(P, pcb.KKMeansConfig(k=3, max_iters=1))
