@@ -66,36 +66,44 @@ class Comm:
     def barrier(self):
         dist.barrier(group=self.group)
 
-    # -- global empty-cluster repair ------------------------------------------------
-    def repair(self, eng, prev, new) -> None:
-        k, d = eng.k, eng.d
-        kd = k * d
-        counts = eng.acc[kd:kd + k]
-        if eng.state[1].item() != 0:           # stopped: nothing to do
+
+
+def repair_protocol(ops, comm, prev, new) -> None:
+    """Global empty-cluster repair across ranks (clustering.py:111-139).
+
+    Same semantics as the single-rank kernel: passes over the clusters empty at
+    the start of each pass, ascending; donor = unmoved point with the largest
+    own distance, lowest *global* index on ties.  Every rank holds the same
+    all-reduced accumulator, so every rank sees the same empty set; per donor
+    the ranks all-gather their best (own, global index, local position) key,
+    the owner applies the move and publishes a delta record that all ranks
+    commit after an all-reduce.  Only runs (one host read of the counts per
+    iteration) when a cluster is globally empty.
+    """
+    k, d = ops.k, ops.d
+    kd = k * d
+    counts = ops.acc[kd:kd + k]
+    if int(ops.state[1].item()) != 0:           # stopped: nothing to do
+        return
+    if not bool((counts == 0).any().item()):
+        return
+    dev = ops.acc.device
+    key = torch.empty(3, dtype=torch.float64, device=dev)
+    delta = torch.empty(d + 4, dtype=torch.float64, device=dev)
+    while True:
+        empties = torch.nonzero(counts == 0).flatten().tolist()
+        if not empties:
             return
-        if not bool((counts == 0).any().item()):
-            return
-        sfx = eng.sfx
-        key = torch.empty(3, dtype=torch.float64, device=eng.dev)
-        delta = torch.empty(d + 4, dtype=torch.float64, device=eng.dev)
-        while True:
-            empties = torch.nonzero(counts == 0).flatten().tolist()
-            if not empties:
-                return
-            for j in empties:
-                L.call("pcb_argmax_own", _p(eng.own), _p(eng.perm), eng.n, self.offset, _p(key),
-                       _stream())
-                keys = torch.stack(self.all_gather(key)).cpu().numpy()
-                # max own distance, lowest global index on ties (clustering.py:135-137)
-                order = np.lexsort((keys[:, 1], -keys[:, 0]))
-                win = order[0]
-                delta.zero_()
-                if win == self.rank:
-                    L.call(f"pcb_repair_apply_{sfx}", _p(eng.P), d, _p(eng.C), _p(eng.perm), _p(prev),
-                           _p(new), _p(eng.own), int(keys[win, 2]), int(j), _p(delta), _stream())
-                self.all_reduce_sum(delta)
-                L.call("pcb_repair_commit", _p(eng.acc), k, d, int(j), _p(delta), _p(eng.state),
-                       _stream())
+        for j in empties:
+            ops.argmax_own(comm.offset, key)
+            keys = torch.stack(comm.all_gather(key)).cpu().numpy()
+            order = np.lexsort((keys[:, 1], -keys[:, 0]))   # max own, then min global index
+            win = int(order[0])
+            delta.zero_()
+            if win == comm.rank:
+                ops.repair_apply(prev, new, int(keys[win, 2]), int(j), delta)
+            comm.all_reduce_sum(delta)
+            ops.repair_commit(int(j), delta)
 
 
 def run_lloyd_sharded(points_local, cfg: KKMeansConfig, n_total: int, offset: int,

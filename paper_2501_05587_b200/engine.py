@@ -119,7 +119,52 @@ class RunOutput:
     update_seconds: float
 
 
-class LloydEngine:
+class ShardSequence:
+    """The per-rank Lloyd iteration, independent of where the numbers live.
+
+    Subclasses provide the numeric steps (`_assign`, `_sort_and_sum`,
+    `_repair_local`, `_finalize`) and the multi-rank repair primitives
+    (`argmax_own`, `repair_apply`, `repair_commit`); the order of operations,
+    the single all-reduce of the fused accumulator and the global repair
+    protocol live here once, shared by the CUDA engine and the CPU test
+    double used by the gloo tests.
+    Attributes used: labels[2], acc, state, k, d, comm.
+    """
+
+    comm = None
+
+    def iteration(self, t: int, check_convergence: bool = False, tol: float = 0.0,
+                  events=None, raw_out=None) -> None:
+        """One Lloyd iteration t (reads labels[t%2], writes labels[(t+1)%2])."""
+        prev, new = self.labels[t % 2], self.labels[(t + 1) % 2]
+        self.acc.zero_()
+        if events is not None:
+            events[0].record()
+        self._assign(prev, new, self.acc, self.state)           # clustering.py:310-311, 146-149
+        if events is not None:
+            events[1].record()
+        self._sort_and_sum(new, self.state)                     # clustering.py:282-288, 148
+        self._allreduce(self.acc)                               # the one collective per iteration
+        if raw_out is not None:
+            raw_out.copy_(new)
+        self._repair(prev, new)                                 # clustering.py:111-139
+        self._finalize(check_convergence, tol)                  # clustering.py:316-324
+        if events is not None:
+            events[2].record()
+
+    def _allreduce(self, t) -> None:
+        if self.comm is not None and self.comm.world_size > 1:
+            self.comm.all_reduce_sum(t)
+
+    def _repair(self, prev, new) -> None:
+        if self.comm is not None and self.comm.world_size > 1:
+            from .distributed import repair_protocol
+            repair_protocol(self, self.comm, prev, new)
+        else:
+            self._repair_local(prev, new)
+
+
+class LloydEngine(ShardSequence):
     """One rank's shard: P (n_local x d) resident in HBM, centroids replicated."""
 
     def __init__(self, points, k: int, *, dtype=np.float32, device=None, variant: str = "auto",
@@ -242,10 +287,6 @@ class LloydEngine:
                        _p(self.cnorm), _stream())
 
     # -- building blocks ---------------------------------------------------------
-    def _allreduce(self, t) -> None:
-        if self.comm is not None and self.comm.world_size > 1:
-            self.comm.all_reduce_sum(t)
-
     def _sort_and_sum(self, labels, state) -> None:
         counts = self.acc[self.k * self.d:]
         L.call("pcb_sort_by_label", _p(labels), self.n, self.k, _p(counts), _p(self.offsets),
@@ -276,10 +317,7 @@ class LloydEngine:
                _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
                self.vcode, _stream())
 
-    def _repair(self, prev, new) -> None:
-        if self.comm is not None and self.comm.world_size > 1:
-            self.comm.repair(self, prev, new)
-            return
+    def _repair_local(self, prev, new) -> None:
         L.call(f"pcb_repair_{self.sfx}", _p(self.P), self.n, self.d, _p(self.C), self.k, _p(self.perm),
                _p(prev), _p(new), _p(self.own), _p(self.acc), _p(self.state), _p(self.repair_scratch),
                self.repair_scratch_bytes, _stream())
@@ -295,24 +333,17 @@ class LloydEngine:
                    _p(self.cnorm), _p(self.obj_hist), _p(self.rep_hist), _p(self.state),
                    int(check_convergence), float(tol), _stream())
 
-    def iteration(self, t: int, check_convergence: bool = False, tol: float = 0.0,
-                  events=None, raw_out=None) -> None:
-        """Enqueue Lloyd iteration t (reads labels[t%2], writes labels[(t+1)%2])."""
-        prev, new = self.labels[t % 2], self.labels[(t + 1) % 2]
-        self.acc.zero_()
-        if events is not None:
-            events[0].record()
-        self._assign(prev, new, self.acc, self.state)
-        if events is not None:
-            events[1].record()
-        self._sort_and_sum(new, self.state)
-        self._allreduce(self.acc)
-        if raw_out is not None:
-            raw_out.copy_(new)
-        self._repair(prev, new)
-        self._finalize(check_convergence, tol)
-        if events is not None:
-            events[2].record()
+    # -- multi-rank repair primitives (distributed.repair_protocol) ---------------
+    def argmax_own(self, offset: int, key_out) -> None:
+        L.call("pcb_argmax_own", _p(self.own), _p(self.perm), self.n, offset, _p(key_out), _stream())
+
+    def repair_apply(self, prev, new, pos: int, j: int, delta) -> None:
+        L.call(f"pcb_repair_apply_{self.sfx}", _p(self.P), self.d, _p(self.C), _p(self.perm), _p(prev),
+               _p(new), _p(self.own), int(pos), int(j), _p(delta), _stream())
+
+    def repair_commit(self, j: int, delta) -> None:
+        L.call("pcb_repair_commit", _p(self.acc), self.k, self.d, int(j), _p(delta), _p(self.state),
+               _stream())
 
     # -- whole fit -----------------------------------------------------------------
     def run(self, max_iters: int, tol: float = 0.0, check_convergence: bool = False,
