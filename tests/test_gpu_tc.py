@@ -169,3 +169,34 @@ def test_screen_full_run_matches_reference():
     ref = oracle.run_lloyd(P, 64, max_iters=8)
     np.testing.assert_allclose(a.objective_history, ref.objective_history, rtol=1e-6)
     np.testing.assert_array_equal(a.labels, ref.labels)
+
+
+# ---------------------------------------------------------------------------
+# delta-chunked P.C.P^T ablation
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,d,k", [(500, 2, 7), (1000, 16, 40), (1500, 100, 33), (600, 784, 20)])
+def test_delta_chunked_lockstep(n, d, k):
+    from paper_2501_05587_b200.engine import LloydEngine
+    P = oracle.make_blobs(n, d, k, seed=d)
+    lab = oracle.init_assignments(n, k, 2)
+    C = oracle.mean_centroids(P, lab, k)
+    eng = LloydEngine(P, k, variant="delta", max_iters=1)
+    pn = oracle.point_norms(P)
+    for t in range(3):
+        ref = oracle.lloyd_step(P, pn, C, lab, k)
+        gpu = eng.step_from(C, lab)
+        check_step(P, C, lab, k, gpu, ref=ref, what=f"delta n={n} d={d} k={k} it{t}")
+        C, lab = ref.centroids, ref.labels
+
+
+def test_delta_chunked_worked_examples():
+    """The attachment's worked values via the chunked kernel (analysis.py oracle)."""
+    from paper_2501_05587_b200.engine import LloydEngine
+    for p, c, want in (([3.0], [7.0], 16.0), ([1.0], [7.0], 36.0), ([5.0, 2.0], [1.0, 4.0], 20.0),
+                       ([4.0, 3.0, 2.0], [5.0, 2.0, 3.0], 3.0)):
+        P = np.array([p], dtype=np.float32)
+        eng = LloydEngine(P, 1, variant="delta", max_iters=1)
+        eng.set_centroids(np.array([c], dtype=np.float32))
+        out = eng.step_from(np.array([c], dtype=np.float32), np.zeros(1, dtype=np.int32))
+        assert out["mind"][0] == pytest.approx(want, abs=1e-5)
+        assert out["mind"][0] == pytest.approx(oracle.augmented_distance(p, c), abs=1e-5)
