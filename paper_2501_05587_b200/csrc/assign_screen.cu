@@ -22,8 +22,11 @@
 // their count is data dependent (~14 % right after a random-label init, ~3 %
 // near convergence on the c3 blobs).
 //
-// Epilogue cost per accumulator element: 1 FFMA + 1 LOP3 + 2.5 FMNMX (pairs,
-// 3-input min), which keeps the ALU pipe just under the TF32 MMA rate at d=128.
+// Epilogue per accumulator element: the running min with its index uses
+// 1 LOP3 + 0.5 FMNMX3 on the ALU pipe; the ambiguity test counts keys within
+// 2E of the running min with saturating FFMAs (1 FFMA.SAT + 1 FADD on the FMA
+// pipe), which is equivalent to the top-2 test (see the update rule in the
+// chunk loop) at less than half the ALU work.
 #include <cudaTypedefs.h>
 
 #include "pcb_common.cuh"
@@ -186,7 +189,23 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
     uint32_t aphase = 0;
     int tile_it = 0;
     for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
-      float R1 = 3.4e38f, R2 = 3.4e38f;
+      const int64_t row = mt * SC_BM + r_in_tile;
+      // rigorous per-row bound on |key_j - OFF - s_j| (see header), rounded up
+      float twoE = 0.0f;
+      {
+        const int64_t rr = row < n ? row : n - 1;
+        const float an = anorm[rr], dan = danorm[rr];
+        const float gerr = dan * Bmax + an * dBmax + dan * dBmax + acc_rel * an * Bmax;
+        const float cbn = Bmax + dBmax;
+        const float kmax = OFF + 2.0f * (an + dan) * cbn + cbn * cbn;
+        twoE = 2.0f * 1.0001f * (2.0f * gerr + 0x1p-16f * kmax);
+      }
+      // counting scale: a key at least twoE/64 below the threshold counts 1
+      const float big = 64.0f / twoE;
+      // Running state: R1 = smallest packed key so far (index r1), cnt = number
+      // of keys <= R1 + twoE (+margin), counted with saturating FFMAs on the
+      // FMA pipe so the ALU pipe only carries the min (FMNMX3) and packing.
+      float R1 = 3.4e38f, cnt = 0.0f;
       int r1 = 0;
       for (int nt = 0; nt < ntiles; ++nt) {
         ptx::mbar_wait(&tfull[abuf], aphase);
@@ -197,57 +216,39 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
           float v[32];
           ptx::tmem_ld_32x32b_x32(taddr + cb, v);
           const float4* cp4 = reinterpret_cast<const float4*>(cprime + nt * BN + cb);
-          // four independent top-2 chains (column pairs mod 4) for ILP
-          float S1a = 3.4e38f, S2a = 3.4e38f, S1b = 3.4e38f, S2b = 3.4e38f;
-          float S1c = 3.4e38f, S2c = 3.4e38f, S1d = 3.4e38f, S2d = 3.4e38f;
+          float ma = 3.4e38f, mb = 3.4e38f;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 c4 = cp4[2 * q];
-            const float4 c5 = cp4[2 * q + 1];
-            const int b0 = 8 * q;
-            const float k0 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 0], c4.x)) & 0xFFFFFFE0u) | cid[b0 + 0]);
-            const float k1 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 1], c4.y)) & 0xFFFFFFE0u) | cid[b0 + 1]);
-            const float k2 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 2], c4.z)) & 0xFFFFFFE0u) | cid[b0 + 2]);
-            const float k3 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 3], c4.w)) & 0xFFFFFFE0u) | cid[b0 + 3]);
-            const float k4 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 4], c5.x)) & 0xFFFFFFE0u) | cid[b0 + 4]);
-            const float k5 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 5], c5.y)) & 0xFFFFFFE0u) | cid[b0 + 5]);
-            const float k6 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 6], c5.z)) & 0xFFFFFFE0u) | cid[b0 + 6]);
-            const float k7 = __uint_as_float((__float_as_uint(fmaf(-2.0f, v[b0 + 7], c5.w)) & 0xFFFFFFE0u) | cid[b0 + 7]);
-            float lo = fminf(k0, k1), hi = fmaxf(k0, k1);
-            S2a = fmin3(S2a, hi, fmaxf(S1a, lo));
-            S1a = fminf(S1a, lo);
-            lo = fminf(k2, k3);
-            hi = fmaxf(k2, k3);
-            S2b = fmin3(S2b, hi, fmaxf(S1b, lo));
-            S1b = fminf(S1b, lo);
-            lo = fminf(k4, k5);
-            hi = fmaxf(k4, k5);
-            S2c = fmin3(S2c, hi, fmaxf(S1c, lo));
-            S1c = fminf(S1c, lo);
-            lo = fminf(k6, k7);
-            hi = fmaxf(k6, k7);
-            S2d = fmin3(S2d, hi, fmaxf(S1d, lo));
-            S1d = fminf(S1d, lo);
+          for (int q = 0; q < 8; ++q) {
+            const float4 c4 = cp4[q];
+            v[4 * q + 0] = fmaf(-2.0f, v[4 * q + 0], c4.x);
+            v[4 * q + 1] = fmaf(-2.0f, v[4 * q + 1], c4.y);
+            v[4 * q + 2] = fmaf(-2.0f, v[4 * q + 2], c4.z);
+            v[4 * q + 3] = fmaf(-2.0f, v[4 * q + 3], c4.w);
+            const float k0 = __uint_as_float((__float_as_uint(v[4 * q + 0]) & 0xFFFFFFE0u) | cid[4 * q + 0]);
+            const float k1 = __uint_as_float((__float_as_uint(v[4 * q + 1]) & 0xFFFFFFE0u) | cid[4 * q + 1]);
+            const float k2 = __uint_as_float((__float_as_uint(v[4 * q + 2]) & 0xFFFFFFE0u) | cid[4 * q + 2]);
+            const float k3 = __uint_as_float((__float_as_uint(v[4 * q + 3]) & 0xFFFFFFE0u) | cid[4 * q + 3]);
+            ma = fmin3(ma, k0, k1);
+            mb = fmin3(mb, k2, k3);
           }
-          // merge the four chains: top-2 of {(S1a,S2a),(S1b,S2b),(S1c,S2c),(S1d,S2d)}
-          const float m_ab = fminf(S1a, S1b), M_ab = fmaxf(S1a, S1b);
-          const float m_cd = fminf(S1c, S1d), M_cd = fmaxf(S1c, S1d);
-          S2a = fmin3(M_ab, S2a, S2b);
-          S2c = fmin3(M_cd, S2c, S2d);
-          S1a = m_ab;
-          S1c = m_cd;
-          S1b = S1c;
-          S2b = S2c;
-          const float S1 = fminf(S1a, S1b);
-          const float S2 = fmin3(S2a, S2b, fmaxf(S1a, S1b));
-          // merge the chunk into the running top-2 (earlier chunks win ties)
-          if (S1 < R1) {
-            R2 = fminf(R1, S2);
-            R1 = S1;
-            r1 = nt * BN + cb + (int)(__float_as_uint(S1) & 31u);
-          } else {
-            R2 = fminf(R2, S1);
+          const float m = fminf(ma, mb);
+          // (a) much better min: every earlier counted key is above the new
+          //     threshold; (b) slightly better: the old min itself stays within
+          //     it, so the row is ambiguous whatever the over-count
+          if (m < R1 - twoE) cnt = 0.0f;
+          if (m < R1) {
+            R1 = m;
+            r1 = nt * BN + cb + (int)(__float_as_uint(m) & 31u);
           }
+          const float thr = R1 + twoE + 0x1p-16f * fabsf(R1);
+          const float thr_big = thr * big;
+          float c0 = 0.0f, c1 = 0.0f;
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            c0 += __saturatef(fmaf(v[i], -big, thr_big));
+            c1 += __saturatef(fmaf(v[i + 1], -big, thr_big));
+          }
+          cnt += c0 + c1;
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[abuf]);
@@ -264,37 +265,36 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
       if (h == 1) {
         if (tile_it >= 2) ptx::mbar_wait(&xreleased[g * 2 + sidx], (use - 1u) & 1u);
         slot[r_in_tile * 3 + 0] = R1;
-        slot[r_in_tile * 3 + 1] = R2;
+        slot[r_in_tile * 3 + 1] = cnt;
         slot[r_in_tile * 3 + 2] = __int_as_float(r1);
         ptx::mbar_arrive(&xwritten[g * 2 + sidx]);
       } else {
         ptx::mbar_wait(&xwritten[g * 2 + sidx], use & 1u);
-        const float oR1 = slot[r_in_tile * 3 + 0], oR2 = slot[r_in_tile * 3 + 1];
+        const float oR1 = slot[r_in_tile * 3 + 0], ocnt = slot[r_in_tile * 3 + 1];
         const int or1 = __float_as_int(slot[r_in_tile * 3 + 2]);
         ptx::mbar_arrive(&xreleased[g * 2 + sidx]);
-        // min over the packed keys; exact-value ties across halves make the row
-        // ambiguous (R2 == R1) and are resolved by the fallback
-        const bool take = (oR1 < R1) || (oR1 == R1 && or1 < r1);
-        R2 = fminf(fmaxf(R1, oR1), fminf(R2, oR2));
-        if (take) { R1 = oR1; r1 = or1; }
-        const int64_t row = mt * SC_BM + r_in_tile;
-        bool amb = false;
-        if (row < n) {
-          labels[row] = r1;
-          const float an = anorm[row], dan = danorm[row];
-          // rigorous per-row bound on |key_j - OFF - s_j| (see header), rounded up
-          const float gerr = dan * Bmax + an * dBmax + dan * dBmax + acc_rel * an * Bmax;
-          const float cbn = Bmax + dBmax;
-          const float kmax = OFF + 2.0f * (an + dan) * cbn + cbn * cbn;
-          const float E = 1.0001f * (2.0f * gerr + 0x1p-16f * kmax);
-          amb = !(R2 > R1 + 2.0f * E);
+        // each half certified its own candidates relative to its own min; the
+        // row is unambiguous iff one half's min undercuts the other's by > 2E
+        // and that half alone has a single candidate
+        bool amb;
+        if (oR1 < R1 - twoE) {
+          amb = ocnt > 1.0f;
+          R1 = oR1;
+          r1 = or1;
+        } else if (R1 < oR1 - twoE) {
+          amb = cnt > 1.0f;
+        } else {
+          amb = true;
+          if (oR1 < R1 || (oR1 == R1 && or1 < r1)) { R1 = oR1; r1 = or1; }
         }
-        const unsigned m = __ballot_sync(0xffffffffu, amb);
-        if (m) {
+        if (row < n) labels[row] = r1;
+        amb = amb && row < n;
+        const unsigned msk = __ballot_sync(0xffffffffu, amb);
+        if (msk) {
           int base = 0;
-          if (lane == 0) base = atomicAdd(amb_count, __popc(m));
+          if (lane == 0) base = atomicAdd(amb_count, __popc(msk));
           base = __shfl_sync(0xffffffffu, base, 0);
-          if (amb) amb_list[base + __popc(m & ((1u << lane) - 1u))] = (int)row;
+          if (amb) amb_list[base + __popc(msk & ((1u << lane) - 1u))] = (int)row;
         }
       }
       ++tile_it;
