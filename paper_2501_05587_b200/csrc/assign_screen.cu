@@ -28,17 +28,17 @@
 // pipe), which is equivalent to the top-2 test (see the update rule in the
 // chunk loop) at less than half the ALU work.
 #include <cudaTypedefs.h>
+#include <cstdlib>
 
 #include "pcb_common.cuh"
 #include "pcb_launch.cuh"
 #include "tc_ptx.cuh"
+#include "screen_common.cuh"
 
 namespace pcb {
 
 constexpr int SC_BM = 128;
-constexpr int SC_BK = 32;
 constexpr int SC_THREADS = 384;  // warps 0-3 control, 4-11 epilogue (2 per TMEM lane group)
-constexpr int SC_KMAX = 6144;  // smem copy of the shifted centroid norms (k <= 6144)
 
 template <int BN>
 struct ScCfg {
@@ -51,20 +51,6 @@ struct ScCfg {
   static constexpr uint32_t kSmem = 1024 + kStages * kStageBytes + kBarBytes + SC_KMAX * 4;
   static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
-
-// chunk-local column ids; held in registers so (key & ~31) | id is a single LOP3
-__constant__ uint32_t kChunkIds[32] = {0,  1,  2,  3,  4,  5,  6,  7,  8,  9,  10, 11, 12, 13, 14, 15,
-                                       16, 17, 18, 19, 20, 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31};
-
-__device__ __forceinline__ float fmin3(float a, float b, float c) {
-  float r;
-  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-
-__device__ __forceinline__ float pack_idx(float key, uint32_t i) {
-  return __uint_as_float((__float_as_uint(key) & 0xFFFFFFE0u) | i);
-}
 
 // bstat layout (f32): [0] max_j |c~_j|, [1] max_j |dc_j|, [2] OFF, [3] spare
 template <int BN>
@@ -420,26 +406,6 @@ count_labels_kernel(const int32_t* __restrict__ labels, const int32_t* __restric
     if (hist[j]) atomicAdd(&acc[L.counts() + j], (double)hist[j]);
 }
 
-static int make_tmap_rows(CUtensorMap* m, const float* base, int64_t rows, int cols, int box_rows) {
-  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-  if (enc == nullptr) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return PCB_ENODEV;
-    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
-  cuuint32_t box[2] = {(cuuint32_t)SC_BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 0 : PCB_EINVAL;
-}
-
 template <int BN>
 static int launch_screen(const float* P, int64_t n, int ld, const float* C, int k, const float* an,
                          const float* dan, const float* cnorm, const float* bstat, int32_t* labels,
@@ -501,6 +467,10 @@ extern "C" int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const 
   if (n > INT32_MAX) return PCB_EUNSUP;
   if (k > SC_KMAX) return PCB_EUNSUP;
   cudaStream_t st = (cudaStream_t)stream;
+  // d <= 128: keep 256 points resident per CTA (assign_screen_res.cu)
+  if (ld <= 4 * SC_BK && getenv("PCB_SCREEN_STREAM") == nullptr)
+    return assign_screen_resident(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count,
+                                  state, st);
   if (k > 128)
     return launch_screen<256>(P_r, n, ld, C_r, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state,
                               st);

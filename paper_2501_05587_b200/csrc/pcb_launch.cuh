@@ -27,4 +27,8 @@ int assign_tc3xtf32_devcount(const float* phi, const float* plo, int ld, const f
                              int d, const float* chi, const float* clo, const float* cnorm, int k,
                              int32_t* lab, const int* n_dev, const long long* state, cudaStream_t st);
 
+int assign_screen_resident(const float* P_r, int64_t n, int ld, const float* C_r, int k, const float* cnorm,
+                           const float* anorm, const float* danorm, const float* bstat, int32_t* labels,
+                           int* amb_list, int* amb_count, const long long* state, cudaStream_t st);
+
 }  // namespace pcb
