@@ -105,7 +105,6 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
   const int64_t mtiles = (n + SC_BM - 1) / SC_BM;
 
   if (warp == 0) {
-    if (lane == 0) {
       const uint64_t pol_a = ptx::policy_evict_first();
       const uint64_t pol_b = ptx::policy_evict_last();
       int stage = 0;
@@ -117,16 +116,18 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
           for (int kc = 0; kc < num_kc; ++kc) {
             ptx::mbar_wait(&empty[stage], phase ^ 1u);
             uint8_t* st = smem + stage * Cfg::kStageBytes;
-            ptx::mbar_expect_tx(&full[stage], Cfg::kStageBytes);
-            ptx::tma_load_2d(&tm_a, &full[stage], st, kc * SC_BK, y_a, pa);
-            ptx::tma_load_2d(&tm_b, &full[stage], st + Cfg::kABytes, kc * SC_BK, nt * BN, pol_b);
+            if (ptx::elect_one()) {
+              ptx::mbar_expect_tx(&full[stage], Cfg::kStageBytes);
+              ptx::tma_load_2d(&tm_a, &full[stage], st, kc * SC_BK, y_a, pa);
+              ptx::tma_load_2d(&tm_b, &full[stage], st + Cfg::kABytes, kc * SC_BK, nt * BN, pol_b);
+            }
+            __syncwarp();
             if (++stage == Cfg::kStages) { stage = 0; phase ^= 1u; }
           }
         }
       }
-    }
+    
   } else if (warp == 1) {
-    if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_tf32<SC_BM, BN>();
       int stage = 0;
       uint32_t phase = 0;
@@ -143,20 +144,24 @@ assign_screen_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
             const uint32_t base = ptx::smem_u32(smem + stage * Cfg::kStageBytes);
             const uint64_t ad = ptx::sdesc_k_sw128(base);
             const uint64_t bd = ptx::sdesc_k_sw128(base + Cfg::kABytes);
+if (ptx::elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < SC_BK / 8; ++ks) {
-              const uint64_t off = (uint64_t)(ks * 8 * 4) >> 4;
-              ptx::umma_tf32(dt, ad + off, bd + off, idesc, (kc | ks) != 0);
+              for (int ks = 0; ks < SC_BK / 8; ++ks) {
+                const uint64_t off = (uint64_t)(ks * 8 * 4) >> 4;
+                ptx::umma_tf32(dt, ad + off, bd + off, idesc, (kc | ks) != 0);
+              }
+              ptx::umma_commit(&empty[stage]);
             }
-            ptx::umma_commit(&empty[stage]);
+            __syncwarp();
             if (++stage == Cfg::kStages) { stage = 0; phase ^= 1u; }
           }
-          ptx::umma_commit(&tfull[abuf]);
+          if (ptx::elect_one()) ptx::umma_commit(&tfull[abuf]);
+          __syncwarp();
           abuf ^= 1;
           if (abuf == 0) aphase ^= 1u;
         }
       }
-    }
+    
   } else if (warp >= 4) {
     // Epilogue: warp w reads TMEM lane group (w % 4); the two warps of a group
     // (half h = 0/1) take alternating 32-column chunks and merge per row tile.

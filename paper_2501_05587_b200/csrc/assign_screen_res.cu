@@ -95,58 +95,60 @@ assign_screen_res_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_
   const int64_t npairs = (n + 255) / 256;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- A producer: both row tiles, chunk by chunk ----------------
-      const uint64_t pol = ptx::policy_evict_first();
-      int it = 0;
-      for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
-        for (int c = 0; c < NKC; ++c) {
-          if (it > 0) ptx::mbar_wait(&aempty[c], (uint32_t)((it - 1) & 1));
+    // ---------------- A producer: both row tiles, chunk by chunk ----------------
+    const uint64_t pol = ptx::policy_evict_first();
+    int it = 0;
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
+      for (int c = 0; c < NKC; ++c) {
+        if (it > 0) ptx::mbar_wait(&aempty[c], (uint32_t)((it - 1) & 1));
+        if (ptx::elect_one()) {
           ptx::mbar_expect_tx(&afull[c], 2 * Cfg::kTileBytes);
           ptx::tma_load_2d(&tm_a, &afull[c], sA + (0 * NKC + c) * Cfg::kTileBytes, c * SC_BK, (int)(pr * 256), pol);
           ptx::tma_load_2d(&tm_a, &afull[c], sA + (1 * NKC + c) * Cfg::kTileBytes, c * SC_BK,
                            (int)(pr * 256 + 128), pol);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 3) {
-    if (lane == 0) {
-      // ---------------- B producer: centroid chunks through the ring ----------------
-      const uint64_t pol = ptx::policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
-        for (int nt = 0; nt < ntiles; ++nt) {
-          for (int c = 0; c < NKC; ++c) {
-            ptx::mbar_wait(&empty[stage], phase ^ 1u);
+    // ---------------- B producer: centroid chunks through the ring ----------------
+    const uint64_t pol = ptx::policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+      for (int nt = 0; nt < ntiles; ++nt) {
+        for (int c = 0; c < NKC; ++c) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1u);
+          if (ptx::elect_one()) {
             ptx::mbar_expect_tx(&full[stage], Cfg::kBBytes);
             ptx::tma_load_2d(&tm_b, &full[stage], sB + stage * Cfg::kBBytes, c * SC_BK, nt * SR_BN, pol);
-            if (++stage == SR_STAGES) { stage = 0; phase ^= 1u; }
           }
+          __syncwarp();
+          if (++stage == SR_STAGES) { stage = 0; phase ^= 1u; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = ptx::idesc_tf32<128, SR_BN>();
-      int stage = 0;
-      uint32_t phase = 0;
-      int abuf = 0;
-      uint32_t aphase = 0;
-      int it = 0;
-      for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
-        for (int nt = 0; nt < ntiles; ++nt) {
-          ptx::mbar_wait(&tempty[abuf], aphase ^ 1u);
+    // ---------------- MMA issuer (warp-uniform loop, one elected lane issues) ----------------
+    constexpr uint32_t idesc = ptx::idesc_tf32<128, SR_BN>();
+    int stage = 0;
+    uint32_t phase = 0;
+    int abuf = 0;
+    uint32_t aphase = 0;
+    int it = 0;
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
+      for (int nt = 0; nt < ntiles; ++nt) {
+        ptx::mbar_wait(&tempty[abuf], aphase ^ 1u);
+        ptx::tc_fence_after();
+        const uint32_t d0 = tmem + (uint32_t)(abuf * 256);
+        for (int c = 0; c < NKC; ++c) {
+          if (nt == 0) ptx::mbar_wait(&afull[c], (uint32_t)(it & 1));
+          ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t d0 = tmem + (uint32_t)(abuf * 256);
-          for (int c = 0; c < NKC; ++c) {
-            if (nt == 0) ptx::mbar_wait(&afull[c], (uint32_t)(it & 1));
-            ptx::mbar_wait(&full[stage], phase);
-            ptx::tc_fence_after();
-            const uint64_t a0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (0 * NKC + c) * Cfg::kTileBytes));
-            const uint64_t a1 = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (1 * NKC + c) * Cfg::kTileBytes));
-            const uint64_t bd = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * Cfg::kBBytes));
+          const uint64_t a0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (0 * NKC + c) * Cfg::kTileBytes));
+          const uint64_t a1 = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (1 * NKC + c) * Cfg::kTileBytes));
+          const uint64_t bd = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * Cfg::kBBytes));
+          if (ptx::elect_one()) {
 #pragma unroll
             for (int ks = 0; ks < SC_BK / 8; ++ks) {
               const uint64_t off = (uint64_t)(ks * 8 * 4) >> 4;
@@ -155,12 +157,14 @@ assign_screen_res_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_
             }
             ptx::umma_commit(&empty[stage]);
             if (nt + 1 == ntiles) ptx::umma_commit(&aempty[c]);  // A chunk free for the next pair
-            if (++stage == SR_STAGES) { stage = 0; phase ^= 1u; }
           }
-          ptx::umma_commit(&tfull[abuf]);
-          abuf ^= 1;
-          if (abuf == 0) aphase ^= 1u;
+          __syncwarp();
+          if (++stage == SR_STAGES) { stage = 0; phase ^= 1u; }
         }
+        if (ptx::elect_one()) ptx::umma_commit(&tfull[abuf]);
+        __syncwarp();
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1u;
       }
     }
   } else if (warp >= 4) {

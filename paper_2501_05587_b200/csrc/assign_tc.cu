@@ -104,7 +104,6 @@ assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_
   const int ntiles = (k + BN - 1) / BN;
 
   if (warp == 0) {
-    if (lane == 0) {
       // ---------------- TMA producer ----------------
       const uint64_t pol_a = ptx::policy_evict_first();
       const uint64_t pol_b = ptx::policy_evict_last();
@@ -116,20 +115,22 @@ assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_
           for (int kc = 0; kc < num_kc; ++kc) {
             ptx::mbar_wait(&empty[stage], phase ^ 1u);
             uint8_t* st = smem + stage * Cfg::kStageBytes;
-            ptx::mbar_expect_tx(&full[stage], Cfg::kStageBytes);
             const uint64_t pa = (nt + 1 == ntiles) ? pol_a : pol_b;  // A re-read per centroid tile
-            ptx::tma_load_2d(&tm_ahi, &full[stage], st, kc * TC_BK, y_a, pa);
-            ptx::tma_load_2d(&tm_alo, &full[stage], st + Cfg::kABytes, kc * TC_BK, y_a, pa);
-            ptx::tma_load_2d(&tm_bhi, &full[stage], st + 2 * Cfg::kABytes, kc * TC_BK, nt * BN, pol_b);
-            ptx::tma_load_2d(&tm_blo, &full[stage], st + 2 * Cfg::kABytes + Cfg::kBBytes, kc * TC_BK,
-                             nt * BN, pol_b);
+            if (ptx::elect_one()) {
+              ptx::mbar_expect_tx(&full[stage], Cfg::kStageBytes);
+              ptx::tma_load_2d(&tm_ahi, &full[stage], st, kc * TC_BK, y_a, pa);
+              ptx::tma_load_2d(&tm_alo, &full[stage], st + Cfg::kABytes, kc * TC_BK, y_a, pa);
+              ptx::tma_load_2d(&tm_bhi, &full[stage], st + 2 * Cfg::kABytes, kc * TC_BK, nt * BN, pol_b);
+              ptx::tma_load_2d(&tm_blo, &full[stage], st + 2 * Cfg::kABytes + Cfg::kBBytes, kc * TC_BK,
+                               nt * BN, pol_b);
+            }
+            __syncwarp();
             if (++stage == Cfg::kStages) { stage = 0; phase ^= 1u; }
           }
         }
       }
-    }
+    
   } else if (warp == 1) {
-    if (lane == 0) {
       // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc = ptx::idesc_tf32<TC_BM, BN>();
       int stage = 0;
@@ -149,22 +150,26 @@ assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_
             const uint64_t alo = ptx::sdesc_k_sw128(base + Cfg::kABytes);
             const uint64_t bhi = ptx::sdesc_k_sw128(base + 2 * Cfg::kABytes);
             const uint64_t blo = ptx::sdesc_k_sw128(base + 2 * Cfg::kABytes + Cfg::kBBytes);
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < TC_BK / 8; ++ks) {
-              const uint64_t off = (uint64_t)(ks * 8 * 4) >> 4;  // 32 bytes per K=8 step
-              ptx::umma_tf32(dt, ahi + off, bhi + off, idesc, (kc | ks) != 0);
-              ptx::umma_tf32(dt, ahi + off, blo + off, idesc, 1u);
-              ptx::umma_tf32(dt, alo + off, bhi + off, idesc, 1u);
+              for (int ks = 0; ks < TC_BK / 8; ++ks) {
+                const uint64_t off = (uint64_t)(ks * 8 * 4) >> 4;  // 32 bytes per K=8 step
+                ptx::umma_tf32(dt, ahi + off, bhi + off, idesc, (kc | ks) != 0);
+                ptx::umma_tf32(dt, ahi + off, blo + off, idesc, 1u);
+                ptx::umma_tf32(dt, alo + off, bhi + off, idesc, 1u);
+              }
+              ptx::umma_commit(&empty[stage]);
             }
-            ptx::umma_commit(&empty[stage]);
+            __syncwarp();
             if (++stage == Cfg::kStages) { stage = 0; phase ^= 1u; }
           }
-          ptx::umma_commit(&tfull[abuf]);
+          if (ptx::elect_one()) ptx::umma_commit(&tfull[abuf]);
+          __syncwarp();
           abuf ^= 1;
           if (abuf == 0) aphase ^= 1u;
         }
       }
-    }
+    
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
     const int ew = warp - 4;  // TMEM lane group ew*32 .. ew*32+31
