@@ -29,6 +29,7 @@
 // chunk loop) at less than half the ALU work.
 #include <cudaTypedefs.h>
 #include <cstdlib>
+#include <cstring>
 
 #include "pcb_common.cuh"
 #include "pcb_launch.cuh"
@@ -472,10 +473,19 @@ extern "C" int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const 
   if (n > INT32_MAX) return PCB_EUNSUP;
   if (k > SC_KMAX) return PCB_EUNSUP;
   cudaStream_t st = (cudaStream_t)stream;
-  // d <= 128: keep 256 points resident per CTA (assign_screen_res.cu)
-  if (ld <= 4 * SC_BK && getenv("PCB_SCREEN_STREAM") == nullptr)
-    return assign_screen_resident(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count,
-                                  state, st);
+  // d <= 128: A-resident kernels; PCB_SCREEN_IMPL = pair (default: CTA pairs,
+  // cta_group::2, assign_screen_2sm.cu) | res (one SM, assign_screen_res.cu) |
+  // stream (this file's kernel)
+  const char* impl = getenv("PCB_SCREEN_IMPL");
+  const bool want_stream = impl != nullptr && strcmp(impl, "stream") == 0;
+  const bool want_res = impl != nullptr && strcmp(impl, "res") == 0;
+  if (ld <= 4 * SC_BK && !want_stream) {
+    if (want_res)
+      return assign_screen_resident(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count,
+                                    state, st);
+    return assign_screen_pair(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count, state,
+                              st);
+  }
   if (k > 128)
     return launch_screen<256>(P_r, n, ld, C_r, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state,
                               st);

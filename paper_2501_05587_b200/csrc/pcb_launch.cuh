@@ -31,4 +31,8 @@ int assign_screen_resident(const float* P_r, int64_t n, int ld, const float* C_r
                            const float* anorm, const float* danorm, const float* bstat, int32_t* labels,
                            int* amb_list, int* amb_count, const long long* state, cudaStream_t st);
 
+int assign_screen_pair(const float* P_r, int64_t n, int ld, const float* C_r, int k, const float* cnorm,
+                       const float* anorm, const float* danorm, const float* bstat, int32_t* labels, int* amb_list,
+                       int* amb_count, const long long* state, cudaStream_t st);
+
 }  // namespace pcb

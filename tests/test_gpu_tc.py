@@ -110,11 +110,13 @@ def test_tc_full_run_matches_ffma_run():
 # ---------------------------------------------------------------------------
 # certified 1xTF32 screening (variant tc1xtf32s)
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("impl", ["pair", "res", "stream"])
 @pytest.mark.parametrize("n,d,k", [(1000, 40, 17), (777, 100, 300), (4096, 64, 64), (300, 32, 1),
                                    (5000, 128, 1024), (2000, 784, 256), (1500, 96, 129), (5000, 64, 4096),
                                    (20000, 128, 1024)])
-def test_screen_lockstep_ragged_shapes(n, d, k):
+def test_screen_lockstep_ragged_shapes(n, d, k, impl, monkeypatch):
     from paper_2501_05587_b200.engine import LloydEngine
+    monkeypatch.setenv("PCB_SCREEN_IMPL", impl)
     P = oracle.make_blobs(n, d, max(k, 1), seed=n + d)
     lab = oracle.init_assignments(n, k, 1)
     C = oracle.mean_centroids(P, lab, k)
