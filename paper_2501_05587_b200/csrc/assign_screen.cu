@@ -173,10 +173,7 @@ if (ptx::elect_one()) {
     // TC accumulation: per K=8 MMA <= 9 terms aligned/truncated at 2^-23 of the
     // largest partial (|partial| <= sum |a~_t c~_t| <= |a~||c~|)
     const float acc_rel = (float)(num_kc * 4 + 2) * 9.0f * 0x1p-23f;
-    // chunk-local column ids held in registers so (key & ~31) | id is one LOP3
-    uint32_t cid[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) cid[i] = kChunkIds[i];
+    const uint32_t msk = kIdxMask;
     int abuf = 0;
     uint32_t aphase = 0;
     int tile_it = 0;
@@ -207,40 +204,7 @@ if (ptx::elect_one()) {
         for (int cb = h * 32; cb < BN; cb += 64) {
           float v[32];
           ptx::tmem_ld_32x32b_x32(taddr + cb, v);
-          const float4* cp4 = reinterpret_cast<const float4*>(cprime + nt * BN + cb);
-          float ma = 3.4e38f, mb = 3.4e38f;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 c4 = cp4[q];
-            v[4 * q + 0] = fmaf(-2.0f, v[4 * q + 0], c4.x);
-            v[4 * q + 1] = fmaf(-2.0f, v[4 * q + 1], c4.y);
-            v[4 * q + 2] = fmaf(-2.0f, v[4 * q + 2], c4.z);
-            v[4 * q + 3] = fmaf(-2.0f, v[4 * q + 3], c4.w);
-            const float k0 = __uint_as_float((__float_as_uint(v[4 * q + 0]) & 0xFFFFFFE0u) | cid[4 * q + 0]);
-            const float k1 = __uint_as_float((__float_as_uint(v[4 * q + 1]) & 0xFFFFFFE0u) | cid[4 * q + 1]);
-            const float k2 = __uint_as_float((__float_as_uint(v[4 * q + 2]) & 0xFFFFFFE0u) | cid[4 * q + 2]);
-            const float k3 = __uint_as_float((__float_as_uint(v[4 * q + 3]) & 0xFFFFFFE0u) | cid[4 * q + 3]);
-            ma = fmin3(ma, k0, k1);
-            mb = fmin3(mb, k2, k3);
-          }
-          const float m = fminf(ma, mb);
-          // (a) much better min: every earlier counted key is above the new
-          //     threshold; (b) slightly better: the old min itself stays within
-          //     it, so the row is ambiguous whatever the over-count
-          if (m < R1 - twoE) cnt = 0.0f;
-          if (m < R1) {
-            R1 = m;
-            r1 = nt * BN + cb + (int)(__float_as_uint(m) & 31u);
-          }
-          const float thr = R1 + twoE + 0x1p-16f * fabsf(R1);
-          const float thr_big = thr * big;
-          float c0 = 0.0f, c1 = 0.0f;
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            c0 += __saturatef(fmaf(v[i], -big, thr_big));
-            c1 += __saturatef(fmaf(v[i + 1], -big, thr_big));
-          }
-          cnt += c0 + c1;
+          screen_chunk(v, cprime + nt * BN + cb, msk, nt * BN + cb, twoE, big, R1, r1, cnt);
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[abuf]);
@@ -473,18 +437,18 @@ extern "C" int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const 
   if (n > INT32_MAX) return PCB_EUNSUP;
   if (k > SC_KMAX) return PCB_EUNSUP;
   cudaStream_t st = (cudaStream_t)stream;
-  // d <= 128: A-resident kernels; PCB_SCREEN_IMPL = pair (default: CTA pairs,
-  // cta_group::2, assign_screen_2sm.cu) | res (one SM, assign_screen_res.cu) |
-  // stream (this file's kernel)
+  // d <= 128: A-resident kernels; PCB_SCREEN_IMPL = res (default: one SM,
+  // assign_screen_res.cu; measured fastest at c3, profiles/r01_screen_ab.md) |
+  // pair (CTA pairs, cta_group::2, assign_screen_2sm.cu) | stream (this file)
   const char* impl = getenv("PCB_SCREEN_IMPL");
   const bool want_stream = impl != nullptr && strcmp(impl, "stream") == 0;
-  const bool want_res = impl != nullptr && strcmp(impl, "res") == 0;
+  const bool want_pair = impl != nullptr && strcmp(impl, "pair") == 0;
   if (ld <= 4 * SC_BK && !want_stream) {
-    if (want_res)
-      return assign_screen_resident(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count,
-                                    state, st);
-    return assign_screen_pair(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count, state,
-                              st);
+    if (want_pair)
+      return assign_screen_pair(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count, state,
+                                st);
+    return assign_screen_resident(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count,
+                                  state, st);
   }
   if (k > 128)
     return launch_screen<256>(P_r, n, ld, C_r, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state,

@@ -25,7 +25,10 @@
 namespace pcb {
 
 constexpr int S2_BN = 256;       // MMA N (centroids per tile, 128 per CTA)
-constexpr int S2_STAGES = 4;
+#ifndef PCB_S2_STAGES
+#define PCB_S2_STAGES 8
+#endif
+constexpr int S2_STAGES = PCB_S2_STAGES;
 constexpr int S2_THREADS = 384;
 
 template <int NKC>
@@ -180,9 +183,7 @@ assign_screen_2sm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_
     const int r_in_tile = g * 32 + lane;
     const float Bmax = bstat[0], dBmax = bstat[1];
     const float acc_rel = (float)(NKC * 4 + 2) * 9.0f * 0x1p-23f;
-    uint32_t cid[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) cid[i] = kChunkIds[i];
+    const uint32_t msk = kIdxMask;
     int abuf = 0;
     uint32_t aphase = 0;
     int tile_it = 0;
@@ -197,11 +198,15 @@ assign_screen_2sm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_
         ptx::mbar_wait(&tfull[abuf], aphase);
         ptx::tc_fence_after();
         const uint32_t taddr = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)(abuf * S2_BN);
+#ifndef PCB_EXP
+#define PCB_EXP 0
+#endif
 #pragma unroll 1
         for (int cb = h * 32; cb < S2_BN; cb += 64) {
           float v[32];
-          ptx::tmem_ld_32x32b_x32(taddr + cb, v);
-          screen_chunk(v, cprime + nt * S2_BN + cb, cid, nt * S2_BN + cb, twoE, big, R1, r1, cnt);
+          if (PCB_EXP != 2) ptx::tmem_ld_32x32b_x32(taddr + cb, v);
+          if (PCB_EXP == 0) screen_chunk(v, cprime + nt * S2_BN + cb, msk, nt * S2_BN + cb, twoE, big, R1, r1, cnt);
+          if (PCB_EXP == 1) R1 = fminf(R1, v[0] + v[31]);
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive_remote(&tempty[abuf], 0);  // the leader's MMA waits on both CTAs

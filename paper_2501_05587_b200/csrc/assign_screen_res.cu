@@ -172,9 +172,7 @@ assign_screen_res_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_
     const int g = warp & 3, h = (warp - 4) >> 2;
     const float Bmax = bstat[0], dBmax = bstat[1];
     const float acc_rel = (float)(NKC * 4 + 2) * 9.0f * 0x1p-23f;
-    uint32_t cid[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) cid[i] = kChunkIds[i];
+    const uint32_t msk = kIdxMask;
     int abuf = 0;
     uint32_t aphase = 0;
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
@@ -188,11 +186,15 @@ assign_screen_res_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_
         ptx::mbar_wait(&tfull[abuf], aphase);
         ptx::tc_fence_after();
         const uint32_t taddr = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)(abuf * 256 + h * 128);
+#ifndef PCB_EXP
+#define PCB_EXP 0
+#endif
 #pragma unroll 1
         for (int cb = 0; cb < SR_BN; cb += 32) {
           float v[32];
-          ptx::tmem_ld_32x32b_x32(taddr + cb, v);
-          screen_chunk(v, cprime + nt * SR_BN + cb, cid, nt * SR_BN + cb, twoE, big, R1, r1, cnt);
+          if (PCB_EXP != 2) ptx::tmem_ld_32x32b_x32(taddr + cb, v);
+          if (PCB_EXP == 0) screen_chunk(v, cprime + nt * SR_BN + cb, msk, nt * SR_BN + cb, twoE, big, R1, r1, cnt);
+          if (PCB_EXP == 1) R1 = fminf(R1, v[0] + v[31]);
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[abuf]);

@@ -10,9 +10,9 @@ namespace pcb {
 constexpr int SC_BK = 32;       // f32 per 128-byte swizzle row (one K chunk)
 constexpr int SC_KMAX = 6144;   // smem copy of the shifted centroid norms (k <= 6144)
 
-// chunk-local column ids; held in registers so (key & ~31) | id is a single LOP3
-static __constant__ uint32_t kChunkIds[32] = {0,  1,  2,  3,  4,  5,  6,  7,  8,  9,  10, 11, 12, 13, 14, 15,
-                                       16, 17, 18, 19, 20, 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31};
+// ~31 read from constant memory so the compiler cannot fold (key & ~31) | id
+// into two immediates: with the mask in a register the pack is one LOP3
+static __constant__ uint32_t kIdxMask = 0xFFFFFFE0u;
 
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
   float r;
@@ -34,24 +34,49 @@ __device__ __forceinline__ float screen_two_e(float an, float dan, float Bmax, f
   return 2.0f * 1.0001f * (2.0f * gerr + 0x1p-16f * kmax);
 }
 
+// Packed f32x2 helpers (FFMA2 / FADD2 on sm_100a: two lanes per issue slot).
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 // One 32-column chunk of accumulators v[] (overwritten with the keys): update
 // the running packed min R1 (index r1) and the count of keys within twoE of it.
+// Per element: 1/2 FFMA2 (key), 1 LOP3 (index pack), 1/2 FMNMX3, 1 FFMA.SAT and
+// 1/2 FADD2 (count) — the epilogue is issue-bound, so the f32x2 forms matter.
+// `msk` is ~31 held in a register so the pack is one LOP3 with the id immediate.
 __device__ __forceinline__ void screen_chunk(float (&v)[32], const float* __restrict__ cprime_chunk,
-                                             const uint32_t (&cid)[32], int col0, float twoE, float big,
+                                             uint32_t msk, int col0, float twoE, float big,
                                              float& R1, int& r1, float& cnt) {
   const float4* cp4 = reinterpret_cast<const float4*>(cprime_chunk);
+  const unsigned long long m2 = f2pack(-2.0f, -2.0f);
   float ma = 3.4e38f, mb = 3.4e38f;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const float4 c4 = cp4[q];
-    v[4 * q + 0] = fmaf(-2.0f, v[4 * q + 0], c4.x);
-    v[4 * q + 1] = fmaf(-2.0f, v[4 * q + 1], c4.y);
-    v[4 * q + 2] = fmaf(-2.0f, v[4 * q + 2], c4.z);
-    v[4 * q + 3] = fmaf(-2.0f, v[4 * q + 3], c4.w);
-    const float k0 = __uint_as_float((__float_as_uint(v[4 * q + 0]) & 0xFFFFFFE0u) | cid[4 * q + 0]);
-    const float k1 = __uint_as_float((__float_as_uint(v[4 * q + 1]) & 0xFFFFFFE0u) | cid[4 * q + 1]);
-    const float k2 = __uint_as_float((__float_as_uint(v[4 * q + 2]) & 0xFFFFFFE0u) | cid[4 * q + 2]);
-    const float k3 = __uint_as_float((__float_as_uint(v[4 * q + 3]) & 0xFFFFFFE0u) | cid[4 * q + 3]);
+    const unsigned long long a = ffma2(f2pack(v[4 * q + 0], v[4 * q + 1]), m2, f2pack(c4.x, c4.y));
+    const unsigned long long b = ffma2(f2pack(v[4 * q + 2], v[4 * q + 3]), m2, f2pack(c4.z, c4.w));
+    f2unpack(a, v[4 * q + 0], v[4 * q + 1]);
+    f2unpack(b, v[4 * q + 2], v[4 * q + 3]);
+    const float k0 = __uint_as_float((__float_as_uint(v[4 * q + 0]) & msk) | (uint32_t)(4 * q + 0));
+    const float k1 = __uint_as_float((__float_as_uint(v[4 * q + 1]) & msk) | (uint32_t)(4 * q + 1));
+    const float k2 = __uint_as_float((__float_as_uint(v[4 * q + 2]) & msk) | (uint32_t)(4 * q + 2));
+    const float k3 = __uint_as_float((__float_as_uint(v[4 * q + 3]) & msk) | (uint32_t)(4 * q + 3));
     ma = fmin3(ma, k0, k1);
     mb = fmin3(mb, k2, k3);
   }
@@ -66,13 +91,15 @@ __device__ __forceinline__ void screen_chunk(float (&v)[32], const float* __rest
   }
   const float thr = R1 + twoE + 0x1p-16f * fabsf(R1);
   const float thr_big = thr * big;
-  float c0 = 0.0f, c1 = 0.0f;
+  unsigned long long c2 = 0ull, d2 = 0ull;
 #pragma unroll
-  for (int i = 0; i < 32; i += 2) {
-    c0 += __saturatef(fmaf(v[i], -big, thr_big));
-    c1 += __saturatef(fmaf(v[i + 1], -big, thr_big));
+  for (int i = 0; i < 32; i += 4) {
+    c2 = fadd2(c2, f2pack(__saturatef(fmaf(v[i], -big, thr_big)), __saturatef(fmaf(v[i + 1], -big, thr_big))));
+    d2 = fadd2(d2, f2pack(__saturatef(fmaf(v[i + 2], -big, thr_big)), __saturatef(fmaf(v[i + 3], -big, thr_big))));
   }
-  cnt += c0 + c1;
+  float x0, x1;
+  f2unpack(fadd2(c2, d2), x0, x1);
+  cnt += x0 + x1;
 }
 
 // Append ambiguous rows to the list (warp-aggregated atomic).

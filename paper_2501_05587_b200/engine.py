@@ -135,8 +135,14 @@ class ShardSequence:
 
     def iteration(self, t: int, check_convergence: bool = False, tol: float = 0.0,
                   events=None, raw_out=None) -> None:
-        """One Lloyd iteration t (reads labels[t%2], writes labels[(t+1)%2])."""
+        """One Lloyd iteration t (reads labels[t%2], writes labels[(t+1)%2]).
+
+        events: optional CUDA events [assign start, assign end, iteration end]
+        plus, optionally, [dominant kernel start, dominant kernel end] (recorded
+        on the launching stream around the distance+argmin kernel itself).
+        """
         prev, new = self.labels[t % 2], self.labels[(t + 1) % 2]
+        self._kev = events[3:5] if events is not None and len(events) >= 5 else None
         self.acc.zero_()
         if events is not None:
             events[0].record()
@@ -297,9 +303,11 @@ class LloydEngine(ShardSequence):
     def _assign(self, prev, new, acc, state) -> None:
         if self.variant == "tc1xtf32s":
             self.amb_count.zero_()
+            self._kmark(0)
             L.call("pcb_assign_screen_f32", _p(self.P_r), self.n, self.ld, _p(self.C_hi), self.k,
                    _p(self.cnorm), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
                    _p(self.amb_list), _p(self.amb_count), _p(state), _stream())
+            self._kmark(1)
             L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.amb_list),
                    _p(self.amb_count), self.ld, _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels),
                    _p(self.pnorm), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(new),
@@ -308,14 +316,22 @@ class LloydEngine(ShardSequence):
                 L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
                        _stream())
             return
+        self._kmark(0)
         if self.variant == "tc3xtf32":
             L.call("pcb_assign_tc_f32", _p(self.P_hi), _p(self.P_lo), self.ld, _p(self.pnorm), self.n,
                    self.d, _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(prev), _p(new),
                    _p(self.mind), _p(acc), _p(state), _stream())
-            return
-        L.call(f"pcb_assign_{self.sfx}", _p(self.P), _p(self.pnorm), self.n, self.d, _p(self.C),
-               _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
-               self.vcode, _stream())
+        else:
+            L.call(f"pcb_assign_{self.sfx}", _p(self.P), _p(self.pnorm), self.n, self.d, _p(self.C),
+                   _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
+                   self.vcode, _stream())
+        self._kmark(1)
+
+    _kev = None
+
+    def _kmark(self, i: int) -> None:
+        if self._kev is not None:
+            self._kev[i].record()
 
     def _repair_local(self, prev, new) -> None:
         L.call(f"pcb_repair_{self.sfx}", _p(self.P), self.n, self.d, _p(self.C), self.k, _p(self.perm),

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Per-kernel launch list (cold, serialised) of a short bench run under ncu.
+cfg=${1:-c3}; impl=${2:-res}; tag=${3:-$cfg_$impl}
+PCB_SCREEN_IMPL=$impl timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 60 -c 60 --csv \
+  --log-file gpurun_out/launches_$tag.csv python bench.py --config $cfg --variant tc1xtf32s --steps 3 --warmup 3 \
+  --no-e2e --no-cpu-baseline > gpurun_out/launches_$tag.log 2>&1
+echo "ncu rc=$?"
+python - "$tag" <<'PY'
+import csv, sys, collections
+rows = list(csv.reader(l for l in open(f"gpurun_out/launches_{sys.argv[1]}.csv") if not l.startswith("==")))
+hdr = rows[0]; ki = hdr.index("Kernel Name"); vi = hdr.index("Metric Value")
+t = collections.defaultdict(list)
+for r in rows[1:]:
+    if len(r) > vi: t[r[ki][:60]].append(float(r[vi].replace(",", "")))
+for k, v in sorted(t.items(), key=lambda x: -sum(x[1])):
+    print(f"{sum(v)/len(v)/1e3:9.3f} us x{len(v):3d}  {k}")
+PY

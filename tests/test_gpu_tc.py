@@ -110,7 +110,7 @@ def test_tc_full_run_matches_ffma_run():
 # ---------------------------------------------------------------------------
 # certified 1xTF32 screening (variant tc1xtf32s)
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("impl", ["pair", "res", "stream"])
+@pytest.mark.parametrize("impl", ["res", "pair", "stream"])
 @pytest.mark.parametrize("n,d,k", [(1000, 40, 17), (777, 100, 300), (4096, 64, 64), (300, 32, 1),
                                    (5000, 128, 1024), (2000, 784, 256), (1500, 96, 129), (5000, 64, 4096),
                                    (20000, 128, 1024)])
