@@ -204,7 +204,6 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2501_05587_b200 import _lib
-    from paper_2501_05587_b200.clustering import init_assignments
     from paper_2501_05587_b200.distributed import Comm, init_from_env, shard_range
     from paper_2501_05587_b200.engine import LloydEngine
 
@@ -220,12 +219,12 @@ def main():
     n, d, k = cfg["n"], cfg["d"], cfg["k"]
     lo, hi = shard_range(n, rank, world)
     P = make_shard(hi - lo, d, k, rank, args.seed, dev)
-    labels0 = init_assignments(n, k, 0)[lo:hi]
     W, K = args.warmup, args.steps
     eng = LloydEngine(P, k, variant=args.variant, comm=comm, n_total=n, max_iters=W + K + 1)
     if comm is not None:
         comm.offset = lo
-    eng.init_centroids_from_labels(labels0)
+    eng.init_labels_device(0, lo)  # init_assignments(n, k, 0), drawn on the device
+    eng.init_centroids_from_labels()
     for t in range(W):
         eng.iteration(t)
     torch.cuda.synchronize()
@@ -339,7 +338,7 @@ def e2e_run(args, cfg, dev):
     torch.cuda.empty_cache()
     it = args.e2e_iters
     c = pcb.KKMeansConfig(k=k, max_iters=it, record_label_history=False)
-    pcb.run_lloyd(P_host[: min(n, 20000)], pcb.KKMeansConfig(k=k, max_iters=2))  # warm libs
+    pcb.run_lloyd(P_host[: min(n, 100_000)], pcb.KKMeansConfig(k=k, max_iters=2))  # warm libs + staging buffers
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = pcb.run_lloyd(P_host, c)

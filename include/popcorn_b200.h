@@ -55,6 +55,24 @@ int pcb_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 int pcb_count_nonfinite_f32(const float* X, int64_t count, unsigned long long* out, void* stream);
 int pcb_count_nonfinite_f64(const double* X, int64_t count, unsigned long long* out, void* stream);
 
+/* ---- on-device init_assignments (clustering.py:91-108) --------------------
+ *   labels[0:n) = Generator(PCG64(seed)).integers(0, k, size=n) as int32,
+ *   then `labels[j] = j` for every empty cluster j, repeated until none is
+ *   empty — bit-identical to the reference (numpy SeedSequence + PCG64 +
+ *   Lemire bounded draws, see init.cu).  Synchronous (reads two ints per
+ *   pass); *passes_out = number of hollow-fill passes.  Returns PCB_EUNSUP
+ *   if the rejection margin is exhausted (probability ~0).
+ *   pcb_pcg64_seed_state: host-only, out4 = {state hi, state lo, inc hi,
+ *   inc lo} of PCG64(seed) after seeding (numpy's bit_generator.state).   */
+int64_t pcb_init_scratch_bytes(int64_t n, int k);
+/* The draw alone: out[0:n) = Generator(PCG64(seed)).integers(0, k, size=n)
+ * (any 1 <= k < 2^31; no hollow fill).  Synchronous. */
+int pcb_bounded_draws(int64_t n, int k, uint64_t seed, int32_t* out, void* scratch, int64_t scratch_bytes,
+                      void* stream);
+int pcb_pcg64_seed_state(uint64_t seed, uint64_t* out4_host);
+int pcb_init_assignments(int64_t n, int k, uint64_t seed, int32_t* labels, void* scratch,
+                         int64_t scratch_bytes, int* passes_out_host, void* stream);
+
 /* ---- one-time point preparation (clustering.py:302: point_norms) ---------- */
 int pcb_point_norms_f32(const float* P, int64_t n, int d, float* pnorm, void* stream);
 int pcb_point_norms_f64(const double* P, int64_t n, int d, double* pnorm, void* stream);

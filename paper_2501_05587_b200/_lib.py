@@ -25,6 +25,10 @@ SIGNATURES = {
     "pcb_device_info": (I32, [I32, P, P, P]),
     "pcb_count_nonfinite_f32": (I32, [P, I64, P, P]),
     "pcb_count_nonfinite_f64": (I32, [P, I64, P, P]),
+    "pcb_init_scratch_bytes": (I64, [I64, I32]),
+    "pcb_pcg64_seed_state": (I32, [ctypes.c_uint64, P]),
+    "pcb_init_assignments": (I32, [I64, I32, ctypes.c_uint64, P, P, I64, P, P]),
+    "pcb_bounded_draws": (I32, [I64, I32, ctypes.c_uint64, P, P, I64, P]),
     "pcb_point_norms_f32": (I32, [P, I64, I32, P, P]),
     "pcb_point_norms_f64": (I32, [P, I64, I32, P, P]),
     "pcb_split_tf32": (I32, [P, I64, I32, I32, P, P, P]),

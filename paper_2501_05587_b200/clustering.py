@@ -7,7 +7,7 @@ for the classical Lloyd path:
                                                variant, device)
 * ``ClusteringResult``   clustering.py:71-88  (+ additive: centroids)
 * ``TimingBreakdown``    clustering.py:34-40
-* ``init_assignments``   clustering.py:91-108 (host PCG64: identical stream)
+* ``init_assignments``   clustering.py:91-108 (host mirror; drivers draw it on the device)
 * ``run_lloyd``          clustering.py:291-325 — same signature
   ``driver(points, cfg) -> ClusteringResult`` as the `_ALGORITHMS` plugins.
 
@@ -95,8 +95,9 @@ class ClusteringResult:
 def init_assignments(n: int, k: int, seed: int) -> np.ndarray:
     """Seeded PCG64 labels with no empty cluster (clustering.py:91-108).
 
-    Host-side on purpose: the PCG64 stream is the reference's fixture
-    (GOLDEN_INIT_100_10_42) and costs O(n) once per fit.
+    The host-returning mirror of the reference function (numpy's own PCG64).
+    The drivers (run_lloyd, run_lloyd_sharded, bench) draw the same stream on
+    the device instead: LloydEngine.init_labels_device / pcb_init_assignments.
     """
     if not 1 <= k <= n:
         raise ValueError(f"k must satisfy 1 <= k <= n, got k={k}, n={n}")
@@ -142,18 +143,18 @@ def run_lloyd(points, cfg: KKMeansConfig) -> ClusteringResult:
     dtype = normalize_dtype(cfg.dtype)
     P, n, d = _prepare_points(points, cfg)
     cfg.validate_for(n)
-    labels0 = init_assignments(n, cfg.k, cfg.seed)
-    eng = LloydEngine(P, cfg.k, dtype=dtype, device=cfg.device, variant=cfg.variant,
-                      max_iters=cfg.max_iters, check_finite=isinstance(P, np.ndarray) and P.size > (1 << 24))
-    if cfg.init is None:
-        eng.init_centroids_from_labels(labels0)
-    else:
+    if cfg.init is not None:
         init = np.asarray(cfg.init)
         if init.shape != (cfg.k, d):
             raise ValueError(f"init centroids must have shape ({cfg.k}, {d}), got {init.shape}")
         if not np.isfinite(init).all():
             raise ValueError("init contains non-finite entries")
-        eng.set_labels(labels0)
+    eng = LloydEngine(P, cfg.k, dtype=dtype, device=cfg.device, variant=cfg.variant,
+                      max_iters=cfg.max_iters, check_finite=isinstance(P, np.ndarray) and P.size > (1 << 24))
+    eng.init_labels_device(cfg.seed)  # init_assignments, clustering.py:91-108, in HBM
+    if cfg.init is None:
+        eng.init_centroids_from_labels()
+    else:
         eng.set_centroids(init)
     out = eng.run(cfg.max_iters, cfg.tol, cfg.check_convergence,
                   record_history=cfg.record_label_history)

@@ -376,6 +376,22 @@ count_labels_kernel(const int32_t* __restrict__ labels, const int32_t* __restric
     if (hist[j]) atomicAdd(&acc[L.counts() + j], (double)hist[j]);
 }
 
+// large-k variant: global f64 atomics straight into acc
+__global__ void count_labels_global_kernel(const int32_t* __restrict__ labels, const int32_t* __restrict__ prev,
+                                           int64_t n, int k, int d, double* __restrict__ acc,
+                                           const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const AccLayout L{k, d};
+  long long chg = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int l = labels[i];
+    atomicAdd(&acc[L.counts() + l], 1.0);
+    if (prev) chg += (prev[i] != l);
+  }
+  chg = warp_sum(chg);
+  if ((threadIdx.x & 31) == 0 && chg) atomicAdd(&acc[L.changed()], (double)chg);
+}
+
 template <int BN>
 static int launch_screen(const float* P, int64_t n, int ld, const float* C, int k, const float* an,
                          const float* dan, const float* cnorm, const float* bstat, int32_t* labels,
@@ -480,8 +496,12 @@ extern "C" int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const
 extern "C" int pcb_count_labels(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
                                 double* acc, const long long* state, void* stream) {
   if (n < 1 || k < 1 || !labels || !acc) return PCB_EINVAL;
-  if (k > 12288) return PCB_EUNSUP;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 4);
+  if (k > 12288) {
+    count_labels_global_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(labels, labels_prev, n, k, d, acc, state);
+    PCB_CHECK_LAUNCH();
+    return 0;
+  }
   count_labels_kernel<<<grid, 256, k * sizeof(int), (cudaStream_t)stream>>>(labels, labels_prev, n, k, d, acc,
                                                                           state);
   PCB_CHECK_LAUNCH();

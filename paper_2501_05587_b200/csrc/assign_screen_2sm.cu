@@ -205,7 +205,7 @@ assign_screen_2sm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_
         for (int cb = h * 32; cb < S2_BN; cb += 64) {
           float v[32];
           if (PCB_EXP != 2) ptx::tmem_ld_32x32b_x32(taddr + cb, v);
-          if (PCB_EXP == 0) screen_chunk(v, cprime + nt * S2_BN + cb, msk, nt * S2_BN + cb, twoE, big, R1, r1, cnt);
+          if (PCB_EXP == 0 || PCB_EXP == 3) screen_chunk(v, cprime + nt * S2_BN + cb, msk, nt * S2_BN + cb, twoE, big, R1, r1, cnt);
           if (PCB_EXP == 1) R1 = fminf(R1, v[0] + v[31]);
         }
         ptx::tc_fence_before();

@@ -175,27 +175,56 @@ assign_screen_res_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_
     const uint32_t msk = kIdxMask;
     int abuf = 0;
     uint32_t aphase = 0;
+    // row norms of the next pair are loaded one pair ahead (their DRAM latency
+    // otherwise stalls the first chunk of every pair)
+    const int64_t r_in = h * 128 + g * 32 + lane;
+    float an_nx = 0.0f, dan_nx = 0.0f;
+    if (blockIdx.x < npairs) {
+      const int64_t row0 = (int64_t)blockIdx.x * 256 + r_in;
+      an_nx = anorm[row0 < n ? row0 : n - 1];
+      dan_nx = danorm[row0 < n ? row0 : n - 1];
+    }
+    // c' of chunk c+1 is read from smem while chunk c is processed (ping-pong
+    // register sets cpA/cpB over the 4 chunks of a tile)
+    float cpA[32], cpB[32];
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
-      const int64_t row = pr * 256 + h * 128 + g * 32 + lane;
-      const int64_t rr = row < n ? row : n - 1;
-      const float twoE = screen_two_e(anorm[rr], danorm[rr], Bmax, dBmax, OFF, acc_rel);
+      const int64_t row = pr * 256 + r_in;
+      const float twoE = screen_two_e(an_nx, dan_nx, Bmax, dBmax, OFF, acc_rel);
       const float big = 64.0f / twoE;
+      if (pr + gridDim.x < npairs) {
+        const int64_t rn = (pr + gridDim.x) * 256 + r_in;
+        an_nx = anorm[rn < n ? rn : n - 1];
+        dan_nx = danorm[rn < n ? rn : n - 1];
+      }
       float R1 = 3.4e38f, cnt = 0.0f;
       int r1 = 0;
+      load_cprime(cpA, cprime);
       for (int nt = 0; nt < ntiles; ++nt) {
         ptx::mbar_wait(&tfull[abuf], aphase);
         ptx::tc_fence_after();
         const uint32_t taddr = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)(abuf * 256 + h * 128);
+        const int c0 = nt * SR_BN;
 #ifndef PCB_EXP
 #define PCB_EXP 0
 #endif
-#pragma unroll 1
-        for (int cb = 0; cb < SR_BN; cb += 32) {
-          float v[32];
-          if (PCB_EXP != 2) ptx::tmem_ld_32x32b_x32(taddr + cb, v);
-          if (PCB_EXP == 0) screen_chunk(v, cprime + nt * SR_BN + cb, msk, nt * SR_BN + cb, twoE, big, R1, r1, cnt);
-          if (PCB_EXP == 1) R1 = fminf(R1, v[0] + v[31]);
-        }
+        static_assert(SR_BN == 128, "the ping-pong below covers 4 chunks per tile");
+        float v[32];
+        load_cprime(cpB, cprime + c0 + 32);
+        if (PCB_EXP != 2) ptx::tmem_ld_32x32b_x32(taddr + 0, v);
+        if (PCB_EXP == 0 || PCB_EXP == 3) screen_chunk_regs(v, cpA, msk, c0 + 0, twoE, big, R1, r1, cnt);
+        if (PCB_EXP == 1) R1 = fminf(R1, v[0] + v[31]);
+        load_cprime(cpA, cprime + c0 + 64);
+        if (PCB_EXP != 2) ptx::tmem_ld_32x32b_x32(taddr + 32, v);
+        if (PCB_EXP == 0 || PCB_EXP == 3) screen_chunk_regs(v, cpB, msk, c0 + 32, twoE, big, R1, r1, cnt);
+        if (PCB_EXP == 1) R1 = fminf(R1, v[0] + v[31]);
+        load_cprime(cpB, cprime + c0 + 96);
+        if (PCB_EXP != 2) ptx::tmem_ld_32x32b_x32(taddr + 64, v);
+        if (PCB_EXP == 0 || PCB_EXP == 3) screen_chunk_regs(v, cpA, msk, c0 + 64, twoE, big, R1, r1, cnt);
+        if (PCB_EXP == 1) R1 = fminf(R1, v[0] + v[31]);
+        if (nt + 1 < ntiles) load_cprime(cpA, cprime + c0 + 128);
+        if (PCB_EXP != 2) ptx::tmem_ld_32x32b_x32(taddr + 96, v);
+        if (PCB_EXP == 0 || PCB_EXP == 3) screen_chunk_regs(v, cpB, msk, c0 + 96, twoE, big, R1, r1, cnt);
+        if (PCB_EXP == 1) R1 = fminf(R1, v[0] + v[31]);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[abuf]);
         abuf ^= 1;

@@ -55,22 +55,37 @@ __device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsign
   return r;
 }
 
-// One 32-column chunk of accumulators v[] (overwritten with the keys): update
-// the running packed min R1 (index r1) and the count of keys within twoE of it.
+// Shifted centroid norms c'_j of one 32-column chunk, smem -> registers.
+__device__ __forceinline__ void load_cprime(float (&cp)[32], const float* __restrict__ cprime_chunk) {
+  const float4* cp4 = reinterpret_cast<const float4*>(cprime_chunk);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+#if defined(PCB_EXP) && PCB_EXP == 3
+    const float4 c4 = make_float4(1.0f * q, 2.0f * q, 3.0f + q, 4.0f + q);  // experiment: no smem reads
+#else
+    const float4 c4 = cp4[q];
+#endif
+    cp[4 * q + 0] = c4.x;
+    cp[4 * q + 1] = c4.y;
+    cp[4 * q + 2] = c4.z;
+    cp[4 * q + 3] = c4.w;
+  }
+}
+
+// One 32-column chunk of accumulators v[] (overwritten with the keys) and its
+// shifted centroid norms cp[]: update the running packed min R1 (index r1) and
+// the count of keys within twoE of it.
 // Per element: 1/2 FFMA2 (key), 1 LOP3 (index pack), 1/2 FMNMX3, 1 FFMA.SAT and
 // 1/2 FADD2 (count) — the epilogue is issue-bound, so the f32x2 forms matter.
 // `msk` is ~31 held in a register so the pack is one LOP3 with the id immediate.
-__device__ __forceinline__ void screen_chunk(float (&v)[32], const float* __restrict__ cprime_chunk,
-                                             uint32_t msk, int col0, float twoE, float big,
-                                             float& R1, int& r1, float& cnt) {
-  const float4* cp4 = reinterpret_cast<const float4*>(cprime_chunk);
+__device__ __forceinline__ void screen_chunk_regs(float (&v)[32], const float (&cp)[32], uint32_t msk, int col0,
+                                                  float twoE, float big, float& R1, int& r1, float& cnt) {
   const unsigned long long m2 = f2pack(-2.0f, -2.0f);
   float ma = 3.4e38f, mb = 3.4e38f;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const float4 c4 = cp4[q];
-    const unsigned long long a = ffma2(f2pack(v[4 * q + 0], v[4 * q + 1]), m2, f2pack(c4.x, c4.y));
-    const unsigned long long b = ffma2(f2pack(v[4 * q + 2], v[4 * q + 3]), m2, f2pack(c4.z, c4.w));
+    const unsigned long long a = ffma2(f2pack(v[4 * q + 0], v[4 * q + 1]), m2, f2pack(cp[4 * q + 0], cp[4 * q + 1]));
+    const unsigned long long b = ffma2(f2pack(v[4 * q + 2], v[4 * q + 3]), m2, f2pack(cp[4 * q + 2], cp[4 * q + 3]));
     f2unpack(a, v[4 * q + 0], v[4 * q + 1]);
     f2unpack(b, v[4 * q + 2], v[4 * q + 3]);
     const float k0 = __uint_as_float((__float_as_uint(v[4 * q + 0]) & msk) | (uint32_t)(4 * q + 0));
@@ -100,6 +115,13 @@ __device__ __forceinline__ void screen_chunk(float (&v)[32], const float* __rest
   float x0, x1;
   f2unpack(fadd2(c2, d2), x0, x1);
   cnt += x0 + x1;
+}
+
+__device__ __forceinline__ void screen_chunk(float (&v)[32], const float* __restrict__ cprime_chunk, uint32_t msk,
+                                             int col0, float twoE, float big, float& R1, int& r1, float& cnt) {
+  float cp[32];
+  load_cprime(cp, cprime_chunk);
+  screen_chunk_regs(v, cp, msk, col0, twoE, big, R1, r1, cnt);
 }
 
 // Append ambiguous rows to the list (warp-aggregated atomic).

@@ -24,7 +24,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .clustering import ClusteringResult, KKMeansConfig, TimingBreakdown, init_assignments
+from .clustering import ClusteringResult, KKMeansConfig, TimingBreakdown
 from .validation import normalize_dtype
 
 
@@ -117,14 +117,12 @@ def run_lloyd_sharded(points_local, cfg: KKMeansConfig, n_total: int, offset: in
     comm.offset = offset
     cfg.validate_for(n_total)
     dtype = normalize_dtype(cfg.dtype)
-    labels0 = init_assignments(n_total, cfg.k, cfg.seed)
-    n_local = int(points_local.shape[0])
     eng = LloydEngine(points_local, cfg.k, dtype=dtype, device=cfg.device, variant=cfg.variant,
                       comm=comm, n_total=n_total, max_iters=cfg.max_iters)
+    eng.init_labels_device(cfg.seed, offset)  # the global stream, sliced to this shard
     if cfg.init is None:
-        eng.init_centroids_from_labels(labels0[offset:offset + n_local])
+        eng.init_centroids_from_labels()
     else:
-        eng.set_labels(labels0[offset:offset + n_local])
         eng.set_centroids(np.asarray(cfg.init))
     out = eng.run(cfg.max_iters, cfg.tol, cfg.check_convergence,
                   record_history=cfg.record_label_history)

@@ -60,3 +60,19 @@ def test_library_is_sm100a():
     so = os.path.join(ROOT, "paper_2501_05587_b200", "lib", "libpopcorn_b200.so")
     data = open(so, "rb").read()
     assert b"sm_100a" in data or b"sm_100" in data
+
+
+def test_pcg64_seed_state_matches_numpy():
+    """pcb_pcg64_seed_state restates numpy's SeedSequence -> PCG64 seeding
+    (the first step of init_assignments, clustering.py:101) on the host."""
+    import numpy as np
+    from paper_2501_05587_b200 import _lib
+    lib = _lib.load()
+    seeds = [0, 1, 42, 2**32 - 1, 2**32, 2**64 - 1] + [int(s) for s in np.random.default_rng(1).integers(0, 2**63, 50)]
+    for seed in seeds:
+        out = (ctypes.c_uint64 * 4)()
+        assert lib.pcb_pcg64_seed_state(seed, out) == 0
+        st = np.random.PCG64(seed).state["state"]
+        assert (out[0] << 64 | out[1], out[2] << 64 | out[3]) == (st["state"], st["inc"]), seed
+    assert lib.pcb_init_scratch_bytes(0, 3) == -1
+    assert lib.pcb_init_assignments(5, 6, 0, None, None, 0, None, None) == -1
