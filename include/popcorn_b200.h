@@ -73,6 +73,27 @@ int pcb_pcg64_seed_state(uint64_t seed, uint64_t* out4_host);
 int pcb_init_assignments(int64_t n, int k, uint64_t seed, int32_t* labels, void* scratch,
                          int64_t scratch_bytes, int* passes_out_host, void* stream);
 
+/* ---- synthesized input (cli.py:102-105) ------------------------------------
+ *   out[0:count) = Generator(PCG64(seed)).random(count) (row-major (n, d) when
+ *   count = n*d), as f64 or rounded to f32 (.astype(f32)); bit-identical.   */
+int pcb_synthesize_uniform(int64_t count, uint64_t seed, int is_f64, void* out, void* stream);
+
+/* ---- dataset text loaders (io.py:16-77), host memory -----------------------
+ *   Dense row-major n x d f32 (is_f64 = 0) or f64 into out_host (libsvm: the
+ *   caller zero-fills it).  Returns 0, a positive errno if the file cannot be
+ *   read, PCB_EINVAL, or PCB_EPARSE with info[4] = {kind, line number, count,
+ *   text length} and the offending text (NUL-terminated) in text; kinds:
+ *   1 malformed label, 2 malformed feature token, 3 feature index out of
+ *   range (text = index), 4 too few libsvm lines (count = found), 5 empty CSV,
+ *   6 non-numeric CSV cell (text = stripped row), 7 wrong CSV column count
+ *   (count = found), 8 wrong CSV row count (count = found).
+ *   nthreads <= 0: all hardware threads.                                   */
+#define PCB_EPARSE   (-4)
+int pcb_load_libsvm(const char* path, int64_t n, int d, int is_f64, void* out_host, int64_t* info,
+                    char* text, int64_t text_len, int nthreads);
+int pcb_load_csv(const char* path, int64_t n, int d, int is_f64, void* out_host, int64_t* info,
+                 char* text, int64_t text_len, int nthreads);
+
 /* ---- one-time point preparation (clustering.py:302: point_norms) ---------- */
 int pcb_point_norms_f32(const float* P, int64_t n, int d, float* pnorm, void* stream);
 int pcb_point_norms_f64(const double* P, int64_t n, int d, double* pnorm, void* stream);

@@ -8,6 +8,7 @@ kernels behind the C ABI in ``include/popcorn_b200.h``.
 from .clustering import (ClusteringResult, KKMeansConfig, TimingBreakdown, init_assignments,
                          lloyd_step, run_lloyd)
 from .estimator import _ALGORITHMS, KernelKMeans
+from .io import load_csv, load_libsvm, synthesize_points, write_results
 from .validation import as_float_matrix, check_labels, normalize_dtype
 
 __version__ = "0.1.0"
@@ -20,7 +21,11 @@ __all__ = [
     "as_float_matrix",
     "check_labels",
     "init_assignments",
+    "load_csv",
+    "load_libsvm",
     "lloyd_step",
     "normalize_dtype",
     "run_lloyd",
+    "synthesize_points",
+    "write_results",
 ]

@@ -29,6 +29,9 @@ SIGNATURES = {
     "pcb_pcg64_seed_state": (I32, [ctypes.c_uint64, P]),
     "pcb_init_assignments": (I32, [I64, I32, ctypes.c_uint64, P, P, I64, P, P]),
     "pcb_bounded_draws": (I32, [I64, I32, ctypes.c_uint64, P, P, I64, P]),
+    "pcb_synthesize_uniform": (I32, [I64, ctypes.c_uint64, I32, P, P]),
+    "pcb_load_libsvm": (I32, [ctypes.c_char_p, I64, I32, I32, P, P, P, I64, I32]),
+    "pcb_load_csv": (I32, [ctypes.c_char_p, I64, I32, I32, P, P, P, I64, I32]),
     "pcb_point_norms_f32": (I32, [P, I64, I32, P, P]),
     "pcb_point_norms_f64": (I32, [P, I64, I32, P, P]),
     "pcb_split_tf32": (I32, [P, I64, I32, I32, P, P, P]),

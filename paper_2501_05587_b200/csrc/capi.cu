@@ -26,6 +26,7 @@ extern "C" const char* pcb_error_string(int code) {
     case PCB_EINVAL: return "popcorn_b200: invalid argument (size or null pointer)";
     case PCB_EUNSUP: return "popcorn_b200: unsupported shape/variant for this kernel";
     case PCB_ENODEV: return "popcorn_b200: no sm_100 (B200) CUDA device";
+    case -4: return "popcorn_b200: dataset parse error (see info/text)";
     default: break;
   }
   if (code > 0) return cudaGetErrorString((cudaError_t)code);

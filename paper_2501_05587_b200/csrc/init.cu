@@ -319,3 +319,41 @@ extern "C" int pcb_init_assignments(int64_t n, int k, uint64_t seed, int32_t* la
   if (passes_out) *passes_out = passes;
   return 0;
 }
+
+// ---- synthesize_points (cli.py:102-105): Generator(PCG64(seed)).random((n, d)) ----
+// numpy's random() = (next_uint64 >> 11) * 2^-53, one PCG64 output per value in
+// row-major order; .astype(f32) rounds to nearest.
+namespace pcb {
+template <typename T>
+__global__ void __launch_bounds__(256)
+uniform_kernel(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count, T* __restrict__ out) {
+  const u128 state0 = ((u128)st_hi << 64) | st_lo, inc = ((u128)inc_hi << 64) | inc_lo;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t o0 = t * kOutPerThread;
+  if (o0 >= count) return;
+  u128 s = pcg_advance(state0, inc, (uint64_t)o0);
+  const u128 M = pcg_mult();
+  for (int q = 0; q < kOutPerThread && o0 + q < count; ++q) {
+    s = s * M + inc;
+    const double v = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+    out[o0 + q] = (T)v;
+  }
+}
+}  // namespace pcb
+
+extern "C" int pcb_synthesize_uniform(int64_t count, uint64_t seed, int is_f64, void* out, void* stream) {
+  if (count < 1 || !out) return PCB_EINVAL;
+  u128 s0, inc;
+  pcg64_from_seed(seed, &s0, &inc);
+  const int64_t threads = (count + kOutPerThread - 1) / kOutPerThread;
+  const unsigned grid = (unsigned)((threads + 255) / 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (is_f64)
+    uniform_kernel<double><<<grid, 256, 0, st>>>((uint64_t)(s0 >> 64), (uint64_t)s0, (uint64_t)(inc >> 64),
+                                                 (uint64_t)inc, count, (double*)out);
+  else
+    uniform_kernel<float><<<grid, 256, 0, st>>>((uint64_t)(s0 >> 64), (uint64_t)s0, (uint64_t)(inc >> 64),
+                                                (uint64_t)inc, count, (float*)out);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}

@@ -56,3 +56,14 @@ def test_sharded_engine_takes_its_slice():
     eng = LloydEngine(P, k, n_total=n)
     eng.init_labels_device(9, 3000)
     np.testing.assert_array_equal(eng.labels[0].cpu().numpy(), oracle.init_assignments(n, k, 9)[3000:7000])
+
+
+@pytest.mark.parametrize("n,d,seed", [(1, 1, 0), (50, 3, 9), (1000, 17, 123), (100_000, 64, 2**40 + 3)])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_synthesize_points_matches_reference(n, d, seed, dt):
+    """cli.synthesize_points (cli.py:102-105): Generator(PCG64(seed)).random((n, d)).astype(dtype)."""
+    from paper_2501_05587_b200.io import synthesize_points
+    got = synthesize_points(n, d, seed, dtype=dt)
+    ref = np.random.Generator(np.random.PCG64(seed)).random((n, d)).astype(dt)
+    assert got.dtype == ref.dtype
+    np.testing.assert_array_equal(got, ref)
