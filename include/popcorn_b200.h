@@ -230,6 +230,51 @@ int pcb_centroid_norms_f32(const float* C, int k, int d, float* cnorm,
                            float* c_hi, float* c_lo, int ld, void* stream);
 int pcb_centroid_norms_f64(const double* C, int k, int d, double* cnorm, void* stream);
 
+/* ==== Kernel K-means (run_popcorn, clustering.py:165-218) ====================
+ * K = kernel(P P^T) is built once in HBM (row-major n x n, leading dimension
+ * ldk >= n, ldk % 4 == 0 for f32 / % 2 for f64), exactly symmetric.
+ * family: 0 linear, 1 polynomial, 2 gaussian, 3 sigmoid (kernels.py:18);
+ * dvec = |p_i|^2 (the Gram diagonal) is required for the gaussian family.
+ * *nonfinite is incremented if any K entry is not finite (require_finite).
+ * pcb_kernel_gram_f32 takes the TF32 split of P (pcb_split_tf32, row stride
+ * ld % 32 == 0): tcgen05 3xTF32 GEMM with the kernel in the epilogue.    */
+int pcb_kernel_gram_f32(const float* P_hi, const float* P_lo, int ld, int64_t n, const float* dvec, float* K,
+                        int64_t ldk, int family, double gamma, double coef, int degree, double sigma,
+                        unsigned long long* nonfinite, void* stream);
+int pcb_kernel_gram_f64(const double* P, int64_t n, int d, const double* dvec, double* K, int64_t ldk,
+                        int family, double gamma, double coef, int degree, double sigma,
+                        unsigned long long* nonfinite, void* stream);
+/* Per iteration (labels_cur -> labels_new), with perm/offsets from
+ * pcb_sort_by_label(labels_cur, ..., cnt, ...), cnt = counts of labels_cur (f64):
+ *   segment sums  S[j, :] = sum_{m in L_j} K[m, :]  (k x lds f64, zeroed here)
+ *   assign        acc = [counts k | cnsum k | objective | changed] (zeroed by
+ *                 the caller); D[i,j] = K[i,i] - 2 S[j,i]/|L_j| + c_j,
+ *                 c_j = (1/|L_j|) sum_{i in L_j} S[l_i,i]/|L_{l_i}|; argmin
+ *                 -> labels_new, own distance, int counts (icounts)
+ *   repair        empty clusters filled by the farthest points (one block)
+ *   finalize      counts/objective/changed of labels_new, history at
+ *                 state[0], convergence; cnt <- counts of labels_new.     */
+int pcb_kk_segment_sums_f32(const float* K, int64_t ldk, int64_t n, const int32_t* perm, const int32_t* offsets,
+                            int k, double* S, int64_t lds, const long long* state, void* stream);
+int pcb_kk_segment_sums_f64(const double* K, int64_t ldk, int64_t n, const int32_t* perm, const int32_t* offsets,
+                            int k, double* S, int64_t lds, const long long* state, void* stream);
+int pcb_kk_assign_f32(const float* K, int64_t ldk, const double* S, int64_t lds, int64_t n, int k,
+                      const double* cnt, double* acc, const int32_t* labels_cur, int32_t* labels_new, double* own,
+                      int* icounts, long long* state, void* stream);
+int pcb_kk_assign_f64(const double* K, int64_t ldk, const double* S, int64_t lds, int64_t n, int k,
+                      const double* cnt, double* acc, const int32_t* labels_cur, int32_t* labels_new, double* own,
+                      int* icounts, long long* state, void* stream);
+int64_t pcb_kk_repair_scratch_bytes(int64_t n, int k);
+int pcb_kk_repair_f32(const float* K, int64_t ldk, const double* S, int64_t lds, int64_t n, int k,
+                      const double* cnt, const double* acc, int32_t* labels, double* own, int* icounts,
+                      long long* state, void* scratch, int64_t scratch_bytes, void* stream);
+int pcb_kk_repair_f64(const double* K, int64_t ldk, const double* S, int64_t lds, int64_t n, int k,
+                      const double* cnt, const double* acc, int32_t* labels, double* own, int* icounts,
+                      long long* state, void* scratch, int64_t scratch_bytes, void* stream);
+int pcb_kk_finalize(const int32_t* labels, const int32_t* labels_prev, const double* own, int64_t n, int k,
+                    double* acc, double* cnt, double* obj_hist, long long* rep_hist, long long* state,
+                    int check_convergence, double tol, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,3 +5,4 @@ baseline legs.  The product package never imports this.
 """
 from .lloyd_oracle import *  # noqa: F401,F403
 from . import lloyd_oracle  # noqa: F401
+from . import kernel_oracle  # noqa: F401,E402

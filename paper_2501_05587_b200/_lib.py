@@ -59,6 +59,16 @@ SIGNATURES = {
     "pcb_centroids_from_acc_f64": (I32, [P, I32, I32, P, P, P]),
     "pcb_centroid_norms_f32": (I32, [P, I32, I32, P, P, P, I32, P]),
     "pcb_centroid_norms_f64": (I32, [P, I32, I32, P, P]),
+    "pcb_kernel_gram_f32": (I32, [P, P, I32, I64, P, P, I64, I32, F64, F64, I32, F64, P, P]),
+    "pcb_kernel_gram_f64": (I32, [P, I64, I32, P, P, I64, I32, F64, F64, I32, F64, P, P]),
+    "pcb_kk_segment_sums_f32": (I32, [P, I64, I64, P, P, I32, P, I64, P, P]),
+    "pcb_kk_segment_sums_f64": (I32, [P, I64, I64, P, P, I32, P, I64, P, P]),
+    "pcb_kk_assign_f32": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, P]),
+    "pcb_kk_assign_f64": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, P]),
+    "pcb_kk_repair_scratch_bytes": (I64, [I64, I32]),
+    "pcb_kk_repair_f32": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, I64, P]),
+    "pcb_kk_repair_f64": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, I64, P]),
+    "pcb_kk_finalize": (I32, [P, P, P, I64, I32, P, P, P, P, P, I32, F64, P]),
 }
 
 ASSIGN_AUTO, ASSIGN_ROWREG, ASSIGN_TILED, ASSIGN_TC3XTF32, ASSIGN_DELTA, ASSIGN_SCREEN = 0, 1, 2, 3, 4, 5

@@ -24,6 +24,7 @@ from typing import Any
 
 import numpy as np
 
+from .kernels import GramMethod, KernelSpec
 from .validation import as_float_matrix, normalize_dtype
 
 LABEL_DTYPE = np.int32
@@ -47,7 +48,8 @@ class TimingBreakdown:
 class KKMeansConfig:
     """Driver settings (clustering.py:43-68).
 
-    ``kernel``/``gram`` are accepted and ignored by Lloyd (clustering.py:292).
+    ``kernel``/``gram`` (KernelSpec/GramMethod, kernels.py) drive run_popcorn
+    and run_baseline; Lloyd ignores them (clustering.py:292).
     Additive fields (defaults reproduce the reference exactly):
       init                 None -> random labels + means (clustering.py:298-300);
                            an array (k, d) -> fixed initial centroids.
@@ -61,8 +63,8 @@ class KKMeansConfig:
     tol: float = 0.0
     check_convergence: bool = False
     seed: int = 0
-    kernel: Any = None
-    gram: Any = None
+    kernel: Any = field(default_factory=KernelSpec)
+    gram: Any = field(default_factory=GramMethod)
     dtype: object = np.float32
     init: Any = None
     record_label_history: bool = True

@@ -1,0 +1,170 @@
+"""Kernel K-means (f4) on the B200 against the oracle and the reference's own runs.
+
+* kernel matrix: every family, f32 (tcgen05 3xTF32 + fused epilogue) and f64
+  (SIMT), vs the oracle in f64; exactly symmetric;
+* lockstep: from each of the reference's label vectors (golden runs of
+  run_popcorn), one device iteration must give the reference's next labels,
+  except rows whose f64 top-2 distance gap is below the f32 noise of the
+  distance terms (1e-5 of |K_ii| + |c_a| + |c_b|), and the same objective
+  within 1e-6 relative (+ that noise);
+* free-running run_popcorn / run_baseline on well-separated data: identical
+  label histories to the reference;
+* repair, convergence, non-finite kernel values.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle.kernel_oracle as ko
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+G = np.load(os.path.join(ROOT, "tests", "golden", "kernel_golden.npz"))
+SPECS = {"linear": dict(family="linear"),
+         "poly2": dict(family="polynomial", gamma=1.0, coef=1.0, degree=2),
+         "poly3": dict(family="polynomial", gamma=0.5, coef=0.25, degree=3),
+         "gauss": dict(family="gaussian", gamma=1.0, sigma=1.5),
+         "sigmoid": dict(family="sigmoid", gamma=0.05, coef=0.1)}
+
+
+def _spec(kw):
+    from paper_2501_05587_b200.kernels import KernelSpec
+    return KernelSpec(**kw)
+
+
+def _device_K(P, kw):
+    import torch
+    from paper_2501_05587_b200.kernels import kernel_matrix
+    Pt = torch.from_numpy(np.ascontiguousarray(P)).cuda()
+    K = kernel_matrix(Pt, _spec(kw))
+    return K[:, :P.shape[0]].cpu().numpy()
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("n,d", [(150, 7), (300, 40), (129, 33), (1, 3), (700, 129)])
+def test_kernel_matrix(name, dt, n, d):
+    g = np.random.default_rng(n * 7 + d)
+    P = (g.standard_normal((n, d)) * (0.3 if name in ("poly3", "sigmoid") else 1.0)).astype(dt)
+    K = _device_K(P, SPECS[name])
+    assert np.array_equal(K, K.T)
+    ref = ko.apply_kernel(ko.compute_gram(P.astype(np.float64), "gemm"), **SPECS[name])
+    scale = np.abs(ref).max() + 1e-30
+    tol = 2e-5 if dt == np.float32 else 1e-12
+    # relative to the matrix scale: the f32 reference itself carries ~1e-6 of it
+    assert np.abs(K - ref).max() <= tol * scale * max(1.0, SPECS[name].get("degree", 1))
+
+
+def test_kernel_matrix_matches_reference_fixture():
+    P = G["kmat_P"]
+    for name in SPECS:
+        K = _device_K(P.astype(np.float32), SPECS[name])
+        ref = G[f"kmat_{name}_f32_syrk"]
+        assert np.abs(K - ref).max() <= 2e-5 * np.abs(ref).max()
+        K64 = _device_K(P.astype(np.float64), SPECS[name])
+        np.testing.assert_allclose(K64, G[f"kmat_{name}_f64_syrk"], rtol=1e-12, atol=1e-12 * np.abs(K64).max())
+
+
+def _run_kw(run):
+    k, iters, seed, f64 = (int(x) for x in G[f"run_{run}_meta"])
+    idx, gamma, coef, degree, sigma = G[f"run_{run}_spec"]
+    fam = SPECS[str(G["spec_names"][int(idx)])]["family"]
+    return k, iters, seed, (np.float64 if f64 else np.float32), dict(family=fam, gamma=float(gamma),
+                                                                      coef=float(coef), degree=int(degree),
+                                                                      sigma=float(sigma))
+
+
+@pytest.mark.parametrize("run", [str(r) for r in G["run_names"]])
+def test_lockstep_vs_reference_runs(run):
+    from paper_2501_05587_b200.kkmeans import KernelEngine
+    k, iters, seed, dt, kw = _run_kw(run)
+    P = G[f"run_{run}_P"].astype(dt)
+    n = P.shape[0]
+    K64 = ko.apply_kernel(ko.compute_gram(P.astype(np.float64), "gemm"), **kw)
+    eng = KernelEngine(P, k, _spec(kw), dtype=dt, max_iters=1)
+    labels = G[f"run_{run}_labels"]
+    prev = ko.init_assignments(n, k, seed)
+    for t in range(iters):
+        got = eng.step_from(prev)
+        D = ko.popcorn_distances(K64, prev, k)  # f64 restatement on the same labels
+        want = labels[t]
+        diff = np.flatnonzero(got["labels"] != want)
+        pn = np.diag(K64)
+        E = ko.spmm_neg2_kvt(K64, *ko.selection(prev, k, np.float64))
+        cterm = D[0] - pn[0] - E[0]  # centroid-norm terms c_j (same for every row)
+        scale = np.abs(pn)[:, None] + np.abs(cterm)[None, :]
+        for i in diff:
+            a, b = int(got["labels"][i]), int(want[i])
+            if got["moved"] or G[f"run_{run}_repairs"][t]:
+                break  # repair picks donors by own distance; covered by objective check
+            gap = abs(D[i, a] - D[i, b])
+            assert gap <= 1e-5 * (scale[i, a] + scale[i, b]), (run, t, i, a, b, gap)
+        ref_obj = float(D[np.arange(n), want].sum())
+        noise = 1e-6 * float(np.abs(D[np.arange(n), want]).sum() + np.abs(np.diag(K64)).sum())
+        assert abs(got["objective"] - ref_obj) <= 1e-6 * abs(ref_obj) + noise, (run, t)
+        prev = want
+
+
+def test_free_running_matches_reference_on_separated_data():
+    import paper_2501_05587_b200 as pcb
+    from paper_2501_05587_b200.kkmeans import run_baseline, run_popcorn
+    for run in ("blobs_poly2_f64", "blobs_sigmoid", "blobs_linear", "blobs_gauss"):
+        k, iters, seed, dt, kw = _run_kw(run)
+        P = G[f"run_{run}_P"]
+        cfg = pcb.KKMeansConfig(k=k, max_iters=iters, seed=seed, kernel=_spec(kw), dtype=dt)
+        res = run_popcorn(P, cfg)
+        np.testing.assert_array_equal(np.stack(res.label_history), G[f"run_{run}_labels"], err_msg=run)
+        np.testing.assert_allclose(res.objective_history, G[f"run_{run}_objective"], rtol=1e-5)
+        base = run_baseline(P, cfg)
+        np.testing.assert_array_equal(base.labels, res.labels)
+        assert res.timings.kernel_matrix_seconds > 0
+
+
+def test_repair_and_convergence():
+    import paper_2501_05587_b200 as pcb
+    from paper_2501_05587_b200.kkmeans import run_popcorn
+    run = "repair_dups"
+    k, iters, seed, dt, kw = _run_kw(run)
+    P = G[f"run_{run}_P"]
+    res = run_popcorn(P, pcb.KKMeansConfig(k=k, max_iters=iters, seed=seed, kernel=_spec(kw), dtype=dt))
+    assert res.repairs.sum() > 0
+    np.testing.assert_array_equal(res.repairs, G[f"run_{run}_repairs"])
+    assert all(np.bincount(lab, minlength=k).min() > 0 for lab in res.label_history)
+    # convergence: blobs settle within 30 iterations; the oracle agrees on the count
+    P2 = G["run_blobs_linear_P"]
+    cfg = pcb.KKMeansConfig(k=4, max_iters=30, check_convergence=True, kernel=_spec(dict(family="linear")))
+    r = run_popcorn(P2, cfg)
+    o = ko.run_popcorn(P2, 4, max_iters=30, check_convergence=True, family="linear")
+    assert r.converged and o.converged and r.iterations_run == o.iterations_run
+
+
+def test_nonfinite_kernel_raises():
+    import paper_2501_05587_b200 as pcb
+    from paper_2501_05587_b200.kkmeans import run_popcorn
+    P = np.full((40, 3), 1e15, dtype=np.float32)
+    with pytest.raises(FloatingPointError):
+        run_popcorn(P, pcb.KKMeansConfig(k=2, kernel=_spec(dict(family="polynomial", degree=3))))
+
+
+@pytest.mark.parametrize("n,d,k", [(3000, 16, 10), (5000, 64, 37), (2048, 3, 5)])
+def test_larger_lockstep_against_oracle(n, d, k):
+    """Sizes past one tile / segment chunk: device step vs the f64 oracle step."""
+    from paper_2501_05587_b200.kkmeans import KernelEngine
+    g = np.random.default_rng(n + k)
+    P = (g.random((n, d)) + g.integers(0, 4, size=(n, 1)) * 0.5).astype(np.float32)
+    kw = dict(family="polynomial", gamma=1.0 / d, coef=1.0, degree=2)
+    K64 = ko.apply_kernel(ko.compute_gram(P.astype(np.float64), "gemm"), **kw)
+    eng = KernelEngine(P, k, _spec(kw), max_iters=1)
+    prev = ko.init_assignments(n, k, 3)
+    got = eng.step_from(prev)
+    D = ko.popcorn_distances(K64, prev, k)
+    ref, moved, _, _ = ko.assignment_step(D, prev, k)  # argmin + repair (clustering.py:142-150)
+    assert got["moved"] == moved
+    diff = np.flatnonzero(got["labels"] != ref)
+    gap = ko.top2_gap(D)
+    assert np.all(gap[diff] <= 1e-5 * (np.abs(np.diag(K64))[diff] + np.abs(D[diff]).max(axis=1))), diff[:10]
+    assert len(diff) <= max(3, n // 1000)
+    own_ref = D[np.arange(n), got["labels"]]
+    np.testing.assert_allclose(got["own"], own_ref, rtol=1e-5, atol=1e-5 * np.abs(np.diag(K64)).max())
