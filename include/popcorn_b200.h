@@ -254,10 +254,12 @@ int pcb_kernel_gram_f64(const double* P, int64_t n, int d, const double* dvec, d
  *   repair        empty clusters filled by the farthest points (one block)
  *   finalize      counts/objective/changed of labels_new, history at
  *                 state[0], convergence; cnt <- counts of labels_new.     */
-int pcb_kk_segment_sums_f32(const float* K, int64_t ldk, int64_t n, const int32_t* perm, const int32_t* offsets,
-                            int k, double* S, int64_t lds, const long long* state, void* stream);
-int pcb_kk_segment_sums_f64(const double* K, int64_t ldk, int64_t n, const int32_t* perm, const int32_t* offsets,
-                            int k, double* S, int64_t lds, const long long* state, void* stream);
+int pcb_kk_segment_sums_f32(const float* K, int64_t ldk, int64_t n, int64_t ncols, const int32_t* perm,
+                            const int32_t* offsets, int k, double* S, int64_t lds, const long long* state,
+                            void* stream);
+int pcb_kk_segment_sums_f64(const double* K, int64_t ldk, int64_t n, int64_t ncols, const int32_t* perm,
+                            const int32_t* offsets, int k, double* S, int64_t lds, const long long* state,
+                            void* stream);
 int pcb_kk_assign_f32(const float* K, int64_t ldk, const double* S, int64_t lds, int64_t n, int k,
                       const double* cnt, double* acc, const int32_t* labels_cur, int32_t* labels_new, double* own,
                       int* icounts, long long* state, void* stream);
@@ -271,6 +273,25 @@ int pcb_kk_repair_f32(const float* K, int64_t ldk, const double* S, int64_t lds,
 int pcb_kk_repair_f64(const double* K, int64_t ldk, const double* S, int64_t lds, int64_t n, int k,
                       const double* cnt, const double* acc, int32_t* labels, double* own, int* icounts,
                       long long* state, void* scratch, int64_t scratch_bytes, void* stream);
+/* Rectangular kernel matrix K (na x nb, leading dimension ldk) = kernel(A B^T)
+ * (kernels.py:143-166 kernel_matrix_between: no pinned gaussian diagonal);
+ * dva/dvb = squared row norms (gaussian only).  f32 takes TF32 splits.     */
+int pcb_kernel_cross_f32(const float* A_hi, const float* A_lo, int64_t na, const float* B_hi, const float* B_lo,
+                         int64_t nb, int ld, const float* dva, const float* dvb, float* K, int64_t ldk, int family,
+                         double gamma, double coef, int degree, double sigma, unsigned long long* nonfinite,
+                         void* stream);
+int pcb_kernel_cross_f64(const double* A, int64_t na, const double* B, int64_t nb, int d, const double* dva,
+                         const double* dvb, double* K, int64_t ldk, int family, double gamma, double coef, int degree,
+                         double sigma, unsigned long long* nonfinite, void* stream);
+/* predict (estimator.py:131-147): out[i] = argmin_j self_i - 2 S[j,i]/|L_j| + cself_j
+ * with S from pcb_kk_segment_sums over the cross matrix (training rows by
+ * label), xn = |x_i|^2 and cself_j = sum_{l,m in L_j} K(l,m) / |L_j|^2.     */
+int pcb_kk_predict_f32(const double* S, int64_t lds, int64_t m, int k, const double* cnt, const double* cself,
+                       const float* xn, int family, double gamma, double coef, int degree, double sigma,
+                       int32_t* out, void* stream);
+int pcb_kk_predict_f64(const double* S, int64_t lds, int64_t m, int k, const double* cnt, const double* cself,
+                       const double* xn, int family, double gamma, double coef, int degree, double sigma,
+                       int32_t* out, void* stream);
 int pcb_kk_finalize(const int32_t* labels, const int32_t* labels_prev, const double* own, int64_t n, int k,
                     double* acc, double* cnt, double* obj_hist, long long* rep_hist, long long* state,
                     int check_convergence, double tol, void* stream);

@@ -191,3 +191,47 @@ def top2_gap(D) -> np.ndarray:
     """Per row: second smallest minus smallest entry (f64)."""
     Ds = np.sort(np.asarray(D, dtype=np.float64), axis=1)
     return Ds[:, 1] - Ds[:, 0] if Ds.shape[1] > 1 else np.full(Ds.shape[0], np.inf)
+
+
+def kernel_matrix_between(X, Y, family="polynomial", gamma=1.0, coef=1.0, degree=2, sigma=1.0):
+    """kernels.py:143-166."""
+    B = X @ Y.T
+    if family == "linear":
+        K = B
+    elif family == "polynomial":
+        K = _int_pow(gamma * B + coef, degree)
+    elif family == "sigmoid":
+        K = np.tanh(gamma * B + coef)
+    else:
+        xn = (X * X).sum(axis=1)
+        yn = (Y * Y).sum(axis=1)
+        expo = (-gamma / (sigma * sigma)) * (-2.0 * B + xn[:, None] + yn[None, :])
+        np.maximum(expo, GAUSSIAN_EXP_FLOOR, out=expo)
+        K = np.exp(expo)
+    return np.ascontiguousarray(K, dtype=X.dtype)
+
+
+def predict_kernel(X_fit, labels, k, X, family="polynomial", gamma=1.0, coef=1.0, degree=2, sigma=1.0):
+    """KernelKMeans.predict for the kernel drivers (estimator.py:137-147, 163-181);
+    also returns D for gap checks."""
+    kw = dict(family=family, gamma=gamma, coef=coef, degree=degree, sigma=sigma)
+    X = np.asarray(X, dtype=X_fit.dtype)
+    cross = kernel_matrix_between(X, X_fit, **kw)
+    sq = (X * X).sum(axis=1)
+    if family == "linear":
+        self_terms = sq
+    elif family == "polynomial":
+        self_terms = (gamma * sq + coef) ** degree
+    elif family == "sigmoid":
+        self_terms = np.tanh(gamma * sq + coef)
+    else:
+        self_terms = np.ones_like(sq)
+    members = [np.flatnonzero(labels == j) for j in range(k)]
+    sizes = np.array([max(m.size, 1) for m in members])
+    cluster_self = np.array([float(kernel_matrix_between(X_fit[m], X_fit[m], **kw).sum()) if m.size else 0.0
+                             for m in members])
+    D = np.empty((X.shape[0], k), dtype=X.dtype)
+    for j in range(k):
+        m = sizes[j]
+        D[:, j] = self_terms - (2.0 / m) * cross[:, members[j]].sum(axis=1) + cluster_self[j] / (m * m)
+    return np.argmin(D, axis=1).astype(LABEL_DTYPE), D

@@ -61,8 +61,12 @@ SIGNATURES = {
     "pcb_centroid_norms_f64": (I32, [P, I32, I32, P, P]),
     "pcb_kernel_gram_f32": (I32, [P, P, I32, I64, P, P, I64, I32, F64, F64, I32, F64, P, P]),
     "pcb_kernel_gram_f64": (I32, [P, I64, I32, P, P, I64, I32, F64, F64, I32, F64, P, P]),
-    "pcb_kk_segment_sums_f32": (I32, [P, I64, I64, P, P, I32, P, I64, P, P]),
-    "pcb_kk_segment_sums_f64": (I32, [P, I64, I64, P, P, I32, P, I64, P, P]),
+    "pcb_kk_segment_sums_f32": (I32, [P, I64, I64, I64, P, P, I32, P, I64, P, P]),
+    "pcb_kk_segment_sums_f64": (I32, [P, I64, I64, I64, P, P, I32, P, I64, P, P]),
+    "pcb_kernel_cross_f32": (I32, [P, P, I64, P, P, I64, I32, P, P, P, I64, I32, F64, F64, I32, F64, P, P]),
+    "pcb_kernel_cross_f64": (I32, [P, I64, P, I64, I32, P, P, P, I64, I32, F64, F64, I32, F64, P, P]),
+    "pcb_kk_predict_f32": (I32, [P, I64, I64, I32, P, P, P, I32, F64, F64, I32, F64, P, P]),
+    "pcb_kk_predict_f64": (I32, [P, I64, I64, I32, P, P, P, I32, F64, F64, I32, F64, P, P]),
     "pcb_kk_assign_f32": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, P]),
     "pcb_kk_assign_f64": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, P]),
     "pcb_kk_repair_scratch_bytes": (I64, [I64, I32]),

@@ -104,8 +104,12 @@ constexpr uint32_t GT_SMEM = 1024 + GT_STAGES * GT_STAGE_BYTES + 1024;
 
 __global__ void __launch_bounds__(GT_THREADS, 1)
 kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
-                      int64_t n, int num_kc, const float* __restrict__ dvec, float* __restrict__ K, int64_t ldk,
-                      KernelFn<float> fn, unsigned long long* __restrict__ nonfinite) {
+                      const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+                      int64_t n, int64_t nb, bool sym, int num_kc, const float* __restrict__ dvec,
+                      const float* __restrict__ dvec_b, float* __restrict__ K, int64_t ldk, KernelFn<float> fn,
+                      unsigned long long* __restrict__ nonfinite) {
+  // sym: K = kernel(A A^T) over the upper tiles, mirrored (B maps unused);
+  // else K (n x nb) = kernel(A B^T) over all tiles (kernel_matrix_between).
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
@@ -119,6 +123,10 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tm_hi);
     ptx::prefetch_tmap(&tm_lo);
+    if (!sym) {
+      ptx::prefetch_tmap(&tm_bhi);
+      ptx::prefetch_tmap(&tm_blo);
+    }
     for (int s = 0; s < GT_STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -135,7 +143,18 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int nt = (int)((n + GT_B - 1) / GT_B);
-  const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
+  const int ntb = (int)((nb + GT_B - 1) / GT_B);
+  const int64_t ntiles = sym ? (int64_t)nt * (nt + 1) / 2 : (int64_t)nt * ntb;
+  auto tile_of = [&](int64_t t, int& I, int& J) {
+    if (sym) {
+      upper_tile(t, nt, I, J);
+    } else {
+      I = (int)(t / ntb);
+      J = (int)(t % ntb);
+    }
+  };
+  const CUtensorMap* bhi = sym ? &tm_hi : &tm_bhi;
+  const CUtensorMap* blo = sym ? &tm_lo : &tm_blo;
 
   if (warp == 0) {
     int stage = 0;
@@ -143,7 +162,7 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
     const uint64_t pol = ptx::policy_evict_last();
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int I, J;
-      upper_tile(t, nt, I, J);
+      tile_of(t, I, J);
       for (int kc = 0; kc < num_kc; ++kc) {
         ptx::mbar_wait(&empty[stage], phase ^ 1u);
         uint8_t* st = smem + stage * GT_STAGE_BYTES;
@@ -151,8 +170,8 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
           ptx::mbar_expect_tx(&full[stage], GT_STAGE_BYTES);
           ptx::tma_load_2d(&tm_hi, &full[stage], st, kc * GT_BK, I * GT_B, pol);
           ptx::tma_load_2d(&tm_lo, &full[stage], st + GT_TILE_BYTES, kc * GT_BK, I * GT_B, pol);
-          ptx::tma_load_2d(&tm_hi, &full[stage], st + 2 * GT_TILE_BYTES, kc * GT_BK, J * GT_B, pol);
-          ptx::tma_load_2d(&tm_lo, &full[stage], st + 3 * GT_TILE_BYTES, kc * GT_BK, J * GT_B, pol);
+          ptx::tma_load_2d(bhi, &full[stage], st + 2 * GT_TILE_BYTES, kc * GT_BK, J * GT_B, pol);
+          ptx::tma_load_2d(blo, &full[stage], st + 3 * GT_TILE_BYTES, kc * GT_BK, J * GT_B, pol);
         }
         __syncwarp();
         if (++stage == GT_STAGES) { stage = 0; phase ^= 1u; }
@@ -201,8 +220,10 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
     bool bad = false;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int I, J;
-      upper_tile(t, nt, I, J);
+      tile_of(t, I, J);
       const int64_t row = (int64_t)I * GT_B + ew * 32 + lane;
+      const int64_t ncol = sym ? n : nb;
+      const float* dv_col = sym ? dvec : dvec_b;
       const float di = (fn.family == kGaussian && row < n) ? dvec[row] : 0.0f;
       ptx::mbar_wait(&tfull[abuf], aphase);
       ptx::tc_fence_after();
@@ -215,9 +236,9 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const int64_t col = c0 + c;
-          const float dj = (fn.family == kGaussian && col < n) ? __ldg(&dvec[col]) : 0.0f;
+          const float dj = (fn.family == kGaussian && col < ncol) ? __ldg(&dv_col[col]) : 0.0f;
           float x = fn.apply(v[c], di, dj);
-          if (fn.family == kGaussian && col == row) x = 1.0f;  // fill_diagonal(K, 1.0)
+          if (sym && fn.family == kGaussian && col == row) x = 1.0f;  // fill_diagonal(K, 1.0)
           v[c] = x;
         }
         // direct stores: row `row`, columns c0.. (upper part only on diagonal tiles)
@@ -225,13 +246,14 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
             const int64_t col = c0 + c;
-            if (col < n && (I != J || col >= row)) {
+            if (col < ncol && (!sym || I != J || col >= row)) {
               K[row * ldk + col] = v[c];
               bad |= !isfinite(v[c]);
             }
           }
         }
         // mirrored stores: column `row` of rows c0.. (a warp writes 32 consecutive floats per c)
+        if (sym)
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const int64_t col = c0 + c;
@@ -259,17 +281,28 @@ constexpr int GS_BK = 16;
 
 template <typename T>
 __global__ void __launch_bounds__(256)
-kernel_gram_simt_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ dvec,
-                        T* __restrict__ K, int64_t ldk, KernelFn<T> fn, unsigned long long* __restrict__ nonfinite) {
+kernel_gram_simt_kernel(const T* __restrict__ P, int64_t n, const T* __restrict__ Q, int64_t nq, bool sym, int d,
+                        const T* __restrict__ dvec, const T* __restrict__ dvec_q, T* __restrict__ K, int64_t ldk,
+                        KernelFn<T> fn, unsigned long long* __restrict__ nonfinite) {
+  // sym: K = kernel(P P^T) (upper tiles, mirrored); else K (n x nq) = kernel(P Q^T)
   __shared__ T As[GS_BK][GS_B + 1];
   __shared__ T Bs[GS_BK][GS_B + 1];
   const int nt = (int)((n + GS_B - 1) / GS_B);
-  const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
+  const int ntq = (int)((nq + GS_B - 1) / GS_B);
+  const int64_t ntiles = sym ? (int64_t)nt * (nt + 1) / 2 : (int64_t)nt * ntq;
+  const T* Qs = sym ? P : Q;
+  const T* dq = sym ? dvec : dvec_q;
+  const int64_t ncol = sym ? n : nq;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4 x 4 outputs each
   bool bad = false;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     int I, J;
-    upper_tile(t, nt, I, J);
+    if (sym) {
+      upper_tile(t, nt, I, J);
+    } else {
+      I = (int)(t / ntq);
+      J = (int)(t % ntq);
+    }
     const int64_t r0 = (int64_t)I * GS_B, c0 = (int64_t)J * GS_B;
     T acc[4][4];
 #pragma unroll
@@ -282,7 +315,7 @@ kernel_gram_simt_kernel(const T* __restrict__ P, int64_t n, int d, const T* __re
         const int kk = e % GS_BK, r = e / GS_BK;
         const int64_t gr = r0 + r, gc = c0 + r;
         As[kk][r] = (gr < n && k0 + kk < d) ? P[gr * d + k0 + kk] : T(0);
-        Bs[kk][r] = (gc < n && k0 + kk < d) ? P[gc * d + k0 + kk] : T(0);
+        Bs[kk][r] = (gc < ncol && k0 + kk < d) ? Qs[gc * d + k0 + kk] : T(0);
       }
       __syncthreads();
 #pragma unroll
@@ -307,12 +340,12 @@ kernel_gram_simt_kernel(const T* __restrict__ P, int64_t n, int d, const T* __re
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t col = c0 + tx + 16 * q;
-        if (col >= n || (I == J && col < row)) continue;
-        const T dj = fn.family == kGaussian ? dvec[col] : T(0);
+        if (col >= ncol || (sym && I == J && col < row)) continue;
+        const T dj = fn.family == kGaussian ? dq[col] : T(0);
         T x = fn.apply(acc[p][q], di, dj);
-        if (fn.family == kGaussian && col == row) x = T(1);
+        if (sym && fn.family == kGaussian && col == row) x = T(1);
         K[row * ldk + col] = x;
-        if (col != row) K[col * ldk + row] = x;
+        if (sym && col != row) K[col * ldk + row] = x;
         bad |= !isfinite(x);
       }
     }
@@ -612,7 +645,35 @@ extern "C" int pcb_kernel_gram_f32(const float* P_hi, const float* P_lo, int ld,
   const int64_t nt = (n + GT_B - 1) / GT_B;
   const int grid = (int)std::min<int64_t>(nt * (nt + 1) / 2, (int64_t)sm_count());
   kernel_gram_tc_kernel<<<grid, GT_THREADS, GT_SMEM, (cudaStream_t)stream>>>(
-      thi, tlo, n, ld / GT_BK, dvec, K, ldk, make_fn<float>(family, gamma, coef, degree, sigma), nonfinite);
+      thi, tlo, thi, tlo, n, n, true, ld / GT_BK, dvec, dvec, K, ldk,
+      make_fn<float>(family, gamma, coef, degree, sigma), nonfinite);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_kernel_cross_f32(const float* A_hi, const float* A_lo, int64_t na, const float* B_hi,
+                                    const float* B_lo, int64_t nb, int ld, const float* dva, const float* dvb,
+                                    float* K, int64_t ldk, int family, double gamma, double coef, int degree,
+                                    double sigma, unsigned long long* nonfinite, void* stream) {
+  if (na < 1 || nb < 1 || ld < 1 || ld % GT_BK != 0 || ldk < nb || !A_hi || !A_lo || !B_hi || !B_lo || !K ||
+      !nonfinite)
+    return PCB_EINVAL;
+  if (bad_family(family, degree, sigma) || (family == kGaussian && (!dva || !dvb))) return PCB_EINVAL;
+  if (na > INT32_MAX || nb > INT32_MAX) return PCB_EUNSUP;
+  CUtensorMap ahi, alo, bhi, blo;
+  int rc;
+  if ((rc = make_tmap_rows_f32(&ahi, A_hi, na, ld))) return rc;
+  if ((rc = make_tmap_rows_f32(&alo, A_lo, na, ld))) return rc;
+  if ((rc = make_tmap_rows_f32(&bhi, B_hi, nb, ld))) return rc;
+  if ((rc = make_tmap_rows_f32(&blo, B_lo, nb, ld))) return rc;
+  cudaError_t e = cudaFuncSetAttribute(kernel_gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)GT_SMEM);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t tiles = ((na + GT_B - 1) / GT_B) * ((nb + GT_B - 1) / GT_B);
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count());
+  kernel_gram_tc_kernel<<<grid, GT_THREADS, GT_SMEM, (cudaStream_t)stream>>>(
+      ahi, alo, bhi, blo, na, nb, false, ld / GT_BK, dva, dvb, K, ldk,
+      make_fn<float>(family, gamma, coef, degree, sigma), nonfinite);
   PCB_CHECK_LAUNCH();
   return 0;
 }
@@ -625,41 +686,105 @@ extern "C" int pcb_kernel_gram_f64(const double* P, int64_t n, int d, const doub
   const int64_t nt = (n + GS_B - 1) / GS_B;
   const int grid = (int)std::min<int64_t>(nt * (nt + 1) / 2, (int64_t)sm_count() * 4);
   kernel_gram_simt_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(
-      P, n, d, dvec, K, ldk, make_fn<double>(family, gamma, coef, degree, sigma), nonfinite);
+      P, n, P, n, true, d, dvec, dvec, K, ldk, make_fn<double>(family, gamma, coef, degree, sigma), nonfinite);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_kernel_cross_f64(const double* A, int64_t na, const double* B, int64_t nb, int d,
+                                    const double* dva, const double* dvb, double* K, int64_t ldk, int family,
+                                    double gamma, double coef, int degree, double sigma,
+                                    unsigned long long* nonfinite, void* stream) {
+  if (na < 1 || nb < 1 || d < 1 || ldk < nb || !A || !B || !K || !nonfinite) return PCB_EINVAL;
+  if (bad_family(family, degree, sigma) || (family == kGaussian && (!dva || !dvb))) return PCB_EINVAL;
+  const int64_t tiles = ((na + GS_B - 1) / GS_B) * ((nb + GS_B - 1) / GS_B);
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 4);
+  kernel_gram_simt_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(
+      A, na, B, nb, false, d, dva, dvb, K, ldk, make_fn<double>(family, gamma, coef, degree, sigma), nonfinite);
   PCB_CHECK_LAUNCH();
   return 0;
 }
 
 template <typename T>
-static int kk_segment_sums(const T* K, int64_t ldk, int64_t n, const int32_t* perm, const int32_t* offsets, int k,
-                           double* S, int64_t lds, const long long* state, cudaStream_t st) {
-  if (n < 1 || k < 1 || ldk < n || lds < n || !K || !perm || !offsets || !S) return PCB_EINVAL;
+static int kk_segment_sums(const T* K, int64_t ldk, int64_t n, int64_t ncols, const int32_t* perm,
+                           const int32_t* offsets, int k, double* S, int64_t lds, const long long* state,
+                           cudaStream_t st) {
+  if (n < 1 || ncols < 1 || k < 1 || ldk < ncols || lds < ncols || !K || !perm || !offsets || !S)
+    return PCB_EINVAL;
   constexpr int VEC = sizeof(T) == 4 ? 4 : 2;
   if (ldk % VEC != 0) return PCB_EINVAL;
   cudaError_t e = cudaMemsetAsync(S, 0, sizeof(double) * (size_t)k * (size_t)lds, st);
   if (e != cudaSuccess) return (int)e;
-  const int64_t colblocks = (n + 256 * VEC - 1) / (256 * VEC);
+  const int64_t colblocks = (ncols + 256 * VEC - 1) / (256 * VEC);
   // enough row chunks for ~4 CTAs per SM, each chunk at least 256 rows
   int64_t chunks = std::max<int64_t>(1, (4 * (int64_t)sm_count() + colblocks - 1) / colblocks);
   chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, n / 256));
   chunks = std::min<int64_t>(chunks, 65535);
   const int64_t chunk = (n + chunks - 1) / chunks;
   dim3 grid((unsigned)colblocks, (unsigned)chunks);
-  kk_segsum_kernel<T, VEC><<<grid, 256, 0, st>>>(K, ldk, n, n, perm, offsets, k, S, lds, chunk, state);
+  kk_segsum_kernel<T, VEC><<<grid, 256, 0, st>>>(K, ldk, n, ncols, perm, offsets, k, S, lds, chunk, state);
   PCB_CHECK_LAUNCH();
   return 0;
 }
 
-extern "C" int pcb_kk_segment_sums_f32(const float* K, int64_t ldk, int64_t n, const int32_t* perm,
-                                       const int32_t* offsets, int k, double* S, int64_t lds,
+extern "C" int pcb_kk_segment_sums_f32(const float* K, int64_t ldk, int64_t n, int64_t ncols,
+                                       const int32_t* perm, const int32_t* offsets, int k, double* S, int64_t lds,
                                        const long long* state, void* stream) {
-  return kk_segment_sums<float>(K, ldk, n, perm, offsets, k, S, lds, state, (cudaStream_t)stream);
+  return kk_segment_sums<float>(K, ldk, n, ncols, perm, offsets, k, S, lds, state, (cudaStream_t)stream);
 }
 
-extern "C" int pcb_kk_segment_sums_f64(const double* K, int64_t ldk, int64_t n, const int32_t* perm,
-                                       const int32_t* offsets, int k, double* S, int64_t lds,
+extern "C" int pcb_kk_segment_sums_f64(const double* K, int64_t ldk, int64_t n, int64_t ncols,
+                                       const int32_t* perm, const int32_t* offsets, int k, double* S, int64_t lds,
                                        const long long* state, void* stream) {
-  return kk_segment_sums<double>(K, ldk, n, perm, offsets, k, S, lds, state, (cudaStream_t)stream);
+  return kk_segment_sums<double>(K, ldk, n, ncols, perm, offsets, k, S, lds, state, (cudaStream_t)stream);
+}
+
+// ---- predict (estimator.py:131-147, kernel drivers) ------------------------
+// D[i, j] = self_i - 2 S[j, i] / |L_j| + cself_j, self_i = _self_kernel(x_i)
+// (estimator.py:163-171) from xn = |x_i|^2; argmin, lowest j on ties.
+template <typename T>
+__global__ void kk_predict_kernel(const double* __restrict__ S, int64_t lds, int64_t m, int k,
+                                  const double* __restrict__ cnt, const double* __restrict__ cself,
+                                  const T* __restrict__ xn, KernelFn<T> fn, int32_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const T sq = xn[i];
+    T self;
+    if (fn.family == kLinear) self = sq;
+    else if (fn.family == kGaussian) self = T(1);
+    else if (fn.family == kSigmoid) self = tanh(fn.add(fn.mul(fn.gamma, sq), fn.coef));
+    else self = pow(fn.add(fn.mul(fn.gamma, sq), fn.coef), (T)fn.degree);
+    double best = INFINITY;
+    int bj = 0;
+    for (int j = 0; j < k; ++j) {
+      const double mj = cnt[j] > 0 ? cnt[j] : 1.0;
+      const double dij = ((double)self - (2.0 / mj) * S[(int64_t)j * lds + i]) + cself[j];
+      if (dij < best) { best = dij; bj = j; }
+    }
+    out[i] = bj;
+  }
+}
+
+extern "C" int pcb_kk_predict_f32(const double* S, int64_t lds, int64_t m, int k, const double* cnt,
+                                  const double* cself, const float* xn, int family, double gamma, double coef,
+                                  int degree, double sigma, int32_t* out, void* stream) {
+  if (m < 1 || k < 1 || !S || !cnt || !cself || !xn || !out || bad_family(family, degree, sigma)) return PCB_EINVAL;
+  const int g = (int)std::min<int64_t>((m + 255) / 256, 8L * sm_count());
+  kk_predict_kernel<float><<<g, 256, 0, (cudaStream_t)stream>>>(S, lds, m, k, cnt, cself, xn,
+                                                                 make_fn<float>(family, gamma, coef, degree, sigma), out);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_kk_predict_f64(const double* S, int64_t lds, int64_t m, int k, const double* cnt,
+                                  const double* cself, const double* xn, int family, double gamma, double coef,
+                                  int degree, double sigma, int32_t* out, void* stream) {
+  if (m < 1 || k < 1 || !S || !cnt || !cself || !xn || !out || bad_family(family, degree, sigma)) return PCB_EINVAL;
+  const int g = (int)std::min<int64_t>((m + 255) / 256, 8L * sm_count());
+  kk_predict_kernel<double><<<g, 256, 0, (cudaStream_t)stream>>>(S, lds, m, k, cnt, cself, xn,
+                                                                   make_fn<double>(family, gamma, coef, degree, sigma),
+                                                                   out);
+  PCB_CHECK_LAUNCH();
+  return 0;
 }
 
 template <typename T>

@@ -93,7 +93,7 @@ class KernelEngine:
             events[0].record()
         L.call("pcb_sort_by_label", _p(prev), n, k, _p(self.cnt), _p(self.offsets), _p(self.cursor),
                _p(self.perm), _p(self.state), _stream())
-        L.call(f"pcb_kk_segment_sums_{sfx}", _p(self.K), self.ldk, n, _p(self.perm), _p(self.offsets), k,
+        L.call(f"pcb_kk_segment_sums_{sfx}", _p(self.K), self.ldk, n, n, _p(self.perm), _p(self.offsets), k,
                _p(self.S), self.ldk, _p(self.state), _stream())
         L.call(f"pcb_kk_assign_{sfx}", _p(self.K), self.ldk, _p(self.S), self.ldk, n, k, _p(self.cnt),
                _p(self.acc), _p(prev), _p(new), _p(self.own), _p(self.icounts), _p(self.state), _stream())
@@ -157,7 +157,7 @@ class KernelEngine:
             self.acc.zero_()
             L.call("pcb_sort_by_label", _p(lab), self.n, self.k, _p(self.cnt), _p(self.offsets), _p(self.cursor),
                    _p(self.perm), None, _stream())
-            L.call(f"pcb_kk_segment_sums_{self.sfx}", _p(self.K), self.ldk, self.n, _p(self.perm),
+            L.call(f"pcb_kk_segment_sums_{self.sfx}", _p(self.K), self.ldk, self.n, self.n, _p(self.perm),
                    _p(self.offsets), self.k, _p(self.S), self.ldk, None, _stream())
             cnt = self.cnt[:self.k].cpu().numpy()
             S = self.S[:, :self.n]
@@ -194,3 +194,72 @@ def run_baseline(points, cfg) -> "ClusteringResult":
 
 
 __all__ = ["KernelEngine", "run_popcorn", "run_baseline", "GramMethod"]
+
+
+def cluster_terms(X_fit, labels, k: int, spec: KernelSpec):
+    """(sizes, c_j) for predict: sizes = max(|L_j|, 1) (estimator.py:175),
+    c_j = sum_{l,m in L_j} K(x_l, x_m) / sizes_j^2 — from the device K."""
+    dt = np.asarray(X_fit).dtype
+    eng = KernelEngine(X_fit, k, spec, dtype=dt, max_iters=1)
+    eng.set_labels(labels)
+    cnt, c = eng.cluster_terms()
+    sizes = np.maximum(cnt, 1.0)
+    c = np.where(cnt > 0, c * (cnt / sizes) ** 2, 0.0)  # empty cluster: self term 0
+    return sizes, c
+
+
+def predict_labels(X_fit, labels, k: int, spec: KernelSpec, sizes, cself, X) -> np.ndarray:
+    """Kernel-trick nearest centroid (estimator.py:137-147) on the device:
+    Kx = kernel(X_fit X^T) (n x m, tcgen05 3xTF32 / SIMT f64), per-cluster
+    row sums of Kx over the training labels, then argmin of
+    self(x) - 2 sum/|L_j| + c_j."""
+    from .kernels import FAMILY_CODE
+    dev = require_cuda(None)
+    dt = np.asarray(X_fit).dtype
+    f64 = dt == np.float64
+    td = torch.float64 if f64 else torch.float32
+    sfx = "f64" if f64 else "f32"
+    with torch.cuda.device(dev):
+        A = torch.from_numpy(np.ascontiguousarray(X_fit)).to(dev)
+        B = torch.from_numpy(np.ascontiguousarray(X, dtype=dt)).to(dev)
+        n, d = int(A.shape[0]), int(A.shape[1])
+        m = int(B.shape[0])
+        ldm = padded_ld(m)
+        an = torch.empty(n, dtype=td, device=dev)
+        bn = torch.empty(m, dtype=td, device=dev)
+        L.call(f"pcb_point_norms_{sfx}", _p(A), n, d, _p(an), _stream())
+        L.call(f"pcb_point_norms_{sfx}", _p(B), m, d, _p(bn), _stream())
+        Kx = torch.empty((n, ldm), dtype=td, device=dev)
+        nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
+        kargs = (FAMILY_CODE[spec.family], float(spec.gamma), float(spec.coef), int(spec.degree),
+                 float(spec.sigma))
+        if f64:
+            L.call("pcb_kernel_cross_f64", _p(A), n, _p(B), m, d, _p(an), _p(bn), _p(Kx), ldm, *kargs,
+                   _p(nonfinite), _stream())
+        else:
+            ld = (d + 31) // 32 * 32
+            ah = torch.empty((n, ld), dtype=torch.float32, device=dev)
+            al = torch.empty_like(ah)
+            bh = torch.empty((m, ld), dtype=torch.float32, device=dev)
+            bl = torch.empty_like(bh)
+            L.call("pcb_split_tf32", _p(A), n, d, ld, _p(ah), _p(al), _stream())
+            L.call("pcb_split_tf32", _p(B), m, d, ld, _p(bh), _p(bl), _stream())
+            L.call("pcb_kernel_cross_f32", _p(ah), _p(al), n, _p(bh), _p(bl), m, ld, _p(an), _p(bn), _p(Kx), ldm,
+                   *kargs, _p(nonfinite), _stream())
+        lab = torch.from_numpy(np.ascontiguousarray(labels, dtype=np.int32)).to(dev)
+        cnt = torch.zeros(k + 2, dtype=torch.float64, device=dev)
+        L.call("pcb_count_labels", _p(lab), None, n, k, 0, _p(cnt), None, _stream())
+        offsets = torch.empty(k + 1, dtype=torch.int32, device=dev)
+        cursor = torch.empty(k, dtype=torch.int32, device=dev)
+        perm = torch.empty(n, dtype=torch.int32, device=dev)
+        L.call("pcb_sort_by_label", _p(lab), n, k, _p(cnt), _p(offsets), _p(cursor), _p(perm), None, _stream())
+        S = torch.empty((k, ldm), dtype=torch.float64, device=dev)
+        L.call(f"pcb_kk_segment_sums_{sfx}", _p(Kx), ldm, n, m, _p(perm), _p(offsets), k, _p(S), ldm, None,
+               _stream())
+        sz = torch.from_numpy(np.ascontiguousarray(sizes, dtype=np.float64)).to(dev)
+        cs = torch.from_numpy(np.ascontiguousarray(cself, dtype=np.float64)).to(dev)
+        out = torch.empty(m, dtype=torch.int32, device=dev)
+        L.call(f"pcb_kk_predict_{sfx}", _p(S), ldm, m, k, _p(sz), _p(cs), _p(bn), *kargs, _p(out), _stream())
+        if int(nonfinite.item()) != 0:
+            raise FloatingPointError(f"kernel_matrix_between[{spec.family}] produced non-finite values")
+        return out.cpu().numpy()

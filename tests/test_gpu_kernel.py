@@ -168,3 +168,27 @@ def test_larger_lockstep_against_oracle(n, d, k):
     assert len(diff) <= max(3, n // 1000)
     own_ref = D[np.arange(n), got["labels"]]
     np.testing.assert_allclose(got["own"], own_ref, rtol=1e-5, atol=1e-5 * np.abs(np.diag(K64)).max())
+
+
+@pytest.mark.parametrize("name", ["poly2", "gauss", "sigmoid", "linear"])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_estimator_predict_kernel_trick(name, dt):
+    """KernelKMeans(algorithm='popcorn').predict vs the reference's predict
+    (estimator.py:131-147) restated in the oracle, on new points."""
+    import paper_2501_05587_b200 as pcb
+    g = np.random.default_rng(11)
+    centers = g.uniform(-2, 2, size=(4, 5))
+    X = (centers[g.integers(0, 4, 400)] + g.normal(0, 0.3, (400, 5))).astype(dt)
+    Xn = (centers[g.integers(0, 4, 150)] + g.normal(0, 0.3, (150, 5))).astype(dt)
+    kw = SPECS[name]
+    est = pcb.KernelKMeans(n_clusters=4, kernel=kw["family"], gamma=kw.get("gamma", 1.0),
+                           coef0=kw.get("coef", 1.0), degree=kw.get("degree", 2), sigma=kw.get("sigma", 1.0),
+                           max_iter=30, dtype=np.dtype(dt).name).fit(X)
+    assert est.converged_
+    np.testing.assert_array_equal(est.predict(X), est.labels_)
+    got = est.predict(Xn)
+    ref, D = ko.predict_kernel(X.astype(np.float64), est.labels_, 4, Xn.astype(np.float64), **kw)
+    diff = np.flatnonzero(got != ref)
+    gap = ko.top2_gap(D)
+    assert np.all(gap[diff] <= 1e-5 * (np.abs(D[diff]).max(axis=1) + 1.0)), diff
+    assert est.score() == -est.inertia_

@@ -151,7 +151,8 @@ def test_predict_matches_assignment():
     from paper_2501_05587_b200 import KernelKMeans
     rng = make_rng(5)
     X = np.vstack([rng.normal(loc=c, scale=0.4, size=(20, 3)) for c in (0.0, 5.0, 10.0)])
-    est = KernelKMeans(n_clusters=3, random_state=3, check_convergence=True, max_iter=100).fit(X)
+    est = KernelKMeans(n_clusters=3, algorithm="lloyd", random_state=3, check_convergence=True,
+                       max_iter=100).fit(X)
     np.testing.assert_array_equal(est.predict(X), est.labels_)
     assert est.score() == -est.inertia_
     assert est.cluster_centers_.shape == (3, 3)
