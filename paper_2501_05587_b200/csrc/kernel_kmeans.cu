@@ -97,10 +97,10 @@ __device__ __forceinline__ void upper_tile(int64_t t, int nt, int& I, int& J) {
 constexpr int GT_B = 128;       // tile edge (UMMA M = N = 128)
 constexpr int GT_BK = 32;
 constexpr int GT_STAGES = 3;
-constexpr int GT_THREADS = 256;
+constexpr int GT_THREADS = 384;  // 4 control warps + 8 epilogue warps (2 per TMEM lane group)
 constexpr uint32_t GT_TILE_BYTES = GT_B * GT_BK * 4;                 // 16 KB
 constexpr uint32_t GT_STAGE_BYTES = 4 * GT_TILE_BYTES;               // A hi/lo, B hi/lo
-constexpr uint32_t GT_SMEM = 1024 + GT_STAGES * GT_STAGE_BYTES + 1024;
+constexpr uint32_t GT_SMEM = 1024 + GT_STAGES * GT_STAGE_BYTES + 1024 + 8 * 32 * 33 * 4;
 
 __global__ void __launch_bounds__(GT_THREADS, 1)
 kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
@@ -133,7 +133,7 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], 128);
+      ptx::mbar_init(&tempty[b], 256);
     }
     ptx::fence_barrier_init();
   }
@@ -214,7 +214,9 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
       if (abuf == 0) aphase ^= 1u;
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;
+    // warp (ew, h): TMEM lane group ew = warp % 4, column half h (64 columns)
+    const int ew = warp & 3, h = (warp - 4) >> 2;
+    float* xt = reinterpret_cast<float*>(bar_area + 1024) + (warp - 4) * 32 * 33;  // per-warp transpose tile
     int abuf = 0;
     uint32_t aphase = 0;
     bool bad = false;
@@ -229,7 +231,7 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
       ptx::tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(abuf * GT_B);
 #pragma unroll 1
-      for (int cb = 0; cb < GT_B; cb += 32) {
+      for (int cb = h * 64; cb < h * 64 + 64; cb += 32) {
         float v[32];
         ptx::tmem_ld_32x32b_x32(taddr + cb, v);
         const int64_t c0 = (int64_t)J * GT_B + cb;
@@ -241,16 +243,25 @@ kernel_gram_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_co
           if (sym && fn.family == kGaussian && col == row) x = 1.0f;  // fill_diagonal(K, 1.0)
           v[c] = x;
         }
-        // direct stores: row `row`, columns c0.. (upper part only on diagonal tiles)
-        if (row < n) {
+        // direct stores: row `row`, columns c0.. (upper part only on diagonal
+        // tiles), transposed through shared memory so that every warp store
+        // writes 32 consecutive floats of one row (thread = column)
+        {
+          const int64_t row0 = (int64_t)I * GT_B + ew * 32;
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
             const int64_t col = c0 + c;
-            if (col < ncol && (!sym || I != J || col >= row)) {
-              K[row * ldk + col] = v[c];
-              bad |= !isfinite(v[c]);
-            }
+            if (row < n && col < ncol && (!sym || I != J || col >= row)) bad |= !isfinite(v[c]);
+            xt[lane * 33 + c] = v[c];
           }
+          __syncwarp();
+          const int64_t col = c0 + lane;
+#pragma unroll 4
+          for (int r = 0; r < 32; ++r) {
+            const int64_t rr = row0 + r;
+            if (rr < n && col < ncol && (!sym || I != J || col >= rr)) K[rr * ldk + col] = xt[r * 33 + lane];
+          }
+          __syncwarp();
         }
         // mirrored stores: column `row` of rows c0.. (a warp writes 32 consecutive floats per c)
         if (sym)
@@ -402,18 +413,24 @@ kk_segsum_kernel(const T* __restrict__ K, int64_t ldk, int64_t n, int64_t ncols,
     for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
     dirty = false;
   };
+  // software pipeline: K rows of batch i+1 are in flight while batch i is
+  // accumulated, and their perm[] entries were fetched one batch earlier.
+  // K is streamed once per iteration (>> L2): loads are evict-first (.cs).
   constexpr int U = 4;
-  for (int64_t s = s0; s < s1; s += U) {
-    T x[U][VEC];
+  auto load_perm = [&](int64_t sb, int (&p)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) p[u] = (sb + u < s1) ? __ldg(&perm[sb + u]) : -1;
+  };
+  auto load_x = [&](const int (&p)[U], T (&x)[U][VEC]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (s + u < s1 && in) {
-        const T* src = K + (int64_t)perm[s + u] * ldk + c;
+      if (p[u] >= 0 && in) {
+        const T* src = K + (int64_t)p[u] * ldk + c;
         if constexpr (VEC == 4) {
-          const float4 q = *reinterpret_cast<const float4*>(src);
+          const float4 q = __ldcs(reinterpret_cast<const float4*>(src));
           x[u][0] = q.x; x[u][1] = q.y; x[u][2] = q.z; x[u][3] = q.w;
         } else {
-          const double2 q = *reinterpret_cast<const double2*>(src);
+          const double2 q = __ldcs(reinterpret_cast<const double2*>(src));
           x[u][0] = q.x; x[u][1] = q.y;
         }
       } else {
@@ -421,10 +438,12 @@ kk_segsum_kernel(const T* __restrict__ K, int64_t ldk, int64_t n, int64_t ncols,
         for (int v = 0; v < VEC; ++v) x[u][v] = T(0);
       }
     }
+  };
+  auto accum = [&](int64_t sb, const T (&x)[U][VEC]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (s + u >= s1) break;
-      while (s + u >= seg_end) {  // next non-empty segment
+      if (sb + u >= s1) break;
+      while (sb + u >= seg_end) {  // next non-empty segment
         flush();
         ++seg;
         seg_end = offsets[seg + 1];
@@ -433,6 +452,19 @@ kk_segsum_kernel(const T* __restrict__ K, int64_t ldk, int64_t n, int64_t ncols,
       for (int v = 0; v < VEC; ++v) acc[v] += (double)x[u][v];
       dirty = true;
     }
+  };
+  int pa[U], pb[U];
+  T xa[U][VEC], xb[U][VEC];
+  load_perm(s0, pa);
+  load_x(pa, xa);
+  load_perm(s0 + U, pb);
+  for (int64_t s = s0; s < s1; s += 2 * U) {
+    load_x(pb, xb);            // rows of batch s + U
+    load_perm(s + 2 * U, pa);  // perm of batch s + 2U
+    accum(s, xa);
+    load_x(pa, xa);            // rows of batch s + 2U
+    load_perm(s + 3 * U, pb);
+    accum(s + U, xb);
   }
   flush();
 }
@@ -716,9 +748,10 @@ static int kk_segment_sums(const T* K, int64_t ldk, int64_t n, int64_t ncols, co
   cudaError_t e = cudaMemsetAsync(S, 0, sizeof(double) * (size_t)k * (size_t)lds, st);
   if (e != cudaSuccess) return (int)e;
   const int64_t colblocks = (ncols + 256 * VEC - 1) / (256 * VEC);
-  // enough row chunks for ~4 CTAs per SM, each chunk at least 256 rows
-  int64_t chunks = std::max<int64_t>(1, (4 * (int64_t)sm_count() + colblocks - 1) / colblocks);
-  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, n / 256));
+  // many small work items (~32 per SM) so the hardware scheduler balances the
+  // SMs; each chunk at least 128 rows (one flush per segment boundary)
+  int64_t chunks = std::max<int64_t>(1, (32 * (int64_t)sm_count() + colblocks - 1) / colblocks);
+  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, n / 128));
   chunks = std::min<int64_t>(chunks, 65535);
   const int64_t chunk = (n + chunks - 1) / chunks;
   dim3 grid((unsigned)colblocks, (unsigned)chunks);
