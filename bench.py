@@ -263,7 +263,7 @@ def main():
     peaks, peak_src = _peaks()
     n_local = hi - lo
     flops = 2.0 * n_local * k * d  # algorithmic: one dot product per point-centroid pair
-    if d <= 32 and eng.variant not in ("tc3xtf32", "tc1xtf32s"):
+    if d <= 32 and eng.variant not in ("tc3xtf32", "tc1xtf32s", "bf16s"):
         # small-d FFMA path: report against HBM (bytes of P read + labels)
         traffic_alg = n_local * (4 * d + 8 + 4) + k * d * 4
         roof = {"bound": "hbm", "achieved": traffic_alg / (kern_ms * 1e-3) / 1e9,
@@ -275,6 +275,8 @@ def main():
         tf32 = peaks["bf16_tflops"] / 2.0
         if eng.variant == "tc3xtf32":  # three TF32 products per dot product
             peak, src = tf32 / 3.0, "3xTF32 effective = bf16 burst / 6"
+        elif eng.variant == "bf16s":  # one BF16 (kind::f16) pass
+            peak, src = peaks["bf16_tflops"], "bf16 burst (dense)"
         else:
             peak, src = tf32, "TF32 = bf16 burst / 2"
         roof = {"bound": "tensor", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": peak,
@@ -282,7 +284,8 @@ def main():
     roof["frac"] = roof["achieved"] / roof["peak"]
     scr = {"res": "assign_screen_res_kernel", "pair": "assign_screen_2sm_kernel",
            "stream": "assign_screen_kernel"}.get(os.environ.get("PCB_SCREEN_IMPL", "res"), "assign_screen_res_kernel")
-    roof["kernel"] = {"tc1xtf32s": scr, "tc3xtf32": "assign_tc3xtf32_kernel"}.get(
+    roof["kernel"] = {"tc1xtf32s": scr, "tc3xtf32": "assign_tc3xtf32_kernel",
+                      "bf16s": "assign_screen_bf16_kernel"}.get(
         eng.variant, f"assign[{eng.variant}]")
     roof["kernel_ms"] = kern_ms
     roof["algorithmic_per_launch"] = f"2*n*k*d = {flops:.4g} flop" if roof["unit"] == "TFLOP/s" else \
@@ -306,7 +309,7 @@ def main():
                    "l2": "inputs larger than L2" if n * d * 4 > 126e6 else "inputs fit in L2 (no flush)"},
         "dists_per_sec": n * k / (ms_per_step * 1e-3),
         "roofline": roof,
-        "gpu_launches": (12 if eng.variant == "tc1xtf32s" else 6) * K,
+        "gpu_launches": {"tc1xtf32s": 12, "bf16s": 15}.get(eng.variant, 6) * K,
         "screen_ambiguous_rows_last_iter": amb,
         "clocks": clocks,
     }

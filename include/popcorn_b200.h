@@ -44,6 +44,7 @@ extern "C" {
 #define PCB_ASSIGN_TC3XTF32  3  /* tcgen05 3xTF32, TMEM accumulators (f32)  */
 #define PCB_ASSIGN_DELTA     4  /* delta-chunked P.C.P^T ablation (f32)     */
 #define PCB_ASSIGN_SCREEN    5  /* tcgen05 1xTF32 certified screening (f32) */
+#define PCB_ASSIGN_SCREEN_BF16 6 /* tcgen05 BF16 certified screening + exact candidates (f32, d <= 256) */
 
 int         pcb_abi_version(void);
 const char* pcb_error_string(int code);
@@ -153,6 +154,33 @@ int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_l
                               int32_t* sub_labels, const float* pnorm, const float* C_hi,
                               const float* C_lo, const float* cnorm, int k, int32_t* labels,
                               const long long* state, void* stream);
+/* Certified BF16 screening variant ("bf16s", see assign_screen_bf16.cu):
+ * one BF16 tensor-core pass (kind::f16) on RN-rounded copies P_b / C_b (row
+ * stride ldb = pcb_screen_bf16_ld(d) BF16 elements) with the same rigorous
+ * per-row bound as the TF32 screen.  Pass 1 labels certified rows and lists
+ * the others with a candidate threshold (amb_list / amb_count / amb_thr,
+ * caller zeroes amb_count); pcb_resolve_screen_bf16 recomputes their keys
+ * (pass 2, compact copy sub_b), collects the candidate columns (<=
+ * pcb_screen_bf16_ncand() per row into cand / cand_n) and takes the exact f64
+ * argmin over them.  Rows with more candidates, or all rows when amb_count >
+ * bypass, are listed in ovf_list / ovf_count for pcb_resolve_ambiguous_f32.
+ *   pcb_screen_prep_points_bf16:    P_b, anorm, danorm, bstat[2] = OFF (per fit)
+ *   pcb_screen_prep_centroids_bf16: C_b, bnorm, dbnorm, bstat[0..1] (per update) */
+int pcb_screen_bf16_ld(int d);
+int pcb_screen_bf16_ncand(void);
+int pcb_screen_prep_points_bf16(const float* P, int64_t n, int d, int ldb, void* P_b, float* anorm,
+                                float* danorm, float* bstat /* 4 */, void* stream);
+int pcb_screen_prep_centroids_bf16(const float* C, int k, int d, int ldb, void* C_b, float* bnorm,
+                                   float* dbnorm, float* bstat, void* stream);
+int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const void* C_b, int k,
+                           const float* cnorm, const float* anorm, const float* danorm,
+                           const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
+                           float* amb_thr, const long long* state, void* stream);
+int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
+                            const float* C, int k, const float* cnorm, const float* bstat,
+                            const int* amb_list, const int* amb_count, const float* amb_thr,
+                            int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
+                            int* ovf_list, int* ovf_count, const long long* state, void* stream);
 int pcb_count_labels(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
                      double* acc, const long long* state, void* stream);
 

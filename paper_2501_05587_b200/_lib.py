@@ -42,6 +42,12 @@ SIGNATURES = {
     "pcb_screen_prep_centroids": (I32, [P, I32, I32, P, P, P, P]),
     "pcb_assign_screen_f32": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P]),
     "pcb_resolve_ambiguous_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P, P, P, I32, P, P, P]),
+    "pcb_screen_bf16_ld": (I32, [I32]),
+    "pcb_screen_bf16_ncand": (I32, []),
+    "pcb_screen_prep_points_bf16": (I32, [P, I64, I32, I32, P, P, P, P, P]),
+    "pcb_screen_prep_centroids_bf16": (I32, [P, I32, I32, I32, P, P, P, P, P]),
+    "pcb_assign_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P, P]),
+    "pcb_resolve_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, I32, P, P, P, P, P, I64, P, P, P, P, P, P, P, P]),
     "pcb_count_labels": (I32, [P, P, I64, I32, I32, P, P, P]),
     "pcb_sort_by_label": (I32, [P, I64, I32, P, P, P, P, P, P]),
     "pcb_segment_sums_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P]),
@@ -76,8 +82,10 @@ SIGNATURES = {
 }
 
 ASSIGN_AUTO, ASSIGN_ROWREG, ASSIGN_TILED, ASSIGN_TC3XTF32, ASSIGN_DELTA, ASSIGN_SCREEN = 0, 1, 2, 3, 4, 5
+ASSIGN_SCREEN_BF16 = 6
 VARIANTS = {"auto": ASSIGN_AUTO, "rowreg": ASSIGN_ROWREG, "tiled": ASSIGN_TILED,
-            "tc3xtf32": ASSIGN_TC3XTF32, "delta": ASSIGN_DELTA, "tc1xtf32s": ASSIGN_SCREEN}
+            "tc3xtf32": ASSIGN_TC3XTF32, "delta": ASSIGN_DELTA, "tc1xtf32s": ASSIGN_SCREEN,
+            "bf16s": ASSIGN_SCREEN_BF16}
 STATE_WORDS = 8
 
 _lib = None

@@ -1,0 +1,615 @@
+// Certified BF16 screening (variant "bf16s"), A-resident, d <= 256.
+//
+// Same certificate as the TF32 screen (assign_screen.cu header), with one
+// BF16 tensor-core pass (tcgen05.mma kind::f16, twice the TF32 rate, half the
+// operand bytes) over RN-rounded operands p~ = bf16(p), c~ = bf16(c):
+//
+//   |<p,c> - <p~,c~>| <= |dp||c~| + |p~||dc| + |dp||dc| + acc
+//
+// (dp = p - p~, dc = c - c~ exact residual norms per row / per centroid; acc
+// bounds the tensor core's f32 accumulation: BF16 products are exact in f32,
+// each K=16 MMA adds at most (16 + 1) roundings relative to the running sum of
+// |products|, charged here as (#MMA + 2) * 2^-19 of |p~||c~|, 16x the f32 unit
+// roundoff per MMA).  Rows whose second-best key is within 2E of the best are
+// ambiguous; unlike the TF32 screen they are resolved in two cheap steps:
+//
+//   pass 1 (CAND = false) all rows: labels of certified rows; ambiguous rows
+//          are appended with their threshold thr = R1 + 2E (+ packing slack)
+//   pass 2 (CAND = true)  the ambiguous rows only (gathered into a compact
+//          copy): the same MMA recomputes every key and the epilogue emits the
+//          candidate columns {j : key_j <= thr} (the exact argmin is among them:
+//          key_j* <= exact_j* + E <= exact_jmin + E <= R1 + 2E)
+//   exact  (pcb_screen_exact) one warp per ambiguous row evaluates
+//          sum_t (p_t - c_jt)^2 in f64 for its <= SB_NCAND candidates and takes
+//          the smallest (lowest index on ties, dense.py:56-68); rows with more
+//          candidates (e.g. right after a random-label init, when every
+//          centroid sits near the global mean) go to the 3xTF32 resolver.
+//
+// Layout (per CTA, 384 threads, one CTA per SM):
+//   smem   A: [2 row tiles][NKC chunks][128 rows x 128 B]  (64 BF16 per row chunk)
+//          B: 4-stage ring of [128 centroids x 128 B] chunks
+//   TMEM   [2 buffers][2 row tiles][128 columns] = 512 columns
+//   warps  0 A producer, 3 B producer, 1 MMA issuer (M=128 N=128 K=16),
+//          2 TMEM allocator, 4-11 epilogue (warp (g, h): lanes 32g.. of tile h)
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include "pcb_common.cuh"
+#include "pcb_launch.cuh"
+#include "screen_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace pcb {
+
+constexpr int SB_BN = 128;
+constexpr int SB_STAGES = 4;
+constexpr int SB_THREADS = 384;
+constexpr int SB_BKE = 64;      // BF16 elements per 128-byte swizzle row
+constexpr int SB_NCAND = 8;     // candidate slots per ambiguous row (pass 2)
+
+template <int NKC>
+struct SbCfg {
+  static constexpr uint32_t kTileBytes = 128 * 128;                 // 128 rows x 128 B
+  static constexpr uint32_t kABytes = 2 * NKC * kTileBytes;         // resident A (2 row tiles)
+  static constexpr uint32_t kBBytes = SB_BN * 128;                  // 16 KB per B stage
+  static constexpr uint32_t kBarBytes = 1024;
+  static constexpr uint32_t kSmem = 1024 + kABytes + SB_STAGES * kBBytes + kBarBytes + SC_KMAX * 4;
+  static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
+};
+
+// Rows handled by a launch: pass 1 = n; pass 2 = the device-side ambiguous
+// count, or 0 when the resolver is bypassed (count above `bypass`).
+__device__ __forceinline__ int64_t sb_rows(int64_t n, const int* amb_count, int64_t bypass) {
+  if (amb_count == nullptr) return n;
+  const int64_t c = *(volatile const int*)amb_count;
+  return c > bypass ? 0 : c;
+}
+
+template <int NKC, bool CAND>
+__global__ void __launch_bounds__(SB_THREADS, 1)
+assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                          const float* __restrict__ anorm, const float* __restrict__ danorm,
+                          const float* __restrict__ cnorm, const float* __restrict__ bstat, int64_t n_in, int k,
+                          int32_t* __restrict__ labels, int* __restrict__ amb_list, int* __restrict__ amb_count,
+                          float* __restrict__ amb_thr, int64_t bypass, int* __restrict__ cand,
+                          int* __restrict__ cand_n, const long long* __restrict__ state) {
+  using Cfg = SbCfg<NKC>;
+  if (stopped(state)) return;
+  const int64_t n = CAND ? sb_rows(n_in, amb_count, bypass) : n_in;
+  if (n == 0) return;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + Cfg::kABytes;
+  uint8_t* bar_area = sB + SB_STAGES * Cfg::kBBytes;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(bar_area);  // [NKC]
+  uint64_t* aempty = afull + NKC;                            // [NKC]
+  uint64_t* full = aempty + NKC;                             // [STAGES]
+  uint64_t* empty = full + SB_STAGES;                        // [STAGES]
+  uint64_t* tfull = empty + SB_STAGES;                       // [2]
+  uint64_t* tempty = tfull + 2;                              // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* cprime = reinterpret_cast<float*>(bar_area + Cfg::kBarBytes);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (k + SB_BN - 1) / SB_BN;
+  const float OFF = bstat[2];
+  for (int j = threadIdx.x; j < ntiles * SB_BN; j += blockDim.x)
+    cprime[j] = j < k ? cnorm[j] + OFF : 3.0e38f;
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm_a);
+    ptx::prefetch_tmap(&tm_b);
+    for (int c = 0; c < NKC; ++c) {
+      ptx::mbar_init(&afull[c], 1);
+      ptx::mbar_init(&aempty[c], 1);
+    }
+    for (int s = 0; s < SB_STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 256);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t npairs = (n + 255) / 256;
+
+  if (warp == 0) {
+    // ---------------- A producer: both row tiles, chunk by chunk ----------------
+    const uint64_t pol = ptx::policy_evict_first();
+    int it = 0;
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
+      for (int c = 0; c < NKC; ++c) {
+        if (it > 0) ptx::mbar_wait(&aempty[c], (uint32_t)((it - 1) & 1));
+        if (ptx::elect_one()) {
+          ptx::mbar_expect_tx(&afull[c], 2 * Cfg::kTileBytes);
+          ptx::tma_load_2d(&tm_a, &afull[c], sA + (0 * NKC + c) * Cfg::kTileBytes, c * SB_BKE, (int)(pr * 256), pol);
+          ptx::tma_load_2d(&tm_a, &afull[c], sA + (1 * NKC + c) * Cfg::kTileBytes, c * SB_BKE,
+                           (int)(pr * 256 + 128), pol);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 3) {
+    // ---------------- B producer: centroid chunks through the ring ----------------
+    const uint64_t pol = ptx::policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+      for (int nt = 0; nt < ntiles; ++nt) {
+        for (int c = 0; c < NKC; ++c) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1u);
+          if (ptx::elect_one()) {
+            ptx::mbar_expect_tx(&full[stage], Cfg::kBBytes);
+            ptx::tma_load_2d(&tm_b, &full[stage], sB + stage * Cfg::kBBytes, c * SB_BKE, nt * SB_BN, pol);
+          }
+          __syncwarp();
+          if (++stage == SB_STAGES) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (warp-uniform loop, one elected lane issues) ----------------
+    constexpr uint32_t idesc = ptx::idesc_bf16<128, SB_BN>();
+    int stage = 0;
+    uint32_t phase = 0;
+    int abuf = 0;
+    uint32_t aphase = 0;
+    int it = 0;
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
+      for (int nt = 0; nt < ntiles; ++nt) {
+        ptx::mbar_wait(&tempty[abuf], aphase ^ 1u);
+        ptx::tc_fence_after();
+        const uint32_t d0 = tmem + (uint32_t)(abuf * 256);
+        for (int c = 0; c < NKC; ++c) {
+          if (nt == 0) ptx::mbar_wait(&afull[c], (uint32_t)(it & 1));
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint64_t a0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (0 * NKC + c) * Cfg::kTileBytes));
+          const uint64_t a1 = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (1 * NKC + c) * Cfg::kTileBytes));
+          const uint64_t bd = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * Cfg::kBBytes));
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {           // 4 x K=16 per 128-byte chunk
+              const uint64_t off = (uint64_t)(ks * 32) >> 4;
+              ptx::umma_f16(d0, a0 + off, bd + off, idesc, (c | ks) != 0);
+              ptx::umma_f16(d0 + 128, a1 + off, bd + off, idesc, (c | ks) != 0);
+            }
+            ptx::umma_commit(&empty[stage]);
+            if (nt + 1 == ntiles) ptx::umma_commit(&aempty[c]);  // A chunk free for the next pair
+          }
+          __syncwarp();
+          if (++stage == SB_STAGES) { stage = 0; phase ^= 1u; }
+        }
+        if (ptx::elect_one()) ptx::umma_commit(&tfull[abuf]);
+        __syncwarp();
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1u;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: warp (g, h) = lanes 32g.. of row tile h ----------------
+    const int g = warp & 3, h = (warp - 4) >> 2;
+    const float Bmax = bstat[0], dBmax = bstat[1];
+    const float acc_rel = (float)(NKC * 4 + 2) * 0x1p-19f;
+    const uint32_t msk = kIdxMask;
+    int abuf = 0;
+    uint32_t aphase = 0;
+    const int64_t r_in = h * 128 + g * 32 + lane;
+    const uint32_t tlane = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * 128);
+    // TMEM loads run one 32-column chunk ahead of the arithmetic (vA / vB by
+    // chunk parity; 4 chunks per tile), across tile and pair boundaries
+    uint32_t vA[32], vB[32];
+    if (blockIdx.x < npairs) {
+      ptx::mbar_wait(&tfull[0], 0);
+      ptx::tc_fence_after();
+      ptx::tmem_ld_32x32b_x32_async(tlane, vA);
+    }
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+      const int64_t row = pr * 256 + r_in;
+      const int64_t rc = row < n ? row : n - 1;
+      const bool last_pair = pr + gridDim.x >= npairs;
+      float twoE = 0.0f, big = 0.0f, thr = 0.0f;
+      int nc = 0;
+      if (CAND) {
+        thr = amb_thr[rc];
+      } else {
+        twoE = screen_two_e(anorm[rc], danorm[rc], Bmax, dBmax, OFF, acc_rel);
+        big = 64.0f / twoE;
+      }
+      float R1 = 3.4e38f, cnt = 0.0f;
+      int r1 = 0;
+      for (int nt = 0; nt < ntiles; ++nt) {
+        const uint32_t taddr = tlane + (uint32_t)(abuf * 256);
+        const int c0 = nt * SB_BN;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t (&cur)[32] = (q & 1) ? vB : vA;
+          uint32_t (&nxt)[32] = (q & 1) ? vA : vB;
+          ptx::tmem_wait_ld(cur);
+          if (q < 3) {
+            ptx::tmem_ld_32x32b_x32_async(taddr + 32 * (q + 1), nxt);
+          } else {
+            // this buffer is fully read: hand it back, prefetch the next one
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[abuf]);
+            abuf ^= 1;
+            if (abuf == 0) aphase ^= 1u;
+            if (nt + 1 < ntiles || !last_pair) {
+              ptx::mbar_wait(&tfull[abuf], aphase);
+              ptx::tc_fence_after();
+              ptx::tmem_ld_32x32b_x32_async(tlane + (uint32_t)(abuf * 256), nxt);
+            }
+          }
+          float v[32], cp[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
+          load_cprime(cp, cprime + c0 + 32 * q);
+          if (CAND) {
+            // candidate mask of the chunk (FSETP + SEL per key), then a short
+            // loop over its set bits (2-3 candidates per row in total)
+            uint32_t bits = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) bits |= (fmaf(v[i], -2.0f, cp[i]) <= thr ? 1u : 0u) << i;
+            while (bits) {
+              const int i = __ffs(bits) - 1;
+              bits &= bits - 1;
+              if (row < n && nc < SB_NCAND) cand[rc * SB_NCAND + nc] = c0 + 32 * q + i;
+              ++nc;
+            }
+          } else {
+            screen_chunk_regs(v, cp, msk, c0 + 32 * q, twoE, big, R1, r1, cnt);
+          }
+        }
+      }
+      if (CAND) {
+        if (row < n) cand_n[row] = nc;
+      } else {
+        if (row < n) labels[row] = r1;
+        const bool amb = row < n && cnt > 1.0f;
+        const unsigned m = __ballot_sync(0xffffffffu, amb);
+        if (m) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(amb_count, __popc(m));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (amb) {
+            const int pos = base + __popc(m & ((1u << lane) - 1u));
+            amb_list[pos] = (int)row;
+            // R1 carries a 5-bit index in its low mantissa bits: 2^-17 relative slack
+            amb_thr[pos] = (R1 + twoE) * (1.0f + 0x1p-14f);
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc<512>(tmem);
+}
+
+static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t rows, int cols, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (enc == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return PCB_ENODEV;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)SB_BKE, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : PCB_EINVAL;
+}
+
+template <int NKC, bool CAND>
+static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
+                              const float* an, const float* dan, const float* cnorm, const float* bstat,
+                              int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
+                              int* cand, int* cand_n, const long long* state, cudaStream_t st) {
+  using Cfg = SbCfg<NKC>;
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_tmap_bf16(&ta, A, n, NKC * SB_BKE, 128))) return rc;
+  if ((rc = make_tmap_bf16(&tb, B, k, NKC * SB_BKE, SB_BN))) return rc;
+  auto kern = assign_screen_bf16_kernel<NKC, CAND>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t npairs = (n + 255) / 256;
+  const int grid = (int)std::min<int64_t>(npairs, (int64_t)sm_count());
+  kern<<<grid, SB_THREADS, Cfg::kSmem, st>>>(ta, tb, an, dan, cnorm, bstat, n, k, labels, amb_list, amb_count,
+                                             amb_thr, bypass, cand, cand_n, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+template <bool CAND>
+static int dispatch_bf16(int ldb, const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
+                         const float* an, const float* dan, const float* cnorm, const float* bstat,
+                         int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
+                         int* cand, int* cand_n, const long long* state, cudaStream_t st) {
+#define PCB_SB_CASE(N)                                                                                      \
+  case N:                                                                                                   \
+    return launch_screen_bf16<N, CAND>(A, n, B, k, an, dan, cnorm, bstat, labels, amb_list, amb_count,      \
+                                       amb_thr, bypass, cand, cand_n, state, st);
+  switch (ldb / SB_BKE) {
+    PCB_SB_CASE(1)
+    PCB_SB_CASE(2)
+    PCB_SB_CASE(3)
+    PCB_SB_CASE(4)
+    default: return PCB_EUNSUP;
+  }
+#undef PCB_SB_CASE
+}
+
+// ---- prep: RN BF16 copies and the residual norms of the bound ----------------------
+
+__device__ __forceinline__ void atomic_max_pos_f(float* addr, float v) {
+  atomicMax(reinterpret_cast<unsigned int*>(addr), __float_as_uint(v));  // v >= 0
+}
+
+// Per row of X (rows x d): |bf16(x)|, |x - bf16(x)| (rounded up), max |x|^2 and
+// the BF16 copy Xb (row stride ldb, zero padded).
+__global__ void __launch_bounds__(256)
+row_bf16_norms_kernel(const float* __restrict__ X, int64_t rows, int d, float* __restrict__ an,
+                      float* __restrict__ dan, float* __restrict__ maxsq, __nv_bfloat16* __restrict__ Xb, int ldb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  float wmax = 0.0f;
+  for (int64_t i = w; i < rows; i += nw) {
+    double s_t = 0.0, s_d = 0.0, s_x = 0.0;
+    for (int t = lane; t < ldb; t += 32) {
+      const float x = t < d ? X[i * d + t] : 0.0f;
+      const __nv_bfloat16 hb = __float2bfloat16_rn(x);
+      Xb[i * ldb + t] = hb;
+      const double h = (double)__bfloat162float(hb);
+      const double dd = (double)x - h;
+      s_t = fma(h, h, s_t);
+      s_d = fma(dd, dd, s_d);
+      s_x = fma((double)x, (double)x, s_x);
+    }
+    s_t = warp_sum(s_t);
+    s_d = warp_sum(s_d);
+    s_x = warp_sum(s_x);
+    if (lane == 0) {
+      an[i] = (float)(sqrt(s_t) * (1.0 + 1e-6));
+      dan[i] = (float)(sqrt(s_d) * (1.0 + 1e-6));
+      wmax = fmaxf(wmax, (float)(s_x * (1.0 + 1e-6)));
+    }
+  }
+  if (lane == 0 && maxsq != nullptr) atomic_max_pos_f(maxsq, wmax);
+}
+
+__global__ void max2_bf16_kernel(const float* __restrict__ b, const float* __restrict__ db, int k,
+                                 float* __restrict__ out) {
+  float m0 = 0.0f, m1 = 0.0f;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) { m0 = fmaxf(m0, b[j]); m1 = fmaxf(m1, db[j]); }
+  atomic_max_pos_f(&out[0], m0);
+  atomic_max_pos_f(&out[1], m1);
+}
+
+__global__ void screen_off_kernel(float* __restrict__ bstat, const float* __restrict__ maxsq) {
+  bstat[2] = 1.01f * (*maxsq) + 1.0f;  // OFF > max |p|^2: every key positive
+}
+
+// Compact copy of the ambiguous rows of Xb (pass-2 input).
+__global__ void __launch_bounds__(256)
+gather_rows_bf16(const __nv_bfloat16* __restrict__ Xb, int ldb, const int* __restrict__ list,
+                 const int* __restrict__ count, int64_t bypass, __nv_bfloat16* __restrict__ out,
+                 const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int64_t cnt = *count;
+  if (cnt > bypass) return;
+  const int per = ldb / 8;  // 16-byte vectors per row
+  const int64_t total = cnt * per;
+  const uint4* src = reinterpret_cast<const uint4*>(Xb);
+  uint4* dst = reinterpret_cast<uint4*>(out);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / per, q = e - r * per;
+    dst[r * per + q] = src[(int64_t)list[r] * per + q];
+  }
+}
+
+// Four consecutive floats q*4 .. q*4+3 of a row (zero past d); 16-byte load
+// when the row is 16-byte aligned (d % 4 == 0).
+__device__ __forceinline__ float4 load4(const float* __restrict__ rowp, int q, int d) {
+  const int t = 4 * q;
+  if ((d & 3) == 0) return t < d ? __ldg(reinterpret_cast<const float4*>(rowp) + q) : make_float4(0, 0, 0, 0);
+  return make_float4(t < d ? rowp[t] : 0.0f, t + 1 < d ? rowp[t + 1] : 0.0f, t + 2 < d ? rowp[t + 2] : 0.0f,
+                     t + 3 < d ? rowp[t + 3] : 0.0f);
+}
+__device__ __forceinline__ double dist4(float4 a, float4 b, double s) {
+  const double e0 = (double)a.x - (double)b.x, e1 = (double)a.y - (double)b.y;
+  const double e2 = (double)a.z - (double)b.z, e3 = (double)a.w - (double)b.w;
+  return fma(e3, e3, fma(e2, e2, fma(e1, e1, fma(e0, e0, s))));
+}
+
+// Exact f64 distances of each ambiguous row to its candidates (8 lanes per
+// row, 4 rows per warp), argmin with the lowest index on ties; rows without a
+// usable candidate list (too many candidates, or the bypass) are appended to
+// the overflow list for the 3xTF32 resolver.
+template <int DQ>
+__global__ void __launch_bounds__(256)
+screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict__ C,
+                    const int* __restrict__ list, const int* __restrict__ count, int64_t bypass,
+                    const int* __restrict__ cand, const int* __restrict__ cand_n, int32_t* __restrict__ labels,
+                    int* __restrict__ ovf_list, int* __restrict__ ovf_count, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int64_t cnt = *count;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (cnt > bypass) {
+    // bypass: the whole list goes to the 3xTF32 resolver (32 entries per warp)
+    for (int64_t b0 = w0 * 32; b0 < cnt; b0 += nw * 32) {
+      const int64_t r = b0 + lane;
+      const bool ok = r < cnt;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      int b = 0;
+      if (lane == 0) b = atomicAdd(ovf_count, __popc(m));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (ok) ovf_list[b + __popc(m & ((1u << lane) - 1u))] = list[r];
+    }
+    return;
+  }
+  const int sub = lane & 7, grp = lane >> 3;
+  for (int64_t rb = w0 * 4; rb < cnt; rb += nw * 4) {
+    const int64_t r = rb + grp;
+    const bool valid = r < cnt;
+    const int row = valid ? list[r] : 0;
+    int nc = valid ? cand_n[r] : 0;
+    const bool ovf = valid && (nc < 1 || nc > SB_NCAND);
+    const unsigned om = __ballot_sync(0xffffffffu, ovf && sub == 0);
+    if (om) {  // one atomic per warp
+      int b = 0;
+      if (lane == 0) b = atomicAdd(ovf_count, __popc(om));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (ovf && sub == 0) ovf_list[b + __popc(om & ((1u << lane) - 1u))] = row;
+    }
+    if (ovf) nc = 0;
+    const int ncmax = __reduce_max_sync(0xffffffffu, nc);
+    // all candidate ids at once (two 16-byte loads), the point row as float4
+    int cj[SB_NCAND];
+    {
+      const int4* cp = reinterpret_cast<const int4*>(cand + r * SB_NCAND);
+      const int4 c0 = nc > 0 ? cp[0] : make_int4(0, 0, 0, 0);
+      const int4 c1 = nc > 4 ? cp[1] : make_int4(0, 0, 0, 0);
+      cj[0] = c0.x; cj[1] = c0.y; cj[2] = c0.z; cj[3] = c0.w;
+      cj[4] = c1.x; cj[5] = c1.y; cj[6] = c1.z; cj[7] = c1.w;
+    }
+    float4 p[DQ];
+#pragma unroll
+    for (int q = 0; q < DQ; ++q) p[q] = nc > 0 ? load4(P + (int64_t)row * d, sub + 8 * q, d) : make_float4(0, 0, 0, 0);
+    double best = 0.0;
+    int bj = -1;
+#pragma unroll
+    for (int c = 0; c < SB_NCAND; c += 2) {
+      if (c >= ncmax) break;
+      const int ja = c < nc ? cj[c] : -1, jb = c + 1 < nc ? cj[c + 1] : -1;
+      float4 xa[DQ], xb[DQ];
+#pragma unroll
+      for (int q = 0; q < DQ; ++q) {
+        xa[q] = ja >= 0 ? load4(C + (int64_t)ja * d, sub + 8 * q, d) : make_float4(0, 0, 0, 0);
+        xb[q] = jb >= 0 ? load4(C + (int64_t)jb * d, sub + 8 * q, d) : make_float4(0, 0, 0, 0);
+      }
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int q = 0; q < DQ; ++q) {
+        sa = dist4(p[q], xa[q], sa);
+        sb = dist4(p[q], xb[q], sb);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+      }
+      if (ja >= 0 && (bj < 0 || sa < best || (sa == best && ja < bj))) { best = sa; bj = ja; }
+      if (jb >= 0 && (bj < 0 || sb < best || (sb == best && jb < bj))) { best = sb; bj = jb; }
+    }
+    if (sub == 0 && bj >= 0) labels[row] = bj;
+  }
+}
+
+}  // namespace pcb
+
+using namespace pcb;
+
+extern "C" int pcb_screen_bf16_ld(int d) { return (d + SB_BKE - 1) / SB_BKE * SB_BKE; }
+extern "C" int pcb_screen_bf16_ncand(void) { return SB_NCAND; }
+
+extern "C" int pcb_screen_prep_points_bf16(const float* P, int64_t n, int d, int ldb, void* P_b, float* anorm,
+                                           float* danorm, float* bstat, void* stream) {
+  if (n < 1 || d < 1 || ldb < d || ldb % SB_BKE || !P || !P_b || !anorm || !danorm || !bstat) return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bstat, 0, 4 * sizeof(float), st);
+  if (e != cudaSuccess) return (int)e;
+  const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, (int64_t)sm_count() * 16);
+  row_bf16_norms_kernel<<<grid, 256, 0, st>>>(P, n, d, anorm, danorm, bstat + 3,
+                                              reinterpret_cast<__nv_bfloat16*>(P_b), ldb);
+  PCB_CHECK_LAUNCH();
+  screen_off_kernel<<<1, 1, 0, st>>>(bstat, bstat + 3);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_screen_prep_centroids_bf16(const float* C, int k, int d, int ldb, void* C_b, float* bnorm,
+                                              float* dbnorm, float* bstat, void* stream) {
+  if (k < 1 || d < 1 || ldb < d || ldb % SB_BKE || !C || !C_b || !bnorm || !dbnorm || !bstat) return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bstat, 0, 2 * sizeof(float), st);
+  if (e != cudaSuccess) return (int)e;
+  row_bf16_norms_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(C, k, d, bnorm, dbnorm, nullptr,
+                                                             reinterpret_cast<__nv_bfloat16*>(C_b), ldb);
+  PCB_CHECK_LAUNCH();
+  max2_bf16_kernel<<<1, 256, 0, st>>>(bnorm, dbnorm, k, bstat);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+// Pass 1 over all n rows: certified labels, ambiguous rows + thresholds.
+extern "C" int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const void* C_b, int k,
+                                      const float* cnorm, const float* anorm, const float* danorm,
+                                      const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
+                                      float* amb_thr, const long long* state, void* stream) {
+  if (n < 1 || ldb < SB_BKE || ldb % SB_BKE || k < 1 || !P_b || !C_b || !cnorm || !anorm || !danorm || !bstat ||
+      !labels || !amb_list || !amb_count || !amb_thr)
+    return PCB_EINVAL;
+  if (n > INT32_MAX || k > SC_KMAX) return PCB_EUNSUP;
+  return dispatch_bf16<false>(ldb, (const __nv_bfloat16*)P_b, n, (const __nv_bfloat16*)C_b, k, anorm, danorm, cnorm,
+                              bstat, labels, amb_list, amb_count, amb_thr, 0, nullptr, nullptr, state,
+                              (cudaStream_t)stream);
+}
+
+// Pass 2 + exact resolution of the ambiguous rows.  Rows left over (more than
+// SB_NCAND candidates, or every row when the ambiguous count exceeds `bypass`)
+// land in ovf_list / ovf_count for the 3xTF32 resolver.
+extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
+                                       const float* C, int k, const float* cnorm, const float* bstat,
+                                       const int* amb_list, const int* amb_count, const float* amb_thr,
+                                       int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
+                                       int* ovf_list, int* ovf_count, const long long* state, void* stream) {
+  if (n < 1 || d < 1 || k < 1 || ldb < d || ldb % SB_BKE || !P || !P_b || !C_b || !C || !cnorm || !bstat ||
+      !amb_list || !amb_count || !amb_thr || !sub_b || !cand || !cand_n || !labels || !ovf_list || !ovf_count)
+    return PCB_EINVAL;
+  if (d > 256) return PCB_EUNSUP;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(ovf_count, 0, sizeof(int), st);
+  if (e != cudaSuccess) return (int)e;
+  const int grid = sm_count() * 8;
+  gather_rows_bf16<<<grid, 256, 0, st>>>((const __nv_bfloat16*)P_b, ldb, amb_list, amb_count, bypass,
+                                         (__nv_bfloat16*)sub_b, state);
+  PCB_CHECK_LAUNCH();
+  int rc = dispatch_bf16<true>(ldb, (const __nv_bfloat16*)sub_b, n, (const __nv_bfloat16*)C_b, k, nullptr, nullptr,
+                               cnorm, bstat, nullptr, nullptr, const_cast<int*>(amb_count),
+                               const_cast<float*>(amb_thr), bypass, cand, cand_n, state, st);
+  if (rc) return rc;
+  const int DQ = (d + 31) / 32;  // float4 per lane (8 lanes per row)
+  const int xgrid = sm_count() * 16;
+#define PCB_EX_CASE(N)                                                                                          \
+  if (DQ <= N) {                                                                                              \
+    screen_exact_kernel<N><<<xgrid, 256, 0, st>>>(P, d, C, amb_list, amb_count, bypass, cand, cand_n, labels, \
+                                                  ovf_list, ovf_count, state);                                \
+  } else
+  PCB_EX_CASE(1)
+  PCB_EX_CASE(2)
+  PCB_EX_CASE(4)
+  PCB_EX_CASE(8)
+  return PCB_EUNSUP;
+#undef PCB_EX_CASE
+  PCB_CHECK_LAUNCH();
+  return 0;
+}

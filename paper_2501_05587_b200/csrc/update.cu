@@ -232,6 +232,115 @@ segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict
   if (lane == 0 && obj != 0.0) atomicAdd(&acc[L.objective()], obj);
 }
 
+// f32 rows with d % 4 == 0 (64 < d <= 512): one warp per slice of sorted ids,
+// lane l owns the float4 columns l + 32 v; four rows (16-byte loads, a whole
+// 512-byte row per warp instruction at d = 128) are in flight per step.
+template <int NV4>
+__global__ void __launch_bounds__(256)
+segsum_v4(const float* __restrict__ P, int64_t n, int d, const int32_t* __restrict__ perm,
+          const int32_t* __restrict__ offsets, int k, const float* __restrict__ C, int64_t slice,
+          double* __restrict__ own_sorted, double* __restrict__ acc, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const AccLayout L{k, d};
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nslices = (n + slice - 1) / slice;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  double obj = 0.0;
+  for (int64_t sl = warp; sl < nslices; sl += nwarps) {
+    const int64_t s0 = sl * slice, s1 = min(n, s0 + slice);
+    int j = segment_of(offsets, k, s0);
+    int64_t jend = offsets[j + 1];
+    double a[NV4][4];
+    float4 c[NV4];
+#pragma unroll
+    for (int v = 0; v < NV4; ++v) {
+      const int f = lane + 32 * v;
+      a[v][0] = a[v][1] = a[v][2] = a[v][3] = 0.0;
+      c[v] = f < d4 ? reinterpret_cast<const float4*>(C + (int64_t)j * d)[f] : z4;
+    }
+    int64_t s = s0;
+    while (s < s1) {
+      if (s >= jend) {
+#pragma unroll
+        for (int v = 0; v < NV4; ++v) {
+          const int f = lane + 32 * v;
+          if (f < d4) {
+            double* dst = acc + (int64_t)j * d + 4 * f;
+            atomicAdd(dst + 0, a[v][0]);
+            atomicAdd(dst + 1, a[v][1]);
+            atomicAdd(dst + 2, a[v][2]);
+            atomicAdd(dst + 3, a[v][3]);
+          }
+          a[v][0] = a[v][1] = a[v][2] = a[v][3] = 0.0;
+        }
+        do { ++j; jend = offsets[j + 1]; } while (s >= jend);
+#pragma unroll
+        for (int v = 0; v < NV4; ++v) {
+          const int f = lane + 32 * v;
+          c[v] = f < d4 ? reinterpret_cast<const float4*>(C + (int64_t)j * d)[f] : z4;
+        }
+      }
+      const int64_t e = min(s1, jend);
+      for (; s < e; s += 4) {
+        const int nr = (int)(e - s < 4 ? e - s : 4);
+        float4 x[4][NV4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float4* row = reinterpret_cast<const float4*>(P + (int64_t)perm[r < nr ? s + r : s] * d);
+#pragma unroll
+          for (int v = 0; v < NV4; ++v) {
+            const int f = lane + 32 * v;
+            x[r][v] = (r < nr && f < d4) ? __ldcs(row + f) : z4;
+          }
+        }
+        double q[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          q[r] = 0.0;
+#pragma unroll
+          for (int v = 0; v < NV4; ++v) {
+            const float xs[4] = {x[r][v].x, x[r][v].y, x[r][v].z, x[r][v].w};
+            const float cs[4] = {c[v].x, c[v].y, c[v].z, c[v].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const double xd = (double)xs[i];
+              a[v][i] += xd;
+              const double ed = xd - (double)cs[i];
+              q[r] = fma(ed, ed, q[r]);
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) q[r] += __shfl_xor_sync(0xffffffffu, q[r], o);
+        }
+        if (lane < nr) {
+          const double qo = lane == 0 ? q[0] : lane == 1 ? q[1] : lane == 2 ? q[2] : q[3];
+          own_sorted[s + lane] = qo;
+        }
+        if (lane == 0) obj += q[0] + (nr > 1 ? q[1] : 0.0) + (nr > 2 ? q[2] : 0.0) + (nr > 3 ? q[3] : 0.0);
+      }
+      s = e;
+    }
+#pragma unroll
+    for (int v = 0; v < NV4; ++v) {
+      const int f = lane + 32 * v;
+      if (f < d4) {
+        double* dst = acc + (int64_t)j * d + 4 * f;
+        atomicAdd(dst + 0, a[v][0]);
+        atomicAdd(dst + 1, a[v][1]);
+        atomicAdd(dst + 2, a[v][2]);
+        atomicAdd(dst + 3, a[v][3]);
+      }
+    }
+  }
+  if (lane == 0 && obj != 0.0) atomicAdd(&acc[L.objective()], obj);
+}
+
 // d <= 16: one thread per slice, the whole row in registers.
 template <typename T, int DP>
 __global__ void __launch_bounds__(256)
@@ -310,13 +419,21 @@ static int segment_sums(const T* P, int64_t n, int d, const int32_t* perm, const
     const int64_t nsl = (n + slice - 1) / slice;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nsl * 32 + 255) / 256, (int64_t)sms * 8));
 #define PCB_SEG_W(NVV) segsum_warp<T, NVV><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, C, slice, own, acc, state)
-    if (d <= 32) PCB_SEG_W(1);
+#define PCB_SEG_V4(NV4) segsum_v4<NV4><<<grid, 256, 0, st>>>((const float*)P, n, d, perm, offsets, k, (const float*)C, slice, own, acc, state)
+    if (sizeof(T) == 4 && d % 4 == 0 && d > 64 && d <= 512) {
+      if (d <= 128) PCB_SEG_V4(1);
+      else if (d <= 256) PCB_SEG_V4(2);
+      else if (d <= 384) PCB_SEG_V4(3);
+      else PCB_SEG_V4(4);
+    }
+    else if (d <= 32) PCB_SEG_W(1);
     else if (d <= 64) PCB_SEG_W(2);
     else if (d <= 128) PCB_SEG_W(4);
     else if (d <= 256) PCB_SEG_W(8);
     else if (d <= 512) PCB_SEG_W(16);
     else PCB_SEG_W(32);
 #undef PCB_SEG_W
+#undef PCB_SEG_V4
   }
   PCB_CHECK_LAUNCH();
   return 0;

@@ -91,8 +91,10 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
     if variant not in L.VARIANTS:
         raise ValueError(f"unknown assign variant {variant!r}; expected one of {tuple(L.VARIANTS)}")
     if variant != "auto":
-        if dtype == _F64 and variant in ("tc3xtf32", "delta", "tc1xtf32s"):
+        if dtype == _F64 and variant in ("tc3xtf32", "delta", "tc1xtf32s", "bf16s"):
             raise ValueError(f"variant {variant!r} is float32-only")
+        if variant == "bf16s" and (d > 256 or k > SCREEN_KMAX):
+            raise ValueError(f"variant 'bf16s' needs d <= 256 and k <= {SCREEN_KMAX}")
         if variant == "rowreg" and d > 32:
             raise ValueError("variant 'rowreg' needs d <= 32")
         if variant == "tc1xtf32s" and k > SCREEN_KMAX:
@@ -102,7 +104,9 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
         return "rowreg"
     if dtype != _F32:
         return "tiled"
-    return "tc1xtf32s" if k <= SCREEN_KMAX else "tc3xtf32"
+    if k > SCREEN_KMAX:
+        return "tc3xtf32"
+    return "bf16s" if d <= 256 else "tc1xtf32s"
 
 
 SCREEN_KMAX = 6144  # assign_screen.cu SC_KMAX
@@ -247,7 +251,7 @@ class LloydEngine(ShardSequence):
             self.ld = 0
             self.P_hi = self.P_lo = self.C_hi = self.C_lo = None
             L.call(f"pcb_point_norms_{self.sfx}", _p(self.P), n, d, _p(self.pnorm), _stream())
-            if self.variant in ("tc3xtf32", "tc1xtf32s"):
+            if self.variant in ("tc3xtf32", "tc1xtf32s", "bf16s"):
                 self.ld = (d + 31) // 32 * 32
                 self.C_hi = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
                 self.C_lo = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
@@ -271,6 +275,33 @@ class LloydEngine(ShardSequence):
                 self.P_r = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 L.call("pcb_screen_prep_points", _p(self.P), n, d, self.ld, _p(self.P_r), _p(self.anorm),
                        _p(self.danorm), _p(self.bstat), _stream())
+            if self.variant == "bf16s":
+                # certified BF16 screening: RN BF16 copy of P, the bound's residual
+                # norms, pass-2 buffers for the ambiguous rows (capacity n) and the
+                # 3xTF32 resolver's compact hi/lo for rows with too many candidates
+                self.ldb = int(L.load().pcb_screen_bf16_ld(d))
+                ncand = int(L.load().pcb_screen_bf16_ncand())
+                self.P_b = torch.empty((n, self.ldb), dtype=torch.bfloat16, device=dev)
+                self.C_b = torch.zeros((kk, self.ldb), dtype=torch.bfloat16, device=dev)
+                self.anorm = torch.empty(n, dtype=torch.float32, device=dev)
+                self.danorm = torch.empty(n, dtype=torch.float32, device=dev)
+                self.bnorm = torch.empty(kk, dtype=torch.float32, device=dev)
+                self.dbnorm = torch.empty(kk, dtype=torch.float32, device=dev)
+                self.bstat = torch.zeros(4, dtype=torch.float32, device=dev)
+                self.amb_list = torch.empty(n, dtype=torch.int32, device=dev)
+                self.amb_count = torch.zeros(1, dtype=torch.int32, device=dev)
+                self.amb_thr = torch.empty(n, dtype=torch.float32, device=dev)
+                self.sub_b = torch.empty((n, self.ldb), dtype=torch.bfloat16, device=dev)
+                self.bypass = max(n // 4, 1)  # more ambiguous rows: straight to 3xTF32
+                self.cand = torch.empty((self.bypass, ncand), dtype=torch.int32, device=dev)
+                self.cand_n = torch.empty(self.bypass, dtype=torch.int32, device=dev)
+                self.ovf_list = torch.empty(n, dtype=torch.int32, device=dev)
+                self.ovf_count = torch.zeros(1, dtype=torch.int32, device=dev)
+                self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
+                self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
+                self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
+                L.call("pcb_screen_prep_points_bf16", _p(self.P), n, d, self.ldb, _p(self.P_b),
+                       _p(self.anorm), _p(self.danorm), _p(self.bstat), _stream())
 
     # -- centroid initialisation ------------------------------------------------
     def set_centroids(self, C) -> None:
@@ -281,6 +312,9 @@ class LloydEngine(ShardSequence):
             self._centroid_norms()
 
     def _screen_centroid_stats(self) -> None:
+        if self.variant == "bf16s":
+            L.call("pcb_screen_prep_centroids_bf16", _p(self.C), self.k, self.d, self.ldb, _p(self.C_b),
+                   _p(self.bnorm), _p(self.dbnorm), _p(self.bstat), _stream())
         if self.variant == "tc1xtf32s":
             L.call("pcb_screen_prep_centroids", _p(self.C), self.k, self.d, _p(self.bnorm),
                    _p(self.dbnorm), _p(self.bstat), _stream())
@@ -344,6 +378,25 @@ class LloydEngine(ShardSequence):
                _p(self.offsets), self.k, _p(self.C), _p(self.own), _p(self.acc), _p(state), _stream())
 
     def _assign(self, prev, new, acc, state) -> None:
+        if self.variant == "bf16s":
+            self.amb_count.zero_()
+            self._kmark(0)
+            L.call("pcb_assign_screen_bf16", _p(self.P_b), self.n, self.ldb, _p(self.C_b), self.k,
+                   _p(self.cnorm), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
+                   _p(self.amb_list), _p(self.amb_count), _p(self.amb_thr), _p(state), _stream())
+            self._kmark(1)
+            L.call("pcb_resolve_screen_bf16", _p(self.P), self.n, self.d, _p(self.P_b), self.ldb,
+                   _p(self.C_b), _p(self.C), self.k, _p(self.cnorm), _p(self.bstat), _p(self.amb_list),
+                   _p(self.amb_count), _p(self.amb_thr), self.bypass, _p(self.sub_b), _p(self.cand),
+                   _p(self.cand_n), _p(new), _p(self.ovf_list), _p(self.ovf_count), _p(state), _stream())
+            L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.ovf_list),
+                   _p(self.ovf_count), self.ld, _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels),
+                   _p(self.pnorm), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(new),
+                   _p(state), _stream())
+            if acc is not None:
+                L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
+                       _stream())
+            return
         if self.variant == "tc1xtf32s":
             self.amb_count.zero_()
             self._kmark(0)
@@ -478,7 +531,7 @@ class LloydEngine(ShardSequence):
             xn = torch.empty(m, dtype=self.tdtype, device=self.dev)
             out = torch.empty(m, dtype=torch.int32, device=self.dev)
             L.call(f"pcb_point_norms_{self.sfx}", _p(Xt), m, self.d, _p(xn), _stream())
-            if self.variant in ("tc3xtf32", "tc1xtf32s"):
+            if self.variant in ("tc3xtf32", "tc1xtf32s", "bf16s"):
                 xh = torch.empty((m, self.ld), dtype=torch.float32, device=self.dev)
                 xl = torch.empty_like(xh)
                 L.call("pcb_split_tf32", _p(Xt), m, self.d, self.ld, _p(xh), _p(xl), _stream())
