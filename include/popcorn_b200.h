@@ -175,12 +175,23 @@ int pcb_screen_prep_centroids_bf16(const float* C, int k, int d, int ldb, void* 
 int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const void* C_b, int k,
                            const float* cnorm, const float* anorm, const float* danorm,
                            const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
-                           float* amb_thr, const long long* state, void* stream);
+                           float* amb_thr, const int32_t* orig, const long long* state, void* stream);
 int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
                             const float* C, int k, const float* cnorm, const float* bstat,
                             const int* amb_list, const int* amb_count, const float* amb_thr,
                             int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
-                            int* ovf_list, int* ovf_count, const long long* state, void* stream);
+                            int* ovf_list, int* ovf_count, const int32_t* orig, const long long* state,
+                            void* stream);
+/* Row layout: P_b / anorm / danorm rebuilt as the rows perm[s] of their
+ * original-order copies Pb0 / an0 / dan0 (from pcb_screen_prep_points_bf16),
+ * orig[s] = perm[s] (perm = point ids sorted by label, pcb_sort_by_label).
+ * With orig != NULL the two calls above read P_b, anorm, danorm in that
+ * layout; labels and ovf_list stay in original row ids (amb_list holds layout
+ * positions).  Rows of a warp then share their nearest centroids, which lets
+ * the screen skip whole 32-column chunks of its epilogue.                   */
+int pcb_screen_relayout_bf16(const void* Pb0, const float* an0, const float* dan0, int64_t n, int ldb,
+                             const int32_t* perm, void* P_b, float* anorm, float* danorm, int32_t* orig,
+                             void* stream);
 int pcb_count_labels(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
                      double* acc, const long long* state, void* stream);
 

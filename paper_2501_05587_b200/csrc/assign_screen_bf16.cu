@@ -72,7 +72,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
                           const float* __restrict__ cnorm, const float* __restrict__ bstat, int64_t n_in, int k,
                           int32_t* __restrict__ labels, int* __restrict__ amb_list, int* __restrict__ amb_count,
                           float* __restrict__ amb_thr, int64_t bypass, int* __restrict__ cand,
-                          int* __restrict__ cand_n, const long long* __restrict__ state) {
+                          int* __restrict__ cand_n, const int32_t* __restrict__ orig,
+                          const long long* __restrict__ state) {
   using Cfg = SbCfg<NKC>;
   if (stopped(state)) return;
   const int64_t n = CAND ? sb_rows(n_in, amb_count, bypass) : n_in;
@@ -251,6 +252,11 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           float v[32], cp[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
+#if defined(PCB_EXP) && PCB_EXP == 2
+          // experiment build: TMEM traffic only (MMA + TMEM-load ceiling)
+          R1 = fminf(R1, v[0] + v[31]);
+          continue;
+#endif
           load_cprime(cp, cprime + c0 + 32 * q);
           if (CAND) {
             // candidate mask of the chunk (FSETP + SEL per key), then a short
@@ -265,14 +271,31 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
               ++nc;
             }
           } else {
-            screen_chunk_regs(v, cp, msk, c0 + 32 * q, twoE, big, R1, r1, cnt);
+            // chunk skip: when no key of the chunk is within the running
+            // threshold for any row of the warp, processing it would leave
+            // (R1, r1, cnt) unchanged — the full update below is skipped.
+            // Rows are laid out by label (pcb_screen_relayout_bf16), so the
+            // rows of a warp see their minima in the same chunks and most
+            // chunks of most warps take this path.
+            const float thr_skip = (R1 + twoE + 0x1p-16f * fabsf(R1)) * (1.0f + 0x1p-16f);
+            float km[32];
+            const unsigned long long m2 = f2pack(-2.0f, -2.0f);
+#pragma unroll
+            for (int i = 0; i < 32; i += 2)
+              f2unpack(ffma2(f2pack(v[i], v[i + 1]), m2, f2pack(cp[i], cp[i + 1])), km[i], km[i + 1]);
+            float mm = fmin3(km[0], km[1], km[2]);
+#pragma unroll
+            for (int i = 3; i < 31; i += 2) mm = fmin3(mm, km[i], km[i + 1]);
+            mm = fminf(mm, km[31]);
+            if (__any_sync(0xffffffffu, mm <= thr_skip))
+              screen_chunk_regs(v, cp, msk, c0 + 32 * q, twoE, big, R1, r1, cnt);
           }
         }
       }
       if (CAND) {
         if (row < n) cand_n[row] = nc;
       } else {
-        if (row < n) labels[row] = r1;
+        if (row < n) labels[orig != nullptr ? orig[row] : row] = r1;
         const bool amb = row < n && cnt > 1.0f;
         const unsigned m = __ballot_sync(0xffffffffu, amb);
         if (m) {
@@ -319,7 +342,8 @@ template <int NKC, bool CAND>
 static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                               const float* an, const float* dan, const float* cnorm, const float* bstat,
                               int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
-                              int* cand, int* cand_n, const long long* state, cudaStream_t st) {
+                              int* cand, int* cand_n, const int32_t* orig, const long long* state,
+                              cudaStream_t st) {
   using Cfg = SbCfg<NKC>;
   CUtensorMap ta, tb;
   int rc;
@@ -331,7 +355,7 @@ static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bflo
   const int64_t npairs = (n + 255) / 256;
   const int grid = (int)std::min<int64_t>(npairs, (int64_t)sm_count());
   kern<<<grid, SB_THREADS, Cfg::kSmem, st>>>(ta, tb, an, dan, cnorm, bstat, n, k, labels, amb_list, amb_count,
-                                             amb_thr, bypass, cand, cand_n, state);
+                                             amb_thr, bypass, cand, cand_n, orig, state);
   PCB_CHECK_LAUNCH();
   return 0;
 }
@@ -340,11 +364,11 @@ template <bool CAND>
 static int dispatch_bf16(int ldb, const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                          const float* an, const float* dan, const float* cnorm, const float* bstat,
                          int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
-                         int* cand, int* cand_n, const long long* state, cudaStream_t st) {
+                         int* cand, int* cand_n, const int32_t* orig, const long long* state, cudaStream_t st) {
 #define PCB_SB_CASE(N)                                                                                      \
   case N:                                                                                                   \
     return launch_screen_bf16<N, CAND>(A, n, B, k, an, dan, cnorm, bstat, labels, amb_list, amb_count,      \
-                                       amb_thr, bypass, cand, cand_n, state, st);
+                                       amb_thr, bypass, cand, cand_n, orig, state, st);
   switch (ldb / SB_BKE) {
     PCB_SB_CASE(1)
     PCB_SB_CASE(2)
@@ -447,7 +471,8 @@ __global__ void __launch_bounds__(256)
 screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict__ C,
                     const int* __restrict__ list, const int* __restrict__ count, int64_t bypass,
                     const int* __restrict__ cand, const int* __restrict__ cand_n, int32_t* __restrict__ labels,
-                    int* __restrict__ ovf_list, int* __restrict__ ovf_count, const long long* __restrict__ state) {
+                    int* __restrict__ ovf_list, int* __restrict__ ovf_count, const int32_t* __restrict__ orig,
+                    const long long* __restrict__ state) {
   if (stopped(state)) return;
   const int64_t cnt = *count;
   const int lane = threadIdx.x & 31;
@@ -462,7 +487,7 @@ screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict_
       int b = 0;
       if (lane == 0) b = atomicAdd(ovf_count, __popc(m));
       b = __shfl_sync(0xffffffffu, b, 0);
-      if (ok) ovf_list[b + __popc(m & ((1u << lane) - 1u))] = list[r];
+      if (ok) ovf_list[b + __popc(m & ((1u << lane) - 1u))] = orig != nullptr ? orig[list[r]] : list[r];
     }
     return;
   }
@@ -470,7 +495,7 @@ screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict_
   for (int64_t rb = w0 * 4; rb < cnt; rb += nw * 4) {
     const int64_t r = rb + grp;
     const bool valid = r < cnt;
-    const int row = valid ? list[r] : 0;
+    const int row = valid ? (orig != nullptr ? orig[list[r]] : list[r]) : 0;  // original row id
     int nc = valid ? cand_n[r] : 0;
     const bool ovf = valid && (nc < 1 || nc > SB_NCAND);
     const unsigned om = __ballot_sync(0xffffffffu, ovf && sub == 0);
@@ -564,13 +589,13 @@ extern "C" int pcb_screen_prep_centroids_bf16(const float* C, int k, int d, int 
 extern "C" int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const void* C_b, int k,
                                       const float* cnorm, const float* anorm, const float* danorm,
                                       const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
-                                      float* amb_thr, const long long* state, void* stream) {
+                                      float* amb_thr, const int32_t* orig, const long long* state, void* stream) {
   if (n < 1 || ldb < SB_BKE || ldb % SB_BKE || k < 1 || !P_b || !C_b || !cnorm || !anorm || !danorm || !bstat ||
       !labels || !amb_list || !amb_count || !amb_thr)
     return PCB_EINVAL;
   if (n > INT32_MAX || k > SC_KMAX) return PCB_EUNSUP;
   return dispatch_bf16<false>(ldb, (const __nv_bfloat16*)P_b, n, (const __nv_bfloat16*)C_b, k, anorm, danorm, cnorm,
-                              bstat, labels, amb_list, amb_count, amb_thr, 0, nullptr, nullptr, state,
+                              bstat, labels, amb_list, amb_count, amb_thr, 0, nullptr, nullptr, orig, state,
                               (cudaStream_t)stream);
 }
 
@@ -581,7 +606,8 @@ extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const v
                                        const float* C, int k, const float* cnorm, const float* bstat,
                                        const int* amb_list, const int* amb_count, const float* amb_thr,
                                        int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
-                                       int* ovf_list, int* ovf_count, const long long* state, void* stream) {
+                                       int* ovf_list, int* ovf_count, const int32_t* orig, const long long* state,
+                                       void* stream) {
   if (n < 1 || d < 1 || k < 1 || ldb < d || ldb % SB_BKE || !P || !P_b || !C_b || !C || !cnorm || !bstat ||
       !amb_list || !amb_count || !amb_thr || !sub_b || !cand || !cand_n || !labels || !ovf_list || !ovf_count)
     return PCB_EINVAL;
@@ -595,14 +621,14 @@ extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const v
   PCB_CHECK_LAUNCH();
   int rc = dispatch_bf16<true>(ldb, (const __nv_bfloat16*)sub_b, n, (const __nv_bfloat16*)C_b, k, nullptr, nullptr,
                                cnorm, bstat, nullptr, nullptr, const_cast<int*>(amb_count),
-                               const_cast<float*>(amb_thr), bypass, cand, cand_n, state, st);
+                               const_cast<float*>(amb_thr), bypass, cand, cand_n, nullptr, state, st);
   if (rc) return rc;
   const int DQ = (d + 31) / 32;  // float4 per lane (8 lanes per row)
   const int xgrid = sm_count() * 16;
 #define PCB_EX_CASE(N)                                                                                          \
   if (DQ <= N) {                                                                                              \
     screen_exact_kernel<N><<<xgrid, 256, 0, st>>>(P, d, C, amb_list, amb_count, bypass, cand, cand_n, labels, \
-                                                  ovf_list, ovf_count, state);                                \
+                                                  ovf_list, ovf_count, orig, state);                          \
   } else
   PCB_EX_CASE(1)
   PCB_EX_CASE(2)
@@ -610,6 +636,45 @@ extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const v
   PCB_EX_CASE(8)
   return PCB_EUNSUP;
 #undef PCB_EX_CASE
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+// Row layout of the screen's inputs: P_b[s] = Pb0[perm[s]] (256-byte BF16
+// rows), anorm/danorm likewise, orig[s] = perm[s]; Pb0 / an0 / dan0 are the
+// original-order copies written once by pcb_screen_prep_points_bf16 and perm
+// is the point-id order of the last counting sort (pcb_sort_by_label).  Rows of
+// one cluster become contiguous, so the rows of a screening warp share their
+// nearest centroids and the epilogue's chunk skip fires; labels and the
+// ambiguous-row resolution keep using original row ids.
+__global__ void __launch_bounds__(256)
+relayout_rows_bf16(const uint4* __restrict__ src, int per, const float* __restrict__ an0,
+                   const float* __restrict__ dan0, const int32_t* __restrict__ perm, int64_t n, uint4* __restrict__ dst,
+                   float* __restrict__ an, float* __restrict__ dan, int32_t* __restrict__ orig) {
+  const int64_t total = n * per;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = e / per, q = e - s * per;
+    const int64_t i = perm[s];
+    dst[e] = __ldcs(src + i * per + q);
+    if (q == 0) {
+      an[s] = an0[i];
+      dan[s] = dan0[i];
+      orig[s] = (int32_t)i;
+    }
+  }
+}
+
+extern "C" int pcb_screen_relayout_bf16(const void* Pb0, const float* an0, const float* dan0, int64_t n, int ldb,
+                                        const int32_t* perm, void* P_b, float* anorm, float* danorm, int32_t* orig,
+                                        void* stream) {
+  if (n < 1 || ldb < SB_BKE || ldb % SB_BKE || !Pb0 || !an0 || !dan0 || !perm || !P_b || !anorm || !danorm || !orig ||
+      Pb0 == P_b)
+    return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int per = ldb / 8;  // 16-byte vectors per row
+  const int grid = (int)std::min<int64_t>((n * per + 255) / 256, (int64_t)sm_count() * 32);
+  relayout_rows_bf16<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(Pb0), per, an0, dan0, perm, n,
+                                           reinterpret_cast<uint4*>(P_b), anorm, danorm, orig);
   PCB_CHECK_LAUNCH();
   return 0;
 }

@@ -178,6 +178,7 @@ class ShardSequence:
         if events is not None:
             events[1].record()
         self._sort_and_sum(new, self.state)                     # clustering.py:282-288, 148
+        self._after_update(t)
         self._allreduce(self.acc)                               # the one collective per iteration
         if raw_out is not None:
             raw_out.copy_(new)
@@ -185,6 +186,9 @@ class ShardSequence:
         self._finalize(check_convergence, tol)                  # clustering.py:316-324
         if events is not None:
             events[2].record()
+
+    def _after_update(self, t: int) -> None:
+        pass
 
     def _allreduce(self, t) -> None:
         if self.comm is not None and self.comm.world_size > 1:
@@ -302,6 +306,7 @@ class LloydEngine(ShardSequence):
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
                 L.call("pcb_screen_prep_points_bf16", _p(self.P), n, d, self.ldb, _p(self.P_b),
                        _p(self.anorm), _p(self.danorm), _p(self.bstat), _stream())
+                self.orig = None  # row layout of P_b / anorm / danorm (None = original order)
 
     # -- centroid initialisation ------------------------------------------------
     def set_centroids(self, C) -> None:
@@ -310,6 +315,27 @@ class LloydEngine(ShardSequence):
             Ct = torch.as_tensor(np.ascontiguousarray(C, dtype=self.dtype).reshape(self.k, self.d))
             self.C.copy_(Ct.to(self.dev))
             self._centroid_norms()
+
+    # Iterations after whose update the bf16 screen's rows are re-laid out by
+    # label (the counting sort of that update): labels settle within a few
+    # iterations, and a stale layout only costs epilogue skips, never results.
+    RELAYOUT_AT = (1, 3)
+
+    def _after_update(self, t: int) -> None:
+        if self.variant == "bf16s" and t in self.RELAYOUT_AT:
+            self.relayout()
+
+    def relayout(self) -> None:
+        """Rebuild P_b / anorm / danorm in the label order of the last update's
+        counting sort (self.perm); see pcb_screen_relayout_bf16."""
+        if self.orig is None:
+            self.orig = torch.empty(self.n, dtype=torch.int32, device=self.dev)
+            self.P_b0, self.an0, self.dan0 = self.P_b, self.anorm, self.danorm  # original-order copies
+            self.P_b = torch.empty_like(self.P_b0)
+            self.anorm = torch.empty_like(self.an0)
+            self.danorm = torch.empty_like(self.dan0)
+        L.call("pcb_screen_relayout_bf16", _p(self.P_b0), _p(self.an0), _p(self.dan0), self.n, self.ldb,
+               _p(self.perm), _p(self.P_b), _p(self.anorm), _p(self.danorm), _p(self.orig), _stream())
 
     def _screen_centroid_stats(self) -> None:
         if self.variant == "bf16s":
@@ -383,12 +409,14 @@ class LloydEngine(ShardSequence):
             self._kmark(0)
             L.call("pcb_assign_screen_bf16", _p(self.P_b), self.n, self.ldb, _p(self.C_b), self.k,
                    _p(self.cnorm), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
-                   _p(self.amb_list), _p(self.amb_count), _p(self.amb_thr), _p(state), _stream())
+                   _p(self.amb_list), _p(self.amb_count), _p(self.amb_thr), _p(self.orig), _p(state),
+                   _stream())
             self._kmark(1)
             L.call("pcb_resolve_screen_bf16", _p(self.P), self.n, self.d, _p(self.P_b), self.ldb,
                    _p(self.C_b), _p(self.C), self.k, _p(self.cnorm), _p(self.bstat), _p(self.amb_list),
                    _p(self.amb_count), _p(self.amb_thr), self.bypass, _p(self.sub_b), _p(self.cand),
-                   _p(self.cand_n), _p(new), _p(self.ovf_list), _p(self.ovf_count), _p(state), _stream())
+                   _p(self.cand_n), _p(new), _p(self.ovf_list), _p(self.ovf_count), _p(self.orig), _p(state),
+                   _stream())
             L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.ovf_list),
                    _p(self.ovf_count), self.ld, _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels),
                    _p(self.pnorm), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(new),

@@ -149,3 +149,32 @@ def test_bf16_predict_matches_assignment():
     P = oracle.make_blobs(5000, 64, 32, seed=9)
     est = pcb.KernelKMeans(n_clusters=32, algorithm="lloyd", max_iter=5, variant="bf16s").fit(P)
     np.testing.assert_array_equal(est.predict(P[:1000]), est.labels_[:1000])
+
+
+def test_bf16_relayout_keeps_results():
+    """Labels, objective and centroids do not depend on the screen's row
+    layout (pcb_screen_relayout_bf16): lockstep steps before and after the
+    rows are re-laid out by label agree bit for bit."""
+    from paper_2501_05587_b200.engine import LloydEngine
+    n, d, k = 30000, 128, 256
+    P = oracle.make_blobs(n, d, k, seed=6)
+    lab = oracle.init_assignments(n, k, 0)
+    C = oracle.mean_centroids(P, lab, k)
+    pn = oracle.point_norms(P)
+    for _ in range(3):
+        ref = oracle.lloyd_step(P, pn, C, lab, k)
+        C, lab = ref.centroids, ref.labels
+    eng = LloydEngine(P, k, variant="bf16s", max_iters=1)
+    a = eng.step_from(C, lab)
+    eng.relayout()  # perm of the step just taken: rows grouped by label
+    assert eng.orig is not None
+    orig = eng.orig.cpu().numpy()
+    assert np.array_equal(np.sort(orig), np.arange(n))
+    assert np.all(np.diff(a["labels"][orig]) >= 0)  # grouped by label
+    b = eng.step_from(C, lab)
+    np.testing.assert_array_equal(a["raw_labels"], b["raw_labels"])
+    np.testing.assert_array_equal(a["labels"], b["labels"])
+    assert abs(a["objective"] - b["objective"]) <= 1e-12 * abs(a["objective"])  # f64 atomics order
+    np.testing.assert_allclose(a["centroids"], b["centroids"], rtol=1e-6)
+    ref = oracle.lloyd_step(P, pn, C, lab, k)
+    check_step(P, C, lab, k, b, ref=ref, what="bf16s after relayout")
