@@ -164,6 +164,8 @@ int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_l
  * pcb_screen_bf16_ncand() per row into cand / cand_n) and takes the exact f64
  * argmin over them.  Rows with more candidates, or all rows when amb_count >
  * bypass, are listed in ovf_list / ovf_count for pcb_resolve_ambiguous_f32.
+ * labels_prev (optional) only orders the centroid tiles of each row pair
+ * (the tile of the pair's previous label first); results do not depend on it.
  *   pcb_screen_prep_points_bf16:    P_b, anorm, danorm, bstat[2] = OFF (per fit)
  *   pcb_screen_prep_centroids_bf16: C_b, bnorm, dbnorm, bstat[0..1] (per update) */
 int pcb_screen_bf16_ld(int d);
@@ -175,7 +177,8 @@ int pcb_screen_prep_centroids_bf16(const float* C, int k, int d, int ldb, void* 
 int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const void* C_b, int k,
                            const float* cnorm, const float* anorm, const float* danorm,
                            const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
-                           float* amb_thr, const int32_t* orig, const long long* state, void* stream);
+                           float* amb_thr, const int32_t* orig, const int32_t* labels_prev,
+                           const long long* state, void* stream);
 int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
                             const float* C, int k, const float* cnorm, const float* bstat,
                             const int* amb_list, const int* amb_count, const float* amb_thr,

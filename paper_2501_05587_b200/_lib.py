@@ -46,7 +46,7 @@ SIGNATURES = {
     "pcb_screen_bf16_ncand": (I32, []),
     "pcb_screen_prep_points_bf16": (I32, [P, I64, I32, I32, P, P, P, P, P]),
     "pcb_screen_prep_centroids_bf16": (I32, [P, I32, I32, I32, P, P, P, P, P]),
-    "pcb_assign_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P, P, P]),
+    "pcb_assign_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "pcb_resolve_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, I32, P, P, P, P, P, I64, P, P, P, P, P, P, P, P, P]),
     "pcb_screen_relayout_bf16": (I32, [P, P, P, I64, I32, P, P, P, P, P, P]),
     "pcb_count_labels": (I32, [P, P, I64, I32, I32, P, P, P]),

@@ -50,12 +50,31 @@ constexpr int SB_NCAND = 8;     // candidate slots per ambiguous row (pass 2)
 template <int NKC>
 struct SbCfg {
   static constexpr uint32_t kTileBytes = 128 * 128;                 // 128 rows x 128 B
-  static constexpr uint32_t kABytes = 2 * NKC * kTileBytes;         // resident A (2 row tiles)
+  // resident A (2 row tiles), double-buffered across row pairs when it fits
+  // (the next pair's rows load while the current pair's MMAs run)
+  static constexpr int kAStages = NKC <= 2 ? 2 : 1;
+  static constexpr uint32_t kAPair = 2 * NKC * kTileBytes;
+  static constexpr uint32_t kABytes = kAStages * kAPair;
   static constexpr uint32_t kBBytes = SB_BN * 128;                  // 16 KB per B stage
   static constexpr uint32_t kBarBytes = 1024;
   static constexpr uint32_t kSmem = 1024 + kABytes + SB_STAGES * kBBytes + kBarBytes + SC_KMAX * 4;
   static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
+
+// First centroid column of a row pair: the previous label of the pair's
+// middle row.  With rows laid out by label most rows of the pair find their
+// minimum next to it, so every role visits its tile first (tiles in rotated
+// order) and the epilogue visits its 32-column chunk first within that tile:
+// the running minimum is set at once and the other chunks are skipped.
+// Visiting order never changes results (certified rows have one candidate;
+// ambiguous rows are resolved exactly, lowest index on ties).
+__device__ __forceinline__ int sb_first_col(const int32_t* lprev, const int32_t* orig, int64_t pr, int64_t n, int k) {
+  if (lprev == nullptr) return 0;
+  int64_t r = pr * 256 + 128;
+  if (r >= n) r = pr * 256;
+  const int l = lprev[orig != nullptr ? (int64_t)orig[r] : r];
+  return (l >= 0 && l < k) ? l : 0;
+}
 
 // Rows handled by a launch: pass 1 = n; pass 2 = the device-side ambiguous
 // count, or 0 when the resolver is bypassed (count above `bypass`).
@@ -73,7 +92,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
                           int32_t* __restrict__ labels, int* __restrict__ amb_list, int* __restrict__ amb_count,
                           float* __restrict__ amb_thr, int64_t bypass, int* __restrict__ cand,
                           int* __restrict__ cand_n, const int32_t* __restrict__ orig,
-                          const long long* __restrict__ state) {
+                          const int32_t* __restrict__ lprev, const long long* __restrict__ state) {
   using Cfg = SbCfg<NKC>;
   if (stopped(state)) return;
   const int64_t n = CAND ? sb_rows(n_in, amb_count, bypass) : n_in;
@@ -84,9 +103,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
   uint8_t* sA = smem;
   uint8_t* sB = smem + Cfg::kABytes;
   uint8_t* bar_area = sB + SB_STAGES * Cfg::kBBytes;
-  uint64_t* afull = reinterpret_cast<uint64_t*>(bar_area);  // [NKC]
-  uint64_t* aempty = afull + NKC;                            // [NKC]
-  uint64_t* full = aempty + NKC;                             // [STAGES]
+  constexpr int AS = Cfg::kAStages;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(bar_area);  // [AS][NKC]
+  uint64_t* aempty = afull + AS * NKC;                       // [AS][NKC]
+  uint64_t* full = aempty + AS * NKC;                        // [STAGES]
   uint64_t* empty = full + SB_STAGES;                        // [STAGES]
   uint64_t* tfull = empty + SB_STAGES;                       // [2]
   uint64_t* tempty = tfull + 2;                              // [2]
@@ -102,8 +122,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     ptx::prefetch_tmap(&tm_a);
     ptx::prefetch_tmap(&tm_b);
     for (int c = 0; c < NKC; ++c) {
-      ptx::mbar_init(&afull[c], 1);
-      ptx::mbar_init(&aempty[c], 1);
+      for (int a = 0; a < AS; ++a) {
+        ptx::mbar_init(&afull[a * NKC + c], 1);
+        ptx::mbar_init(&aempty[a * NKC + c], 1);
+      }
     }
     for (int s = 0; s < SB_STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -128,11 +150,14 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     int it = 0;
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
       for (int c = 0; c < NKC; ++c) {
-        if (it > 0) ptx::mbar_wait(&aempty[c], (uint32_t)((it - 1) & 1));
+        const int ab = it % AS;
+        uint8_t* sAp = sA + ab * Cfg::kAPair;
+        if (it >= AS) ptx::mbar_wait(&aempty[ab * NKC + c], (uint32_t)((it / AS - 1) & 1));
         if (ptx::elect_one()) {
-          ptx::mbar_expect_tx(&afull[c], 2 * Cfg::kTileBytes);
-          ptx::tma_load_2d(&tm_a, &afull[c], sA + (0 * NKC + c) * Cfg::kTileBytes, c * SB_BKE, (int)(pr * 256), pol);
-          ptx::tma_load_2d(&tm_a, &afull[c], sA + (1 * NKC + c) * Cfg::kTileBytes, c * SB_BKE,
+          ptx::mbar_expect_tx(&afull[ab * NKC + c], 2 * Cfg::kTileBytes);
+          ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (0 * NKC + c) * Cfg::kTileBytes, c * SB_BKE,
+                           (int)(pr * 256), pol);
+          ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (1 * NKC + c) * Cfg::kTileBytes, c * SB_BKE,
                            (int)(pr * 256 + 128), pol);
         }
         __syncwarp();
@@ -143,13 +168,19 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     const uint64_t pol = ptx::policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
+    // first tile of the next pair fetched one pair ahead (two dependent
+    // global loads would otherwise stall the ring at every pair boundary)
+    int t0_nx = blockIdx.x < npairs ? sb_first_col(lprev, orig, blockIdx.x, n, k) / SB_BN : 0;
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+      const int t0 = t0_nx;
+      if (pr + gridDim.x < npairs) t0_nx = sb_first_col(lprev, orig, pr + gridDim.x, n, k) / SB_BN;
       for (int nt = 0; nt < ntiles; ++nt) {
+        const int tile = nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles;
         for (int c = 0; c < NKC; ++c) {
           ptx::mbar_wait(&empty[stage], phase ^ 1u);
           if (ptx::elect_one()) {
             ptx::mbar_expect_tx(&full[stage], Cfg::kBBytes);
-            ptx::tma_load_2d(&tm_b, &full[stage], sB + stage * Cfg::kBBytes, c * SB_BKE, nt * SB_BN, pol);
+            ptx::tma_load_2d(&tm_b, &full[stage], sB + stage * Cfg::kBBytes, c * SB_BKE, tile * SB_BN, pol);
           }
           __syncwarp();
           if (++stage == SB_STAGES) { stage = 0; phase ^= 1u; }
@@ -170,11 +201,13 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         ptx::tc_fence_after();
         const uint32_t d0 = tmem + (uint32_t)(abuf * 256);
         for (int c = 0; c < NKC; ++c) {
-          if (nt == 0) ptx::mbar_wait(&afull[c], (uint32_t)(it & 1));
+          const int ab = it % AS;
+          uint8_t* sAp = sA + ab * Cfg::kAPair;
+          if (nt == 0) ptx::mbar_wait(&afull[ab * NKC + c], (uint32_t)((it / AS) & 1));
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint64_t a0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (0 * NKC + c) * Cfg::kTileBytes));
-          const uint64_t a1 = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (1 * NKC + c) * Cfg::kTileBytes));
+          const uint64_t a0 = ptx::sdesc_k_sw128(ptx::smem_u32(sAp + (0 * NKC + c) * Cfg::kTileBytes));
+          const uint64_t a1 = ptx::sdesc_k_sw128(ptx::smem_u32(sAp + (1 * NKC + c) * Cfg::kTileBytes));
           const uint64_t bd = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * Cfg::kBBytes));
           if (ptx::elect_one()) {
 #pragma unroll
@@ -184,7 +217,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
               ptx::umma_f16(d0 + 128, a1 + off, bd + off, idesc, (c | ks) != 0);
             }
             ptx::umma_commit(&empty[stage]);
-            if (nt + 1 == ntiles) ptx::umma_commit(&aempty[c]);  // A chunk free for the next pair
+            if (nt + 1 == ntiles) ptx::umma_commit(&aempty[ab * NKC + c]);  // A chunk free again
           }
           __syncwarp();
           if (++stage == SB_STAGES) { stage = 0; phase ^= 1u; }
@@ -208,10 +241,28 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     // TMEM loads run one 32-column chunk ahead of the arithmetic (vA / vB by
     // chunk parity; 4 chunks per tile), across tile and pair boundaries
     uint32_t vA[32], vB[32];
+    // per-row inputs of the next pair are fetched one pair ahead: their DRAM
+    // latency would otherwise hold both TMEM buffers (and the MMAs) at every
+    // pair boundary
+    float an_nx = 0.0f, dan_nx = 0.0f;
+    int fc_nx = 0;
+    int64_t out_nx = 0;
+    auto fetch_pair = [&](int64_t p) {
+      const int64_t rr = p * 256 + r_in < n ? p * 256 + r_in : n - 1;
+      out_nx = (!CAND && orig != nullptr) ? (int64_t)orig[rr] : rr;
+      if (CAND) {
+        an_nx = amb_thr[rr];
+      } else {
+        an_nx = anorm[rr];
+        dan_nx = danorm[rr];
+      }
+      fc_nx = sb_first_col(lprev, orig, p, n, k);
+    };
     if (blockIdx.x < npairs) {
+      fetch_pair(blockIdx.x);
       ptx::mbar_wait(&tfull[0], 0);
       ptx::tc_fence_after();
-      ptx::tmem_ld_32x32b_x32_async(tlane, vA);
+      ptx::tmem_ld_32x32b_x32_async(tlane + 32 * ((fc_nx % SB_BN) / 32), vA);
     }
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
       const int64_t row = pr * 256 + r_in;
@@ -220,23 +271,28 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       float twoE = 0.0f, big = 0.0f, thr = 0.0f;
       int nc = 0;
       if (CAND) {
-        thr = amb_thr[rc];
+        thr = an_nx;
       } else {
-        twoE = screen_two_e(anorm[rc], danorm[rc], Bmax, dBmax, OFF, acc_rel);
+        twoE = screen_two_e(an_nx, dan_nx, Bmax, dBmax, OFF, acc_rel);
         big = 64.0f / twoE;
       }
+      const int t0 = fc_nx / SB_BN, q0 = (fc_nx % SB_BN) / 32;
+      const int64_t out_row = out_nx;  // original row id (label store)
+      if (!last_pair) fetch_pair(pr + gridDim.x);
       float R1 = 3.4e38f, cnt = 0.0f;
       int r1 = 0;
       for (int nt = 0; nt < ntiles; ++nt) {
         const uint32_t taddr = tlane + (uint32_t)(abuf * 256);
-        const int c0 = nt * SB_BN;
+        const int c0 = (nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles) * SB_BN;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint32_t (&cur)[32] = (q & 1) ? vB : vA;
           uint32_t (&nxt)[32] = (q & 1) ? vA : vB;
           ptx::tmem_wait_ld(cur);
+          const int qe = nt == 0 ? ((q + q0) & 3) : q;  // chunk of the tile held by cur
           if (q < 3) {
-            ptx::tmem_ld_32x32b_x32_async(taddr + 32 * (q + 1), nxt);
+            const int qn = nt == 0 ? ((q + 1 + q0) & 3) : q + 1;
+            ptx::tmem_ld_32x32b_x32_async(taddr + 32 * qn, nxt);
           } else {
             // this buffer is fully read: hand it back, prefetch the next one
             ptx::tc_fence_before();
@@ -246,7 +302,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             if (nt + 1 < ntiles || !last_pair) {
               ptx::mbar_wait(&tfull[abuf], aphase);
               ptx::tc_fence_after();
-              ptx::tmem_ld_32x32b_x32_async(tlane + (uint32_t)(abuf * 256), nxt);
+              // first chunk of the next pair: read fc_nx only here, a pair after
+              // its (two dependent) loads were issued
+              const int qn = nt + 1 < ntiles ? 0 : (fc_nx % SB_BN) / 32;
+              ptx::tmem_ld_32x32b_x32_async(tlane + (uint32_t)(abuf * 256) + 32 * qn, nxt);
             }
           }
           float v[32], cp[32];
@@ -257,7 +316,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           R1 = fminf(R1, v[0] + v[31]);
           continue;
 #endif
-          load_cprime(cp, cprime + c0 + 32 * q);
+          load_cprime(cp, cprime + c0 + 32 * qe);
           if (CAND) {
             // candidate mask of the chunk (FSETP + SEL per key), then a short
             // loop over its set bits (2-3 candidates per row in total)
@@ -267,7 +326,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             while (bits) {
               const int i = __ffs(bits) - 1;
               bits &= bits - 1;
-              if (row < n && nc < SB_NCAND) cand[rc * SB_NCAND + nc] = c0 + 32 * q + i;
+              if (row < n && nc < SB_NCAND) cand[rc * SB_NCAND + nc] = c0 + 32 * qe + i;
               ++nc;
             }
           } else {
@@ -287,16 +346,30 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
 #pragma unroll
             for (int i = 3; i < 31; i += 2) mm = fmin3(mm, km[i], km[i + 1]);
             mm = fminf(mm, km[31]);
-            if (__any_sync(0xffffffffu, mm <= thr_skip))
-              screen_chunk_regs(v, cp, msk, c0 + 32 * q, twoE, big, R1, r1, cnt);
+#if defined(PCB_EXP) && PCB_EXP == 5
+            // experiment build: skip-path cost only (results invalid)
+            if (__any_sync(0xffffffffu, mm <= thr_skip)) R1 = fminf(R1, mm);
+#else
+            if (__any_sync(0xffffffffu, mm <= thr_skip)) {
+              screen_chunk_keys(km, msk, c0 + 32 * qe, twoE, big, R1, r1, cnt);
+#if defined(PCB_EXP) && PCB_EXP == 6
+              // experiment build: count full-path chunks per position (q + 4 * nt) in state[8..]
+              if (lane == 0) atomicAdd((unsigned long long*)state + 8 + (nt < 8 ? nt * 4 + q : 32), 1ull);
+#endif
+            }
+#endif
           }
         }
       }
       if (CAND) {
         if (row < n) cand_n[row] = nc;
       } else {
-        if (row < n) labels[orig != nullptr ? orig[row] : row] = r1;
+        if (row < n) labels[out_row] = r1;
+#if defined(PCB_EXP) && PCB_EXP == 7
+        const bool amb = false;  // experiment build: no ambiguous-row append
+#else
         const bool amb = row < n && cnt > 1.0f;
+#endif
         const unsigned m = __ballot_sync(0xffffffffu, amb);
         if (m) {
           int base = 0;
@@ -342,8 +415,8 @@ template <int NKC, bool CAND>
 static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                               const float* an, const float* dan, const float* cnorm, const float* bstat,
                               int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
-                              int* cand, int* cand_n, const int32_t* orig, const long long* state,
-                              cudaStream_t st) {
+                              int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev,
+                              const long long* state, cudaStream_t st) {
   using Cfg = SbCfg<NKC>;
   CUtensorMap ta, tb;
   int rc;
@@ -355,7 +428,7 @@ static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bflo
   const int64_t npairs = (n + 255) / 256;
   const int grid = (int)std::min<int64_t>(npairs, (int64_t)sm_count());
   kern<<<grid, SB_THREADS, Cfg::kSmem, st>>>(ta, tb, an, dan, cnorm, bstat, n, k, labels, amb_list, amb_count,
-                                             amb_thr, bypass, cand, cand_n, orig, state);
+                                             amb_thr, bypass, cand, cand_n, orig, lprev, state);
   PCB_CHECK_LAUNCH();
   return 0;
 }
@@ -364,11 +437,12 @@ template <bool CAND>
 static int dispatch_bf16(int ldb, const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                          const float* an, const float* dan, const float* cnorm, const float* bstat,
                          int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
-                         int* cand, int* cand_n, const int32_t* orig, const long long* state, cudaStream_t st) {
+                         int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev, const long long* state,
+                         cudaStream_t st) {
 #define PCB_SB_CASE(N)                                                                                      \
   case N:                                                                                                   \
     return launch_screen_bf16<N, CAND>(A, n, B, k, an, dan, cnorm, bstat, labels, amb_list, amb_count,      \
-                                       amb_thr, bypass, cand, cand_n, orig, state, st);
+                                       amb_thr, bypass, cand, cand_n, orig, lprev, state, st);
   switch (ldb / SB_BKE) {
     PCB_SB_CASE(1)
     PCB_SB_CASE(2)
@@ -589,13 +663,14 @@ extern "C" int pcb_screen_prep_centroids_bf16(const float* C, int k, int d, int 
 extern "C" int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const void* C_b, int k,
                                       const float* cnorm, const float* anorm, const float* danorm,
                                       const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
-                                      float* amb_thr, const int32_t* orig, const long long* state, void* stream) {
+                                      float* amb_thr, const int32_t* orig, const int32_t* labels_prev,
+                                      const long long* state, void* stream) {
   if (n < 1 || ldb < SB_BKE || ldb % SB_BKE || k < 1 || !P_b || !C_b || !cnorm || !anorm || !danorm || !bstat ||
       !labels || !amb_list || !amb_count || !amb_thr)
     return PCB_EINVAL;
   if (n > INT32_MAX || k > SC_KMAX) return PCB_EUNSUP;
   return dispatch_bf16<false>(ldb, (const __nv_bfloat16*)P_b, n, (const __nv_bfloat16*)C_b, k, anorm, danorm, cnorm,
-                              bstat, labels, amb_list, amb_count, amb_thr, 0, nullptr, nullptr, orig, state,
+                              bstat, labels, amb_list, amb_count, amb_thr, 0, nullptr, nullptr, orig, labels_prev, state,
                               (cudaStream_t)stream);
 }
 
@@ -621,7 +696,7 @@ extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const v
   PCB_CHECK_LAUNCH();
   int rc = dispatch_bf16<true>(ldb, (const __nv_bfloat16*)sub_b, n, (const __nv_bfloat16*)C_b, k, nullptr, nullptr,
                                cnorm, bstat, nullptr, nullptr, const_cast<int*>(amb_count),
-                               const_cast<float*>(amb_thr), bypass, cand, cand_n, nullptr, state, st);
+                               const_cast<float*>(amb_thr), bypass, cand, cand_n, nullptr, nullptr, state, st);
   if (rc) return rc;
   const int DQ = (d + 31) / 32;  // float4 per lane (8 lanes per row)
   const int xgrid = sm_count() * 16;

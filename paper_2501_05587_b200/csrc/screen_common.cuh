@@ -78,16 +78,15 @@ __device__ __forceinline__ void load_cprime(float (&cp)[32], const float* __rest
 // Per element: 1/2 FFMA2 (key), 1 LOP3 (index pack), 1/2 FMNMX3, 1 FFMA.SAT and
 // 1/2 FADD2 (count) — the epilogue is issue-bound, so the f32x2 forms matter.
 // `msk` is ~31 held in a register so the pack is one LOP3 with the id immediate.
-__device__ __forceinline__ void screen_chunk_regs(float (&v)[32], const float (&cp)[32], uint32_t msk, int col0,
-                                                  float twoE, float big, float& R1, int& r1, float& cnt) {
-  const unsigned long long m2 = f2pack(-2.0f, -2.0f);
+__device__ __forceinline__ void screen_update(const float (&v)[32], float m, int col0, float twoE, float big,
+                                              float& R1, int& r1, float& cnt);
+
+// Same on keys already formed (v[i] = cp[i] - 2 acc[i]).
+__device__ __forceinline__ void screen_chunk_keys(const float (&v)[32], uint32_t msk, int col0, float twoE, float big,
+                                                  float& R1, int& r1, float& cnt) {
   float ma = 3.4e38f, mb = 3.4e38f;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const unsigned long long a = ffma2(f2pack(v[4 * q + 0], v[4 * q + 1]), m2, f2pack(cp[4 * q + 0], cp[4 * q + 1]));
-    const unsigned long long b = ffma2(f2pack(v[4 * q + 2], v[4 * q + 3]), m2, f2pack(cp[4 * q + 2], cp[4 * q + 3]));
-    f2unpack(a, v[4 * q + 0], v[4 * q + 1]);
-    f2unpack(b, v[4 * q + 2], v[4 * q + 3]);
     const float k0 = __uint_as_float((__float_as_uint(v[4 * q + 0]) & msk) | (uint32_t)(4 * q + 0));
     const float k1 = __uint_as_float((__float_as_uint(v[4 * q + 1]) & msk) | (uint32_t)(4 * q + 1));
     const float k2 = __uint_as_float((__float_as_uint(v[4 * q + 2]) & msk) | (uint32_t)(4 * q + 2));
@@ -95,7 +94,12 @@ __device__ __forceinline__ void screen_chunk_regs(float (&v)[32], const float (&
     ma = fmin3(ma, k0, k1);
     mb = fmin3(mb, k2, k3);
   }
-  const float m = fminf(ma, mb);
+  screen_update(v, fminf(ma, mb), col0, twoE, big, R1, r1, cnt);
+}
+
+// Running-min / ambiguity-count update of one chunk with packed minimum m.
+__device__ __forceinline__ void screen_update(const float (&v)[32], float m, int col0, float twoE, float big,
+                                              float& R1, int& r1, float& cnt) {
   // (a) much better min: every earlier counted key is above the new threshold;
   // (b) slightly better: the old min stays within it, so the row is ambiguous
   //     whatever the over-count
@@ -115,6 +119,26 @@ __device__ __forceinline__ void screen_chunk_regs(float (&v)[32], const float (&
   float x0, x1;
   f2unpack(fadd2(c2, d2), x0, x1);
   cnt += x0 + x1;
+}
+
+__device__ __forceinline__ void screen_chunk_regs(float (&v)[32], const float (&cp)[32], uint32_t msk, int col0,
+                                                  float twoE, float big, float& R1, int& r1, float& cnt) {
+  const unsigned long long m2 = f2pack(-2.0f, -2.0f);
+  float ma = 3.4e38f, mb = 3.4e38f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const unsigned long long a = ffma2(f2pack(v[4 * q + 0], v[4 * q + 1]), m2, f2pack(cp[4 * q + 0], cp[4 * q + 1]));
+    const unsigned long long b = ffma2(f2pack(v[4 * q + 2], v[4 * q + 3]), m2, f2pack(cp[4 * q + 2], cp[4 * q + 3]));
+    f2unpack(a, v[4 * q + 0], v[4 * q + 1]);
+    f2unpack(b, v[4 * q + 2], v[4 * q + 3]);
+    const float k0 = __uint_as_float((__float_as_uint(v[4 * q + 0]) & msk) | (uint32_t)(4 * q + 0));
+    const float k1 = __uint_as_float((__float_as_uint(v[4 * q + 1]) & msk) | (uint32_t)(4 * q + 1));
+    const float k2 = __uint_as_float((__float_as_uint(v[4 * q + 2]) & msk) | (uint32_t)(4 * q + 2));
+    const float k3 = __uint_as_float((__float_as_uint(v[4 * q + 3]) & msk) | (uint32_t)(4 * q + 3));
+    ma = fmin3(ma, k0, k1);
+    mb = fmin3(mb, k2, k3);
+  }
+  screen_update(v, fminf(ma, mb), col0, twoE, big, R1, r1, cnt);
 }
 
 __device__ __forceinline__ void screen_chunk(float (&v)[32], const float* __restrict__ cprime_chunk, uint32_t msk,

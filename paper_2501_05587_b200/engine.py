@@ -409,8 +409,8 @@ class LloydEngine(ShardSequence):
             self._kmark(0)
             L.call("pcb_assign_screen_bf16", _p(self.P_b), self.n, self.ldb, _p(self.C_b), self.k,
                    _p(self.cnorm), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
-                   _p(self.amb_list), _p(self.amb_count), _p(self.amb_thr), _p(self.orig), _p(state),
-                   _stream())
+                   _p(self.amb_list), _p(self.amb_count), _p(self.amb_thr), _p(self.orig), _p(prev),
+                   _p(state), _stream())
             self._kmark(1)
             L.call("pcb_resolve_screen_bf16", _p(self.P), self.n, self.d, _p(self.P_b), self.ldb,
                    _p(self.C_b), _p(self.C), self.k, _p(self.cnorm), _p(self.bstat), _p(self.amb_list),
