@@ -216,6 +216,29 @@ int pcb_segment_sums_f64(const double* P, int64_t n, int d, const int32_t* perm,
                          const int32_t* offsets, int k, const double* C, double* own_sorted,
                          double* acc, const long long* state, void* stream);
 
+/* ---- delta centroid update (update.cu).  Per rank, S (k x d f64) holds the
+ *      per-cluster sums of the rank's rows for the current labels.  After the
+ *      assignment (acc holds the new local counts and changed):
+ *   pcb_update_mode  -> state[6] = 1 (delta) unless force_full, more than
+ *                       frac * n rows changed, a local count is 0, or a repair
+ *                       marked S stale (state[7]); 0 = full update
+ *   pcb_sort_by_label / pcb_segment_sums_*: no-ops in delta mode
+ *   pcb_delta_update_*: delta mode: S += rows that joined, -= rows that left
+ *                       (changed rows only), acc sums <- S, acc objective <-
+ *                       Q - 2 sum_j <c_j, S_j> + sum_j n_j |c_j|^2 (exact
+ *                       identity for sum_i |p_i - c_l(i)|^2, clustering.py:148);
+ *                       full mode: S <- acc sums.  Q = pcb_sum_squares_*(P).  */
+int pcb_update_mode(const double* acc, int k, int d, int64_t n, double frac, int force_full,
+                    long long* state, void* stream);
+int pcb_delta_update_f32(const float* P, int64_t n, int d, const int32_t* labels_prev, const int32_t* labels,
+                         const float* C, int k, double* S, const double* Q, double* acc,
+                         const long long* state, void* stream);
+int pcb_delta_update_f64(const double* P, int64_t n, int d, const int32_t* labels_prev, const int32_t* labels,
+                         const double* C, int k, double* S, const double* Q, double* acc,
+                         const long long* state, void* stream);
+int pcb_sum_squares_f32(const float* X, int64_t count, double* out, void* stream);
+int pcb_sum_squares_f64(const double* X, int64_t count, double* out, void* stream);
+
 /* ---- empty-cluster repair (clustering.py:111-139), single-rank, on device.
  *   For each empty cluster j ascending: the not-yet-moved point with the
  *   largest own distance (lowest index on ties) moves to j; repeated while any

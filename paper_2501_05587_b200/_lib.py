@@ -42,6 +42,11 @@ SIGNATURES = {
     "pcb_screen_prep_centroids": (I32, [P, I32, I32, P, P, P, P]),
     "pcb_assign_screen_f32": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P]),
     "pcb_resolve_ambiguous_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P, P, P, I32, P, P, P]),
+    "pcb_update_mode": (I32, [P, I32, I32, I64, F64, I32, P, P]),
+    "pcb_delta_update_f32": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),
+    "pcb_delta_update_f64": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),
+    "pcb_sum_squares_f32": (I32, [P, I64, P, P]),
+    "pcb_sum_squares_f64": (I32, [P, I64, P, P]),
     "pcb_screen_bf16_ld": (I32, [I32]),
     "pcb_screen_bf16_ncand": (I32, []),
     "pcb_screen_prep_points_bf16": (I32, [P, I64, I32, I32, P, P, P, P, P]),

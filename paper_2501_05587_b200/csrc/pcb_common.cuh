@@ -31,12 +31,20 @@ struct AccLayout {
 // Device loop state shared by all per-iteration kernels (int64 words):
 //   [0] iterations recorded, [1] stop flag, [2] converged flag,
 //   [3] repairs (moved points) of the current iteration,
-//   [4] finalize block ticket, [5] non-finite distance seen, [6..7] spare
-enum StateWord { kIters = 0, kStop = 1, kConverged = 2, kMoved = 3, kTicket = 4, kNanFlag = 5,
-                 kStateWords = 8 };
+//   [4] finalize block ticket, [5] non-finite distance seen,
+//   [6] centroid-update mode of the iteration (0 full, 1 delta; update.cu),
+//   [7] persistent per-cluster sums stale (a repair moved points)
+enum StateWord { kIters = 0, kStop = 1, kConverged = 2, kMoved = 3, kTicket = 4, kNanFlag = 5, kMode = 6,
+                 kSumsStale = 7, kStateWords = 8 };
 
 __device__ __forceinline__ bool stopped(const long long* state) {
   return state != nullptr && ((volatile const long long*)state)[kStop] != 0;
+}
+
+// Delta centroid update this iteration: the counting sort / segmented sums of
+// the full update are skipped (they exit at once).
+__device__ __forceinline__ bool delta_mode(const long long* state) {
+  return state != nullptr && ((volatile const long long*)state)[kMode] == 1;
 }
 
 template <typename T>

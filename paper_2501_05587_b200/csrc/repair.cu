@@ -131,6 +131,7 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
             labels[donor] = j;
             own[g.s] = -INFINITY;
             atomicAdd((unsigned long long*)&state[kMoved], 1ull);
+            state[kSumsStale] = 1;  // the delta update's per-cluster sums miss this move
           }
         }
       }
@@ -256,6 +257,7 @@ __global__ void repair_commit_kernel(double* __restrict__ acc, int k, int d, int
     acc[L.objective()] += delta[d + 1];
     acc[L.changed()] += delta[d + 2];
     state[kMoved] += 1;
+    state[kSumsStale] = 1;
   }
 }
 

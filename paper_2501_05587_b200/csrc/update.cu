@@ -25,7 +25,7 @@ namespace pcb {
 __global__ void __launch_bounds__(1024)
 scan_counts(const double* __restrict__ counts, int k, int32_t* __restrict__ offsets,
             int32_t* __restrict__ cursor, const long long* __restrict__ state) {
-  if (stopped(state)) return;
+  if (stopped(state) || delta_mode(state)) return;
   __shared__ int warp_tot[32];
   __shared__ int carry_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -65,7 +65,7 @@ scan_counts(const double* __restrict__ counts, int k, int32_t* __restrict__ offs
 __global__ void __launch_bounds__(256)
 scatter_by_label(const int32_t* __restrict__ labels, int64_t n, int32_t* __restrict__ cursor,
                  int32_t* __restrict__ perm, const long long* __restrict__ state) {
-  if (stopped(state)) return;
+  if (stopped(state) || delta_mode(state)) return;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
@@ -93,7 +93,7 @@ constexpr int SC_EPT = 16;
 __global__ void __launch_bounds__(256)
 scatter_by_label_blocked(const int32_t* __restrict__ labels, int64_t n, int k, int32_t* __restrict__ cursor,
                          int32_t* __restrict__ perm, const long long* __restrict__ state) {
-  if (stopped(state)) return;
+  if (stopped(state) || delta_mode(state)) return;
   extern __shared__ int sm[];
   int* hist = sm;
   int* base = sm + k;
@@ -148,7 +148,7 @@ segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict
             const int32_t* __restrict__ offsets, int k, const T* __restrict__ C, int64_t slice,
             double* __restrict__ own_sorted, double* __restrict__ acc,
             const long long* __restrict__ state) {
-  if (stopped(state)) return;
+  if (stopped(state) || delta_mode(state)) return;
   const AccLayout L{k, d};
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256)
 segsum_v4(const float* __restrict__ P, int64_t n, int d, const int32_t* __restrict__ perm,
           const int32_t* __restrict__ offsets, int k, const float* __restrict__ C, int64_t slice,
           double* __restrict__ own_sorted, double* __restrict__ acc, const long long* __restrict__ state) {
-  if (stopped(state)) return;
+  if (stopped(state) || delta_mode(state)) return;
   const AccLayout L{k, d};
   const int lane = threadIdx.x & 31;
   const int d4 = d >> 2;
@@ -348,7 +348,7 @@ segsum_thread(const T* __restrict__ P, int64_t n, int d, const int32_t* __restri
               const int32_t* __restrict__ offsets, int k, const T* __restrict__ C, int64_t slice,
               double* __restrict__ own_sorted, double* __restrict__ acc,
               const long long* __restrict__ state) {
-  if (stopped(state)) return;
+  if (stopped(state) || delta_mode(state)) return;
   const AccLayout L{k, d};
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -439,6 +439,117 @@ static int segment_sums(const T* P, int64_t n, int d, const int32_t* perm, const
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Delta centroid update.  Near convergence few labels change per iteration,
+// so instead of re-summing every row the rank keeps its per-cluster f64 sums S
+// (of its own rows, for the current labels) and adds/subtracts only the rows
+// whose label changed.  The objective then follows from the sums exactly:
+//   sum_i |p_i - c_l(i)|^2 = Q - 2 sum_j <c_j, S_j> + sum_j n_j |c_j|^2,
+// Q = sum_i |p_i|^2 (f64, once per fit), c = the centroids the labels were
+// assigned against (clustering.py:148 evaluates the same sum row by row).
+// The full update (counting sort + segmented sums, exact own distances) runs
+// whenever more than `frac` of the rows changed, a local cluster count is 0
+// (the repair needs own distances), the sums are not valid yet, or a repair
+// moved points (state[kSumsStale]); it refreshes S.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+update_mode_kernel(const double* __restrict__ acc, int k, int d, int64_t n, double frac, int force_full,
+                   long long* __restrict__ state) {
+  const AccLayout L{k, d};
+  __shared__ int any_empty;
+  if (threadIdx.x == 0) any_empty = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x)
+    if (acc[L.counts() + j] < 0.5) any_empty = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const bool full = force_full || any_empty || state[kSumsStale] != 0 || acc[L.changed()] > frac * (double)n;
+    state[kMode] = full ? 0 : 1;
+    state[kSumsStale] = 0;
+  }
+}
+
+// Changed rows only: S[new] += p, S[prev] -= p (f64), one warp per row.
+template <typename T>
+__global__ void __launch_bounds__(256)
+delta_sums_kernel(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict__ prev,
+                  const int32_t* __restrict__ labels, double* __restrict__ S, const long long* __restrict__ state) {
+  if (stopped(state) || !delta_mode(state)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = w * 32; base < n; base += nw * 32) {
+    const int64_t i = base + lane;
+    int a = 0, b = 0;
+    if (i < n) { a = prev[i]; b = labels[i]; }
+    unsigned m = __ballot_sync(0xffffffffu, i < n && a != b);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t r = base + src;
+      const int ja = __shfl_sync(0xffffffffu, a, src), jb = __shfl_sync(0xffffffffu, b, src);
+      for (int t = lane; t < d; t += 32) {
+        const double x = (double)P[r * d + t];
+        atomicAdd(&S[(int64_t)jb * d + t], x);
+        atomicAdd(&S[(int64_t)ja * d + t], -x);
+      }
+    }
+  }
+}
+
+// Full mode: S <- the sums just computed.  Delta mode: acc sums <- S and the
+// objective from the identity above.
+template <typename T>
+__global__ void __launch_bounds__(256)
+delta_finish_kernel(const T* __restrict__ C, int k, int d, double* __restrict__ acc, double* __restrict__ S,
+                    const double* __restrict__ Q, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const AccLayout L{k, d};
+  const int64_t kd = (int64_t)k * d;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  if (!delta_mode(state)) {
+    for (int64_t e = tid; e < kd; e += nth) S[e] = acc[e];
+    return;
+  }
+  double part = 0.0;
+  for (int64_t e = tid; e < kd; e += nth) {
+    const double s = S[e];
+    acc[e] = s;
+    const double c = (double)C[e];
+    part += c * (acc[L.counts() + e / d] * c - 2.0 * s);
+  }
+  part = warp_sum(part);
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) b += red[i];
+    if (blockIdx.x == 0) b += *Q;
+    atomicAdd(&acc[L.objective()], b);
+  }
+}
+
+// sum of squares of all entries, f64 (Q of the objective identity)
+template <typename T>
+__global__ void __launch_bounds__(256)
+sum_squares_kernel(const T* __restrict__ X, int64_t count, double* __restrict__ out) {
+  double part = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    const double x = (double)X[e];
+    part = fma(x, x, part);
+  }
+  part = warp_sum(part);
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) b += red[i];
+    atomicAdd(out, b);
+  }
+}
+
 }  // namespace pcb
 
 extern "C" int pcb_sort_by_label(const int32_t* labels, int64_t n, int k, const double* counts,
@@ -474,4 +585,57 @@ extern "C" int pcb_segment_sums_f64(const double* P, int64_t n, int d, const int
                                     double* acc, const long long* state, void* stream) {
   return pcb::segment_sums<double>(P, n, d, perm, offsets, k, C, own_sorted, acc, state,
                                    (cudaStream_t)stream);
+}
+
+extern "C" int pcb_update_mode(const double* acc, int k, int d, int64_t n, double frac, int force_full,
+                               long long* state, void* stream) {
+  if (k < 1 || d < 1 || n < 1 || !acc || !state) return PCB_EINVAL;
+  pcb::update_mode_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(acc, k, d, n, frac, force_full, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename T>
+static int delta_update(const T* P, int64_t n, int d, const int32_t* prev, const int32_t* labels, const T* C, int k,
+                        double* S, const double* Q, double* acc, const long long* state, cudaStream_t st) {
+  if (n < 1 || d < 1 || k < 1 || !P || !prev || !labels || !C || !S || !Q || !acc || !state) return PCB_EINVAL;
+  const int sms = pcb::sm_count();
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+  pcb::delta_sums_kernel<T><<<grid, 256, 0, st>>>(P, n, d, prev, labels, S, state);
+  PCB_CHECK_LAUNCH();
+  const int64_t kd = (int64_t)k * d;
+  const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((kd + 255) / 256, (int64_t)sms * 4));
+  pcb::delta_finish_kernel<T><<<g2, 256, 0, st>>>(C, k, d, acc, S, Q, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_delta_update_f32(const float* P, int64_t n, int d, const int32_t* prev, const int32_t* labels,
+                                    const float* C, int k, double* S, const double* Q, double* acc,
+                                    const long long* state, void* stream) {
+  return delta_update<float>(P, n, d, prev, labels, C, k, S, Q, acc, state, (cudaStream_t)stream);
+}
+
+extern "C" int pcb_delta_update_f64(const double* P, int64_t n, int d, const int32_t* prev, const int32_t* labels,
+                                    const double* C, int k, double* S, const double* Q, double* acc,
+                                    const long long* state, void* stream) {
+  return delta_update<double>(P, n, d, prev, labels, C, k, S, Q, acc, state, (cudaStream_t)stream);
+}
+
+template <typename T>
+static int sum_squares(const T* X, int64_t count, double* out, cudaStream_t st) {
+  if (count < 1 || !X || !out) return PCB_EINVAL;
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
+  if (e != cudaSuccess) return (int)e;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)pcb::sm_count() * 8));
+  pcb::sum_squares_kernel<T><<<grid, 256, 0, st>>>(X, count, out);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_sum_squares_f32(const float* X, int64_t count, double* out, void* stream) {
+  return sum_squares<float>(X, count, out, (cudaStream_t)stream);
+}
+extern "C" int pcb_sum_squares_f64(const double* X, int64_t count, double* out, void* stream) {
+  return sum_squares<double>(X, count, out, (cudaStream_t)stream);
 }

@@ -18,6 +18,7 @@ only for device memory, streams, pinned host buffers and torch.distributed.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -177,7 +178,7 @@ class ShardSequence:
         self._assign(prev, new, self.acc, self.state)           # clustering.py:310-311, 146-149
         if events is not None:
             events[1].record()
-        self._sort_and_sum(new, self.state)                     # clustering.py:282-288, 148
+        self._update(prev, new)                                 # clustering.py:282-288, 148
         self._after_update(t)
         self._allreduce(self.acc)                               # the one collective per iteration
         if raw_out is not None:
@@ -186,6 +187,9 @@ class ShardSequence:
         self._finalize(check_convergence, tol)                  # clustering.py:316-324
         if events is not None:
             events[2].record()
+
+    def _update(self, prev, new) -> None:
+        self._sort_and_sum(new, self.state)
 
     def _after_update(self, t: int) -> None:
         pass
@@ -207,7 +211,9 @@ class LloydEngine(ShardSequence):
 
     def __init__(self, points, k: int, *, dtype=np.float32, device=None, variant: str = "auto",
                  comm=None, n_total: int | None = None, max_iters: int = 30,
-                 check_finite: bool = False):
+                 check_finite: bool = False, update: str = "auto"):
+        if update not in ("auto", "full"):
+            raise ValueError(f"update must be 'auto' or 'full', got {update!r}")
         self.dev = require_cuda(device)
         self.dtype = np.dtype(dtype)
         self.tdtype = torch.float32 if self.dtype == _F32 else torch.float64
@@ -251,10 +257,16 @@ class LloydEngine(ShardSequence):
             sb = int(L.load().pcb_repair_scratch_bytes(kk))
             self.repair_scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
             self.repair_scratch_bytes = sb
+            # delta centroid update (update.cu): persistent local sums S, Q = sum |p|^2
+            self.delta_frac = float(os.environ.get("PCB_DELTA_FRAC", "0.05")) if update == "auto" else -1.0
+            self.S = torch.zeros(kk * d, dtype=torch.float64, device=dev)
+            self.Q = torch.zeros(1, dtype=torch.float64, device=dev)
+            self.sums_valid = False
             # split operands for the tensor-core path
             self.ld = 0
             self.P_hi = self.P_lo = self.C_hi = self.C_lo = None
             L.call(f"pcb_point_norms_{self.sfx}", _p(self.P), n, d, _p(self.pnorm), _stream())
+            L.call(f"pcb_sum_squares_{self.sfx}", _p(self.P), n * d, _p(self.Q), _stream())
             if self.variant in ("tc3xtf32", "tc1xtf32s", "bf16s"):
                 self.ld = (d + 31) // 32 * 32
                 self.C_hi = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
@@ -355,6 +367,7 @@ class LloydEngine(ShardSequence):
 
     def set_labels(self, labels_local: np.ndarray, counts_global: np.ndarray | None = None) -> None:
         """Labels of this shard (clustering.py:298); previous labels of iteration 1."""
+        self.sums_valid = False
         with torch.cuda.device(self.dev):
             lab = torch.from_numpy(np.ascontiguousarray(labels_local, dtype=np.int32))
             self.labels[0].copy_(lab.to(self.dev))
@@ -366,6 +379,7 @@ class LloydEngine(ShardSequence):
         (numpy's PCG64 stream, bit-identical; see init.cu) and this shard's
         rows [offset, offset + n) become the labels of iteration 0.
         """
+        self.sums_valid = False
         with torch.cuda.device(self.dev):
             if self.n_total == self.n:
                 init_labels(self.n, self.k, seed, self.dev, out=self.labels[0])
@@ -402,6 +416,20 @@ class LloydEngine(ShardSequence):
                _p(self.cursor), _p(self.perm), _p(state), _stream())
         L.call(f"pcb_segment_sums_{self.sfx}", _p(self.P), self.n, self.d, _p(self.perm),
                _p(self.offsets), self.k, _p(self.C), _p(self.own), _p(self.acc), _p(state), _stream())
+
+    def _update(self, prev, new) -> None:
+        """Centroid sums of the new labels: full counting sort + segmented sums,
+        or the delta update over the changed rows (decided on the device,
+        pcb_update_mode; see update.cu)."""
+        if self.delta_frac < 0:
+            self._sort_and_sum(new, self.state)
+            return
+        L.call("pcb_update_mode", _p(self.acc), self.k, self.d, self.n, self.delta_frac,
+               int(not self.sums_valid), _p(self.state), _stream())
+        self._sort_and_sum(new, self.state)  # no-ops in delta mode
+        L.call(f"pcb_delta_update_{self.sfx}", _p(self.P), self.n, self.d, _p(prev), _p(new), _p(self.C),
+               self.k, _p(self.S), _p(self.Q), _p(self.acc), _p(self.state), _stream())
+        self.sums_valid = True
 
     def _assign(self, prev, new, acc, state) -> None:
         if self.variant == "bf16s":
