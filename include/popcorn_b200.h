@@ -167,20 +167,26 @@ int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_l
  * labels_prev (optional) only orders the centroid tiles of each row pair
  * (the tile of the pair's previous label first); results do not depend on it.
  *   pcb_screen_prep_points_bf16:    P_b, anorm, danorm, bstat[2] = OFF (per fit)
- *   pcb_screen_prep_centroids_bf16: C_b, bnorm, dbnorm, bstat[0..1] (per update) */
+ *   pcb_screen_prep_centroids_bf16: C_b = -2 bf16(C) (kpad rows), C_aug = |c|^2 + OFF
+ *                                   as three BF16 pieces per row (the augmented K
+ *                                   step: q = [p, 1], the paper's q.C.q^T form, so
+ *                                   the MMA produces the ranking keys), bnorm, dbnorm,
+ *                                   bstat[0..1] (per update) */
 int pcb_screen_bf16_ld(int d);
 int pcb_screen_bf16_ncand(void);
 int pcb_screen_prep_points_bf16(const float* P, int64_t n, int d, int ldb, void* P_b, float* anorm,
                                 float* danorm, float* bstat /* 4 */, void* stream);
-int pcb_screen_prep_centroids_bf16(const float* C, int k, int d, int ldb, void* C_b, float* bnorm,
-                                   float* dbnorm, float* bstat, void* stream);
+int pcb_screen_bf16_kpad(int k);   /* rows of C_b / C_aug: k rounded up to 128 */
+int pcb_screen_bf16_aug(void);     /* BF16 columns per C_aug row (16) */
+int pcb_screen_prep_centroids_bf16(const float* C, const float* cnorm, int k, int d, int ldb, void* C_b,
+                                   void* C_aug, float* bnorm, float* dbnorm, float* bstat, void* stream);
 int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const void* C_b, int k,
-                           const float* cnorm, const float* anorm, const float* danorm,
+                           const void* C_aug, const float* anorm, const float* danorm,
                            const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
                            float* amb_thr, const int32_t* orig, const int32_t* labels_prev,
                            const long long* state, void* stream);
 int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
-                            const float* C, int k, const float* cnorm, const float* bstat,
+                            const float* C, int k, const void* C_aug, const float* bstat,
                             const int* amb_list, const int* amb_count, const float* amb_thr,
                             int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
                             int* ovf_list, int* ovf_count, const int32_t* orig, const long long* state,

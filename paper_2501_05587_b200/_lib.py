@@ -50,7 +50,9 @@ SIGNATURES = {
     "pcb_screen_bf16_ld": (I32, [I32]),
     "pcb_screen_bf16_ncand": (I32, []),
     "pcb_screen_prep_points_bf16": (I32, [P, I64, I32, I32, P, P, P, P, P]),
-    "pcb_screen_prep_centroids_bf16": (I32, [P, I32, I32, I32, P, P, P, P, P]),
+    "pcb_screen_prep_centroids_bf16": (I32, [P, P, I32, I32, I32, P, P, P, P, P, P]),
+    "pcb_screen_bf16_kpad": (I32, [I32]),
+    "pcb_screen_bf16_aug": (I32, []),
     "pcb_assign_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "pcb_resolve_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, I32, P, P, P, P, P, I64, P, P, P, P, P, P, P, P, P]),
     "pcb_screen_relayout_bf16": (I32, [P, P, P, I64, I32, P, P, P, P, P, P]),

@@ -46,6 +46,7 @@ constexpr int SB_STAGES = 4;
 constexpr int SB_THREADS = 384;
 constexpr int SB_BKE = 64;      // BF16 elements per 128-byte swizzle row
 constexpr int SB_NCAND = 8;     // candidate slots per ambiguous row (pass 2)
+constexpr int SB_AUG = 16;      // augmented K columns per centroid: |c|^2 + OFF as 3 BF16 pieces, 13 zeros
 
 template <int NKC>
 struct SbCfg {
@@ -55,9 +56,12 @@ struct SbCfg {
   static constexpr int kAStages = NKC <= 2 ? 2 : 1;
   static constexpr uint32_t kAPair = 2 * NKC * kTileBytes;
   static constexpr uint32_t kABytes = kAStages * kAPair;
-  static constexpr uint32_t kBBytes = SB_BN * 128;                  // 16 KB per B stage
+  static constexpr uint32_t kBBytes = SB_BN * 128;                  // 16 KB centroid chunk per B stage
+  static constexpr uint32_t kAugBytes = SB_BN * 32;                 // + the K=16 augmented columns
+  static constexpr uint32_t kStageB = kBBytes + kAugBytes;          // 20 KB (1024-aligned)
+  static constexpr uint32_t kAAug = 128 * 32;                       // constant A columns [1 1 1 0 ..]
   static constexpr uint32_t kBarBytes = 1024;
-  static constexpr uint32_t kSmem = 1024 + kABytes + SB_STAGES * kBBytes + kBarBytes + SC_KMAX * 4;
+  static constexpr uint32_t kSmem = 1024 + kABytes + SB_STAGES * kStageB + kAAug + kBarBytes;
   static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
@@ -87,8 +91,8 @@ __device__ __forceinline__ int64_t sb_rows(int64_t n, const int* amb_count, int6
 template <int NKC, bool CAND>
 __global__ void __launch_bounds__(SB_THREADS, 1)
 assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                          const float* __restrict__ anorm, const float* __restrict__ danorm,
-                          const float* __restrict__ cnorm, const float* __restrict__ bstat, int64_t n_in, int k,
+                          const __grid_constant__ CUtensorMap tm_baug, const float* __restrict__ anorm,
+                          const float* __restrict__ danorm, const float* __restrict__ bstat, int64_t n_in, int k,
                           int32_t* __restrict__ labels, int* __restrict__ amb_list, int* __restrict__ amb_count,
                           float* __restrict__ amb_thr, int64_t bypass, int* __restrict__ cand,
                           int* __restrict__ cand_n, const int32_t* __restrict__ orig,
@@ -102,7 +106,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
   uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + Cfg::kABytes;
-  uint8_t* bar_area = sB + SB_STAGES * Cfg::kBBytes;
+  uint8_t* sAaug = sB + SB_STAGES * Cfg::kStageB;
+  uint8_t* bar_area = sAaug + Cfg::kAAug;
   constexpr int AS = Cfg::kAStages;
   uint64_t* afull = reinterpret_cast<uint64_t*>(bar_area);  // [AS][NKC]
   uint64_t* aempty = afull + AS * NKC;                       // [AS][NKC]
@@ -111,16 +116,25 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
   uint64_t* tfull = empty + SB_STAGES;                       // [2]
   uint64_t* tempty = tfull + 2;                              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* cprime = reinterpret_cast<float*>(bar_area + Cfg::kBarBytes);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (k + SB_BN - 1) / SB_BN;
   const float OFF = bstat[2];
-  for (int j = threadIdx.x; j < ntiles * SB_BN; j += blockDim.x)
-    cprime[j] = j < k ? cnorm[j] + OFF : 3.0e38f;
+  // constant A columns of the augmented K step, no-swizzle K-major layout
+  // [2 K halves][128 rows][16 B]: every row = (1, 1, 1, 0, ..., 0), so the MMA
+  // adds h1 + h2 + h3 = |c|^2 + OFF (the B side) to -2 <p~, c~>: the paper's
+  // augmented form q.C.q^T with q = [p, 1] computed by the tensor core.
+  for (int i = threadIdx.x; i < 2 * 128; i += blockDim.x) {
+    const uint32_t one2 = 0x3F803F80u;  // bf16 (1, 1)
+    uint4 u = make_uint4(0u, 0u, 0u, 0u);
+    if (i < 128) u = make_uint4(one2, 0x00003F80u, 0u, 0u);
+    reinterpret_cast<uint4*>(sAaug)[i] = u;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> UMMA reads
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tm_a);
     ptx::prefetch_tmap(&tm_b);
+    ptx::prefetch_tmap(&tm_baug);
     for (int c = 0; c < NKC; ++c) {
       for (int a = 0; a < AS; ++a) {
         ptx::mbar_init(&afull[a * NKC + c], 1);
@@ -179,8 +193,14 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         for (int c = 0; c < NKC; ++c) {
           ptx::mbar_wait(&empty[stage], phase ^ 1u);
           if (ptx::elect_one()) {
-            ptx::mbar_expect_tx(&full[stage], Cfg::kBBytes);
-            ptx::tma_load_2d(&tm_b, &full[stage], sB + stage * Cfg::kBBytes, c * SB_BKE, tile * SB_BN, pol);
+            uint8_t* st = sB + stage * Cfg::kStageB;
+            const bool last = c + 1 == NKC;  // the tile's augmented columns ride with its last chunk
+            ptx::mbar_expect_tx(&full[stage], Cfg::kBBytes + (last ? Cfg::kAugBytes : 0u));
+            ptx::tma_load_2d(&tm_b, &full[stage], st, c * SB_BKE, tile * SB_BN, pol);
+            if (last) {
+              ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes, 0, tile * SB_BN, pol);
+              ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes + SB_BN * 16, 8, tile * SB_BN, pol);
+            }
           }
           __syncwarp();
           if (++stage == SB_STAGES) { stage = 0; phase ^= 1u; }
@@ -208,13 +228,20 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           ptx::tc_fence_after();
           const uint64_t a0 = ptx::sdesc_k_sw128(ptx::smem_u32(sAp + (0 * NKC + c) * Cfg::kTileBytes));
           const uint64_t a1 = ptx::sdesc_k_sw128(ptx::smem_u32(sAp + (1 * NKC + c) * Cfg::kTileBytes));
-          const uint64_t bd = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * Cfg::kBBytes));
+          const uint64_t bd = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * Cfg::kStageB));
           if (ptx::elect_one()) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {           // 4 x K=16 per 128-byte chunk
               const uint64_t off = (uint64_t)(ks * 32) >> 4;
               ptx::umma_f16(d0, a0 + off, bd + off, idesc, (c | ks) != 0);
               ptx::umma_f16(d0 + 128, a1 + off, bd + off, idesc, (c | ks) != 0);
+            }
+            if (c + 1 == NKC) {  // augmented K step: + (|c|^2 + OFF) in three BF16 pieces
+              const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
+              const uint64_t ba = ptx::sdesc_k_none(ptx::smem_u32(sB + stage * Cfg::kStageB + Cfg::kBBytes),
+                                                    SB_BN * 16, 128);
+              ptx::umma_f16(d0, aa, ba, idesc, 1u);
+              ptx::umma_f16(d0 + 128, aa, ba, idesc, 1u);
             }
             ptx::umma_commit(&empty[stage]);
             if (nt + 1 == ntiles) ptx::umma_commit(&aempty[ab * NKC + c]);  // A chunk free again
@@ -232,7 +259,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     // ---------------- epilogue: warp (g, h) = lanes 32g.. of row tile h ----------------
     const int g = warp & 3, h = (warp - 4) >> 2;
     const float Bmax = bstat[0], dBmax = bstat[1];
-    const float acc_rel = (float)(NKC * 4 + 2) * 0x1p-19f;
+    const float acc_rel = (float)(NKC * 4 + 3) * 0x1p-19f;
     const uint32_t msk = kIdxMask;
     int abuf = 0;
     uint32_t aphase = 0;
@@ -273,7 +300,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       if (CAND) {
         thr = an_nx;
       } else {
-        twoE = screen_two_e(an_nx, dan_nx, Bmax, dBmax, OFF, acc_rel);
+        twoE = screen_two_e_aug(an_nx, dan_nx, Bmax, dBmax, OFF, acc_rel);
         big = 64.0f / twoE;
       }
       const int t0 = fc_nx / SB_BN, q0 = (fc_nx % SB_BN) / 32;
@@ -308,7 +335,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
               ptx::tmem_ld_32x32b_x32_async(tlane + (uint32_t)(abuf * 256) + 32 * qn, nxt);
             }
           }
-          float v[32], cp[32];
+          float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
 #if defined(PCB_EXP) && PCB_EXP == 2
@@ -316,13 +343,12 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           R1 = fminf(R1, v[0] + v[31]);
           continue;
 #endif
-          load_cprime(cp, cprime + c0 + 32 * qe);
           if (CAND) {
             // candidate mask of the chunk (FSETP + SEL per key), then a short
             // loop over its set bits (2-3 candidates per row in total)
             uint32_t bits = 0;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) bits |= (fmaf(v[i], -2.0f, cp[i]) <= thr ? 1u : 0u) << i;
+            for (int i = 0; i < 32; ++i) bits |= (v[i] <= thr ? 1u : 0u) << i;
             while (bits) {
               const int i = __ffs(bits) - 1;
               bits &= bits - 1;
@@ -337,11 +363,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             // rows of a warp see their minima in the same chunks and most
             // chunks of most warps take this path.
             const float thr_skip = (R1 + twoE + 0x1p-16f * fabsf(R1)) * (1.0f + 0x1p-16f);
-            float km[32];
-            const unsigned long long m2 = f2pack(-2.0f, -2.0f);
-#pragma unroll
-            for (int i = 0; i < 32; i += 2)
-              f2unpack(ffma2(f2pack(v[i], v[i + 1]), m2, f2pack(cp[i], cp[i + 1])), km[i], km[i + 1]);
+            const float (&km)[32] = v;  // the MMA produced the keys (augmented K step)
             float mm = fmin3(km[0], km[1], km[2]);
 #pragma unroll
             for (int i = 3; i < 31; i += 2) mm = fmin3(mm, km[i], km[i + 1]);
@@ -391,7 +413,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
   if (warp == 2) ptx::tmem_dealloc<512>(tmem);
 }
 
-static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t rows, int cols, int box_rows) {
+static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t rows, int cols, int box_rows,
+                          int box_cols = SB_BKE, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (enc == nullptr) {
     cudaDriverEntryPointQueryResult q;
@@ -403,31 +426,33 @@ static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t row
   }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {(cuuint32_t)SB_BKE, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(base), dims, strides, box,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : PCB_EINVAL;
 }
 
 template <int NKC, bool CAND>
 static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
-                              const float* an, const float* dan, const float* cnorm, const float* bstat,
+                              const float* an, const float* dan, const __nv_bfloat16* Baug, const float* bstat,
                               int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
                               int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev,
                               const long long* state, cudaStream_t st) {
   using Cfg = SbCfg<NKC>;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tg;
   int rc;
+  const int64_t kpad = (k + SB_BN - 1) / SB_BN * SB_BN;  // B / Baug hold kpad rows (padding: key = +huge)
   if ((rc = make_tmap_bf16(&ta, A, n, NKC * SB_BKE, 128))) return rc;
-  if ((rc = make_tmap_bf16(&tb, B, k, NKC * SB_BKE, SB_BN))) return rc;
+  if ((rc = make_tmap_bf16(&tb, B, kpad, NKC * SB_BKE, SB_BN))) return rc;
+  if ((rc = make_tmap_bf16(&tg, Baug, kpad, SB_AUG, SB_BN, 8, CU_TENSOR_MAP_SWIZZLE_NONE))) return rc;
   auto kern = assign_screen_bf16_kernel<NKC, CAND>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   if (e != cudaSuccess) return (int)e;
   const int64_t npairs = (n + 255) / 256;
   const int grid = (int)std::min<int64_t>(npairs, (int64_t)sm_count());
-  kern<<<grid, SB_THREADS, Cfg::kSmem, st>>>(ta, tb, an, dan, cnorm, bstat, n, k, labels, amb_list, amb_count,
+  kern<<<grid, SB_THREADS, Cfg::kSmem, st>>>(ta, tb, tg, an, dan, bstat, n, k, labels, amb_list, amb_count,
                                              amb_thr, bypass, cand, cand_n, orig, lprev, state);
   PCB_CHECK_LAUNCH();
   return 0;
@@ -435,13 +460,13 @@ static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bflo
 
 template <bool CAND>
 static int dispatch_bf16(int ldb, const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
-                         const float* an, const float* dan, const float* cnorm, const float* bstat,
+                         const float* an, const float* dan, const __nv_bfloat16* Baug, const float* bstat,
                          int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
                          int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev, const long long* state,
                          cudaStream_t st) {
 #define PCB_SB_CASE(N)                                                                                      \
   case N:                                                                                                   \
-    return launch_screen_bf16<N, CAND>(A, n, B, k, an, dan, cnorm, bstat, labels, amb_list, amb_count,      \
+    return launch_screen_bf16<N, CAND>(A, n, B, k, an, dan, Baug, bstat, labels, amb_list, amb_count,       \
                                        amb_thr, bypass, cand, cand_n, orig, lprev, state, st);
   switch (ldb / SB_BKE) {
     PCB_SB_CASE(1)
@@ -463,7 +488,8 @@ __device__ __forceinline__ void atomic_max_pos_f(float* addr, float v) {
 // the BF16 copy Xb (row stride ldb, zero padded).
 __global__ void __launch_bounds__(256)
 row_bf16_norms_kernel(const float* __restrict__ X, int64_t rows, int d, float* __restrict__ an,
-                      float* __restrict__ dan, float* __restrict__ maxsq, __nv_bfloat16* __restrict__ Xb, int ldb) {
+                      float* __restrict__ dan, float* __restrict__ maxsq, __nv_bfloat16* __restrict__ Xb, int ldb,
+                      float out_scale = 1.0f) {
   const int lane = threadIdx.x & 31;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -473,7 +499,7 @@ row_bf16_norms_kernel(const float* __restrict__ X, int64_t rows, int d, float* _
     for (int t = lane; t < ldb; t += 32) {
       const float x = t < d ? X[i * d + t] : 0.0f;
       const __nv_bfloat16 hb = __float2bfloat16_rn(x);
-      Xb[i * ldb + t] = hb;
+      Xb[i * ldb + t] = out_scale == 1.0f ? hb : __float2bfloat16_rn(out_scale * __bfloat162float(hb));  // exact
       const double h = (double)__bfloat162float(hb);
       const double dd = (double)x - h;
       s_t = fma(h, h, s_t);
@@ -627,6 +653,32 @@ screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict_
 
 using namespace pcb;
 
+// Augmented B columns of centroid j: |c_j|^2 + OFF split into three BF16
+// pieces (24 significant bits; the f32 key arithmetic allowance of the bound
+// covers the rest), zeros after; padding rows j >= k get a huge key.
+__global__ void centroid_aug_kernel(const float* __restrict__ cnorm, const float* __restrict__ bstat, int k, int kpad,
+                                    __nv_bfloat16* __restrict__ aug) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= kpad) return;
+  uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = make_uint4(0u, 0u, 0u, 0u);
+  __nv_bfloat16 h1, h2, h3;
+  if (j < k) {
+    const float cp = cnorm[j] + bstat[2];
+    h1 = __float2bfloat16_rn(cp);
+    const float r1 = cp - __bfloat162float(h1);  // exact (Sterbenz-like: |r1| << cp)
+    h2 = __float2bfloat16_rn(r1);
+    h3 = __float2bfloat16_rn(r1 - __bfloat162float(h2));
+  } else {
+    h1 = __float2bfloat16_rn(3.0e38f);
+    h2 = h3 = __float2bfloat16_rn(0.0f);
+  }
+  lo.x = (uint32_t)__bfloat16_as_ushort(h1) | ((uint32_t)__bfloat16_as_ushort(h2) << 16);
+  lo.y = (uint32_t)__bfloat16_as_ushort(h3);
+  uint4* dst = reinterpret_cast<uint4*>(aug + (int64_t)j * SB_AUG);
+  dst[0] = lo;
+  dst[1] = hi;
+}
+
 extern "C" int pcb_screen_bf16_ld(int d) { return (d + SB_BKE - 1) / SB_BKE * SB_BKE; }
 extern "C" int pcb_screen_bf16_ncand(void) { return SB_NCAND; }
 
@@ -645,14 +697,24 @@ extern "C" int pcb_screen_prep_points_bf16(const float* P, int64_t n, int d, int
   return 0;
 }
 
-extern "C" int pcb_screen_prep_centroids_bf16(const float* C, int k, int d, int ldb, void* C_b, float* bnorm,
+extern "C" int pcb_screen_bf16_kpad(int k) { return (k + SB_BN - 1) / SB_BN * SB_BN; }
+extern "C" int pcb_screen_bf16_aug(void) { return SB_AUG; }
+
+extern "C" int pcb_screen_prep_centroids_bf16(const float* C, const float* cnorm, int k, int d, int ldb, void* C_b,
+                                              void* C_aug, float* bnorm,
                                               float* dbnorm, float* bstat, void* stream) {
-  if (k < 1 || d < 1 || ldb < d || ldb % SB_BKE || !C || !C_b || !bnorm || !dbnorm || !bstat) return PCB_EINVAL;
+  if (k < 1 || d < 1 || ldb < d || ldb % SB_BKE || !C || !cnorm || !C_b || !C_aug || !bnorm || !dbnorm || !bstat)
+    return PCB_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(bstat, 0, 2 * sizeof(float), st);
   if (e != cudaSuccess) return (int)e;
+  // B operand rows are -2 bf16(c) (exact scaling): the MMA accumulates the key
+  // |c|^2 + OFF - 2 <p~, c~> directly (centroid_aug_kernel supplies |c|^2 + OFF)
   row_bf16_norms_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(C, k, d, bnorm, dbnorm, nullptr,
-                                                             reinterpret_cast<__nv_bfloat16*>(C_b), ldb);
+                                                             reinterpret_cast<__nv_bfloat16*>(C_b), ldb, -2.0f);
+  PCB_CHECK_LAUNCH();
+  const int kpad = (k + SB_BN - 1) / SB_BN * SB_BN;
+  centroid_aug_kernel<<<(kpad + 127) / 128, 128, 0, st>>>(cnorm, bstat, k, kpad, reinterpret_cast<__nv_bfloat16*>(C_aug));
   PCB_CHECK_LAUNCH();
   max2_bf16_kernel<<<1, 256, 0, st>>>(bnorm, dbnorm, k, bstat);
   PCB_CHECK_LAUNCH();
@@ -661,15 +723,16 @@ extern "C" int pcb_screen_prep_centroids_bf16(const float* C, int k, int d, int 
 
 // Pass 1 over all n rows: certified labels, ambiguous rows + thresholds.
 extern "C" int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const void* C_b, int k,
-                                      const float* cnorm, const float* anorm, const float* danorm,
+                                      const void* C_aug, const float* anorm, const float* danorm,
                                       const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
                                       float* amb_thr, const int32_t* orig, const int32_t* labels_prev,
                                       const long long* state, void* stream) {
-  if (n < 1 || ldb < SB_BKE || ldb % SB_BKE || k < 1 || !P_b || !C_b || !cnorm || !anorm || !danorm || !bstat ||
+  if (n < 1 || ldb < SB_BKE || ldb % SB_BKE || k < 1 || !P_b || !C_b || !C_aug || !anorm || !danorm || !bstat ||
       !labels || !amb_list || !amb_count || !amb_thr)
     return PCB_EINVAL;
   if (n > INT32_MAX || k > SC_KMAX) return PCB_EUNSUP;
-  return dispatch_bf16<false>(ldb, (const __nv_bfloat16*)P_b, n, (const __nv_bfloat16*)C_b, k, anorm, danorm, cnorm,
+  return dispatch_bf16<false>(ldb, (const __nv_bfloat16*)P_b, n, (const __nv_bfloat16*)C_b, k, anorm, danorm,
+                              (const __nv_bfloat16*)C_aug,
                               bstat, labels, amb_list, amb_count, amb_thr, 0, nullptr, nullptr, orig, labels_prev, state,
                               (cudaStream_t)stream);
 }
@@ -678,12 +741,12 @@ extern "C" int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const
 // SB_NCAND candidates, or every row when the ambiguous count exceeds `bypass`)
 // land in ovf_list / ovf_count for the 3xTF32 resolver.
 extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
-                                       const float* C, int k, const float* cnorm, const float* bstat,
+                                       const float* C, int k, const void* C_aug, const float* bstat,
                                        const int* amb_list, const int* amb_count, const float* amb_thr,
                                        int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
                                        int* ovf_list, int* ovf_count, const int32_t* orig, const long long* state,
                                        void* stream) {
-  if (n < 1 || d < 1 || k < 1 || ldb < d || ldb % SB_BKE || !P || !P_b || !C_b || !C || !cnorm || !bstat ||
+  if (n < 1 || d < 1 || k < 1 || ldb < d || ldb % SB_BKE || !P || !P_b || !C_b || !C || !C_aug || !bstat ||
       !amb_list || !amb_count || !amb_thr || !sub_b || !cand || !cand_n || !labels || !ovf_list || !ovf_count)
     return PCB_EINVAL;
   if (d > 256) return PCB_EUNSUP;
@@ -695,7 +758,7 @@ extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const v
                                          (__nv_bfloat16*)sub_b, state);
   PCB_CHECK_LAUNCH();
   int rc = dispatch_bf16<true>(ldb, (const __nv_bfloat16*)sub_b, n, (const __nv_bfloat16*)C_b, k, nullptr, nullptr,
-                               cnorm, bstat, nullptr, nullptr, const_cast<int*>(amb_count),
+                               (const __nv_bfloat16*)C_aug, bstat, nullptr, nullptr, const_cast<int*>(amb_count),
                                const_cast<float*>(amb_thr), bypass, cand, cand_n, nullptr, nullptr, state, st);
   if (rc) return rc;
   const int DQ = (d + 31) / 32;  // float4 per lane (8 lanes per row)

@@ -34,6 +34,16 @@ __device__ __forceinline__ float screen_two_e(float an, float dan, float Bmax, f
   return 2.0f * 1.0001f * (2.0f * gerr + 0x1p-16f * kmax);
 }
 
+// Same bound when the MMA itself adds |c|^2 + OFF (augmented K step): the
+// f32 accumulation error also scales with the key magnitude (acc_rel * kmax).
+__device__ __forceinline__ float screen_two_e_aug(float an, float dan, float Bmax, float dBmax, float OFF,
+                                                  float acc_rel) {
+  const float gerr = dan * Bmax + an * dBmax + dan * dBmax + acc_rel * an * Bmax;
+  const float cbn = Bmax + dBmax;
+  const float kmax = OFF + 2.0f * (an + dan) * cbn + cbn * cbn;
+  return 2.0f * 1.0001f * (2.0f * gerr + (0x1p-16f + acc_rel) * kmax);
+}
+
 // Packed f32x2 helpers (FFMA2 / FADD2 on sm_100a: two lanes per issue slot).
 __device__ __forceinline__ unsigned long long f2pack(float a, float b) {
   unsigned long long r;

@@ -87,6 +87,18 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
   return d;
 }
 
+// K-major, no swizzle: core matrices of 8 rows x 16 B (rows 16 B apart), LBO =
+// byte distance between the two K-adjacent core matrices, SBO = between
+// 8-row groups (canonical ((8,n),2):((1,SBO),LBO) in 16-byte units).
+__device__ __forceinline__ uint64_t sdesc_k_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;   // descriptor version (Blackwell); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
 // Instruction descriptor for kind::tf32 (F32 accumulate, A/B K-major).
 template <int M, int N>
 __host__ __device__ constexpr uint32_t idesc_tf32() {

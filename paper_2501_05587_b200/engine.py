@@ -298,7 +298,10 @@ class LloydEngine(ShardSequence):
                 self.ldb = int(L.load().pcb_screen_bf16_ld(d))
                 ncand = int(L.load().pcb_screen_bf16_ncand())
                 self.P_b = torch.empty((n, self.ldb), dtype=torch.bfloat16, device=dev)
-                self.C_b = torch.zeros((kk, self.ldb), dtype=torch.bfloat16, device=dev)
+                kpad = int(L.load().pcb_screen_bf16_kpad(kk))
+                self.C_b = torch.zeros((kpad, self.ldb), dtype=torch.bfloat16, device=dev)
+                self.C_aug = torch.zeros((kpad, int(L.load().pcb_screen_bf16_aug())), dtype=torch.bfloat16,
+                                         device=dev)
                 self.anorm = torch.empty(n, dtype=torch.float32, device=dev)
                 self.danorm = torch.empty(n, dtype=torch.float32, device=dev)
                 self.bnorm = torch.empty(kk, dtype=torch.float32, device=dev)
@@ -351,8 +354,8 @@ class LloydEngine(ShardSequence):
 
     def _screen_centroid_stats(self) -> None:
         if self.variant == "bf16s":
-            L.call("pcb_screen_prep_centroids_bf16", _p(self.C), self.k, self.d, self.ldb, _p(self.C_b),
-                   _p(self.bnorm), _p(self.dbnorm), _p(self.bstat), _stream())
+            L.call("pcb_screen_prep_centroids_bf16", _p(self.C), _p(self.cnorm), self.k, self.d, self.ldb,
+                   _p(self.C_b), _p(self.C_aug), _p(self.bnorm), _p(self.dbnorm), _p(self.bstat), _stream())
         if self.variant == "tc1xtf32s":
             L.call("pcb_screen_prep_centroids", _p(self.C), self.k, self.d, _p(self.bnorm),
                    _p(self.dbnorm), _p(self.bstat), _stream())
@@ -436,12 +439,12 @@ class LloydEngine(ShardSequence):
             self.amb_count.zero_()
             self._kmark(0)
             L.call("pcb_assign_screen_bf16", _p(self.P_b), self.n, self.ldb, _p(self.C_b), self.k,
-                   _p(self.cnorm), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
+                   _p(self.C_aug), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
                    _p(self.amb_list), _p(self.amb_count), _p(self.amb_thr), _p(self.orig), _p(prev),
                    _p(state), _stream())
             self._kmark(1)
             L.call("pcb_resolve_screen_bf16", _p(self.P), self.n, self.d, _p(self.P_b), self.ldb,
-                   _p(self.C_b), _p(self.C), self.k, _p(self.cnorm), _p(self.bstat), _p(self.amb_list),
+                   _p(self.C_b), _p(self.C), self.k, _p(self.C_aug), _p(self.bstat), _p(self.amb_list),
                    _p(self.amb_count), _p(self.amb_thr), self.bypass, _p(self.sub_b), _p(self.cand),
                    _p(self.cand_n), _p(new), _p(self.ovf_list), _p(self.ovf_count), _p(self.orig), _p(state),
                    _stream())
