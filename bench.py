@@ -257,6 +257,8 @@ def main():
     if st[5] != 0:
         raise SystemExit("non-finite distances during the bench")
     amb = int(eng.amb_count.item()) if getattr(eng, "amb_count", None) is not None else None
+    if amb is not None and getattr(eng, "two_count", None) is not None:
+        amb += int(eng.two_count.item())  # two-candidate rows resolved without the second pass
 
     ms_per_step = ms / K
     value = 1e3 / ms_per_step  # whole-job iterations/s (all ranks, n total)

@@ -164,6 +164,9 @@ int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_l
  * pcb_screen_bf16_ncand() per row into cand / cand_n) and takes the exact f64
  * argmin over them.  Rows with more candidates, or all rows when amb_count >
  * bypass, are listed in ovf_list / ovf_count for pcb_resolve_ambiguous_f32.
+ * Rows with exactly two keys within the bound skip pass 2: pass 1 lists them
+ * in two_list as (original row, candidate, candidate) triplets (two_count,
+ * caller zeroes) and the resolver evaluates both exactly.
  * labels_prev (optional) only orders the centroid tiles of each row pair
  * (the tile of the pair's previous label first); results do not depend on it.
  *   pcb_screen_prep_points_bf16:    P_b, anorm, danorm, bstat[2] = OFF (per fit)
@@ -184,13 +187,13 @@ int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const void* C_b,
                            const void* C_aug, const float* anorm, const float* danorm,
                            const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
                            float* amb_thr, const int32_t* orig, const int32_t* labels_prev,
-                           const long long* state, void* stream);
+                           int* two_list, int* two_count, const long long* state, void* stream);
 int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
                             const float* C, int k, const void* C_aug, const float* bstat,
                             const int* amb_list, const int* amb_count, const float* amb_thr,
                             int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
-                            int* ovf_list, int* ovf_count, const int32_t* orig, const long long* state,
-                            void* stream);
+                            int* ovf_list, int* ovf_count, const int32_t* orig, const int* two_list,
+                            const int* two_count, const long long* state, void* stream);
 /* Row layout: P_b / anorm / danorm rebuilt as the rows perm[s] of their
  * original-order copies Pb0 / an0 / dan0 (from pcb_screen_prep_points_bf16),
  * orig[s] = perm[s] (perm = point ids sorted by label, pcb_sort_by_label).

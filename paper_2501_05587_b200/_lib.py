@@ -53,8 +53,9 @@ SIGNATURES = {
     "pcb_screen_prep_centroids_bf16": (I32, [P, P, I32, I32, I32, P, P, P, P, P, P]),
     "pcb_screen_bf16_kpad": (I32, [I32]),
     "pcb_screen_bf16_aug": (I32, []),
-    "pcb_assign_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
-    "pcb_resolve_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, I32, P, P, P, P, P, I64, P, P, P, P, P, P, P, P, P]),
+    "pcb_assign_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "pcb_resolve_screen_bf16": (I32, [P, I64, I32, P, I32, P, P, I32, P, P, P, P, P, I64, P, P, P, P, P, P, P, P, P,
+                                      P, P]),
     "pcb_screen_relayout_bf16": (I32, [P, P, P, I64, I32, P, P, P, P, P, P]),
     "pcb_count_labels": (I32, [P, P, I64, I32, I32, P, P, P]),
     "pcb_sort_by_label": (I32, [P, I64, I32, P, P, P, P, P, P]),

@@ -96,7 +96,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
                           int32_t* __restrict__ labels, int* __restrict__ amb_list, int* __restrict__ amb_count,
                           float* __restrict__ amb_thr, int64_t bypass, int* __restrict__ cand,
                           int* __restrict__ cand_n, const int32_t* __restrict__ orig,
-                          const int32_t* __restrict__ lprev, const long long* __restrict__ state) {
+                          const int32_t* __restrict__ lprev, int* __restrict__ two_list, int* __restrict__ two_count,
+                          const long long* __restrict__ state) {
   using Cfg = SbCfg<NKC>;
   if (stopped(state)) return;
   const int64_t n = CAND ? sb_rows(n_in, amb_count, bypass) : n_in;
@@ -306,8 +307,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       const int t0 = fc_nx / SB_BN, q0 = (fc_nx % SB_BN) / 32;
       const int64_t out_row = out_nx;  // original row id (label store)
       if (!last_pair) fetch_pair(pr + gridDim.x);
-      float R1 = 3.4e38f, cnt = 0.0f;
-      int r1 = 0;
+      float R1 = 3.4e38f, R2 = 3.4e38f, cnt = 0.0f;
+      int r1 = 0, r2 = 0;
       for (int nt = 0; nt < ntiles; ++nt) {
         const uint32_t taddr = tlane + (uint32_t)(abuf * 256);
         const int c0 = (nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles) * SB_BN;
@@ -373,7 +374,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             if (__any_sync(0xffffffffu, mm <= thr_skip)) R1 = fminf(R1, mm);
 #else
             if (__any_sync(0xffffffffu, mm <= thr_skip)) {
-              screen_chunk_keys(km, msk, c0 + 32 * qe, twoE, big, R1, r1, cnt);
+              screen_chunk_top2(km, msk, c0 + 32 * qe, twoE, R1, r1, R2, r2, cnt);
 #if defined(PCB_EXP) && PCB_EXP == 6
               // experiment build: count full-path chunks per position (q + 4 * nt) in state[8..]
               if (lane == 0) atomicAdd((unsigned long long*)state + 8 + (nt < 8 ? nt * 4 + q : 32), 1ull);
@@ -387,10 +388,25 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         if (row < n) cand_n[row] = nc;
       } else {
         if (row < n) labels[out_row] = r1;
+        // exactly two keys within the bound: the candidates are r1, r2 (exact
+        // f64 resolution, no second pass); more: pass 2 finds them
+        const bool two = row < n && cnt == 2.0f;
+        const unsigned m2 = __ballot_sync(0xffffffffu, two);
+        if (m2) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(two_count, __popc(m2));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (two) {
+            const int pos = base + __popc(m2 & ((1u << lane) - 1u));
+            two_list[3 * pos + 0] = (int)out_row;
+            two_list[3 * pos + 1] = r1;
+            two_list[3 * pos + 2] = r2;
+          }
+        }
 #if defined(PCB_EXP) && PCB_EXP == 7
         const bool amb = false;  // experiment build: no ambiguous-row append
 #else
-        const bool amb = row < n && cnt > 1.0f;
+        const bool amb = row < n && cnt > 2.0f;
 #endif
         const unsigned m = __ballot_sync(0xffffffffu, amb);
         if (m) {
@@ -439,7 +455,7 @@ static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bflo
                               const float* an, const float* dan, const __nv_bfloat16* Baug, const float* bstat,
                               int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
                               int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev,
-                              const long long* state, cudaStream_t st) {
+                              int* two_list, int* two_count, const long long* state, cudaStream_t st) {
   using Cfg = SbCfg<NKC>;
   CUtensorMap ta, tb, tg;
   int rc;
@@ -453,7 +469,7 @@ static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bflo
   const int64_t npairs = (n + 255) / 256;
   const int grid = (int)std::min<int64_t>(npairs, (int64_t)sm_count());
   kern<<<grid, SB_THREADS, Cfg::kSmem, st>>>(ta, tb, tg, an, dan, bstat, n, k, labels, amb_list, amb_count,
-                                             amb_thr, bypass, cand, cand_n, orig, lprev, state);
+                                             amb_thr, bypass, cand, cand_n, orig, lprev, two_list, two_count, state);
   PCB_CHECK_LAUNCH();
   return 0;
 }
@@ -462,12 +478,12 @@ template <bool CAND>
 static int dispatch_bf16(int ldb, const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                          const float* an, const float* dan, const __nv_bfloat16* Baug, const float* bstat,
                          int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
-                         int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev, const long long* state,
-                         cudaStream_t st) {
+                         int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev, int* two_list,
+                         int* two_count, const long long* state, cudaStream_t st) {
 #define PCB_SB_CASE(N)                                                                                      \
   case N:                                                                                                   \
     return launch_screen_bf16<N, CAND>(A, n, B, k, an, dan, Baug, bstat, labels, amb_list, amb_count,       \
-                                       amb_thr, bypass, cand, cand_n, orig, lprev, state, st);
+                                       amb_thr, bypass, cand, cand_n, orig, lprev, two_list, two_count, state, st);
   switch (ldb / SB_BKE) {
     PCB_SB_CASE(1)
     PCB_SB_CASE(2)
@@ -572,31 +588,38 @@ screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict_
                     const int* __restrict__ list, const int* __restrict__ count, int64_t bypass,
                     const int* __restrict__ cand, const int* __restrict__ cand_n, int32_t* __restrict__ labels,
                     int* __restrict__ ovf_list, int* __restrict__ ovf_count, const int32_t* __restrict__ orig,
+                    const int* __restrict__ two_list, const int* __restrict__ two_count,
                     const long long* __restrict__ state) {
   if (stopped(state)) return;
-  const int64_t cnt = *count;
+  const int64_t cnt_amb = *count;
+  const int64_t cnt2 = two_count != nullptr ? *two_count : 0;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  if (cnt > bypass) {
-    // bypass: the whole list goes to the 3xTF32 resolver (32 entries per warp)
-    for (int64_t b0 = w0 * 32; b0 < cnt; b0 += nw * 32) {
+  const bool bypassed = cnt_amb > bypass;
+  if (bypassed) {
+    // bypass: the whole pass-1 list goes to the 3xTF32 resolver (32 entries per warp)
+    for (int64_t b0 = w0 * 32; b0 < cnt_amb; b0 += nw * 32) {
       const int64_t r = b0 + lane;
-      const bool ok = r < cnt;
+      const bool ok = r < cnt_amb;
       const unsigned m = __ballot_sync(0xffffffffu, ok);
       int b = 0;
       if (lane == 0) b = atomicAdd(ovf_count, __popc(m));
       b = __shfl_sync(0xffffffffu, b, 0);
       if (ok) ovf_list[b + __popc(m & ((1u << lane) - 1u))] = orig != nullptr ? orig[list[r]] : list[r];
     }
-    return;
   }
+  // rows [0, cntA): pass-2 candidate lists; [cntA, cntA + cnt2): two-candidate rows of pass 1
+  const int64_t cntA = bypassed ? 0 : cnt_amb;
+  const int64_t cnt = cntA + cnt2;
   const int sub = lane & 7, grp = lane >> 3;
   for (int64_t rb = w0 * 4; rb < cnt; rb += nw * 4) {
     const int64_t r = rb + grp;
     const bool valid = r < cnt;
-    const int row = valid ? (orig != nullptr ? orig[list[r]] : list[r]) : 0;  // original row id
-    int nc = valid ? cand_n[r] : 0;
+    const bool is2 = r >= cntA;
+    const int64_t r2i = r - cntA;
+    const int row = !valid ? 0 : is2 ? two_list[3 * r2i] : (orig != nullptr ? orig[list[r]] : list[r]);  // original id
+    int nc = !valid ? 0 : is2 ? 2 : cand_n[r];
     const bool ovf = valid && (nc < 1 || nc > SB_NCAND);
     const unsigned om = __ballot_sync(0xffffffffu, ovf && sub == 0);
     if (om) {  // one atomic per warp
@@ -609,7 +632,12 @@ screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict_
     const int ncmax = __reduce_max_sync(0xffffffffu, nc);
     // all candidate ids at once (two 16-byte loads), the point row as float4
     int cj[SB_NCAND];
-    {
+    if (is2) {
+      cj[0] = valid ? two_list[3 * r2i + 1] : 0;
+      cj[1] = valid ? two_list[3 * r2i + 2] : 0;
+#pragma unroll
+      for (int i = 2; i < SB_NCAND; ++i) cj[i] = 0;
+    } else {
       const int4* cp = reinterpret_cast<const int4*>(cand + r * SB_NCAND);
       const int4 c0 = nc > 0 ? cp[0] : make_int4(0, 0, 0, 0);
       const int4 c1 = nc > 4 ? cp[1] : make_int4(0, 0, 0, 0);
@@ -726,14 +754,15 @@ extern "C" int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const
                                       const void* C_aug, const float* anorm, const float* danorm,
                                       const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
                                       float* amb_thr, const int32_t* orig, const int32_t* labels_prev,
-                                      const long long* state, void* stream) {
+                                      int* two_list, int* two_count, const long long* state, void* stream) {
   if (n < 1 || ldb < SB_BKE || ldb % SB_BKE || k < 1 || !P_b || !C_b || !C_aug || !anorm || !danorm || !bstat ||
       !labels || !amb_list || !amb_count || !amb_thr)
     return PCB_EINVAL;
   if (n > INT32_MAX || k > SC_KMAX) return PCB_EUNSUP;
   return dispatch_bf16<false>(ldb, (const __nv_bfloat16*)P_b, n, (const __nv_bfloat16*)C_b, k, anorm, danorm,
                               (const __nv_bfloat16*)C_aug,
-                              bstat, labels, amb_list, amb_count, amb_thr, 0, nullptr, nullptr, orig, labels_prev, state,
+                              bstat, labels, amb_list, amb_count, amb_thr, 0, nullptr, nullptr, orig, labels_prev,
+                              two_list, two_count, state,
                               (cudaStream_t)stream);
 }
 
@@ -744,8 +773,8 @@ extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const v
                                        const float* C, int k, const void* C_aug, const float* bstat,
                                        const int* amb_list, const int* amb_count, const float* amb_thr,
                                        int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
-                                       int* ovf_list, int* ovf_count, const int32_t* orig, const long long* state,
-                                       void* stream) {
+                                       int* ovf_list, int* ovf_count, const int32_t* orig, const int* two_list,
+                                       const int* two_count, const long long* state, void* stream) {
   if (n < 1 || d < 1 || k < 1 || ldb < d || ldb % SB_BKE || !P || !P_b || !C_b || !C || !C_aug || !bstat ||
       !amb_list || !amb_count || !amb_thr || !sub_b || !cand || !cand_n || !labels || !ovf_list || !ovf_count)
     return PCB_EINVAL;
@@ -759,14 +788,15 @@ extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const v
   PCB_CHECK_LAUNCH();
   int rc = dispatch_bf16<true>(ldb, (const __nv_bfloat16*)sub_b, n, (const __nv_bfloat16*)C_b, k, nullptr, nullptr,
                                (const __nv_bfloat16*)C_aug, bstat, nullptr, nullptr, const_cast<int*>(amb_count),
-                               const_cast<float*>(amb_thr), bypass, cand, cand_n, nullptr, nullptr, state, st);
+                               const_cast<float*>(amb_thr), bypass, cand, cand_n, nullptr, nullptr, nullptr, nullptr,
+                               state, st);
   if (rc) return rc;
   const int DQ = (d + 31) / 32;  // float4 per lane (8 lanes per row)
   const int xgrid = sm_count() * 16;
 #define PCB_EX_CASE(N)                                                                                          \
   if (DQ <= N) {                                                                                              \
     screen_exact_kernel<N><<<xgrid, 256, 0, st>>>(P, d, C, amb_list, amb_count, bypass, cand, cand_n, labels, \
-                                                  ovf_list, ovf_count, orig, state);                          \
+                                                  ovf_list, ovf_count, orig, two_list, two_count, state);     \
   } else
   PCB_EX_CASE(1)
   PCB_EX_CASE(2)

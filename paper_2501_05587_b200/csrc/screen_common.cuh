@@ -91,6 +91,51 @@ __device__ __forceinline__ void load_cprime(float (&cp)[32], const float* __rest
 __device__ __forceinline__ void screen_update(const float (&v)[32], float m, int col0, float twoE, float big,
                                               float& R1, int& r1, float& cnt);
 
+// Full update of one chunk of keys v[] with the running best two packed keys
+// (R1, r1), (R2, r2) and an exact integer count of keys within the threshold
+// (so that cnt == 2 identifies rows whose candidates are exactly r1 and r2:
+// an over-count only happens when the minimum dropped by less than 2E, and
+// then the old minimum is itself within the final threshold).
+__device__ __forceinline__ void screen_chunk_top2(const float (&v)[32], uint32_t msk, int col0, float twoE, float& R1,
+                                                  int& r1, float& R2, int& r2, float& cnt) {
+  float ma = 3.4e38f, mb = 3.4e38f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float k0 = __uint_as_float((__float_as_uint(v[4 * q + 0]) & msk) | (uint32_t)(4 * q + 0));
+    const float k1 = __uint_as_float((__float_as_uint(v[4 * q + 1]) & msk) | (uint32_t)(4 * q + 1));
+    const float k2 = __uint_as_float((__float_as_uint(v[4 * q + 2]) & msk) | (uint32_t)(4 * q + 2));
+    const float k3 = __uint_as_float((__float_as_uint(v[4 * q + 3]) & msk) | (uint32_t)(4 * q + 3));
+    ma = fmin3(ma, k0, k1);
+    mb = fmin3(mb, k2, k3);
+  }
+  const float m = fminf(ma, mb);
+  // second smallest packed key of the chunk (packed keys are distinct)
+  float sa = 3.4e38f, sb = 3.4e38f;
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    const float k0 = __uint_as_float((__float_as_uint(v[i]) & msk) | (uint32_t)i);
+    const float k1 = __uint_as_float((__float_as_uint(v[i + 1]) & msk) | (uint32_t)(i + 1));
+    sa = fminf(sa, k0 == m ? 3.4e38f : k0);
+    sb = fminf(sb, k1 == m ? 3.4e38f : k1);
+  }
+  const float m2 = fminf(sa, sb);
+  if (m < R1 - twoE) cnt = 0.0f;
+  if (m < R1) {
+    if (m2 < R1) { R2 = m2; r2 = col0 + (int)(__float_as_uint(m2) & 31u); }
+    else { R2 = R1; r2 = r1; }
+    R1 = m;
+    r1 = col0 + (int)(__float_as_uint(m) & 31u);
+  } else if (m < R2) {
+    R2 = m;
+    r2 = col0 + (int)(__float_as_uint(m) & 31u);
+  }
+  const float thr = R1 + twoE + 0x1p-16f * fabsf(R1);
+  float c = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) c += v[i] <= thr ? 1.0f : 0.0f;
+  cnt += c;
+}
+
 // Same on keys already formed (v[i] = cp[i] - 2 acc[i]).
 __device__ __forceinline__ void screen_chunk_keys(const float (&v)[32], uint32_t msk, int col0, float twoE, float big,
                                                   float& R1, int& r1, float& cnt) {

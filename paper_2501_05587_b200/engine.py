@@ -310,6 +310,8 @@ class LloydEngine(ShardSequence):
                 self.amb_list = torch.empty(n, dtype=torch.int32, device=dev)
                 self.amb_count = torch.zeros(1, dtype=torch.int32, device=dev)
                 self.amb_thr = torch.empty(n, dtype=torch.float32, device=dev)
+                self.two_list = torch.empty(3 * n, dtype=torch.int32, device=dev)  # (row, r1, r2)
+                self.two_count = torch.zeros(1, dtype=torch.int32, device=dev)
                 self.sub_b = torch.empty((n, self.ldb), dtype=torch.bfloat16, device=dev)
                 self.bypass = max(n // 4, 1)  # more ambiguous rows: straight to 3xTF32
                 self.cand = torch.empty((self.bypass, ncand), dtype=torch.int32, device=dev)
@@ -437,17 +439,18 @@ class LloydEngine(ShardSequence):
     def _assign(self, prev, new, acc, state) -> None:
         if self.variant == "bf16s":
             self.amb_count.zero_()
+            self.two_count.zero_()
             self._kmark(0)
             L.call("pcb_assign_screen_bf16", _p(self.P_b), self.n, self.ldb, _p(self.C_b), self.k,
                    _p(self.C_aug), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
                    _p(self.amb_list), _p(self.amb_count), _p(self.amb_thr), _p(self.orig), _p(prev),
-                   _p(state), _stream())
+                   _p(self.two_list), _p(self.two_count), _p(state), _stream())
             self._kmark(1)
             L.call("pcb_resolve_screen_bf16", _p(self.P), self.n, self.d, _p(self.P_b), self.ldb,
                    _p(self.C_b), _p(self.C), self.k, _p(self.C_aug), _p(self.bstat), _p(self.amb_list),
                    _p(self.amb_count), _p(self.amb_thr), self.bypass, _p(self.sub_b), _p(self.cand),
-                   _p(self.cand_n), _p(new), _p(self.ovf_list), _p(self.ovf_count), _p(self.orig), _p(state),
-                   _stream())
+                   _p(self.cand_n), _p(new), _p(self.ovf_list), _p(self.ovf_count), _p(self.orig),
+                   _p(self.two_list), _p(self.two_count), _p(state), _stream())
             L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.ovf_list),
                    _p(self.ovf_count), self.ld, _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels),
                    _p(self.pnorm), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(new),
