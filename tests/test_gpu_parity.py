@@ -178,3 +178,27 @@ def test_device_side_finiteness_check():
     P[12345, 7] = np.inf
     with pytest.raises(ValueError, match="non-finite"):
         pcb.run_lloyd(P, pcb.KKMeansConfig(k=3, max_iters=1))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_repair_many_empty_clusters(dtype):
+    """Hundreds of clusters empty at once (duplicate centroids): the batched
+    top-E donor selection must pick the reference's donors, in order
+    (repair_empty_clusters applied to the device's own raw labels with exact
+    distances)."""
+    rng = make_rng(31)
+    n, d, k = 40000, 8, 300
+    P = rng.normal(0, 1, size=(n, d)).astype(dtype)
+    C = np.repeat(rng.normal(0, 1, size=(1, d)), k, axis=0).astype(dtype)
+    C[:10] = rng.normal(0, 1, size=(10, d)).astype(dtype)  # 10 live centroids, 290 duplicates
+    lab = np.zeros(n, dtype=np.int32)
+    eng = _engine(P, k, dtype, "tiled" if dtype == np.float64 else "auto")
+    gpu = eng.step_from(C, lab)
+    raw = gpu["raw_labels"]
+    assert np.bincount(raw, minlength=k).min() == 0
+    P64, C64 = P.astype(np.float64), C.astype(np.float64)
+    D = ((P64[:, None, :] - C64[None, :, :]) ** 2).sum(-1)
+    ref = oracle.repair_empty_clusters(raw, D, k)
+    assert int((ref != raw).sum()) >= 280
+    assert gpu["moved"] == int((ref != raw).sum())
+    np.testing.assert_array_equal(gpu["labels"], ref)
