@@ -32,6 +32,7 @@
 //   warps  0 A producer, 3 B producer, 1 MMA issuer (M=128 N=128 K=16),
 //          2 TMEM allocator, 4-11 epilogue (warp (g, h): lanes 32g.. of tile h)
 #include <cuda_bf16.h>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include "pcb_common.cuh"
@@ -47,22 +48,34 @@ constexpr int SB_THREADS = 384;
 constexpr int SB_BKE = 64;      // BF16 elements per 128-byte swizzle row
 constexpr int SB_NCAND = 8;     // candidate slots per ambiguous row (pass 2)
 constexpr int SB_AUG = 16;      // augmented K columns per centroid: |c|^2 + OFF as 3 BF16 pieces, 13 zeros
+constexpr int SB_KPAD = 256;    // centroid rows of C_b / C_aug are padded to a multiple of the widest tile
 
-template <int NKC>
+// W = false: centroid tiles of 128 (MMA N = 128), TMEM = 2 buffers x 2 row
+//            tiles x 128 columns, 8 epilogue warps on both row tiles.
+// W = true  (d <= 128): centroid tiles of 256 (MMA N = 256: 96 instead of 128
+//            bytes of shared-memory operands per cycle at full MMA rate), TMEM =
+//            one 256-column accumulator per row tile; the MMAs of the two row
+//            tiles alternate, so each row tile's 4 epilogue warps (full rows,
+//            8 chunks per tile) overlap the other row tile's MMAs.
+template <int NKC, bool W = false>
 struct SbCfg {
+  static constexpr int kBN = W ? 256 : 128;                         // centroids per tile
+  static constexpr int kChunks = kBN / 32;                          // epilogue chunks per tile
+  static constexpr int kStages = W ? 3 : SB_STAGES;
   static constexpr uint32_t kTileBytes = 128 * 128;                 // 128 rows x 128 B
   // resident A (2 row tiles), double-buffered across row pairs when it fits
   // (the next pair's rows load while the current pair's MMAs run)
-  static constexpr int kAStages = NKC <= 2 ? 2 : 1;
+  static constexpr int kAStages = (!W && NKC <= 2) ? 2 : 1;
   static constexpr uint32_t kAPair = 2 * NKC * kTileBytes;
   static constexpr uint32_t kABytes = kAStages * kAPair;
-  static constexpr uint32_t kBBytes = SB_BN * 128;                  // 16 KB centroid chunk per B stage
-  static constexpr uint32_t kAugBytes = SB_BN * 32;                 // + the K=16 augmented columns
-  static constexpr uint32_t kStageB = kBBytes + kAugBytes;          // 20 KB (1024-aligned)
+  static constexpr uint32_t kBBytes = kBN * 128;                    // centroid chunk per B stage
+  static constexpr uint32_t kAugBytes = kBN * 32;                   // + the K=16 augmented columns
+  static constexpr uint32_t kStageB = kBBytes + kAugBytes;          // 1024-aligned
   static constexpr uint32_t kAAug = 128 * 32;                       // constant A columns [1 1 1 0 ..]
   static constexpr uint32_t kBarBytes = 1024;
-  static constexpr uint32_t kSmem = 1024 + kABytes + SB_STAGES * kStageB + kAAug + kBarBytes;
+  static constexpr uint32_t kSmem = 1024 + kABytes + kStages * kStageB + kAAug + kBarBytes;
   static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
+  static_assert(!W || NKC <= 2, "the wide layout keeps a whole tile's chunks in the ring");
 };
 
 // First centroid column of a row pair: the previous label of the pair's
@@ -88,7 +101,7 @@ __device__ __forceinline__ int64_t sb_rows(int64_t n, const int* amb_count, int6
   return c > bypass ? 0 : c;
 }
 
-template <int NKC, bool CAND>
+template <int NKC, bool CAND, bool W>
 __global__ void __launch_bounds__(SB_THREADS, 1)
 assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                           const __grid_constant__ CUtensorMap tm_baug, const float* __restrict__ anorm,
@@ -98,7 +111,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
                           int* __restrict__ cand_n, const int32_t* __restrict__ orig,
                           const int32_t* __restrict__ lprev, int* __restrict__ two_list, int* __restrict__ two_count,
                           const long long* __restrict__ state) {
-  using Cfg = SbCfg<NKC>;
+  using Cfg = SbCfg<NKC, W>;
+  constexpr int BN = Cfg::kBN, CH = Cfg::kChunks, STAGES = Cfg::kStages;
   if (stopped(state)) return;
   const int64_t n = CAND ? sb_rows(n_in, amb_count, bypass) : n_in;
   if (n == 0) return;
@@ -107,19 +121,19 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
   uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + Cfg::kABytes;
-  uint8_t* sAaug = sB + SB_STAGES * Cfg::kStageB;
+  uint8_t* sAaug = sB + STAGES * Cfg::kStageB;
   uint8_t* bar_area = sAaug + Cfg::kAAug;
   constexpr int AS = Cfg::kAStages;
   uint64_t* afull = reinterpret_cast<uint64_t*>(bar_area);  // [AS][NKC]
   uint64_t* aempty = afull + AS * NKC;                       // [AS][NKC]
   uint64_t* full = aempty + AS * NKC;                        // [STAGES]
-  uint64_t* empty = full + SB_STAGES;                        // [STAGES]
-  uint64_t* tfull = empty + SB_STAGES;                       // [2]
+  uint64_t* empty = full + STAGES;                           // [STAGES]
+  uint64_t* tfull = empty + STAGES;                          // [2] (W: per row tile)
   uint64_t* tempty = tfull + 2;                              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = (k + SB_BN - 1) / SB_BN;
+  const int ntiles = (k + BN - 1) / BN;
   const float OFF = bstat[2];
   // constant A columns of the augmented K step, no-swizzle K-major layout
   // [2 K halves][128 rows][16 B]: every row = (1, 1, 1, 0, ..., 0), so the MMA
@@ -142,13 +156,13 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         ptx::mbar_init(&aempty[a * NKC + c], 1);
       }
     }
-    for (int s = 0; s < SB_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], 256);
+      ptx::mbar_init(&tempty[b], W ? 128 : 256);
     }
     ptx::fence_barrier_init();
   }
@@ -185,10 +199,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     uint32_t phase = 0;
     // first tile of the next pair fetched one pair ahead (two dependent
     // global loads would otherwise stall the ring at every pair boundary)
-    int t0_nx = blockIdx.x < npairs ? sb_first_col(lprev, orig, blockIdx.x, n, k) / SB_BN : 0;
+    int t0_nx = blockIdx.x < npairs ? sb_first_col(lprev, orig, blockIdx.x, n, k) / BN : 0;
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
       const int t0 = t0_nx;
-      if (pr + gridDim.x < npairs) t0_nx = sb_first_col(lprev, orig, pr + gridDim.x, n, k) / SB_BN;
+      if (pr + gridDim.x < npairs) t0_nx = sb_first_col(lprev, orig, pr + gridDim.x, n, k) / BN;
       for (int nt = 0; nt < ntiles; ++nt) {
         const int tile = nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles;
         for (int c = 0; c < NKC; ++c) {
@@ -197,20 +211,80 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             uint8_t* st = sB + stage * Cfg::kStageB;
             const bool last = c + 1 == NKC;  // the tile's augmented columns ride with its last chunk
             ptx::mbar_expect_tx(&full[stage], Cfg::kBBytes + (last ? Cfg::kAugBytes : 0u));
-            ptx::tma_load_2d(&tm_b, &full[stage], st, c * SB_BKE, tile * SB_BN, pol);
+            ptx::tma_load_2d(&tm_b, &full[stage], st, c * SB_BKE, tile * BN, pol);
             if (last) {
-              ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes, 0, tile * SB_BN, pol);
-              ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes + SB_BN * 16, 8, tile * SB_BN, pol);
+              ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes, 0, tile * BN, pol);
+              ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes + BN * 16, 8, tile * BN, pol);
             }
           }
           __syncwarp();
-          if (++stage == SB_STAGES) { stage = 0; phase ^= 1u; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (warp-uniform loop, one elected lane issues) ----------------
-    constexpr uint32_t idesc = ptx::idesc_bf16<128, SB_BN>();
+    constexpr uint32_t idesc = ptx::idesc_bf16<128, BN>();
+    if constexpr (W) {
+      // both row tiles per centroid tile; the tile's NKC chunk stages stay
+      // resident until the second row tile's MMAs have read them
+      int stage = 0;
+      uint32_t phase = 0, tpar = 0;
+      int it = 0;
+      for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
+        for (int nt = 0; nt < ntiles; ++nt) {
+          int stc[NKC];
+          uint32_t phc[NKC];
+#pragma unroll
+          for (int c = 0; c < NKC; ++c) {
+            stc[c] = stage;
+            phc[c] = phase;
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          }
+#pragma unroll
+          for (int rt = 0; rt < 2; ++rt) {
+            ptx::mbar_wait(&tempty[rt], tpar ^ 1u);
+            ptx::tc_fence_after();
+            const uint32_t d0 = tmem + (uint32_t)(rt * 256);
+#pragma unroll
+            for (int c = 0; c < NKC; ++c) {
+              if (rt == 0) {
+                if (nt == 0) ptx::mbar_wait(&afull[c], (uint32_t)(it & 1));
+                ptx::mbar_wait(&full[stc[c]], phc[c]);
+                ptx::tc_fence_after();
+              }
+              const uint64_t ad = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (rt * NKC + c) * Cfg::kTileBytes));
+              const uint64_t bd = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stc[c] * Cfg::kStageB));
+              if (ptx::elect_one()) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                  const uint64_t off = (uint64_t)(ks * 32) >> 4;
+                  ptx::umma_f16(d0, ad + off, bd + off, idesc, (c | ks) != 0);
+                }
+                if (c + 1 == NKC) {
+                  const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
+                  const uint64_t ba = ptx::sdesc_k_none(ptx::smem_u32(sB + stc[c] * Cfg::kStageB + Cfg::kBBytes),
+                                                        BN * 16, 128);
+                  ptx::umma_f16(d0, aa, ba, idesc, 1u);
+                }
+              }
+              __syncwarp();
+            }
+            if (ptx::elect_one()) ptx::umma_commit(&tfull[rt]);
+            __syncwarp();
+          }
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int c = 0; c < NKC; ++c) {
+              ptx::umma_commit(&empty[stc[c]]);
+              if (nt + 1 == ntiles) ptx::umma_commit(&aempty[c]);
+            }
+          }
+          __syncwarp();
+          tpar ^= 1u;
+        }
+      }
+    } else {
     int stage = 0;
     uint32_t phase = 0;
     int abuf = 0;
@@ -240,7 +314,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             if (c + 1 == NKC) {  // augmented K step: + (|c|^2 + OFF) in three BF16 pieces
               const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
               const uint64_t ba = ptx::sdesc_k_none(ptx::smem_u32(sB + stage * Cfg::kStageB + Cfg::kBBytes),
-                                                    SB_BN * 16, 128);
+                                                    BN * 16, 128);
               ptx::umma_f16(d0, aa, ba, idesc, 1u);
               ptx::umma_f16(d0 + 128, aa, ba, idesc, 1u);
             }
@@ -248,7 +322,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             if (nt + 1 == ntiles) ptx::umma_commit(&aempty[ab * NKC + c]);  // A chunk free again
           }
           __syncwarp();
-          if (++stage == SB_STAGES) { stage = 0; phase ^= 1u; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
         if (ptx::elect_one()) ptx::umma_commit(&tfull[abuf]);
         __syncwarp();
@@ -256,6 +330,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         if (abuf == 0) aphase ^= 1u;
       }
     }
+    }  // !W
   } else if (warp >= 4) {
     // ---------------- epilogue: warp (g, h) = lanes 32g.. of row tile h ----------------
     const int g = warp & 3, h = (warp - 4) >> 2;
@@ -265,7 +340,21 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     int abuf = 0;
     uint32_t aphase = 0;
     const int64_t r_in = h * 128 + g * 32 + lane;
-    const uint32_t tlane = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * 128);
+    // TMEM of this warp's 32 rows: W = its row tile's single 256-column
+    // accumulator; otherwise buffer b at columns b * 256 + h * 128
+    const uint32_t tlane = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * (W ? 256 : 128));
+    uint32_t tph = 0;  // W: phase of this row tile's accumulator
+    auto tbar = [&]() { return W ? h : abuf; };
+    auto tphase = [&]() { return W ? tph : aphase; };
+    auto tbase = [&]() { return tlane + (uint32_t)(W ? 0 : abuf * 256); };
+    auto tnext = [&]() {
+      if (W) {
+        tph ^= 1u;
+      } else {
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1u;
+      }
+    };
     // TMEM loads run one 32-column chunk ahead of the arithmetic (vA / vB by
     // chunk parity; 4 chunks per tile), across tile and pair boundaries
     uint32_t vA[32], vB[32];
@@ -288,9 +377,9 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     };
     if (blockIdx.x < npairs) {
       fetch_pair(blockIdx.x);
-      ptx::mbar_wait(&tfull[0], 0);
+      ptx::mbar_wait(&tfull[tbar()], 0);
       ptx::tc_fence_after();
-      ptx::tmem_ld_32x32b_x32_async(tlane + 32 * ((fc_nx % SB_BN) / 32), vA);
+      ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * ((fc_nx % BN) / 32), vA);
     }
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
       const int64_t row = pr * 256 + r_in;
@@ -304,36 +393,35 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         twoE = screen_two_e_aug(an_nx, dan_nx, Bmax, dBmax, OFF, acc_rel);
         big = 64.0f / twoE;
       }
-      const int t0 = fc_nx / SB_BN, q0 = (fc_nx % SB_BN) / 32;
+      const int t0 = fc_nx / BN, q0 = (fc_nx % BN) / 32;
       const int64_t out_row = out_nx;  // original row id (label store)
       if (!last_pair) fetch_pair(pr + gridDim.x);
       float R1 = 3.4e38f, R2 = 3.4e38f, cnt = 0.0f;
       int r1 = 0, r2 = 0;
       for (int nt = 0; nt < ntiles; ++nt) {
-        const uint32_t taddr = tlane + (uint32_t)(abuf * 256);
-        const int c0 = (nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles) * SB_BN;
+        const uint32_t taddr = tbase();
+        const int c0 = (nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles) * BN;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < CH; ++q) {
           uint32_t (&cur)[32] = (q & 1) ? vB : vA;
           uint32_t (&nxt)[32] = (q & 1) ? vA : vB;
           ptx::tmem_wait_ld(cur);
-          const int qe = nt == 0 ? ((q + q0) & 3) : q;  // chunk of the tile held by cur
-          if (q < 3) {
-            const int qn = nt == 0 ? ((q + 1 + q0) & 3) : q + 1;
+          const int qe = nt == 0 ? ((q + q0) & (CH - 1)) : q;  // chunk of the tile held by cur
+          if (q < CH - 1) {
+            const int qn = nt == 0 ? ((q + 1 + q0) & (CH - 1)) : q + 1;
             ptx::tmem_ld_32x32b_x32_async(taddr + 32 * qn, nxt);
           } else {
-            // this buffer is fully read: hand it back, prefetch the next one
+            // this accumulator is fully read: hand it back, prefetch the next one
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&tempty[abuf]);
-            abuf ^= 1;
-            if (abuf == 0) aphase ^= 1u;
+            ptx::mbar_arrive(&tempty[tbar()]);
+            tnext();
             if (nt + 1 < ntiles || !last_pair) {
-              ptx::mbar_wait(&tfull[abuf], aphase);
+              ptx::mbar_wait(&tfull[tbar()], tphase());
               ptx::tc_fence_after();
               // first chunk of the next pair: read fc_nx only here, a pair after
               // its (two dependent) loads were issued
-              const int qn = nt + 1 < ntiles ? 0 : (fc_nx % SB_BN) / 32;
-              ptx::tmem_ld_32x32b_x32_async(tlane + (uint32_t)(abuf * 256) + 32 * qn, nxt);
+              const int qn = nt + 1 < ntiles ? 0 : (fc_nx % BN) / 32;
+              ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * qn, nxt);
             }
           }
           float v[32];
@@ -377,7 +465,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
               screen_chunk_top2(km, msk, c0 + 32 * qe, twoE, R1, r1, R2, r2, cnt);
 #if defined(PCB_EXP) && PCB_EXP == 6
               // experiment build: count full-path chunks per position (q + 4 * nt) in state[8..]
-              if (lane == 0) atomicAdd((unsigned long long*)state + 8 + (nt < 8 ? nt * 4 + q : 32), 1ull);
+              if (lane == 0) atomicAdd((unsigned long long*)state + 8 + (nt < 8 ? nt * 4 + (q & 3) : 32), 1ull);
 #endif
             }
 #endif
@@ -450,20 +538,20 @@ static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t row
   return r == CUDA_SUCCESS ? 0 : PCB_EINVAL;
 }
 
-template <int NKC, bool CAND>
+template <int NKC, bool CAND, bool W>
 static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                               const float* an, const float* dan, const __nv_bfloat16* Baug, const float* bstat,
                               int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
                               int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev,
                               int* two_list, int* two_count, const long long* state, cudaStream_t st) {
-  using Cfg = SbCfg<NKC>;
+  using Cfg = SbCfg<NKC, W>;
   CUtensorMap ta, tb, tg;
   int rc;
-  const int64_t kpad = (k + SB_BN - 1) / SB_BN * SB_BN;  // B / Baug hold kpad rows (padding: key = +huge)
+  const int64_t kpad = (k + SB_KPAD - 1) / SB_KPAD * SB_KPAD;  // B / Baug hold kpad rows (padding: key = +huge)
   if ((rc = make_tmap_bf16(&ta, A, n, NKC * SB_BKE, 128))) return rc;
-  if ((rc = make_tmap_bf16(&tb, B, kpad, NKC * SB_BKE, SB_BN))) return rc;
-  if ((rc = make_tmap_bf16(&tg, Baug, kpad, SB_AUG, SB_BN, 8, CU_TENSOR_MAP_SWIZZLE_NONE))) return rc;
-  auto kern = assign_screen_bf16_kernel<NKC, CAND>;
+  if ((rc = make_tmap_bf16(&tb, B, kpad, NKC * SB_BKE, Cfg::kBN))) return rc;
+  if ((rc = make_tmap_bf16(&tg, Baug, kpad, SB_AUG, Cfg::kBN, 8, CU_TENSOR_MAP_SWIZZLE_NONE))) return rc;
+  auto kern = assign_screen_bf16_kernel<NKC, CAND, W>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   if (e != cudaSuccess) return (int)e;
   const int64_t npairs = (n + 255) / 256;
@@ -480,15 +568,19 @@ static int dispatch_bf16(int ldb, const __nv_bfloat16* A, int64_t n, const __nv_
                          int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
                          int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev, int* two_list,
                          int* two_count, const long long* state, cudaStream_t st) {
-#define PCB_SB_CASE(N)                                                                                      \
-  case N:                                                                                                   \
-    return launch_screen_bf16<N, CAND>(A, n, B, k, an, dan, Baug, bstat, labels, amb_list, amb_count,       \
-                                       amb_thr, bypass, cand, cand_n, orig, lprev, two_list, two_count, state, st);
+#define PCB_SB_CASE(N, WIDE)                                                                                \
+    return launch_screen_bf16<N, CAND, WIDE>(A, n, B, k, an, dan, Baug, bstat, labels, amb_list, amb_count, \
+                                             amb_thr, bypass, cand, cand_n, orig, lprev, two_list, two_count, \
+                                             state, st);
+  // d <= 128: N = 128 tiles; PCB_SCREEN_WIDE=1 selects the N = 256 layout
+  // (measured slower at c3 / c5: 2.52 vs 2.37 ms, 65 vs 56 ms; MMA-only 2.14
+  // vs 2.03 ms — the BF16 MMA rate, not shared-memory operand bandwidth, binds)
+  static const bool narrow = getenv("PCB_SCREEN_WIDE") == nullptr;
   switch (ldb / SB_BKE) {
-    PCB_SB_CASE(1)
-    PCB_SB_CASE(2)
-    PCB_SB_CASE(3)
-    PCB_SB_CASE(4)
+    case 1: if (narrow) { PCB_SB_CASE(1, false) } else { PCB_SB_CASE(1, true) }
+    case 2: if (narrow) { PCB_SB_CASE(2, false) } else { PCB_SB_CASE(2, true) }
+    case 3: PCB_SB_CASE(3, false)
+    case 4: PCB_SB_CASE(4, false)
     default: return PCB_EUNSUP;
   }
 #undef PCB_SB_CASE
@@ -725,7 +817,7 @@ extern "C" int pcb_screen_prep_points_bf16(const float* P, int64_t n, int d, int
   return 0;
 }
 
-extern "C" int pcb_screen_bf16_kpad(int k) { return (k + SB_BN - 1) / SB_BN * SB_BN; }
+extern "C" int pcb_screen_bf16_kpad(int k) { return (k + SB_KPAD - 1) / SB_KPAD * SB_KPAD; }
 extern "C" int pcb_screen_bf16_aug(void) { return SB_AUG; }
 
 extern "C" int pcb_screen_prep_centroids_bf16(const float* C, const float* cnorm, int k, int d, int ldb, void* C_b,
@@ -741,7 +833,7 @@ extern "C" int pcb_screen_prep_centroids_bf16(const float* C, const float* cnorm
   row_bf16_norms_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(C, k, d, bnorm, dbnorm, nullptr,
                                                              reinterpret_cast<__nv_bfloat16*>(C_b), ldb, -2.0f);
   PCB_CHECK_LAUNCH();
-  const int kpad = (k + SB_BN - 1) / SB_BN * SB_BN;
+  const int kpad = (k + SB_KPAD - 1) / SB_KPAD * SB_KPAD;
   centroid_aug_kernel<<<(kpad + 127) / 128, 128, 0, st>>>(cnorm, bstat, k, kpad, reinterpret_cast<__nv_bfloat16*>(C_aug));
   PCB_CHECK_LAUNCH();
   max2_bf16_kernel<<<1, 256, 0, st>>>(bnorm, dbnorm, k, bstat);
