@@ -265,7 +265,7 @@ def main():
     peaks, peak_src = _peaks()
     n_local = hi - lo
     flops = 2.0 * n_local * k * d  # algorithmic: one dot product per point-centroid pair
-    if d <= 32 and eng.variant not in ("tc3xtf32", "tc1xtf32s", "bf16s"):
+    if d <= 32 and eng.variant not in ("tc3xtf32", "tc1xtf32s", "bf16s", "fp8s"):
         # small-d FFMA path: report against HBM (bytes of P read + labels)
         traffic_alg = n_local * (4 * d + 8 + 4) + k * d * 4
         roof = {"bound": "hbm", "achieved": traffic_alg / (kern_ms * 1e-3) / 1e9,
@@ -279,6 +279,8 @@ def main():
             peak, src = tf32 / 3.0, "3xTF32 effective = bf16 burst / 6"
         elif eng.variant == "bf16s":  # one BF16 (kind::f16) pass
             peak, src = peaks["bf16_tflops"], "bf16 burst (dense)"
+        elif eng.variant == "fp8s":  # one E4M3 (kind::f8f6f4) pass: twice the BF16 rate
+            peak, src = 2.0 * peaks["bf16_tflops"], "fp8 = 2 x bf16 burst (dense, derived)"
         else:
             peak, src = tf32, "TF32 = bf16 burst / 2"
         roof = {"bound": "tensor", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": peak,
@@ -287,7 +289,7 @@ def main():
     scr = {"res": "assign_screen_res_kernel", "pair": "assign_screen_2sm_kernel",
            "stream": "assign_screen_kernel"}.get(os.environ.get("PCB_SCREEN_IMPL", "res"), "assign_screen_res_kernel")
     roof["kernel"] = {"tc1xtf32s": scr, "tc3xtf32": "assign_tc3xtf32_kernel",
-                      "bf16s": "assign_screen_bf16_kernel"}.get(
+                      "bf16s": "assign_screen_bf16_kernel", "fp8s": "assign_screen_bf16_kernel<F8>"}.get(
         eng.variant, f"assign[{eng.variant}]")
     roof["kernel_ms"] = kern_ms
     roof["algorithmic_per_launch"] = f"2*n*k*d = {flops:.4g} flop" if roof["unit"] == "TFLOP/s" else \
@@ -304,14 +306,14 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32",
+        "vs_baseline": None, "dtype": "f32",  # inputs/results f32; the screen's operands are bf16/e4m3, certified exact
         "data": "synthetic blobs generated on device (centers U(-10,10), N(0,1) noise)",
         "config": {"workload": f"{args.config}: n={n} d={d} k={k}", "n": n, "d": d, "k": k,
                    "variant": eng.variant, "parallelism": f"dp{world} row-sharded",
                    "l2": "inputs larger than L2" if n * d * 4 > 126e6 else "inputs fit in L2 (no flush)"},
         "dists_per_sec": n * k / (ms_per_step * 1e-3),
         "roofline": roof,
-        "gpu_launches": {"tc1xtf32s": 12, "bf16s": 15}.get(eng.variant, 6) * K,
+        "gpu_launches": {"tc1xtf32s": 12, "bf16s": 15, "fp8s": 15}.get(eng.variant, 6) * K,
         "screen_ambiguous_rows_last_iter": amb,
         "clocks": clocks,
     }

@@ -45,6 +45,7 @@ extern "C" {
 #define PCB_ASSIGN_DELTA     4  /* delta-chunked P.C.P^T ablation (f32)     */
 #define PCB_ASSIGN_SCREEN    5  /* tcgen05 1xTF32 certified screening (f32) */
 #define PCB_ASSIGN_SCREEN_BF16 6 /* tcgen05 BF16 certified screening + exact candidates (f32, d <= 256) */
+#define PCB_ASSIGN_SCREEN_FP8  7 /* same with E4M3 operands (kind::f8f6f4), scaled keys (f32, d <= 256) */
 
 int         pcb_abi_version(void);
 const char* pcb_error_string(int code);
@@ -178,7 +179,7 @@ int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_l
 int pcb_screen_bf16_ld(int d);
 int pcb_screen_bf16_ncand(void);
 int pcb_screen_prep_points_bf16(const float* P, int64_t n, int d, int ldb, void* P_b, float* anorm,
-                                float* danorm, float* bstat /* 4 */, void* stream);
+                                float* danorm, float* bstat /* 16 */, void* stream);
 int pcb_screen_bf16_kpad(int k);   /* rows of C_b / C_aug: k rounded up to 128 */
 int pcb_screen_bf16_aug(void);     /* BF16 columns per C_aug row (16) */
 int pcb_screen_prep_centroids_bf16(const float* C, const float* cnorm, int k, int d, int ldb, void* C_b,
@@ -204,6 +205,26 @@ int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, i
 int pcb_screen_relayout_bf16(const void* Pb0, const float* an0, const float* dan0, int64_t n, int ldb,
                              const int32_t* perm, void* P_b, float* anorm, float* danorm, int32_t* orig,
                              void* stream);
+/* E4M3 screening variant ("fp8s"): the same kernels and contract as the BF16
+ * one with E4M3 operand rows of ld8 = pcb_screen_fp8_ld(d) bytes (power-of-two
+ * scales chosen on the device, bstat of 16 floats; the keys are scaled by
+ * S = bstat[4] and so are amb_thr).                                          */
+int pcb_screen_fp8_ld(int d);
+int pcb_screen_prep_points_fp8(const float* P, int64_t n, int d, int ld8, void* P_q, float* anorm,
+                               float* danorm, float* bstat /* 16 */, void* stream);
+int pcb_screen_prep_centroids_fp8(const float* C, const float* cnorm, int k, int d, int ld8, void* C_q,
+                                  void* C_aug, float* bnorm, float* dbnorm, float* bstat, void* stream);
+int pcb_assign_screen_fp8(const void* P_q, int64_t n, int ld8, const void* C_q, int k, const void* C_aug,
+                          const float* anorm, const float* danorm, const float* bstat, int32_t* labels,
+                          int* amb_list, int* amb_count, float* amb_thr, const int32_t* orig,
+                          const int32_t* labels_prev, int* two_list, int* two_count,
+                          const long long* state, void* stream);
+int pcb_resolve_screen_fp8(const float* P, int64_t n, int d, const void* P_q, int ld8, const void* C_q,
+                           const float* C, int k, const void* C_aug, const float* bstat,
+                           const int* amb_list, const int* amb_count, const float* amb_thr,
+                           int64_t bypass, void* sub_q, int* cand, int* cand_n, int32_t* labels,
+                           int* ovf_list, int* ovf_count, const int32_t* orig, const int* two_list,
+                           const int* two_count, const long long* state, void* stream);
 int pcb_count_labels(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
                      double* acc, const long long* state, void* stream);
 

@@ -47,6 +47,12 @@ SIGNATURES = {
     "pcb_delta_update_f64": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),
     "pcb_sum_squares_f32": (I32, [P, I64, P, P]),
     "pcb_sum_squares_f64": (I32, [P, I64, P, P]),
+    "pcb_screen_fp8_ld": (I32, [I32]),
+    "pcb_screen_prep_points_fp8": (I32, [P, I64, I32, I32, P, P, P, P, P]),
+    "pcb_screen_prep_centroids_fp8": (I32, [P, P, I32, I32, I32, P, P, P, P, P, P]),
+    "pcb_assign_screen_fp8": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "pcb_resolve_screen_fp8": (I32, [P, I64, I32, P, I32, P, P, I32, P, P, P, P, P, I64, P, P, P, P, P, P, P, P, P,
+                                     P, P]),
     "pcb_screen_bf16_ld": (I32, [I32]),
     "pcb_screen_bf16_ncand": (I32, []),
     "pcb_screen_prep_points_bf16": (I32, [P, I64, I32, I32, P, P, P, P, P]),
@@ -92,9 +98,10 @@ SIGNATURES = {
 
 ASSIGN_AUTO, ASSIGN_ROWREG, ASSIGN_TILED, ASSIGN_TC3XTF32, ASSIGN_DELTA, ASSIGN_SCREEN = 0, 1, 2, 3, 4, 5
 ASSIGN_SCREEN_BF16 = 6
+ASSIGN_SCREEN_FP8 = 7
 VARIANTS = {"auto": ASSIGN_AUTO, "rowreg": ASSIGN_ROWREG, "tiled": ASSIGN_TILED,
             "tc3xtf32": ASSIGN_TC3XTF32, "delta": ASSIGN_DELTA, "tc1xtf32s": ASSIGN_SCREEN,
-            "bf16s": ASSIGN_SCREEN_BF16}
+            "bf16s": ASSIGN_SCREEN_BF16, "fp8s": ASSIGN_SCREEN_FP8}
 STATE_WORDS = 8
 
 _lib = None

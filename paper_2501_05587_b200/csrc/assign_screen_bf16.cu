@@ -101,7 +101,7 @@ __device__ __forceinline__ int64_t sb_rows(int64_t n, const int* amb_count, int6
   return c > bypass ? 0 : c;
 }
 
-template <int NKC, bool CAND, bool W>
+template <int NKC, bool CAND, bool W, bool F8>
 __global__ void __launch_bounds__(SB_THREADS, 1)
 assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                           const __grid_constant__ CUtensorMap tm_baug, const float* __restrict__ anorm,
@@ -224,7 +224,13 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (warp-uniform loop, one elected lane issues) ----------------
-    constexpr uint32_t idesc = ptx::idesc_bf16<128, BN>();
+    constexpr uint32_t idesc = ptx::idesc_bf16<128, BN>();  // the augmented K step is BF16 in both modes
+    constexpr uint32_t idesc_main = F8 ? ptx::idesc_e4m3<128, BN>() : idesc;
+    // main K steps: 32 bytes of each operand row per MMA (K = 16 BF16 / 32 E4M3)
+    auto mma_main = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+      if constexpr (F8) ptx::umma_f8(d, a, b, idesc_main, acc);
+      else ptx::umma_f16(d, a, b, idesc_main, acc);
+    };
     if constexpr (W) {
       // both row tiles per centroid tile; the tile's NKC chunk stages stay
       // resident until the second row tile's MMAs have read them
@@ -259,7 +265,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                   const uint64_t off = (uint64_t)(ks * 32) >> 4;
-                  ptx::umma_f16(d0, ad + off, bd + off, idesc, (c | ks) != 0);
+                  mma_main(d0, ad + off, bd + off, (c | ks) != 0);
                 }
                 if (c + 1 == NKC) {
                   const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
@@ -308,8 +314,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {           // 4 x K=16 per 128-byte chunk
               const uint64_t off = (uint64_t)(ks * 32) >> 4;
-              ptx::umma_f16(d0, a0 + off, bd + off, idesc, (c | ks) != 0);
-              ptx::umma_f16(d0 + 128, a1 + off, bd + off, idesc, (c | ks) != 0);
+              mma_main(d0, a0 + off, bd + off, (c | ks) != 0);
+              mma_main(d0 + 128, a1 + off, bd + off, (c | ks) != 0);
             }
             if (c + 1 == NKC) {  // augmented K step: + (|c|^2 + OFF) in three BF16 pieces
               const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
@@ -335,7 +341,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     // ---------------- epilogue: warp (g, h) = lanes 32g.. of row tile h ----------------
     const int g = warp & 3, h = (warp - 4) >> 2;
     const float Bmax = bstat[0], dBmax = bstat[1];
-    const float acc_rel = (float)(NKC * 4 + 3) * 0x1p-19f;
+    // BF16 / E4M3 products are exact in f32; each MMA adds at most (K + 1)
+    // roundings relative to the running sum of |products| (K = 16 / 32)
+    const float acc_rel = (float)(NKC * 4 + 3) * (F8 ? 0x1p-18f : 0x1p-19f);
+    const float kscale = bstat[4];  // keys come out of the MMA scaled by S = sp * sc (1 for BF16)
     const uint32_t msk = kIdxMask;
     int abuf = 0;
     uint32_t aphase = 0;
@@ -390,7 +399,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       if (CAND) {
         thr = an_nx;
       } else {
-        twoE = screen_two_e_aug(an_nx, dan_nx, Bmax, dBmax, OFF, acc_rel);
+        twoE = kscale * screen_two_e_aug(an_nx, dan_nx, Bmax, dBmax, OFF, acc_rel);
         big = 64.0f / twoE;
       }
       const int t0 = fc_nx / BN, q0 = (fc_nx % BN) / 32;
@@ -538,7 +547,7 @@ static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t row
   return r == CUDA_SUCCESS ? 0 : PCB_EINVAL;
 }
 
-template <int NKC, bool CAND, bool W>
+template <int NKC, bool CAND, bool W, bool F8>
 static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                               const float* an, const float* dan, const __nv_bfloat16* Baug, const float* bstat,
                               int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
@@ -548,10 +557,10 @@ static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bflo
   CUtensorMap ta, tb, tg;
   int rc;
   const int64_t kpad = (k + SB_KPAD - 1) / SB_KPAD * SB_KPAD;  // B / Baug hold kpad rows (padding: key = +huge)
-  if ((rc = make_tmap_bf16(&ta, A, n, NKC * SB_BKE, 128))) return rc;
+  if ((rc = make_tmap_bf16(&ta, A, n, NKC * SB_BKE, 128))) return rc;  // 128-byte chunks: F8 rows viewed as BF16 pairs
   if ((rc = make_tmap_bf16(&tb, B, kpad, NKC * SB_BKE, Cfg::kBN))) return rc;
   if ((rc = make_tmap_bf16(&tg, Baug, kpad, SB_AUG, Cfg::kBN, 8, CU_TENSOR_MAP_SWIZZLE_NONE))) return rc;
-  auto kern = assign_screen_bf16_kernel<NKC, CAND, W>;
+  auto kern = assign_screen_bf16_kernel<NKC, CAND, W, F8>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   if (e != cudaSuccess) return (int)e;
   const int64_t npairs = (n + 255) / 256;
@@ -562,14 +571,14 @@ static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bflo
   return 0;
 }
 
-template <bool CAND>
+template <bool CAND, bool F8 = false>
 static int dispatch_bf16(int ldb, const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                          const float* an, const float* dan, const __nv_bfloat16* Baug, const float* bstat,
                          int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
                          int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev, int* two_list,
                          int* two_count, const long long* state, cudaStream_t st) {
 #define PCB_SB_CASE(N, WIDE)                                                                                \
-    return launch_screen_bf16<N, CAND, WIDE>(A, n, B, k, an, dan, Baug, bstat, labels, amb_list, amb_count, \
+    return launch_screen_bf16<N, CAND, WIDE, F8>(A, n, B, k, an, dan, Baug, bstat, labels, amb_list, amb_count, \
                                              amb_thr, bypass, cand, cand_n, orig, lprev, two_list, two_count, \
                                              state, st);
   // d <= 128: N = 128 tiles; PCB_SCREEN_WIDE=1 selects the N = 256 layout
@@ -635,6 +644,7 @@ __global__ void max2_bf16_kernel(const float* __restrict__ b, const float* __res
 }
 
 __global__ void screen_off_kernel(float* __restrict__ bstat, const float* __restrict__ maxsq) {
+  bstat[4] = 1.0f;  // key scale (BF16: the MMA emits unscaled keys)
   bstat[2] = 1.01f * (*maxsq) + 1.0f;  // OFF > max |p|^2: every key positive
 }
 
@@ -783,7 +793,7 @@ __global__ void centroid_aug_kernel(const float* __restrict__ cnorm, const float
   uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = make_uint4(0u, 0u, 0u, 0u);
   __nv_bfloat16 h1, h2, h3;
   if (j < k) {
-    const float cp = cnorm[j] + bstat[2];
+    const float cp = (cnorm[j] + bstat[2]) * bstat[4];  // keys carry the operand scales S (E4M3; 1 for BF16)
     h1 = __float2bfloat16_rn(cp);
     const float r1 = cp - __bfloat162float(h1);  // exact (Sterbenz-like: |r1| << cp)
     h2 = __float2bfloat16_rn(r1);
@@ -861,13 +871,15 @@ extern "C" int pcb_assign_screen_bf16(const void* P_b, int64_t n, int ldb, const
 // Pass 2 + exact resolution of the ambiguous rows.  Rows left over (more than
 // SB_NCAND candidates, or every row when the ambiguous count exceeds `bypass`)
 // land in ovf_list / ovf_count for the 3xTF32 resolver.
-extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
-                                       const float* C, int k, const void* C_aug, const float* bstat,
-                                       const int* amb_list, const int* amb_count, const float* amb_thr,
-                                       int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
-                                       int* ovf_list, int* ovf_count, const int32_t* orig, const int* two_list,
-                                       const int* two_count, const long long* state, void* stream) {
-  if (n < 1 || d < 1 || k < 1 || ldb < d || ldb % SB_BKE || !P || !P_b || !C_b || !C || !C_aug || !bstat ||
+// ldb in BF16 units (E4M3 rows: bytes / 2)
+template <bool F8>
+static int resolve_screen(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
+                          const float* C, int k, const void* C_aug, const float* bstat,
+                          const int* amb_list, const int* amb_count, const float* amb_thr,
+                          int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
+                          int* ovf_list, int* ovf_count, const int32_t* orig, const int* two_list,
+                          const int* two_count, const long long* state, void* stream) {
+  if (n < 1 || d < 1 || k < 1 || ldb % SB_BKE || !P || !P_b || !C_b || !C || !C_aug || !bstat ||
       !amb_list || !amb_count || !amb_thr || !sub_b || !cand || !cand_n || !labels || !ovf_list || !ovf_count)
     return PCB_EINVAL;
   if (d > 256) return PCB_EUNSUP;
@@ -878,7 +890,7 @@ extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const v
   gather_rows_bf16<<<grid, 256, 0, st>>>((const __nv_bfloat16*)P_b, ldb, amb_list, amb_count, bypass,
                                          (__nv_bfloat16*)sub_b, state);
   PCB_CHECK_LAUNCH();
-  int rc = dispatch_bf16<true>(ldb, (const __nv_bfloat16*)sub_b, n, (const __nv_bfloat16*)C_b, k, nullptr, nullptr,
+  int rc = dispatch_bf16<true, F8>(ldb, (const __nv_bfloat16*)sub_b, n, (const __nv_bfloat16*)C_b, k, nullptr, nullptr,
                                (const __nv_bfloat16*)C_aug, bstat, nullptr, nullptr, const_cast<int*>(amb_count),
                                const_cast<float*>(amb_thr), bypass, cand, cand_n, nullptr, nullptr, nullptr, nullptr,
                                state, st);
@@ -898,6 +910,18 @@ extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const v
 #undef PCB_EX_CASE
   PCB_CHECK_LAUNCH();
   return 0;
+}
+
+extern "C" int pcb_resolve_screen_bf16(const float* P, int64_t n, int d, const void* P_b, int ldb, const void* C_b,
+                                       const float* C, int k, const void* C_aug, const float* bstat,
+                                       const int* amb_list, const int* amb_count, const float* amb_thr,
+                                       int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
+                                       int* ovf_list, int* ovf_count, const int32_t* orig, const int* two_list,
+                                       const int* two_count, const long long* state, void* stream) {
+  if (ldb < d) return PCB_EINVAL;
+  return resolve_screen<false>(P, n, d, P_b, ldb, C_b, C, k, C_aug, bstat, amb_list, amb_count, amb_thr, bypass,
+                               sub_b, cand, cand_n, labels, ovf_list, ovf_count, orig, two_list, two_count, state,
+                               stream);
 }
 
 // Row layout of the screen's inputs: P_b[s] = Pb0[perm[s]] (256-byte BF16
@@ -937,4 +961,157 @@ extern "C" int pcb_screen_relayout_bf16(const void* Pb0, const float* an0, const
                                            reinterpret_cast<uint4*>(P_b), anorm, danorm, orig);
   PCB_CHECK_LAUNCH();
   return 0;
+}
+
+// ---- E4M3 screening ("fp8s"): same kernels, operands in E4M3 ---------------------
+// One E4M3 pass (kind::f8f6f4, twice the BF16 rate) over p~ = e4m3(p sp) / sp
+// and c~ = e4m3(-2 c sc) / (-2 sc), power-of-two scales sp, sc chosen on the
+// device from max |p| (once) and max |c| (per update) so the largest entry maps
+// to <= 448; the MMA emits keys scaled by S = sp sc (bstat[4]), the augmented
+// BF16 step adds S (|c|^2 + OFF), and the bound (unscaled residual norms, E4M3
+// half-ulp 2^-4) is scaled by S in the epilogue.  Rows are 128-byte chunks like
+// the BF16 ones (viewed as BF16 pairs by the tensor maps).
+__device__ __forceinline__ uint8_t to_e4m3(float x) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(x), "f"(x));
+  return (uint8_t)(r & 0xFFu);
+}
+__device__ __forceinline__ float from_e4m3(uint8_t q) {
+  uint32_t r;
+  const uint16_t in = (uint16_t)q | (uint16_t)((uint16_t)q << 8);
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"(in));
+  return __half2float(__ushort_as_half((unsigned short)(r & 0xFFFFu)));
+}
+
+__global__ void maxabs_kernel(const float* __restrict__ X, int64_t count, float* __restrict__ out) {
+  float m = 0.0f;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(X[e]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_pos_f(out, m);
+}
+
+// power-of-two scale with maxabs * mult * scale <= 448 (E4M3 max finite)
+__global__ void e4m3_scale_kernel(const float* __restrict__ maxabs, float mult, float* __restrict__ scale,
+                                  float* __restrict__ S, const float* __restrict__ other) {
+  const float m = *maxabs * mult;
+  float sc = 1.0f;
+  if (m > 0.0f && isfinite(m)) {
+    sc = exp2f(floorf(log2f(448.0f / m)));
+    while (m * sc > 448.0f) sc *= 0.5f;
+    while (m * sc * 2.0f <= 448.0f) sc *= 2.0f;
+  }
+  *scale = sc;
+  if (S != nullptr) *S = sc * *other;
+}
+
+// Per row: E4M3 copy of mult * scale * x (row stride ld8 bytes, zero padded),
+// |x~| and |x - x~| (unscaled, rounded up), max |x|^2.
+__global__ void __launch_bounds__(256)
+row_e4m3_norms_kernel(const float* __restrict__ X, int64_t rows, int d, float* __restrict__ an, float* __restrict__ dan,
+                      float* __restrict__ maxsq, uint8_t* __restrict__ Xq, int ld8, const float* __restrict__ scale,
+                      float mult) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float s = *scale * mult, inv = 1.0f / s;  // exact: powers of two
+  float wmax = 0.0f;
+  for (int64_t i = w; i < rows; i += nw) {
+    double s_t = 0.0, s_d = 0.0, s_x = 0.0;
+    for (int t = lane; t < ld8; t += 32) {
+      const float x = t < d ? X[i * d + t] : 0.0f;
+      const uint8_t q = to_e4m3(x * s);
+      Xq[i * ld8 + t] = q;
+      const double h = (double)(from_e4m3(q) * inv);
+      const double dd = (double)x - h;
+      s_t = fma(h, h, s_t);
+      s_d = fma(dd, dd, s_d);
+      s_x = fma((double)x, (double)x, s_x);
+    }
+    s_t = warp_sum(s_t);
+    s_d = warp_sum(s_d);
+    s_x = warp_sum(s_x);
+    if (lane == 0) {
+      an[i] = (float)(sqrt(s_t) * (1.0 + 1e-6));
+      dan[i] = (float)(sqrt(s_d) * (1.0 + 1e-6));
+      wmax = fmaxf(wmax, (float)(s_x * (1.0 + 1e-6)));
+    }
+  }
+  if (lane == 0 && maxsq != nullptr) atomic_max_pos_f(maxsq, wmax);
+}
+
+extern "C" int pcb_screen_fp8_ld(int d) { return (d + 127) / 128 * 128; }
+
+// bstat (16 floats): [0] max|c~| [1] max|dc| [2] OFF [3] scratch [4] S = sp sc
+// [5] sp [6] max|p| [7] max|c| [8] sc
+extern "C" int pcb_screen_prep_points_fp8(const float* P, int64_t n, int d, int ld8, void* P_q, float* anorm,
+                                          float* danorm, float* bstat, void* stream) {
+  if (n < 1 || d < 1 || ld8 < d || ld8 % 128 || !P || !P_q || !anorm || !danorm || !bstat) return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bstat, 0, 16 * sizeof(float), st);
+  if (e != cudaSuccess) return (int)e;
+  const int g1 = (int)std::min<int64_t>((n * d + 255) / 256, (int64_t)sm_count() * 16);
+  maxabs_kernel<<<g1, 256, 0, st>>>(P, n * d, bstat + 6);
+  PCB_CHECK_LAUNCH();
+  e4m3_scale_kernel<<<1, 1, 0, st>>>(bstat + 6, 1.0f, bstat + 5, nullptr, nullptr);
+  PCB_CHECK_LAUNCH();
+  const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, (int64_t)sm_count() * 16);
+  row_e4m3_norms_kernel<<<grid, 256, 0, st>>>(P, n, d, anorm, danorm, bstat + 3, (uint8_t*)P_q, ld8, bstat + 5, 1.0f);
+  PCB_CHECK_LAUNCH();
+  screen_off_kernel<<<1, 1, 0, st>>>(bstat, bstat + 3);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_screen_prep_centroids_fp8(const float* C, const float* cnorm, int k, int d, int ld8, void* C_q,
+                                             void* C_aug, float* bnorm, float* dbnorm, float* bstat, void* stream) {
+  if (k < 1 || d < 1 || ld8 < d || ld8 % 128 || !C || !cnorm || !C_q || !C_aug || !bnorm || !dbnorm || !bstat)
+    return PCB_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bstat, 0, 2 * sizeof(float), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(bstat + 7, 0, sizeof(float), st);
+  if (e != cudaSuccess) return (int)e;
+  const int g1 = (int)std::min<int64_t>(((int64_t)k * d + 255) / 256, (int64_t)sm_count() * 4);
+  maxabs_kernel<<<g1, 256, 0, st>>>(C, (int64_t)k * d, bstat + 7);
+  PCB_CHECK_LAUNCH();
+  // B rows are e4m3(-2 c sc): the factor -2 is part of the scaled value
+  e4m3_scale_kernel<<<1, 1, 0, st>>>(bstat + 7, 2.0f, bstat + 8, bstat + 4, bstat + 5);
+  PCB_CHECK_LAUNCH();
+  row_e4m3_norms_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(C, k, d, bnorm, dbnorm, nullptr, (uint8_t*)C_q, ld8,
+                                                             bstat + 8, -2.0f);
+  PCB_CHECK_LAUNCH();
+  max2_bf16_kernel<<<1, 256, 0, st>>>(bnorm, dbnorm, k, bstat);
+  PCB_CHECK_LAUNCH();
+  const int kpad = (k + SB_KPAD - 1) / SB_KPAD * SB_KPAD;
+  centroid_aug_kernel<<<(kpad + 127) / 128, 128, 0, st>>>(cnorm, bstat, k, kpad, reinterpret_cast<__nv_bfloat16*>(C_aug));
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_assign_screen_fp8(const void* P_q, int64_t n, int ld8, const void* C_q, int k, const void* C_aug,
+                                     const float* anorm, const float* danorm, const float* bstat, int32_t* labels,
+                                     int* amb_list, int* amb_count, float* amb_thr, const int32_t* orig,
+                                     const int32_t* labels_prev, int* two_list, int* two_count,
+                                     const long long* state, void* stream) {
+  if (n < 1 || ld8 < 128 || ld8 % 128 || k < 1 || !P_q || !C_q || !C_aug || !anorm || !danorm || !bstat || !labels ||
+      !amb_list || !amb_count || !amb_thr)
+    return PCB_EINVAL;
+  if (n > INT32_MAX) return PCB_EUNSUP;
+  return dispatch_bf16<false, true>(ld8 / 2, (const __nv_bfloat16*)P_q, n, (const __nv_bfloat16*)C_q, k, anorm,
+                                    danorm, (const __nv_bfloat16*)C_aug, bstat, labels, amb_list, amb_count, amb_thr,
+                                    0, nullptr, nullptr, orig, labels_prev, two_list, two_count, state,
+                                    (cudaStream_t)stream);
+}
+
+extern "C" int pcb_resolve_screen_fp8(const float* P, int64_t n, int d, const void* P_q, int ld8, const void* C_q,
+                                      const float* C, int k, const void* C_aug, const float* bstat,
+                                      const int* amb_list, const int* amb_count, const float* amb_thr,
+                                      int64_t bypass, void* sub_q, int* cand, int* cand_n, int32_t* labels,
+                                      int* ovf_list, int* ovf_count, const int32_t* orig, const int* two_list,
+                                      const int* two_count, const long long* state, void* stream) {
+  if (ld8 < 128 || ld8 % 128 || ld8 < d) return PCB_EINVAL;
+  return resolve_screen<true>(P, n, d, P_q, ld8 / 2, C_q, C, k, C_aug, bstat, amb_list, amb_count, amb_thr, bypass,
+                              sub_q, cand, cand_n, labels, ovf_list, ovf_count, orig, two_list, two_count, state,
+                              stream);
 }

@@ -92,10 +92,10 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
     if variant not in L.VARIANTS:
         raise ValueError(f"unknown assign variant {variant!r}; expected one of {tuple(L.VARIANTS)}")
     if variant != "auto":
-        if dtype == _F64 and variant in ("tc3xtf32", "delta", "tc1xtf32s", "bf16s"):
+        if dtype == _F64 and variant in ("tc3xtf32", "delta", "tc1xtf32s", "bf16s", "fp8s"):
             raise ValueError(f"variant {variant!r} is float32-only")
-        if variant == "bf16s" and (d > 256 or k > SCREEN_KMAX):
-            raise ValueError(f"variant 'bf16s' needs d <= 256 and k <= {SCREEN_KMAX}")
+        if variant in ("bf16s", "fp8s") and (d > 256 or k > SCREEN_KMAX):
+            raise ValueError(f"variant {variant!r} needs d <= 256 and k <= {SCREEN_KMAX}")
         if variant == "rowreg" and d > 32:
             raise ValueError("variant 'rowreg' needs d <= 32")
         if variant == "tc1xtf32s" and k > SCREEN_KMAX:
@@ -107,7 +107,11 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
         return "tiled"
     if k > SCREEN_KMAX:
         return "tc3xtf32"
-    return "bf16s" if d <= 256 else "tc1xtf32s"
+    if d > 256:
+        return "tc1xtf32s"
+    # E4M3 rows are 128-byte chunks: for d <= 64 they would be half padding and
+    # cost what the BF16 pass costs, with a looser bound (more near-ties)
+    return "fp8s" if d > 64 else "bf16s"
 
 
 SCREEN_KMAX = 6144  # assign_screen.cu SC_KMAX
@@ -267,7 +271,7 @@ class LloydEngine(ShardSequence):
             self.P_hi = self.P_lo = self.C_hi = self.C_lo = None
             L.call(f"pcb_point_norms_{self.sfx}", _p(self.P), n, d, _p(self.pnorm), _stream())
             L.call(f"pcb_sum_squares_{self.sfx}", _p(self.P), n * d, _p(self.Q), _stream())
-            if self.variant in ("tc3xtf32", "tc1xtf32s", "bf16s"):
+            if self.variant in ("tc3xtf32", "tc1xtf32s", "bf16s", "fp8s"):
                 self.ld = (d + 31) // 32 * 32
                 self.C_hi = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
                 self.C_lo = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
@@ -291,13 +295,20 @@ class LloydEngine(ShardSequence):
                 self.P_r = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 L.call("pcb_screen_prep_points", _p(self.P), n, d, self.ld, _p(self.P_r), _p(self.anorm),
                        _p(self.danorm), _p(self.bstat), _stream())
-            if self.variant == "bf16s":
+            if self.variant in ("bf16s", "fp8s"):
                 # certified BF16 screening: RN BF16 copy of P, the bound's residual
                 # norms, pass-2 buffers for the ambiguous rows (capacity n) and the
                 # 3xTF32 resolver's compact hi/lo for rows with too many candidates
-                self.ldb = int(L.load().pcb_screen_bf16_ld(d))
+                # operand rows: BF16 (ldb elements) or E4M3 (ld8 bytes); ldb is the
+                # row length in BF16 units either way (what the tensor maps see)
+                self.q8 = self.variant == "fp8s"
+                if self.q8:
+                    self.ld8 = int(L.load().pcb_screen_fp8_ld(d))
+                    self.ldb = self.ld8 // 2
+                else:
+                    self.ldb = int(L.load().pcb_screen_bf16_ld(d))
                 ncand = int(L.load().pcb_screen_bf16_ncand())
-                self.P_b = torch.empty((n, self.ldb), dtype=torch.bfloat16, device=dev)
+                self.P_b = torch.empty((n, self.ldb), dtype=torch.bfloat16, device=dev)  # E4M3 bytes when q8
                 kpad = int(L.load().pcb_screen_bf16_kpad(kk))
                 self.C_b = torch.zeros((kpad, self.ldb), dtype=torch.bfloat16, device=dev)
                 self.C_aug = torch.zeros((kpad, int(L.load().pcb_screen_bf16_aug())), dtype=torch.bfloat16,
@@ -306,7 +317,7 @@ class LloydEngine(ShardSequence):
                 self.danorm = torch.empty(n, dtype=torch.float32, device=dev)
                 self.bnorm = torch.empty(kk, dtype=torch.float32, device=dev)
                 self.dbnorm = torch.empty(kk, dtype=torch.float32, device=dev)
-                self.bstat = torch.zeros(4, dtype=torch.float32, device=dev)
+                self.bstat = torch.zeros(16, dtype=torch.float32, device=dev)
                 self.amb_list = torch.empty(n, dtype=torch.int32, device=dev)
                 self.amb_count = torch.zeros(1, dtype=torch.int32, device=dev)
                 self.amb_thr = torch.empty(n, dtype=torch.float32, device=dev)
@@ -321,8 +332,12 @@ class LloydEngine(ShardSequence):
                 self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
-                L.call("pcb_screen_prep_points_bf16", _p(self.P), n, d, self.ldb, _p(self.P_b),
-                       _p(self.anorm), _p(self.danorm), _p(self.bstat), _stream())
+                if self.q8:
+                    L.call("pcb_screen_prep_points_fp8", _p(self.P), n, d, self.ld8, _p(self.P_b),
+                           _p(self.anorm), _p(self.danorm), _p(self.bstat), _stream())
+                else:
+                    L.call("pcb_screen_prep_points_bf16", _p(self.P), n, d, self.ldb, _p(self.P_b),
+                           _p(self.anorm), _p(self.danorm), _p(self.bstat), _stream())
                 self.orig = None  # row layout of P_b / anorm / danorm (None = original order)
 
     # -- centroid initialisation ------------------------------------------------
@@ -339,7 +354,7 @@ class LloydEngine(ShardSequence):
     RELAYOUT_AT = (1, 3)
 
     def _after_update(self, t: int) -> None:
-        if self.variant == "bf16s" and t in self.RELAYOUT_AT:
+        if self.variant in ("bf16s", "fp8s") and t in self.RELAYOUT_AT:
             self.relayout()
 
     def relayout(self) -> None:
@@ -355,9 +370,10 @@ class LloydEngine(ShardSequence):
                _p(self.perm), _p(self.P_b), _p(self.anorm), _p(self.danorm), _p(self.orig), _stream())
 
     def _screen_centroid_stats(self) -> None:
-        if self.variant == "bf16s":
-            L.call("pcb_screen_prep_centroids_bf16", _p(self.C), _p(self.cnorm), self.k, self.d, self.ldb,
-                   _p(self.C_b), _p(self.C_aug), _p(self.bnorm), _p(self.dbnorm), _p(self.bstat), _stream())
+        if self.variant in ("bf16s", "fp8s"):
+            L.call("pcb_screen_prep_centroids_fp8" if self.q8 else "pcb_screen_prep_centroids_bf16", _p(self.C),
+                   _p(self.cnorm), self.k, self.d, self.ld8 if self.q8 else self.ldb, _p(self.C_b), _p(self.C_aug),
+                   _p(self.bnorm), _p(self.dbnorm), _p(self.bstat), _stream())
         if self.variant == "tc1xtf32s":
             L.call("pcb_screen_prep_centroids", _p(self.C), self.k, self.d, _p(self.bnorm),
                    _p(self.dbnorm), _p(self.bstat), _stream())
@@ -437,16 +453,19 @@ class LloydEngine(ShardSequence):
         self.sums_valid = True
 
     def _assign(self, prev, new, acc, state) -> None:
-        if self.variant == "bf16s":
+        if self.variant in ("bf16s", "fp8s"):
             self.amb_count.zero_()
             self.two_count.zero_()
             self._kmark(0)
-            L.call("pcb_assign_screen_bf16", _p(self.P_b), self.n, self.ldb, _p(self.C_b), self.k,
+            ldq = self.ld8 if self.q8 else self.ldb
+            L.call("pcb_assign_screen_fp8" if self.q8 else "pcb_assign_screen_bf16", _p(self.P_b), self.n, ldq,
+                   _p(self.C_b), self.k,
                    _p(self.C_aug), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
                    _p(self.amb_list), _p(self.amb_count), _p(self.amb_thr), _p(self.orig), _p(prev),
                    _p(self.two_list), _p(self.two_count), _p(state), _stream())
             self._kmark(1)
-            L.call("pcb_resolve_screen_bf16", _p(self.P), self.n, self.d, _p(self.P_b), self.ldb,
+            L.call("pcb_resolve_screen_fp8" if self.q8 else "pcb_resolve_screen_bf16", _p(self.P), self.n,
+                   self.d, _p(self.P_b), ldq,
                    _p(self.C_b), _p(self.C), self.k, _p(self.C_aug), _p(self.bstat), _p(self.amb_list),
                    _p(self.amb_count), _p(self.amb_thr), self.bypass, _p(self.sub_b), _p(self.cand),
                    _p(self.cand_n), _p(new), _p(self.ovf_list), _p(self.ovf_count), _p(self.orig),
@@ -593,7 +612,7 @@ class LloydEngine(ShardSequence):
             xn = torch.empty(m, dtype=self.tdtype, device=self.dev)
             out = torch.empty(m, dtype=torch.int32, device=self.dev)
             L.call(f"pcb_point_norms_{self.sfx}", _p(Xt), m, self.d, _p(xn), _stream())
-            if self.variant in ("tc3xtf32", "tc1xtf32s", "bf16s"):
+            if self.variant in ("tc3xtf32", "tc1xtf32s", "bf16s", "fp8s"):
                 xh = torch.empty((m, self.ld), dtype=torch.float32, device=self.dev)
                 xl = torch.empty_like(xh)
                 L.call("pcb_split_tf32", _p(Xt), m, self.d, self.ld, _p(xh), _p(xl), _stream())

@@ -16,6 +16,12 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
+@pytest.fixture(params=["bf16s", "fp8s"])
+def screen_variant(request):
+    """Both certified screens: BF16 (kind::f16) and E4M3 (kind::f8f6f4)."""
+    return request.param
+
+
 @pytest.fixture(scope="module", autouse=True)
 def _need_cuda():
     if not torch.cuda.is_available():
@@ -34,12 +40,12 @@ def _exact(P, C):
 @pytest.mark.parametrize("n,d,k", [(1000, 40, 17), (777, 100, 300), (4096, 64, 64), (300, 33, 1),
                                    (5000, 128, 1024), (1500, 96, 129), (5000, 64, 4096),
                                    (3000, 256, 200), (2500, 200, 77), (20000, 128, 1024)])
-def test_bf16_lockstep_ragged_shapes(n, d, k):
+def test_bf16_lockstep_ragged_shapes(n, d, k, screen_variant):
     from paper_2501_05587_b200.engine import LloydEngine
     P = oracle.make_blobs(n, d, max(k, 1), seed=n + d)
     lab = oracle.init_assignments(n, k, 1)
     C = oracle.mean_centroids(P, lab, k)
-    eng = LloydEngine(P, k, variant="bf16s", max_iters=1)
+    eng = LloydEngine(P, k, variant=screen_variant, max_iters=1)
     pn = oracle.point_norms(P)
     for t in range(4):
         ref = oracle.lloyd_step(P, pn, C, lab, k)
@@ -49,7 +55,7 @@ def test_bf16_lockstep_ragged_shapes(n, d, k):
 
 
 @pytest.mark.parametrize("spread", [3.0, 0.3])
-def test_bf16_labels_are_exact_argmin(spread):
+def test_bf16_labels_are_exact_argmin(spread, screen_variant):
     """Certified rows and candidate-resolved rows carry the exact f64 argmin;
     only rows sent on to the 3xTF32 resolver may differ, and only inside the
     1e-5 gap exemption."""
@@ -58,7 +64,7 @@ def test_bf16_labels_are_exact_argmin(spread):
     n, d, k = 6000, 128, 512
     P = rng.normal(0, 3, size=(n, d)).astype(np.float32)
     C = (rng.normal(0, spread, size=(k, d)) + 1.0).astype(np.float32)
-    eng = LloydEngine(P, k, variant="bf16s", max_iters=1)
+    eng = LloydEngine(P, k, variant=screen_variant, max_iters=1)
     out = eng.step_from(C, np.zeros(n, dtype=np.int32))
     amb, ovf = int(eng.amb_count.item()), int(eng.ovf_count.item())
     exact, gap = _exact(P, C)
@@ -70,7 +76,7 @@ def test_bf16_labels_are_exact_argmin(spread):
     print(f"spread {spread}: ambiguous {amb}/{n}, overflow {ovf}")
 
 
-def test_bf16_duplicate_centroids_tie_to_lowest_index():
+def test_bf16_duplicate_centroids_tie_to_lowest_index(screen_variant):
     from paper_2501_05587_b200.engine import LloydEngine
     rng = make_rng(22)
     n, d, k = 3000, 64, 64
@@ -78,7 +84,7 @@ def test_bf16_duplicate_centroids_tie_to_lowest_index():
     C = rng.normal(0, 1, size=(k, d)).astype(np.float32)
     C[40] = C[7]
     C[63] = C[7]
-    eng = LloydEngine(P, k, variant="bf16s", max_iters=1)
+    eng = LloydEngine(P, k, variant=screen_variant, max_iters=1)
     out = eng.step_from(C, np.zeros(n, dtype=np.int32))
     assert not np.any(out["raw_labels"] == 40)
     assert not np.any(out["raw_labels"] == 63)
@@ -86,7 +92,7 @@ def test_bf16_duplicate_centroids_tie_to_lowest_index():
     np.testing.assert_array_equal(out["raw_labels"], exact)
 
 
-def test_bf16_candidate_overflow_goes_to_3xtf32():
+def test_bf16_candidate_overflow_goes_to_3xtf32(screen_variant):
     """A cluster of 12 near-identical centroids gives its points more
     candidates than the pass-2 list holds (8): those rows take the 3xTF32
     path, the rest stay exact."""
@@ -97,7 +103,7 @@ def test_bf16_candidate_overflow_goes_to_3xtf32():
     C[50:62] = C[50] + rng.normal(0, 1e-3, size=(12, d)).astype(np.float32)
     true = rng.integers(0, k, size=n)
     P = (C[true] + rng.normal(0, 1, size=(n, d))).astype(np.float32)
-    eng = LloydEngine(P, k, variant="bf16s", max_iters=1)
+    eng = LloydEngine(P, k, variant=screen_variant, max_iters=1)
     out = eng.step_from(C, np.zeros(n, dtype=np.int32))
     ovf = int(eng.ovf_count.item())
     assert ovf > 0
@@ -117,7 +123,7 @@ def test_bf16_candidate_overflow_goes_to_3xtf32():
     assert np.all(Dg - De <= 2.0 ** -20 * scale)
 
 
-def test_bf16_bypass_when_most_rows_ambiguous():
+def test_bf16_bypass_when_most_rows_ambiguous(screen_variant):
     """Centroids bunched near the global mean (as right after a random-label
     init at large n): most rows are ambiguous, the candidate pass is bypassed
     and every ambiguous row goes to the 3xTF32 resolver."""
@@ -127,7 +133,7 @@ def test_bf16_bypass_when_most_rows_ambiguous():
     P = oracle.make_blobs(n, d, k, seed=5)
     C = (P.mean(0)[None, :] + rng.normal(0, 1e-2, size=(k, d))).astype(np.float32)
     lab = rng.integers(0, k, size=n).astype(np.int32)
-    eng = LloydEngine(P, k, variant="bf16s", max_iters=1)
+    eng = LloydEngine(P, k, variant=screen_variant, max_iters=1)
     ref = oracle.lloyd_step(P, oracle.point_norms(P), C, lab, k)
     gpu = eng.step_from(C, lab)
     assert int(eng.amb_count.item()) > n // 4
@@ -135,23 +141,23 @@ def test_bf16_bypass_when_most_rows_ambiguous():
     check_step(P, C, lab, k, gpu, ref=ref, what="bf16s bypass")
 
 
-def test_bf16_full_run_matches_reference():
+def test_bf16_full_run_matches_reference(screen_variant):
     import paper_2501_05587_b200 as pcb
     P = oracle.make_blobs(20000, 128, 64, seed=4)
-    a = pcb.run_lloyd(P, pcb.KKMeansConfig(k=64, max_iters=8, variant="bf16s"))
+    a = pcb.run_lloyd(P, pcb.KKMeansConfig(k=64, max_iters=8, variant=screen_variant))
     ref = oracle.run_lloyd(P, 64, max_iters=8)
     np.testing.assert_allclose(a.objective_history, ref.objective_history, rtol=1e-6)
     np.testing.assert_array_equal(a.labels, ref.labels)
 
 
-def test_bf16_predict_matches_assignment():
+def test_bf16_predict_matches_assignment(screen_variant):
     import paper_2501_05587_b200 as pcb
     P = oracle.make_blobs(5000, 64, 32, seed=9)
-    est = pcb.KernelKMeans(n_clusters=32, algorithm="lloyd", max_iter=5, variant="bf16s").fit(P)
+    est = pcb.KernelKMeans(n_clusters=32, algorithm="lloyd", max_iter=5, variant=screen_variant).fit(P)
     np.testing.assert_array_equal(est.predict(P[:1000]), est.labels_[:1000])
 
 
-def test_bf16_relayout_keeps_results():
+def test_bf16_relayout_keeps_results(screen_variant):
     """Labels, objective and centroids do not depend on the screen's row
     layout (pcb_screen_relayout_bf16): lockstep steps before and after the
     rows are re-laid out by label agree bit for bit."""
@@ -164,7 +170,7 @@ def test_bf16_relayout_keeps_results():
     for _ in range(3):
         ref = oracle.lloyd_step(P, pn, C, lab, k)
         C, lab = ref.centroids, ref.labels
-    eng = LloydEngine(P, k, variant="bf16s", max_iters=1)
+    eng = LloydEngine(P, k, variant=screen_variant, max_iters=1)
     a = eng.step_from(C, lab)
     eng.relayout()  # perm of the step just taken: rows grouped by label
     assert eng.orig is not None

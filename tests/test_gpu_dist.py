@@ -43,7 +43,7 @@ def _run_world(case, world, tmp_path):
     return parts, labels
 
 
-@pytest.mark.parametrize("variant,n,d,k,world", [("bf16s", 24000, 96, 40, 2), ("rowreg", 30000, 8, 16, 3),
+@pytest.mark.parametrize("variant,n,d,k,world", [("fp8s", 24000, 96, 40, 2), ("bf16s", 20000, 64, 30, 2), ("rowreg", 30000, 8, 16, 3),
                                                  ("tc3xtf32", 12000, 64, 24, 2)])
 def test_multirank_matches_single_rank(variant, n, d, k, world, tmp_path):
     import paper_2501_05587_b200 as pcb

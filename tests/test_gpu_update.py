@@ -33,7 +33,7 @@ def _run(P, k, update, variant="auto", iters=20, dtype=np.float32):
     return out, modes, cents, eng
 
 
-@pytest.mark.parametrize("variant,n,d,k", [("bf16s", 40000, 128, 64), ("rowreg", 30000, 16, 32),
+@pytest.mark.parametrize("variant,n,d,k", [("bf16s", 40000, 128, 64), ("fp8s", 40000, 128, 64), ("rowreg", 30000, 16, 32),
                                            ("tiled", 20000, 48, 40), ("tc3xtf32", 20000, 64, 50)])
 def test_delta_matches_full_update(variant, n, d, k):
     P = oracle.make_blobs(n, d, k, seed=3)
