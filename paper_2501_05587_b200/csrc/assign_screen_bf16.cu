@@ -46,7 +46,7 @@ constexpr int SB_BN = 128;
 constexpr int SB_STAGES = 4;
 constexpr int SB_THREADS = 384;
 constexpr int SB_BKE = 64;      // BF16 elements per 128-byte swizzle row
-constexpr int SB_NCAND = 8;     // candidate slots per ambiguous row (pass 2)
+constexpr int SB_NCAND = 64;    // candidate slots per ambiguous row (pass 2)
 constexpr int SB_AUG = 16;      // augmented K columns per centroid: |c|^2 + OFF as 3 BF16 pieces, 13 zeros
 constexpr int SB_KPAD = 256;    // centroid rows of C_b / C_aug are padded to a multiple of the widest tile
 
@@ -674,6 +674,10 @@ __device__ __forceinline__ float4 load4(const float* __restrict__ rowp, int q, i
   return make_float4(t < d ? rowp[t] : 0.0f, t + 1 < d ? rowp[t + 1] : 0.0f, t + 2 < d ? rowp[t + 2] : 0.0f,
                      t + 3 < d ? rowp[t + 3] : 0.0f);
 }
+__device__ __forceinline__ float dist4f(float4 a, float4 b, float s) {
+  const float e0 = a.x - b.x, e1 = a.y - b.y, e2 = a.z - b.z, e3 = a.w - b.w;
+  return fmaf(e3, e3, fmaf(e2, e2, fmaf(e1, e1, fmaf(e0, e0, s))));
+}
 __device__ __forceinline__ double dist4(float4 a, float4 b, double s) {
   const double e0 = (double)a.x - (double)b.x, e1 = (double)a.y - (double)b.y;
   const double e2 = (double)a.z - (double)b.z, e3 = (double)a.w - (double)b.w;
@@ -685,7 +689,7 @@ __device__ __forceinline__ double dist4(float4 a, float4 b, double s) {
 // usable candidate list (too many candidates, or the bypass) are appended to
 // the overflow list for the 3xTF32 resolver.
 template <int DQ>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, DQ <= 4 ? 4 : 2)  // latency-bound: keep >= 32 warps per SM
 screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict__ C,
                     const int* __restrict__ list, const int* __restrict__ count, int64_t bypass,
                     const int* __restrict__ cand, const int* __restrict__ cand_n, int32_t* __restrict__ labels,
@@ -733,47 +737,63 @@ screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict_
     if (ovf) nc = 0;
     const int ncmax = __reduce_max_sync(0xffffffffu, nc);
     // all candidate ids at once (two 16-byte loads), the point row as float4
-    int cj[SB_NCAND];
-    if (is2) {
-      cj[0] = valid ? two_list[3 * r2i + 1] : 0;
-      cj[1] = valid ? two_list[3 * r2i + 2] : 0;
-#pragma unroll
-      for (int i = 2; i < SB_NCAND; ++i) cj[i] = 0;
-    } else {
-      const int4* cp = reinterpret_cast<const int4*>(cand + r * SB_NCAND);
-      const int4 c0 = nc > 0 ? cp[0] : make_int4(0, 0, 0, 0);
-      const int4 c1 = nc > 4 ? cp[1] : make_int4(0, 0, 0, 0);
-      cj[0] = c0.x; cj[1] = c0.y; cj[2] = c0.z; cj[3] = c0.w;
-      cj[4] = c1.x; cj[5] = c1.y; cj[6] = c1.z; cj[7] = c1.w;
-    }
+    // candidate ids straight from the lists (L2) as the loop needs them
+    auto cand_id = [&](int c) -> int {
+      return is2 ? two_list[3 * r2i + 1 + c] : cand[r * SB_NCAND + c];
+    };
     float4 p[DQ];
 #pragma unroll
     for (int q = 0; q < DQ; ++q) p[q] = nc > 0 ? load4(P + (int64_t)row * d, sub + 8 * q, d) : make_float4(0, 0, 0, 0);
-    double best = 0.0;
+    // f32 distances first: sum (p - c)^2 has relative error <= (d + 8) 2^-23
+    // (positive terms); the winner is certain unless the runner-up is within
+    // that margin — then (rarely) the row is redone in f64, ties included
+    const float brel = (float)(d + 8) * 0x1p-23f;
+    float f1 = 3.4e38f, f2 = 3.4e38f;
     int bj = -1;
-#pragma unroll
-    for (int c = 0; c < SB_NCAND; c += 2) {
-      if (c >= ncmax) break;
-      const int ja = c < nc ? cj[c] : -1, jb = c + 1 < nc ? cj[c + 1] : -1;
+    for (int c = 0; c < ncmax; c += 2) {
+      const int ja = c < nc ? cand_id(c) : -1, jb = c + 1 < nc ? cand_id(c + 1) : -1;
       float4 xa[DQ], xb[DQ];
 #pragma unroll
       for (int q = 0; q < DQ; ++q) {
         xa[q] = ja >= 0 ? load4(C + (int64_t)ja * d, sub + 8 * q, d) : make_float4(0, 0, 0, 0);
         xb[q] = jb >= 0 ? load4(C + (int64_t)jb * d, sub + 8 * q, d) : make_float4(0, 0, 0, 0);
       }
-      double sa = 0.0, sb = 0.0;
+      float sa = 0.0f, sb = 0.0f;
 #pragma unroll
       for (int q = 0; q < DQ; ++q) {
-        sa = dist4(p[q], xa[q], sa);
-        sb = dist4(p[q], xb[q], sb);
+        sa = dist4f(p[q], xa[q], sa);
+        sb = dist4f(p[q], xb[q], sb);
       }
 #pragma unroll
       for (int o = 4; o > 0; o >>= 1) {
         sa += __shfl_xor_sync(0xffffffffu, sa, o);
         sb += __shfl_xor_sync(0xffffffffu, sb, o);
       }
-      if (ja >= 0 && (bj < 0 || sa < best || (sa == best && ja < bj))) { best = sa; bj = ja; }
-      if (jb >= 0 && (bj < 0 || sb < best || (sb == best && jb < bj))) { best = sb; bj = jb; }
+      if (ja >= 0) {
+        if (sa < f1) { f2 = f1; f1 = sa; bj = ja; } else if (sa < f2) { f2 = sa; }
+      }
+      if (jb >= 0) {
+        if (sb < f1) { f2 = f1; f1 = sb; bj = jb; } else if (sb < f2) { f2 = sb; }
+      }
+    }
+    const bool unsure = nc > 1 && f2 * (1.0f - brel) <= f1 * (1.0f + brel);
+    if (__any_sync(0xffffffffu, unsure)) {
+      // exact f64 pass for the rows whose f32 margin is too thin
+      double best = 0.0;
+      int bj64 = -1;
+      for (int c = 0; c < ncmax; ++c) {
+        const int j = (unsure && c < nc) ? cand_id(c) : -1;
+        double s64 = 0.0;
+        if (j >= 0) {
+#pragma unroll
+          for (int q = 0; q < DQ; ++q) s64 = dist4(p[q], load4(C + (int64_t)j * d, sub + 8 * q, d), s64);
+        }
+        s64 += __shfl_xor_sync(0xffffffffu, s64, 4);
+        s64 += __shfl_xor_sync(0xffffffffu, s64, 2);
+        s64 += __shfl_xor_sync(0xffffffffu, s64, 1);
+        if (j >= 0 && (bj64 < 0 || s64 < best || (s64 == best && j < bj64))) { best = s64; bj64 = j; }
+      }
+      if (unsure) bj = bj64;
     }
     if (sub == 0 && bj >= 0) labels[row] = bj;
   }

@@ -93,15 +93,15 @@ def test_bf16_duplicate_centroids_tie_to_lowest_index(screen_variant):
 
 
 def test_bf16_candidate_overflow_goes_to_3xtf32(screen_variant):
-    """A cluster of 12 near-identical centroids gives its points more
-    candidates than the pass-2 list holds (8): those rows take the 3xTF32
+    """A cluster of 70 near-identical centroids gives its points more
+    candidates than the pass-2 list holds (64): those rows take the 3xTF32
     path, the rest stay exact."""
     from paper_2501_05587_b200.engine import LloydEngine
     rng = make_rng(23)
-    n, d, k = 4000, 96, 64
+    n, d, k = 4000, 96, 200
     C = rng.uniform(-10, 10, size=(k, d)).astype(np.float32)
-    C[50:62] = C[50] + rng.normal(0, 1e-3, size=(12, d)).astype(np.float32)
-    true = rng.integers(0, k, size=n)
+    C[:70] = C[0] + rng.normal(0, 1e-3, size=(70, d)).astype(np.float32)
+    true = np.where(rng.random(n) < 0.1, 0, rng.integers(70, k, size=n))
     P = (C[true] + rng.normal(0, 1, size=(n, d))).astype(np.float32)
     eng = LloydEngine(P, k, variant=screen_variant, max_iters=1)
     out = eng.step_from(C, np.zeros(n, dtype=np.int32))
