@@ -370,22 +370,32 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     // per-row inputs of the next pair are fetched one pair ahead: their DRAM
     // latency would otherwise hold both TMEM buffers (and the MMAs) at every
     // pair boundary
+    // Loaded values are kept raw (32-bit) until used: a conversion right after
+    // the load (e.g. sign-extending a row id) would wait for it at once.  The
+    // first column (orig -> previous label) is a dependent pair of loads: the
+    // second one is issued a chunk later (fetch_pair_b).
     float an_nx = 0.0f, dan_nx = 0.0f;
-    int fc_nx = 0;
-    int64_t out_nx = 0;
+    int fc_nx = 0, out_nx = 0, mid_nx = 0;
     auto fetch_pair = [&](int64_t p) {
       const int64_t rr = p * 256 + r_in < n ? p * 256 + r_in : n - 1;
-      out_nx = (!CAND && orig != nullptr) ? (int64_t)orig[rr] : rr;
+      out_nx = (!CAND && orig != nullptr) ? orig[rr] : (int)rr;
       if (CAND) {
         an_nx = amb_thr[rr];
       } else {
         an_nx = anorm[rr];
         dan_nx = danorm[rr];
       }
-      fc_nx = sb_first_col(lprev, orig, p, n, k);
+      int64_t rm = p * 256 + 128;
+      if (rm >= n) rm = p * 256;
+      mid_nx = (lprev != nullptr && orig != nullptr) ? orig[rm] : (int)rm;
+    };
+    auto fetch_pair_b = [&]() {
+      const int l = lprev != nullptr ? lprev[mid_nx] : 0;
+      fc_nx = (l >= 0 && l < k) ? l : 0;
     };
     if (blockIdx.x < npairs) {
       fetch_pair(blockIdx.x);
+      fetch_pair_b();
       ptx::mbar_wait(&tfull[tbar()], 0);
       ptx::tc_fence_after();
       ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * ((fc_nx % BN) / 32), vA);
@@ -403,7 +413,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         big = 64.0f / twoE;
       }
       const int t0 = fc_nx / BN, q0 = (fc_nx % BN) / 32;
-      const int64_t out_row = out_nx;  // original row id (label store)
+      const int out_row = out_nx;  // original row id (label store)
       if (!last_pair) fetch_pair(pr + gridDim.x);
       float R1 = 3.4e38f, R2 = 3.4e38f, cnt = 0.0f;
       int r1 = 0, r2 = 0;
@@ -415,6 +425,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           uint32_t (&cur)[32] = (q & 1) ? vB : vA;
           uint32_t (&nxt)[32] = (q & 1) ? vA : vB;
           ptx::tmem_wait_ld(cur);
+          if (nt == 0 && q == CH - 1 && !last_pair) fetch_pair_b();  // its first load was issued a tile ago
           const int qe = nt == 0 ? ((q + q0) & (CH - 1)) : q;  // chunk of the tile held by cur
           if (q < CH - 1) {
             const int qn = nt == 0 ? ((q + 1 + q0) & (CH - 1)) : q + 1;
