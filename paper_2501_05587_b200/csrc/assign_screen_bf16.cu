@@ -473,10 +473,14 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             // chunks of most warps take this path.
             const float thr_skip = (R1 + twoE + 0x1p-16f * fabsf(R1)) * (1.0f + 0x1p-16f);
             const float (&km)[32] = v;  // the MMA produced the keys (augmented K step)
-            float mm = fmin3(km[0], km[1], km[2]);
+            // minimum of the chunk as a depth-4 tree of 3-input mins (a chain
+            // of 16 dependent FMNMX3 sits on every chunk's critical path)
+            float t[11];
 #pragma unroll
-            for (int i = 3; i < 31; i += 2) mm = fmin3(mm, km[i], km[i + 1]);
-            mm = fminf(mm, km[31]);
+            for (int i = 0; i < 10; ++i) t[i] = fmin3(km[3 * i], km[3 * i + 1], km[3 * i + 2]);
+            t[10] = fminf(km[30], km[31]);
+            const float mm = fminf(fmin3(fmin3(t[0], t[1], t[2]), fmin3(t[3], t[4], t[5]), fmin3(t[6], t[7], t[8])),
+                                   fminf(t[9], t[10]));
 #if defined(PCB_EXP) && PCB_EXP == 5
             // experiment build: skip-path cost only (results invalid)
             if (__any_sync(0xffffffffu, mm <= thr_skip)) R1 = fminf(R1, mm);
