@@ -57,16 +57,19 @@ constexpr int SB_KPAD = 256;    // centroid rows of C_b / C_aug are padded to a 
 //            one 256-column accumulator per row tile; the MMAs of the two row
 //            tiles alternate, so each row tile's 4 epilogue warps (full rows,
 //            8 chunks per tile) overlap the other row tile's MMAs.
-template <int NKC, bool W = false>
+// RT = row tiles of 128 resident per CTA (2; 1 for rows longer than 4 chunks,
+// whose operand tiles would not fit twice).
+template <int NKC, bool W = false, int RT = 2>
 struct SbCfg {
+  static constexpr int kRows = 128 * RT;                            // rows per "pair"
   static constexpr int kBN = W ? 256 : 128;                         // centroids per tile
   static constexpr int kChunks = kBN / 32;                          // epilogue chunks per tile
   static constexpr int kStages = W ? 3 : SB_STAGES;
   static constexpr uint32_t kTileBytes = 128 * 128;                 // 128 rows x 128 B
   // resident A (2 row tiles), double-buffered across row pairs when it fits
   // (the next pair's rows load while the current pair's MMAs run)
-  static constexpr int kAStages = (!W && NKC <= 2) ? 2 : 1;
-  static constexpr uint32_t kAPair = 2 * NKC * kTileBytes;
+  static constexpr int kAStages = (!W && RT * NKC <= 4) ? 2 : 1;
+  static constexpr uint32_t kAPair = RT * NKC * kTileBytes;
   static constexpr uint32_t kABytes = kAStages * kAPair;
   static constexpr uint32_t kBBytes = kBN * 128;                    // centroid chunk per B stage
   static constexpr uint32_t kAugBytes = kBN * 32;                   // + the K=16 augmented columns
@@ -76,6 +79,7 @@ struct SbCfg {
   static constexpr uint32_t kSmem = 1024 + kABytes + kStages * kStageB + kAAug + kBarBytes;
   static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
   static_assert(!W || NKC <= 2, "the wide layout keeps a whole tile's chunks in the ring");
+  static_assert(!W || RT == 2, "the wide layout alternates two row tiles");
 };
 
 // First centroid column of a row pair: the previous label of the pair's
@@ -85,10 +89,11 @@ struct SbCfg {
 // the running minimum is set at once and the other chunks are skipped.
 // Visiting order never changes results (certified rows have one candidate;
 // ambiguous rows are resolved exactly, lowest index on ties).
-__device__ __forceinline__ int sb_first_col(const int32_t* lprev, const int32_t* orig, int64_t pr, int64_t n, int k) {
+__device__ __forceinline__ int sb_first_col(const int32_t* lprev, const int32_t* orig, int64_t pr, int64_t n, int k,
+                                            int rows) {
   if (lprev == nullptr) return 0;
-  int64_t r = pr * 256 + 128;
-  if (r >= n) r = pr * 256;
+  int64_t r = pr * rows + rows / 2;
+  if (r >= n) r = pr * rows;
   const int l = lprev[orig != nullptr ? (int64_t)orig[r] : r];
   return (l >= 0 && l < k) ? l : 0;
 }
@@ -101,7 +106,7 @@ __device__ __forceinline__ int64_t sb_rows(int64_t n, const int* amb_count, int6
   return c > bypass ? 0 : c;
 }
 
-template <int NKC, bool CAND, bool W, bool F8>
+template <int NKC, bool CAND, bool W, bool F8, int RT>
 __global__ void __launch_bounds__(SB_THREADS, 1)
 assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                           const __grid_constant__ CUtensorMap tm_baug, const float* __restrict__ anorm,
@@ -111,8 +116,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
                           int* __restrict__ cand_n, const int32_t* __restrict__ orig,
                           const int32_t* __restrict__ lprev, int* __restrict__ two_list, int* __restrict__ two_count,
                           const long long* __restrict__ state) {
-  using Cfg = SbCfg<NKC, W>;
-  constexpr int BN = Cfg::kBN, CH = Cfg::kChunks, STAGES = Cfg::kStages;
+  using Cfg = SbCfg<NKC, W, RT>;
+  constexpr int BN = Cfg::kBN, CH = Cfg::kChunks, STAGES = Cfg::kStages, PR = Cfg::kRows;
   if (stopped(state)) return;
   const int64_t n = CAND ? sb_rows(n_in, amb_count, bypass) : n_in;
   if (n == 0) return;
@@ -162,7 +167,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], W ? 128 : 256);
+      ptx::mbar_init(&tempty[b], W ? 128 : 128 * RT);
     }
     ptx::fence_barrier_init();
   }
@@ -171,7 +176,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t npairs = (n + 255) / 256;
+  const int64_t npairs = (n + PR - 1) / PR;
 
   if (warp == 0) {
     // ---------------- A producer: both row tiles, chunk by chunk ----------------
@@ -183,11 +188,12 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         uint8_t* sAp = sA + ab * Cfg::kAPair;
         if (it >= AS) ptx::mbar_wait(&aempty[ab * NKC + c], (uint32_t)((it / AS - 1) & 1));
         if (ptx::elect_one()) {
-          ptx::mbar_expect_tx(&afull[ab * NKC + c], 2 * Cfg::kTileBytes);
+          ptx::mbar_expect_tx(&afull[ab * NKC + c], RT * Cfg::kTileBytes);
           ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (0 * NKC + c) * Cfg::kTileBytes, c * SB_BKE,
-                           (int)(pr * 256), pol);
-          ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (1 * NKC + c) * Cfg::kTileBytes, c * SB_BKE,
-                           (int)(pr * 256 + 128), pol);
+                           (int)(pr * PR), pol);
+          if (RT == 2)
+            ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (1 * NKC + c) * Cfg::kTileBytes, c * SB_BKE,
+                             (int)(pr * PR + 128), pol);
         }
         __syncwarp();
       }
@@ -199,10 +205,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     uint32_t phase = 0;
     // first tile of the next pair fetched one pair ahead (two dependent
     // global loads would otherwise stall the ring at every pair boundary)
-    int t0_nx = blockIdx.x < npairs ? sb_first_col(lprev, orig, blockIdx.x, n, k) / BN : 0;
+    int t0_nx = blockIdx.x < npairs ? sb_first_col(lprev, orig, blockIdx.x, n, k, PR) / BN : 0;
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
       const int t0 = t0_nx;
-      if (pr + gridDim.x < npairs) t0_nx = sb_first_col(lprev, orig, pr + gridDim.x, n, k) / BN;
+      if (pr + gridDim.x < npairs) t0_nx = sb_first_col(lprev, orig, pr + gridDim.x, n, k, PR) / BN;
       for (int nt = 0; nt < ntiles; ++nt) {
         const int tile = nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles;
         for (int c = 0; c < NKC; ++c) {
@@ -315,14 +321,14 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             for (int ks = 0; ks < 4; ++ks) {           // 4 x K=16 per 128-byte chunk
               const uint64_t off = (uint64_t)(ks * 32) >> 4;
               mma_main(d0, a0 + off, bd + off, (c | ks) != 0);
-              mma_main(d0 + 128, a1 + off, bd + off, (c | ks) != 0);
+              if (RT == 2) mma_main(d0 + 128, a1 + off, bd + off, (c | ks) != 0);
             }
             if (c + 1 == NKC) {  // augmented K step: + (|c|^2 + OFF) in three BF16 pieces
               const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
               const uint64_t ba = ptx::sdesc_k_none(ptx::smem_u32(sB + stage * Cfg::kStageB + Cfg::kBBytes),
                                                     BN * 16, 128);
               ptx::umma_f16(d0, aa, ba, idesc, 1u);
-              ptx::umma_f16(d0 + 128, aa, ba, idesc, 1u);
+              if (RT == 2) ptx::umma_f16(d0 + 128, aa, ba, idesc, 1u);
             }
             ptx::umma_commit(&empty[stage]);
             if (nt + 1 == ntiles) ptx::umma_commit(&aempty[ab * NKC + c]);  // A chunk free again
@@ -337,7 +343,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       }
     }
     }  // !W
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 4 + 4 * RT) {
     // ---------------- epilogue: warp (g, h) = lanes 32g.. of row tile h ----------------
     const int g = warp & 3, h = (warp - 4) >> 2;
     const float Bmax = bstat[0], dBmax = bstat[1];
@@ -377,7 +383,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     float an_nx = 0.0f, dan_nx = 0.0f;
     int fc_nx = 0, out_nx = 0, mid_nx = 0;
     auto fetch_pair = [&](int64_t p) {
-      const int64_t rr = p * 256 + r_in < n ? p * 256 + r_in : n - 1;
+      const int64_t rr = p * PR + r_in < n ? p * PR + r_in : n - 1;
       out_nx = (!CAND && orig != nullptr) ? orig[rr] : (int)rr;
       if (CAND) {
         an_nx = amb_thr[rr];
@@ -385,8 +391,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         an_nx = anorm[rr];
         dan_nx = danorm[rr];
       }
-      int64_t rm = p * 256 + 128;
-      if (rm >= n) rm = p * 256;
+      int64_t rm = p * PR + PR / 2;
+      if (rm >= n) rm = p * PR;
       mid_nx = (lprev != nullptr && orig != nullptr) ? orig[rm] : (int)rm;
     };
     auto fetch_pair_b = [&]() {
@@ -401,7 +407,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * ((fc_nx % BN) / 32), vA);
     }
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
-      const int64_t row = pr * 256 + r_in;
+      const int64_t row = pr * PR + r_in;
       const int64_t rc = row < n ? row : n - 1;
       const bool last_pair = pr + gridDim.x >= npairs;
       float twoE = 0.0f, big = 0.0f, thr = 0.0f;
@@ -562,23 +568,23 @@ static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t row
   return r == CUDA_SUCCESS ? 0 : PCB_EINVAL;
 }
 
-template <int NKC, bool CAND, bool W, bool F8>
+template <int NKC, bool CAND, bool W, bool F8, int RT = 2>
 static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                               const float* an, const float* dan, const __nv_bfloat16* Baug, const float* bstat,
                               int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
                               int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev,
                               int* two_list, int* two_count, const long long* state, cudaStream_t st) {
-  using Cfg = SbCfg<NKC, W>;
+  using Cfg = SbCfg<NKC, W, RT>;
   CUtensorMap ta, tb, tg;
   int rc;
   const int64_t kpad = (k + SB_KPAD - 1) / SB_KPAD * SB_KPAD;  // B / Baug hold kpad rows (padding: key = +huge)
   if ((rc = make_tmap_bf16(&ta, A, n, NKC * SB_BKE, 128))) return rc;  // 128-byte chunks: F8 rows viewed as BF16 pairs
   if ((rc = make_tmap_bf16(&tb, B, kpad, NKC * SB_BKE, Cfg::kBN))) return rc;
   if ((rc = make_tmap_bf16(&tg, Baug, kpad, SB_AUG, Cfg::kBN, 8, CU_TENSOR_MAP_SWIZZLE_NONE))) return rc;
-  auto kern = assign_screen_bf16_kernel<NKC, CAND, W, F8>;
+  auto kern = assign_screen_bf16_kernel<NKC, CAND, W, F8, RT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   if (e != cudaSuccess) return (int)e;
-  const int64_t npairs = (n + 255) / 256;
+  const int64_t npairs = (n + Cfg::kRows - 1) / Cfg::kRows;
   const int grid = (int)std::min<int64_t>(npairs, (int64_t)sm_count());
   kern<<<grid, SB_THREADS, Cfg::kSmem, st>>>(ta, tb, tg, an, dan, bstat, n, k, labels, amb_list, amb_count,
                                              amb_thr, bypass, cand, cand_n, orig, lprev, two_list, two_count, state);
@@ -605,6 +611,16 @@ static int dispatch_bf16(int ldb, const __nv_bfloat16* A, int64_t n, const __nv_
     case 2: if (narrow) { PCB_SB_CASE(2, false) } else { PCB_SB_CASE(2, true) }
     case 3: PCB_SB_CASE(3, false)
     case 4: PCB_SB_CASE(4, false)
+#define PCB_SB_CASE1(N)                                                                                     \
+    return launch_screen_bf16<N, CAND, false, F8, 1>(A, n, B, k, an, dan, Baug, bstat, labels, amb_list,    \
+                                                     amb_count, amb_thr, bypass, cand, cand_n, orig, lprev,  \
+                                                     two_list, two_count, state, st);
+    // longer rows: one resident row tile of 128 (the operand chunks of two would not fit)
+    case 5: PCB_SB_CASE1(5)
+    case 6: PCB_SB_CASE1(6)
+    case 7: PCB_SB_CASE1(7)
+    case 8: PCB_SB_CASE1(8)
+#undef PCB_SB_CASE1
     default: return PCB_EUNSUP;
   }
 #undef PCB_SB_CASE
@@ -678,6 +694,59 @@ gather_rows_bf16(const __nv_bfloat16* __restrict__ Xb, int ldb, const int* __res
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / per, q = e - r * per;
     dst[r * per + q] = src[(int64_t)list[r] * per + q];
+  }
+}
+
+// Rows longer than 256: one warp per ambiguous row, lanes over d, exact f64
+// distances to its candidates (same lists, ties to the lowest index).
+__global__ void __launch_bounds__(256)
+screen_exact_wide_kernel(const float* __restrict__ P, int d, const float* __restrict__ C,
+                         const int* __restrict__ list, const int* __restrict__ count, int64_t bypass,
+                         const int* __restrict__ cand, const int* __restrict__ cand_n, int32_t* __restrict__ labels,
+                         int* __restrict__ ovf_list, int* __restrict__ ovf_count, const int32_t* __restrict__ orig,
+                         const int* __restrict__ two_list, const int* __restrict__ two_count,
+                         const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int64_t cnt_amb = *count;
+  const int64_t cnt2 = two_count != nullptr ? *two_count : 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool bypassed = cnt_amb > bypass;
+  if (bypassed) {
+    for (int64_t b0 = w0 * 32; b0 < cnt_amb; b0 += nw * 32) {
+      const int64_t r = b0 + lane;
+      const bool ok = r < cnt_amb;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      int b = 0;
+      if (lane == 0) b = atomicAdd(ovf_count, __popc(m));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (ok) ovf_list[b + __popc(m & ((1u << lane) - 1u))] = orig != nullptr ? orig[list[r]] : list[r];
+    }
+  }
+  const int64_t cntA = bypassed ? 0 : cnt_amb;
+  for (int64_t r = w0; r < cntA + cnt2; r += nw) {
+    const bool is2 = r >= cntA;
+    const int64_t r2i = r - cntA;
+    const int row = is2 ? two_list[3 * r2i] : (orig != nullptr ? orig[list[r]] : list[r]);
+    const int nc = is2 ? 2 : cand_n[r];
+    if (nc < 1 || nc > SB_NCAND) {
+      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = row;
+      continue;
+    }
+    double best = 0.0;
+    int bj = -1;
+    for (int c = 0; c < nc; ++c) {
+      const int j = is2 ? two_list[3 * r2i + 1 + c] : cand[r * SB_NCAND + c];
+      double s = 0.0;
+      for (int t = lane; t < d; t += 32) {
+        const double e = (double)P[(int64_t)row * d + t] - (double)C[(int64_t)j * d + t];
+        s = fma(e, e, s);
+      }
+      s = warp_sum(s);
+      if (bj < 0 || s < best || (s == best && j < bj)) { best = s; bj = j; }
+    }
+    if (lane == 0) labels[row] = bj;
   }
 }
 
@@ -917,7 +986,6 @@ static int resolve_screen(const float* P, int64_t n, int d, const void* P_b, int
   if (n < 1 || d < 1 || k < 1 || ldb % SB_BKE || !P || !P_b || !C_b || !C || !C_aug || !bstat ||
       !amb_list || !amb_count || !amb_thr || !sub_b || !cand || !cand_n || !labels || !ovf_list || !ovf_count)
     return PCB_EINVAL;
-  if (d > 256) return PCB_EUNSUP;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(ovf_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return (int)e;
@@ -941,7 +1009,8 @@ static int resolve_screen(const float* P, int64_t n, int d, const void* P_b, int
   PCB_EX_CASE(2)
   PCB_EX_CASE(4)
   PCB_EX_CASE(8)
-  return PCB_EUNSUP;
+  screen_exact_wide_kernel<<<xgrid, 256, 0, st>>>(P, d, C, amb_list, amb_count, bypass, cand, cand_n, labels, ovf_list,
+                                                  ovf_count, orig, two_list, two_count, state);
 #undef PCB_EX_CASE
   PCB_CHECK_LAUNCH();
   return 0;

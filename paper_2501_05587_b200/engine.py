@@ -94,8 +94,9 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
     if variant != "auto":
         if dtype == _F64 and variant in ("tc3xtf32", "delta", "tc1xtf32s", "bf16s", "fp8s"):
             raise ValueError(f"variant {variant!r} is float32-only")
-        if variant in ("bf16s", "fp8s") and (d > 256 or k > SCREEN_KMAX):
-            raise ValueError(f"variant {variant!r} needs d <= 256 and k <= {SCREEN_KMAX}")
+        dmax = 1024 if variant == "fp8s" else 512  # 8 operand chunks of 128 bytes
+        if variant in ("bf16s", "fp8s") and (d > dmax or k > SCREEN_KMAX):
+            raise ValueError(f"variant {variant!r} needs d <= {dmax} and k <= {SCREEN_KMAX}")
         if variant == "rowreg" and d > 32:
             raise ValueError("variant 'rowreg' needs d <= 32")
         if variant == "tc1xtf32s" and k > SCREEN_KMAX:
@@ -107,7 +108,7 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
         return "tiled"
     if k > SCREEN_KMAX:
         return "tc3xtf32"
-    if d > 256:
+    if d > 1024:
         return "tc1xtf32s"
     # E4M3 rows are 128-byte chunks: for d <= 64 they would be half padding and
     # cost what the BF16 pass costs, with a looser bound (more near-ties)

@@ -184,3 +184,22 @@ def test_bf16_relayout_keeps_results(screen_variant):
     np.testing.assert_allclose(a["centroids"], b["centroids"], rtol=1e-6)
     ref = oracle.lloyd_step(P, pn, C, lab, k)
     check_step(P, C, lab, k, b, ref=ref, what="bf16s after relayout")
+
+
+@pytest.mark.parametrize("variant,n,d,k", [("fp8s", 3000, 784, 256), ("fp8s", 1500, 1000, 60),
+                                           ("fp8s", 2000, 300, 129), ("bf16s", 2000, 400, 100),
+                                           ("bf16s", 1200, 512, 64)])
+def test_long_rows_one_resident_tile(variant, n, d, k):
+    """Rows of 5-8 operand chunks run with one resident row tile of 128 and
+    the warp-per-row exact resolver (d > 256)."""
+    from paper_2501_05587_b200.engine import LloydEngine
+    P = oracle.make_blobs(n, d, k, seed=d)
+    lab = oracle.init_assignments(n, k, 2)
+    C = oracle.mean_centroids(P, lab, k)
+    eng = LloydEngine(P, k, variant=variant, max_iters=1)
+    pn = oracle.point_norms(P)
+    for t in range(4):
+        ref = oracle.lloyd_step(P, pn, C, lab, k)
+        gpu = eng.step_from(C, lab)
+        check_step(P, C, lab, k, gpu, ref=ref, what=f"{variant} n={n} d={d} k={k} it{t}")
+        C, lab = ref.centroids, ref.labels
