@@ -697,9 +697,28 @@ gather_rows_bf16(const __nv_bfloat16* __restrict__ Xb, int ldb, const int* __res
   }
 }
 
-// Rows longer than 256: one warp per ambiguous row, lanes over d, exact f64
-// distances to its candidates (same lists, ties to the lowest index).
-__global__ void __launch_bounds__(256)
+// Four consecutive floats q*4 .. q*4+3 of a row (zero past d); 16-byte load
+// when the row is 16-byte aligned (d % 4 == 0).
+__device__ __forceinline__ float4 load4(const float* __restrict__ rowp, int q, int d) {
+  const int t = 4 * q;
+  if ((d & 3) == 0) return t < d ? __ldg(reinterpret_cast<const float4*>(rowp) + q) : make_float4(0, 0, 0, 0);
+  return make_float4(t < d ? rowp[t] : 0.0f, t + 1 < d ? rowp[t + 1] : 0.0f, t + 2 < d ? rowp[t + 2] : 0.0f,
+                     t + 3 < d ? rowp[t + 3] : 0.0f);
+}
+__device__ __forceinline__ float dist4f(float4 a, float4 b, float s) {
+  const float e0 = a.x - b.x, e1 = a.y - b.y, e2 = a.z - b.z, e3 = a.w - b.w;
+  return fmaf(e3, e3, fmaf(e2, e2, fmaf(e1, e1, fmaf(e0, e0, s))));
+}
+__device__ __forceinline__ double dist4(float4 a, float4 b, double s) {
+  const double e0 = (double)a.x - (double)b.x, e1 = (double)a.y - (double)b.y;
+  const double e2 = (double)a.z - (double)b.z, e3 = (double)a.w - (double)b.w;
+  return fma(e3, e3, fma(e2, e2, fma(e1, e1, fma(e0, e0, s))));
+}
+
+// Rows longer than 256: 8 lanes per ambiguous row (4 rows per warp, float4
+// lanes, 4 loads of each row in flight), f32 distances with the (d + 8) 2^-23
+// margin, f64 for thin margins; same lists, ties to the lowest index.
+__global__ void __launch_bounds__(256, 3)
 screen_exact_wide_kernel(const float* __restrict__ P, int d, const float* __restrict__ C,
                          const int* __restrict__ list, const int* __restrict__ count, int64_t bypass,
                          const int* __restrict__ cand, const int* __restrict__ cand_n, int32_t* __restrict__ labels,
@@ -725,47 +744,100 @@ screen_exact_wide_kernel(const float* __restrict__ P, int d, const float* __rest
     }
   }
   const int64_t cntA = bypassed ? 0 : cnt_amb;
-  for (int64_t r = w0; r < cntA + cnt2; r += nw) {
+  const int64_t cnt = cntA + cnt2;
+  const int sub = lane & 7, grp = lane >> 3;
+  const float brel = (float)(d + 8) * 0x1p-23f;
+  const bool vec = (d & 3) == 0;
+  const int d4 = d >> 2;
+  for (int64_t rb = w0 * 4; rb < cnt; rb += nw * 4) {
+    const int64_t r = rb + grp;
+    const bool valid = r < cnt;
     const bool is2 = r >= cntA;
     const int64_t r2i = r - cntA;
-    const int row = is2 ? two_list[3 * r2i] : (orig != nullptr ? orig[list[r]] : list[r]);
-    const int nc = is2 ? 2 : cand_n[r];
-    if (nc < 1 || nc > SB_NCAND) {
-      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = row;
-      continue;
+    const int row = !valid ? 0 : is2 ? two_list[3 * r2i] : (orig != nullptr ? orig[list[r]] : list[r]);
+    int nc = !valid ? 0 : is2 ? 2 : cand_n[r];
+    const bool ovf = valid && (nc < 1 || nc > SB_NCAND);
+    const unsigned om = __ballot_sync(0xffffffffu, ovf && sub == 0);
+    if (om) {
+      int b = 0;
+      if (lane == 0) b = atomicAdd(ovf_count, __popc(om));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (ovf && sub == 0) ovf_list[b + __popc(om & ((1u << lane) - 1u))] = row;
     }
-    double best = 0.0;
+    if (ovf) nc = 0;
+    const int ncmax = __reduce_max_sync(0xffffffffu, nc);
+    auto cand_id = [&](int c) -> int { return is2 ? two_list[3 * r2i + 1 + c] : cand[r * SB_NCAND + c]; };
+    const float* prow = P + (int64_t)row * d;
+    float f1 = 3.4e38f, f2 = 3.4e38f;
     int bj = -1;
-    for (int c = 0; c < nc; ++c) {
-      const int j = is2 ? two_list[3 * r2i + 1 + c] : cand[r * SB_NCAND + c];
-      double s = 0.0;
-      for (int t = lane; t < d; t += 32) {
-        const double e = (double)P[(int64_t)row * d + t] - (double)C[(int64_t)j * d + t];
-        s = fma(e, e, s);
+    for (int c = 0; c < ncmax; c += 2) {
+      const int ja = c < nc ? cand_id(c) : -1, jb = c + 1 < nc ? cand_id(c + 1) : -1;
+      const float* ra = C + (int64_t)(ja >= 0 ? ja : 0) * d;
+      const float* rb2 = C + (int64_t)(jb >= 0 ? jb : (ja >= 0 ? ja : 0)) * d;
+      float sa = 0.0f, sb = 0.0f;
+      if (ja >= 0) {
+        if (vec) {
+          const float4* p4 = reinterpret_cast<const float4*>(prow);
+          const float4* a4 = reinterpret_cast<const float4*>(ra);
+          const float4* b4 = reinterpret_cast<const float4*>(rb2);
+          for (int f0 = sub; f0 < d4; f0 += 32) {
+            float4 x[4], ya[4], yb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int f = f0 + 8 * u;
+              const bool ok = f < d4;
+              x[u] = ok ? __ldg(p4 + f) : make_float4(0, 0, 0, 0);
+              ya[u] = ok ? __ldg(a4 + f) : make_float4(0, 0, 0, 0);
+              yb[u] = ok ? __ldg(b4 + f) : make_float4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              sa = dist4f(x[u], ya[u], sa);
+              sb = dist4f(x[u], yb[u], sb);
+            }
+          }
+        } else {
+          for (int t = sub; t < d; t += 8) {
+            const float x = prow[t];
+            const float ea = x - ra[t], eb = x - rb2[t];
+            sa = fmaf(ea, ea, sa);
+            sb = fmaf(eb, eb, sb);
+          }
+        }
       }
-      s = warp_sum(s);
-      if (bj < 0 || s < best || (s == best && j < bj)) { best = s; bj = j; }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+      }
+      if (ja >= 0) {
+        if (sa < f1) { f2 = f1; f1 = sa; bj = ja; } else if (sa < f2) { f2 = sa; }
+      }
+      if (jb >= 0) {
+        if (sb < f1) { f2 = f1; f1 = sb; bj = jb; } else if (sb < f2) { f2 = sb; }
+      }
     }
-    if (lane == 0) labels[row] = bj;
+    const bool unsure = nc > 1 && f2 * (1.0f - brel) <= f1 * (1.0f + brel);
+    if (__any_sync(0xffffffffu, unsure)) {
+      double best = 0.0;
+      int bj64 = -1;
+      for (int c = 0; c < ncmax; ++c) {
+        const int j = (unsure && c < nc) ? cand_id(c) : -1;
+        double s64 = 0.0;
+        if (j >= 0)
+          for (int t = sub; t < d; t += 8) {
+            const double e = (double)prow[t] - (double)C[(int64_t)j * d + t];
+            s64 = fma(e, e, s64);
+          }
+        s64 += __shfl_xor_sync(0xffffffffu, s64, 4);
+        s64 += __shfl_xor_sync(0xffffffffu, s64, 2);
+        s64 += __shfl_xor_sync(0xffffffffu, s64, 1);
+        if (j >= 0 && (bj64 < 0 || s64 < best || (s64 == best && j < bj64))) { best = s64; bj64 = j; }
+      }
+      if (unsure) bj = bj64;
+    }
+    if (sub == 0 && bj >= 0) labels[row] = bj;
   }
-}
-
-// Four consecutive floats q*4 .. q*4+3 of a row (zero past d); 16-byte load
-// when the row is 16-byte aligned (d % 4 == 0).
-__device__ __forceinline__ float4 load4(const float* __restrict__ rowp, int q, int d) {
-  const int t = 4 * q;
-  if ((d & 3) == 0) return t < d ? __ldg(reinterpret_cast<const float4*>(rowp) + q) : make_float4(0, 0, 0, 0);
-  return make_float4(t < d ? rowp[t] : 0.0f, t + 1 < d ? rowp[t + 1] : 0.0f, t + 2 < d ? rowp[t + 2] : 0.0f,
-                     t + 3 < d ? rowp[t + 3] : 0.0f);
-}
-__device__ __forceinline__ float dist4f(float4 a, float4 b, float s) {
-  const float e0 = a.x - b.x, e1 = a.y - b.y, e2 = a.z - b.z, e3 = a.w - b.w;
-  return fmaf(e3, e3, fmaf(e2, e2, fmaf(e1, e1, fmaf(e0, e0, s))));
-}
-__device__ __forceinline__ double dist4(float4 a, float4 b, double s) {
-  const double e0 = (double)a.x - (double)b.x, e1 = (double)a.y - (double)b.y;
-  const double e2 = (double)a.z - (double)b.z, e3 = (double)a.w - (double)b.w;
-  return fma(e3, e3, fma(e2, e2, fma(e1, e1, fma(e0, e0, s))));
 }
 
 // Exact f64 distances of each ambiguous row to its candidates (8 lanes per
