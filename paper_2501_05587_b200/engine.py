@@ -541,7 +541,14 @@ class LloydEngine(ShardSequence):
 
     # -- whole fit -----------------------------------------------------------------
     def run(self, max_iters: int, tol: float = 0.0, check_convergence: bool = False,
-            record_history: bool = True, timing: bool = True) -> RunOutput:
+            record_history: bool = True, timing: bool = True, graph: bool = True) -> RunOutput:
+        """The whole fit.  Small single-rank fits are recorded once into a CUDA
+        graph and replayed (every decision inside an iteration is taken on the
+        device, and the host-side schedule — full update at the start,
+        relayouts — is known in advance), which removes the launch gaps between
+        the ~30 small kernels of an iteration; large fits are GPU-bound and run
+        eagerly, as do multi-rank fits (the repair protocol reads the global
+        counts on the host)."""
         if max_iters > self.max_iters:
             raise ValueError("max_iters exceeds the engine's history capacity")
         with torch.cuda.device(self.dev):
@@ -549,16 +556,45 @@ class LloydEngine(ShardSequence):
             hist = None
             if record_history:
                 hist = torch.empty((max_iters, self.n), dtype=torch.int32, pin_memory=True)
+            # graphs pay off where launches dominate (small n k d); a large fit
+            # is GPU-bound and instantiating ~1000 nodes would only add latency
+            small = 2.0 * self.n * self.k * self.d < 1e11
+            use_graph = graph and small and (self.comm is None or self.comm.world_size == 1)
+            evs = self.iterations(0, max_iters, check_convergence, tol, timing, hist, use_graph)
+            torch.cuda.current_stream().synchronize()
+            return self.collect(hist, evs)
+
+    def iterations(self, t0: int, count: int, check_convergence: bool = False, tol: float = 0.0,
+                   timing: bool = True, hist=None, graph: bool = True, nev: int = 3):
+        """Iterations t0 .. t0+count-1, eagerly or as one captured CUDA graph
+        (replayed once).  Returns the per-iteration timing events (nev each)."""
+        def body(external):
             evs = []
-            for t in range(max_iters):
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
+            for t in range(t0, t0 + count):
+                ev = ([torch.cuda.Event(enable_timing=True, external=external) for _ in range(nev)]
+                      if timing else None)
                 self.iteration(t, check_convergence, tol, ev)
                 if ev is not None:
                     evs.append(ev)
                 if hist is not None:
                     hist[t].copy_(self.labels[(t + 1) % 2], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            return self.collect(hist, evs)
+            return evs
+        if graph:
+            saved = self.sums_valid
+            try:
+                g = torch.cuda.CUDAGraph()
+                cs = torch.cuda.Stream(self.dev)
+                cs.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(cs), torch.cuda.graph(g, stream=cs):
+                    evs = body(True)
+                torch.cuda.current_stream().wait_stream(cs)
+                g.replay()
+                self._graph = g  # kept alive until the next run (its nodes reference our buffers)
+                return evs
+            except Exception:  # capture unsupported here: run the same kernels eagerly
+                self.sums_valid = saved
+                torch.cuda.synchronize()
+        return body(False)
 
     def collect(self, hist=None, evs=()) -> RunOutput:
         st = self.state.cpu().numpy()
