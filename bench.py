@@ -196,9 +196,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph")
+    ap.add_argument("--n-override", type=int, default=0, help="diagnostics only: rows of the config")
     ap.add_argument("--e2e-iters", type=int, default=30)
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.n_override > 0:
+        cfg["n"] = args.n_override
     if args.impl == "reference":
         return run_reference(args, cfg)
 

@@ -3,7 +3,7 @@
 # usage: scripts/launches.sh [config] [variant] [tag]
 cfg=${1:-c3}; variant=${2:-auto}; tag=${3:-${cfg}_${variant}}
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 80 -c 80 --csv \
-  --log-file gpurun_out/launches_$tag.csv python bench.py --config $cfg --variant $variant --steps 3 --warmup 3 \
+  --log-file gpurun_out/launches_$tag.csv python bench.py --config $cfg --variant $variant --steps 3 --warmup 3 --no-graph $EXTRA \
   --no-e2e --no-cpu-baseline > gpurun_out/launches_$tag.log 2>&1
 echo "ncu rc=$?"
 python - "$tag" <<'PY'
