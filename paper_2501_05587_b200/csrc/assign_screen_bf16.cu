@@ -59,19 +59,23 @@ constexpr int SB_KPAD = 256;    // centroid rows of C_b / C_aug are padded to a 
 //            8 chunks per tile) overlap the other row tile's MMAs.
 // RT = row tiles of 128 resident per CTA (2; 1 for rows longer than 4 chunks,
 // whose operand tiles would not fit twice).
-template <int NKC, bool W = false, int RT = 2>
+// CB = bytes per operand row chunk: 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B,
+// E4M3 rows of d <= 64, so they are not half padding).
+template <int NKC, bool W = false, int RT = 2, int CB = 128>
 struct SbCfg {
+  static constexpr int kChunkBytes = CB;
+  static constexpr int kKSteps = CB / 32;                           // MMAs per chunk (32 bytes of each row)
   static constexpr int kRows = 128 * RT;                            // rows per "pair"
   static constexpr int kBN = W ? 256 : 128;                         // centroids per tile
   static constexpr int kChunks = kBN / 32;                          // epilogue chunks per tile
   static constexpr int kStages = W ? 3 : SB_STAGES;
-  static constexpr uint32_t kTileBytes = 128 * 128;                 // 128 rows x 128 B
+  static constexpr uint32_t kTileBytes = 128 * CB;                  // 128 rows x CB bytes
   // resident A (2 row tiles), double-buffered across row pairs when it fits
   // (the next pair's rows load while the current pair's MMAs run)
   static constexpr int kAStages = (!W && RT * NKC <= 4) ? 2 : 1;
   static constexpr uint32_t kAPair = RT * NKC * kTileBytes;
   static constexpr uint32_t kABytes = kAStages * kAPair;
-  static constexpr uint32_t kBBytes = kBN * 128;                    // centroid chunk per B stage
+  static constexpr uint32_t kBBytes = kBN * CB;                     // centroid chunk per B stage
   static constexpr uint32_t kAugBytes = kBN * 32;                   // + the K=16 augmented columns
   static constexpr uint32_t kStageB = kBBytes + kAugBytes;          // 1024-aligned
   static constexpr uint32_t kAAug = 128 * 32;                       // constant A columns [1 1 1 0 ..]
@@ -106,7 +110,7 @@ __device__ __forceinline__ int64_t sb_rows(int64_t n, const int* amb_count, int6
   return c > bypass ? 0 : c;
 }
 
-template <int NKC, bool CAND, bool W, bool F8, int RT>
+template <int NKC, bool CAND, bool W, bool F8, int RT, int CB>
 __global__ void __launch_bounds__(SB_THREADS, 1)
 assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                           const __grid_constant__ CUtensorMap tm_baug, const float* __restrict__ anorm,
@@ -116,8 +120,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
                           int* __restrict__ cand_n, const int32_t* __restrict__ orig,
                           const int32_t* __restrict__ lprev, int* __restrict__ two_list, int* __restrict__ two_count,
                           const long long* __restrict__ state) {
-  using Cfg = SbCfg<NKC, W, RT>;
+  using Cfg = SbCfg<NKC, W, RT, CB>;
   constexpr int BN = Cfg::kBN, CH = Cfg::kChunks, STAGES = Cfg::kStages, PR = Cfg::kRows;
+  constexpr int XC = CB / 2;  // chunk width in the tensor maps' BF16 units
+  auto sdesc = [](uint32_t a) { return CB == 128 ? ptx::sdesc_k_sw128(a) : ptx::sdesc_k_sw64(a); };
   if (stopped(state)) return;
   const int64_t n = CAND ? sb_rows(n_in, amb_count, bypass) : n_in;
   if (n == 0) return;
@@ -189,10 +195,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         if (it >= AS) ptx::mbar_wait(&aempty[ab * NKC + c], (uint32_t)((it / AS - 1) & 1));
         if (ptx::elect_one()) {
           ptx::mbar_expect_tx(&afull[ab * NKC + c], RT * Cfg::kTileBytes);
-          ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (0 * NKC + c) * Cfg::kTileBytes, c * SB_BKE,
+          ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (0 * NKC + c) * Cfg::kTileBytes, c * XC,
                            (int)(pr * PR), pol);
           if (RT == 2)
-            ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (1 * NKC + c) * Cfg::kTileBytes, c * SB_BKE,
+            ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (1 * NKC + c) * Cfg::kTileBytes, c * XC,
                              (int)(pr * PR + 128), pol);
         }
         __syncwarp();
@@ -217,7 +223,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             uint8_t* st = sB + stage * Cfg::kStageB;
             const bool last = c + 1 == NKC;  // the tile's augmented columns ride with its last chunk
             ptx::mbar_expect_tx(&full[stage], Cfg::kBBytes + (last ? Cfg::kAugBytes : 0u));
-            ptx::tma_load_2d(&tm_b, &full[stage], st, c * SB_BKE, tile * BN, pol);
+            ptx::tma_load_2d(&tm_b, &full[stage], st, c * XC, tile * BN, pol);
             if (last) {
               ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes, 0, tile * BN, pol);
               ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes + BN * 16, 8, tile * BN, pol);
@@ -265,11 +271,11 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
                 ptx::mbar_wait(&full[stc[c]], phc[c]);
                 ptx::tc_fence_after();
               }
-              const uint64_t ad = ptx::sdesc_k_sw128(ptx::smem_u32(sA + (rt * NKC + c) * Cfg::kTileBytes));
-              const uint64_t bd = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stc[c] * Cfg::kStageB));
+              const uint64_t ad = sdesc(ptx::smem_u32(sA + (rt * NKC + c) * Cfg::kTileBytes));
+              const uint64_t bd = sdesc(ptx::smem_u32(sB + stc[c] * Cfg::kStageB));
               if (ptx::elect_one()) {
 #pragma unroll
-                for (int ks = 0; ks < 4; ++ks) {
+                for (int ks = 0; ks < Cfg::kKSteps; ++ks) {
                   const uint64_t off = (uint64_t)(ks * 32) >> 4;
                   mma_main(d0, ad + off, bd + off, (c | ks) != 0);
                 }
@@ -313,12 +319,12 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           if (nt == 0) ptx::mbar_wait(&afull[ab * NKC + c], (uint32_t)((it / AS) & 1));
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint64_t a0 = ptx::sdesc_k_sw128(ptx::smem_u32(sAp + (0 * NKC + c) * Cfg::kTileBytes));
-          const uint64_t a1 = ptx::sdesc_k_sw128(ptx::smem_u32(sAp + (1 * NKC + c) * Cfg::kTileBytes));
-          const uint64_t bd = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * Cfg::kStageB));
+          const uint64_t a0 = sdesc(ptx::smem_u32(sAp + (0 * NKC + c) * Cfg::kTileBytes));
+          const uint64_t a1 = sdesc(ptx::smem_u32(sAp + (1 * NKC + c) * Cfg::kTileBytes));
+          const uint64_t bd = sdesc(ptx::smem_u32(sB + stage * Cfg::kStageB));
           if (ptx::elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {           // 4 x K=16 per 128-byte chunk
+            for (int ks = 0; ks < Cfg::kKSteps; ++ks) {  // 32 bytes of each row per MMA
               const uint64_t off = (uint64_t)(ks * 32) >> 4;
               mma_main(d0, a0 + off, bd + off, (c | ks) != 0);
               if (RT == 2) mma_main(d0 + 128, a1 + off, bd + off, (c | ks) != 0);
@@ -568,20 +574,22 @@ static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t row
   return r == CUDA_SUCCESS ? 0 : PCB_EINVAL;
 }
 
-template <int NKC, bool CAND, bool W, bool F8, int RT = 2>
+template <int NKC, bool CAND, bool W, bool F8, int RT = 2, int CB = 128>
 static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bfloat16* B, int k,
                               const float* an, const float* dan, const __nv_bfloat16* Baug, const float* bstat,
                               int32_t* labels, int* amb_list, int* amb_count, float* amb_thr, int64_t bypass,
                               int* cand, int* cand_n, const int32_t* orig, const int32_t* lprev,
                               int* two_list, int* two_count, const long long* state, cudaStream_t st) {
-  using Cfg = SbCfg<NKC, W, RT>;
+  using Cfg = SbCfg<NKC, W, RT, CB>;
   CUtensorMap ta, tb, tg;
   int rc;
   const int64_t kpad = (k + SB_KPAD - 1) / SB_KPAD * SB_KPAD;  // B / Baug hold kpad rows (padding: key = +huge)
-  if ((rc = make_tmap_bf16(&ta, A, n, NKC * SB_BKE, 128))) return rc;  // 128-byte chunks: F8 rows viewed as BF16 pairs
-  if ((rc = make_tmap_bf16(&tb, B, kpad, NKC * SB_BKE, Cfg::kBN))) return rc;
+  // CB-byte chunks (E4M3 rows viewed as BF16 pairs)
+  const CUtensorMapSwizzle swz = CB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  if ((rc = make_tmap_bf16(&ta, A, n, NKC * CB / 2, 128, CB / 2, swz))) return rc;
+  if ((rc = make_tmap_bf16(&tb, B, kpad, NKC * CB / 2, Cfg::kBN, CB / 2, swz))) return rc;
   if ((rc = make_tmap_bf16(&tg, Baug, kpad, SB_AUG, Cfg::kBN, 8, CU_TENSOR_MAP_SWIZZLE_NONE))) return rc;
-  auto kern = assign_screen_bf16_kernel<NKC, CAND, W, F8, RT>;
+  auto kern = assign_screen_bf16_kernel<NKC, CAND, W, F8, RT, CB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   if (e != cudaSuccess) return (int)e;
   const int64_t npairs = (n + Cfg::kRows - 1) / Cfg::kRows;
@@ -606,6 +614,10 @@ static int dispatch_bf16(int ldb, const __nv_bfloat16* A, int64_t n, const __nv_
   // (measured slower at c3 / c5: 2.52 vs 2.37 ms, 65 vs 56 ms; MMA-only 2.14
   // vs 2.03 ms — the BF16 MMA rate, not shared-memory operand bandwidth, binds)
   static const bool narrow = getenv("PCB_SCREEN_WIDE") == nullptr;
+  if (F8 && ldb == 32)  // E4M3 rows of 64 bytes (d <= 64): SWIZZLE_64B chunks
+    return launch_screen_bf16<1, CAND, false, F8, 2, 64>(A, n, B, k, an, dan, Baug, bstat, labels, amb_list,
+                                                        amb_count, amb_thr, bypass, cand, cand_n, orig, lprev,
+                                                        two_list, two_count, state, st);
   switch (ldb / SB_BKE) {
     case 1: if (narrow) { PCB_SB_CASE(1, false) } else { PCB_SB_CASE(1, true) }
     case 2: if (narrow) { PCB_SB_CASE(2, false) } else { PCB_SB_CASE(2, true) }
@@ -1055,7 +1067,7 @@ static int resolve_screen(const float* P, int64_t n, int d, const void* P_b, int
                           int64_t bypass, void* sub_b, int* cand, int* cand_n, int32_t* labels,
                           int* ovf_list, int* ovf_count, const int32_t* orig, const int* two_list,
                           const int* two_count, const long long* state, void* stream) {
-  if (n < 1 || d < 1 || k < 1 || ldb % SB_BKE || !P || !P_b || !C_b || !C || !C_aug || !bstat ||
+  if (n < 1 || d < 1 || k < 1 || (ldb % SB_BKE && !(F8 && ldb == 32)) || !P || !P_b || !C_b || !C || !C_aug || !bstat ||
       !amb_list || !amb_count || !amb_thr || !sub_b || !cand || !cand_n || !labels || !ovf_list || !ovf_count)
     return PCB_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1127,7 +1139,7 @@ relayout_rows_bf16(const uint4* __restrict__ src, int per, const float* __restri
 extern "C" int pcb_screen_relayout_bf16(const void* Pb0, const float* an0, const float* dan0, int64_t n, int ldb,
                                         const int32_t* perm, void* P_b, float* anorm, float* danorm, int32_t* orig,
                                         void* stream) {
-  if (n < 1 || ldb < SB_BKE || ldb % SB_BKE || !Pb0 || !an0 || !dan0 || !perm || !P_b || !anorm || !danorm || !orig ||
+  if (n < 1 || ldb < 8 || ldb % 8 || !Pb0 || !an0 || !dan0 || !perm || !P_b || !anorm || !danorm || !orig ||
       Pb0 == P_b)
     return PCB_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1217,13 +1229,14 @@ row_e4m3_norms_kernel(const float* __restrict__ X, int64_t rows, int d, float* _
   if (lane == 0 && maxsq != nullptr) atomic_max_pos_f(maxsq, wmax);
 }
 
-extern "C" int pcb_screen_fp8_ld(int d) { return (d + 127) / 128 * 128; }
+extern "C" int pcb_screen_fp8_ld(int d) { return d <= 64 ? 64 : (d + 127) / 128 * 128; }
 
 // bstat (16 floats): [0] max|c~| [1] max|dc| [2] OFF [3] scratch [4] S = sp sc
 // [5] sp [6] max|p| [7] max|c| [8] sc
 extern "C" int pcb_screen_prep_points_fp8(const float* P, int64_t n, int d, int ld8, void* P_q, float* anorm,
                                           float* danorm, float* bstat, void* stream) {
-  if (n < 1 || d < 1 || ld8 < d || ld8 % 128 || !P || !P_q || !anorm || !danorm || !bstat) return PCB_EINVAL;
+  if (n < 1 || d < 1 || ld8 < d || (ld8 % 128 && ld8 != 64) || !P || !P_q || !anorm || !danorm || !bstat)
+    return PCB_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(bstat, 0, 16 * sizeof(float), st);
   if (e != cudaSuccess) return (int)e;
@@ -1242,7 +1255,8 @@ extern "C" int pcb_screen_prep_points_fp8(const float* P, int64_t n, int d, int 
 
 extern "C" int pcb_screen_prep_centroids_fp8(const float* C, const float* cnorm, int k, int d, int ld8, void* C_q,
                                              void* C_aug, float* bnorm, float* dbnorm, float* bstat, void* stream) {
-  if (k < 1 || d < 1 || ld8 < d || ld8 % 128 || !C || !cnorm || !C_q || !C_aug || !bnorm || !dbnorm || !bstat)
+  if (k < 1 || d < 1 || ld8 < d || (ld8 % 128 && ld8 != 64) || !C || !cnorm || !C_q || !C_aug || !bnorm || !dbnorm ||
+      !bstat)
     return PCB_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(bstat, 0, 2 * sizeof(float), st);
@@ -1270,7 +1284,8 @@ extern "C" int pcb_assign_screen_fp8(const void* P_q, int64_t n, int ld8, const 
                                      int* amb_list, int* amb_count, float* amb_thr, const int32_t* orig,
                                      const int32_t* labels_prev, int* two_list, int* two_count,
                                      const long long* state, void* stream) {
-  if (n < 1 || ld8 < 128 || ld8 % 128 || k < 1 || !P_q || !C_q || !C_aug || !anorm || !danorm || !bstat || !labels ||
+  if (n < 1 || ld8 < 64 || (ld8 % 128 && ld8 != 64) || k < 1 || !P_q || !C_q || !C_aug || !anorm || !danorm ||
+      !bstat || !labels ||
       !amb_list || !amb_count || !amb_thr)
     return PCB_EINVAL;
   if (n > INT32_MAX) return PCB_EUNSUP;
@@ -1286,7 +1301,7 @@ extern "C" int pcb_resolve_screen_fp8(const float* P, int64_t n, int d, const vo
                                       int64_t bypass, void* sub_q, int* cand, int* cand_n, int32_t* labels,
                                       int* ovf_list, int* ovf_count, const int32_t* orig, const int* two_list,
                                       const int* two_count, const long long* state, void* stream) {
-  if (ld8 < 128 || ld8 % 128 || ld8 < d) return PCB_EINVAL;
+  if (ld8 < 64 || (ld8 % 128 && ld8 != 64) || ld8 < d) return PCB_EINVAL;
   return resolve_screen<true>(P, n, d, P_q, ld8 / 2, C_q, C, k, C_aug, bstat, amb_list, amb_count, amb_thr, bypass,
                               sub_q, cand, cand_n, labels, ovf_list, ovf_count, orig, two_list, two_count, state,
                               stream);

@@ -87,6 +87,17 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
   return d;
 }
 
+// K-major, 64-byte swizzle: rows of 64 B, 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t sdesc_k_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;             // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(512u >> 4) << 32;    // SBO
+  d |= (uint64_t)1u << 46;             // descriptor version (Blackwell)
+  d |= (uint64_t)4u << 61;             // SWIZZLE_64B
+  return d;
+}
+
 // K-major, no swizzle: core matrices of 8 rows x 16 B (rows 16 B apart), LBO =
 // byte distance between the two K-adjacent core matrices, SBO = between
 // 8-row groups (canonical ((8,n),2):((1,SBO),LBO) in 16-byte units).

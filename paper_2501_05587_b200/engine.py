@@ -110,9 +110,9 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
         return "tc3xtf32"
     if d > 1024:
         return "tc1xtf32s"
-    # E4M3 rows are 128-byte chunks: for d <= 64 they would be half padding and
-    # cost what the BF16 pass costs, with a looser bound (more near-ties)
-    return "fp8s" if d > 64 else "bf16s"
+    # E4M3 operands: half the bytes and twice the tensor rate of BF16 (rows of
+    # d <= 64 use 64-byte SWIZZLE_64B chunks); the certificate keeps labels exact
+    return "fp8s"
 
 
 SCREEN_KMAX = 6144  # assign_screen.cu SC_KMAX
