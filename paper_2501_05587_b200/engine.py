@@ -43,6 +43,18 @@ _STAGE_CHUNK = 1 << 23  # elements per pinned staging buffer (32 MiB of f32)
 _STAGE_BUFS = 4         # measured on the B200 host: 4 x 32 MiB reach ~45 GB/s (scripts/h2d_probe.py)
 
 
+def _staging(dev: torch.device, dtype: torch.dtype):
+    """The device's pinned staging buffers viewed as `dtype` (one set per
+    element size: int32 labels reuse the f32 buffers of the point upload)."""
+    isz = torch.empty(0, dtype=dtype).element_size()
+    key = (dev.index, isz)
+    if key not in _STAGING:
+        bufs = [torch.empty(_STAGE_CHUNK * isz, dtype=torch.uint8, pin_memory=True) for _ in range(_STAGE_BUFS)]
+        _STAGING[key] = (bufs, [torch.cuda.Event() for _ in range(_STAGE_BUFS)], torch.cuda.Stream(dev))
+    bufs, evs, cs = _STAGING[key]
+    return [b.view(dtype) for b in bufs], evs, cs
+
+
 def h2d_staged(host: np.ndarray, dev: torch.device) -> torch.Tensor:
     """Host (pageable numpy) -> device copy through reusable pinned staging
     buffers on a side stream: the (multi-threaded) CPU memcpy of chunk i+1
@@ -54,11 +66,7 @@ def h2d_staged(host: np.ndarray, dev: torch.device) -> torch.Tensor:
     if flat.numel() <= _STAGE_CHUNK:
         out.copy_(src)
         return out
-    key = (dev.index, src.dtype)
-    if key not in _STAGING:
-        bufs = [torch.empty(_STAGE_CHUNK, dtype=src.dtype, pin_memory=True) for _ in range(_STAGE_BUFS)]
-        _STAGING[key] = (bufs, [torch.cuda.Event() for _ in range(_STAGE_BUFS)], torch.cuda.Stream(dev))
-    bufs, evs, cs = _STAGING[key]
+    bufs, evs, cs = _staging(dev, src.dtype)
     dflat = out.view(-1)
     cs.wait_stream(torch.cuda.current_stream(dev))
     for i, off in enumerate(range(0, flat.numel(), _STAGE_CHUNK)):
@@ -70,6 +78,40 @@ def h2d_staged(host: np.ndarray, dev: torch.device) -> torch.Tensor:
             dflat[off:off + m].copy_(bufs[b][:m], non_blocking=True)
             evs[b].record(cs)
     torch.cuda.current_stream(dev).wait_stream(cs)
+    return out
+
+
+def d2h_staged(src: torch.Tensor) -> np.ndarray:
+    """Device -> host (numpy) copy through the same reusable pinned staging
+    buffers: the DMA of chunk i+1 overlaps the CPU copy of chunk i out of
+    pinned memory (a plain .cpu() of a large tensor lands in pageable memory
+    at a fraction of the bus rate)."""
+    src = src.contiguous()
+    flat = src.view(-1)
+    if flat.numel() <= _STAGE_CHUNK:
+        return src.cpu().numpy()
+    dev = src.device
+    out = np.empty(tuple(src.shape), dtype=torch.empty(0, dtype=src.dtype).numpy().dtype)
+    oflat = torch.from_numpy(out).view(-1)
+    bufs, evs, cs = _staging(dev, src.dtype)
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    chunks = list(range(0, flat.numel(), _STAGE_CHUNK))
+    def issue(i):
+        b = i % len(bufs)
+        off = chunks[i]
+        m = min(_STAGE_CHUNK, flat.numel() - off)
+        with torch.cuda.stream(cs):
+            bufs[b][:m].copy_(flat[off:off + m], non_blocking=True)
+            evs[b].record(cs)
+    for i in range(min(len(bufs), len(chunks))):
+        issue(i)
+    for i, off in enumerate(chunks):
+        b = i % len(bufs)
+        m = min(_STAGE_CHUNK, flat.numel() - off)
+        evs[b].synchronize()
+        oflat[off:off + m].copy_(bufs[b][:m])
+        if i + len(bufs) < len(chunks):
+            issue(i + len(bufs))
     return out
 
 
@@ -601,7 +643,7 @@ class LloydEngine(ShardSequence):
         if st[5] != 0:
             raise ValueError("row_argmin: matrix contains NaN")  # dense.py:66-67 semantics
         iters = int(st[0])
-        labels = self.labels[iters % 2].cpu().numpy()
+        labels = d2h_staged(self.labels[iters % 2])
         dist_s = upd_s = 0.0
         for ev in list(evs)[:iters]:
             dist_s += ev[0].elapsed_time(ev[1]) / 1e3
