@@ -219,6 +219,24 @@ def top2_gap_f64(P, centroids, chunk: int = 16384):
     return d1, gap
 
 
+def top2_gap_abs_f64(P, centroids, chunk: int = 16384):
+    """Absolute top-2 gap d2 - d1 per point in f64 (inf for k = 1): compared with
+    the reference's own f32 expansion error in the parity checker."""
+    P64 = np.asarray(P, dtype=np.float64)
+    C64 = np.asarray(centroids, dtype=np.float64)
+    n = P64.shape[0]
+    out = np.full(n, np.inf)
+    if C64.shape[0] == 1:
+        return out
+    cn = (C64 * C64).sum(1)
+    for s in range(0, n, chunk):
+        blk = P64[s:s + chunk]
+        D = (blk * blk).sum(1)[:, None] - 2.0 * blk @ C64.T + cn[None, :]
+        part = np.partition(D, 1, axis=1)[:, :2]
+        out[s:s + chunk] = part[:, 1] - part[:, 0]
+    return out
+
+
 # -- full driver (clustering.py:291-325) ---------------------------------------
 @dataclass
 class OracleTimings:

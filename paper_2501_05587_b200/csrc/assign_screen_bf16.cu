@@ -329,7 +329,11 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
               mma_main(d0, a0 + off, bd + off, (c | ks) != 0);
               if (RT == 2) mma_main(d0 + 128, a1 + off, bd + off, (c | ks) != 0);
             }
+#if defined(PCB_EXP) && PCB_EXP == 8
+            if (false) {  // experiment build: no augmented step (keys wrong, timing only)
+#else
             if (c + 1 == NKC) {  // augmented K step: + (|c|^2 + OFF) in three BF16 pieces
+#endif
               const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
               const uint64_t ba = ptx::sdesc_k_none(ptx::smem_u32(sB + stage * Cfg::kStageB + Cfg::kBBytes),
                                                     BN * 16, 128);
@@ -459,7 +463,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
-#if defined(PCB_EXP) && PCB_EXP == 2
+#if defined(PCB_EXP) && (PCB_EXP == 2 || PCB_EXP == 8)
           // experiment build: TMEM traffic only (MMA + TMEM-load ceiling)
           R1 = fminf(R1, v[0] + v[31]);
           continue;

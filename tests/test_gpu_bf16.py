@@ -203,3 +203,29 @@ def test_long_rows_one_resident_tile(variant, n, d, k):
         gpu = eng.step_from(C, lab)
         check_step(P, C, lab, k, gpu, ref=ref, what=f"{variant} n={n} d={d} k={k} it{t}")
         C, lab = ref.centroids, ref.labels
+
+
+@pytest.mark.parametrize("case", ["wide_range", "identical", "integer_grid"])
+def test_screen_hard_inputs(case, screen_variant):
+    """Inputs that stress the low-precision screen: a wide dynamic range across
+    columns (E4M3 scale set by the largest entry, small entries subnormal),
+    all points identical (every key tied), small integers (exact ties between
+    centroids).  Labels must still match the reference step."""
+    from paper_2501_05587_b200.engine import LloydEngine
+    rng = make_rng(41)
+    n, d, k = 3000, 48, 24
+    if case == "wide_range":
+        P = (rng.normal(size=(n, d)) * np.logspace(-3, 3, d)[None, :]).astype(np.float32)
+    elif case == "identical":
+        P = np.repeat(rng.normal(size=(1, d)), n, axis=0).astype(np.float32)
+    else:
+        P = rng.integers(0, 4, size=(n, d)).astype(np.float32)
+    lab = oracle.init_assignments(n, k, 3)
+    C = oracle.mean_centroids(P, lab, k)
+    eng = LloydEngine(P, k, variant=screen_variant, max_iters=1)
+    pn = oracle.point_norms(P)
+    for t in range(3):
+        ref = oracle.lloyd_step(P, pn, C, lab, k)
+        gpu = eng.step_from(C, lab)
+        check_step(P, C, lab, k, gpu, ref=ref, what=f"{screen_variant} {case} it{t}")
+        C, lab = ref.centroids, ref.labels
