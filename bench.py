@@ -340,7 +340,11 @@ def main():
                    "l2": "inputs larger than L2" if n * d * 4 > 126e6 else "inputs fit in L2 (no flush)"},
         "dists_per_sec": n * k / (ms_per_step * 1e-3),
         "roofline": roof,
-        "gpu_launches": {"tc1xtf32s": 12, "bf16s": 15, "fp8s": 15}.get(eng.variant, 6) * K,
+        # library kernels per steady-state iteration (counted from the ncu launch
+        # lists in profiles/), plus the relayouts that fall inside the window
+        "gpu_launches": {"fp8s": 21, "bf16s": 19, "tc1xtf32s": 15}.get(eng.variant, 9) * K
+                        + sum(1 for t in getattr(eng, "RELAYOUT_AT", ()) if W <= t < W + K
+                              and eng.variant in ("fp8s", "bf16s")),
         "screen_ambiguous_rows_last_iter": amb,
         "clocks": clocks,
     }
