@@ -274,14 +274,18 @@ int pcb_sum_squares_f64(const double* X, int64_t count, double* out, void* strea
  *   largest own distance (lowest index on ties) moves to j; repeated while any
  *   cluster is empty.  Reads own_sorted/perm from the update kernel, adjusts
  *   acc (sums, counts, objective, changed) and state[3] (repairs).  No-op
- *   when no cluster is empty.  One cooperative launch.                     */
+ *   when no cluster is empty.  One cooperative launch.  `sums` (nullable):
+ *   the delta update's persistent per-cluster f64 sums, moved in step with
+ *   acc; when NULL a move marks them stale (the next update runs full).   */
 int64_t pcb_repair_scratch_bytes(int k);   /* device scratch the caller provides */
 int pcb_repair_f32(const float* P, int64_t n, int d, const float* C, int k, const int32_t* perm,
                    const int32_t* labels_prev, int32_t* labels, double* own_sorted, double* acc,
-                   long long* state, void* scratch, int64_t scratch_bytes, void* stream);
+                   long long* state, void* scratch, int64_t scratch_bytes, double* sums,
+                   void* stream);
 int pcb_repair_f64(const double* P, int64_t n, int d, const double* C, int k, const int32_t* perm,
                    const int32_t* labels_prev, int32_t* labels, double* own_sorted, double* acc,
-                   long long* state, void* scratch, int64_t scratch_bytes, void* stream);
+                   long long* state, void* scratch, int64_t scratch_bytes, double* sums,
+                   void* stream);
 
 /* Multi-rank repair (host-orchestrated).  argmax_own writes
  * [own distance, global point index, local sorted position] of this rank's

@@ -68,8 +68,8 @@ SIGNATURES = {
     "pcb_segment_sums_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P]),
     "pcb_segment_sums_f64": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P]),
     "pcb_repair_scratch_bytes": (I64, [I32]),
-    "pcb_repair_f32": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, I64, P]),
-    "pcb_repair_f64": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, I64, P]),
+    "pcb_repair_f32": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, I64, P, P]),
+    "pcb_repair_f64": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, I64, P, P]),
     "pcb_argmax_own": (I32, [P, P, I64, I64, P, P]),
     "pcb_repair_apply_f32": (I32, [P, I32, P, P, P, P, P, I64, I32, P, P]),
     "pcb_repair_apply_f64": (I32, [P, I32, P, P, P, P, P, I64, I32, P, P]),

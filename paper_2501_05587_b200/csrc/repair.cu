@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(256)
 repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C, int k,
               const int32_t* __restrict__ perm, const int32_t* __restrict__ labels_prev,
               int32_t* __restrict__ labels, double* __restrict__ own, double* __restrict__ acc,
-              long long* __restrict__ state, RepairScratch* __restrict__ sc) {
+              long long* __restrict__ state, RepairScratch* __restrict__ sc, double* __restrict__ S) {
   if (stopped(state)) return;
   cg::grid_group grid = cg::this_grid();
   const AccLayout L{k, d};
@@ -205,6 +205,10 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
           const double p = (double)P[donor * d + t];
           atomicAdd(&acc[(int64_t)old * d + t], -p);
           atomicAdd(&acc[(int64_t)j * d + t], p);
+          if (S != nullptr) {  // keep the delta update's per-cluster sums in step
+            atomicAdd(&S[(int64_t)old * d + t], -p);
+            atomicAdd(&S[(int64_t)j * d + t], p);
+          }
         }
         if (lane == 0) {
           const double dnew = pair_distance(P, C, d, donor, j);
@@ -218,7 +222,7 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
           labels[donor] = j;
           own[q] = -INFINITY;
           atomicAdd((unsigned long long*)&state[kMoved], 1ull);
-          state[kSumsStale] = 1;  // the delta update's per-cluster sums miss this move
+          if (S == nullptr) state[kSumsStale] = 1;  // the delta update's per-cluster sums miss this move
         }
       }
       grid.sync();  // own / labels of the moves visible to the next selection
@@ -234,7 +238,7 @@ static size_t repair_scratch(int k) { return sizeof(RepairScratch) + sizeof(int)
 template <typename T>
 static int repair(const T* P, int64_t n, int d, const T* C, int k, const int32_t* perm,
                   const int32_t* lp, int32_t* lab, double* own, double* acc, long long* state,
-                  void* scratch, int64_t scratch_bytes, cudaStream_t st) {
+                  void* scratch, int64_t scratch_bytes, double* S, cudaStream_t st) {
   if (n < 1 || d < 1 || k < 1 || !P || !C || !perm || !lab || !own || !acc || !state || !scratch)
     return PCB_EINVAL;
   if (n > INT32_MAX) return PCB_EUNSUP;
@@ -248,7 +252,7 @@ static int repair(const T* P, int64_t n, int d, const T* C, int k, const int32_t
   RepairScratch* sc = (RepairScratch*)scratch;
   void* args[] = {(void*)&P,   (void*)&n,   (void*)&d,   (void*)&C,     (void*)&k,
                   (void*)&perm, (void*)&lp, (void*)&lab, (void*)&own, (void*)&acc,
-                  (void*)&state, (void*)&sc};
+                  (void*)&state, (void*)&sc, (void*)&S};
   e = cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(256), args, 0, st);
   return (int)e;
 }
@@ -260,17 +264,17 @@ extern "C" int64_t pcb_repair_scratch_bytes(int k) { return (int64_t)pcb::repair
 extern "C" int pcb_repair_f32(const float* P, int64_t n, int d, const float* C, int k,
                               const int32_t* perm, const int32_t* labels_prev, int32_t* labels,
                               double* own_sorted, double* acc, long long* state, void* scratch,
-                              int64_t scratch_bytes, void* stream) {
+                              int64_t scratch_bytes, double* sums, void* stream) {
   return pcb::repair<float>(P, n, d, C, k, perm, labels_prev, labels, own_sorted, acc, state, scratch,
-                            scratch_bytes, (cudaStream_t)stream);
+                            scratch_bytes, sums, (cudaStream_t)stream);
 }
 
 extern "C" int pcb_repair_f64(const double* P, int64_t n, int d, const double* C, int k,
                               const int32_t* perm, const int32_t* labels_prev, int32_t* labels,
                               double* own_sorted, double* acc, long long* state, void* scratch,
-                              int64_t scratch_bytes, void* stream) {
+                              int64_t scratch_bytes, double* sums, void* stream) {
   return pcb::repair<double>(P, n, d, C, k, perm, labels_prev, labels, own_sorted, acc, state, scratch,
-                             scratch_bytes, (cudaStream_t)stream);
+                            scratch_bytes, sums, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------------------

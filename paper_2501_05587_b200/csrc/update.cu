@@ -449,8 +449,9 @@ static int segment_sums(const T* P, int64_t n, int d, const int32_t* perm, const
 // assigned against (clustering.py:148 evaluates the same sum row by row).
 // The full update (counting sort + segmented sums, exact own distances) runs
 // whenever more than `frac` of the rows changed, a local cluster count is 0
-// (the repair needs own distances), the sums are not valid yet, or a repair
-// moved points (state[kSumsStale]); it refreshes S.
+// (the repair needs own distances), the sums are not valid yet, or a
+// multi-rank repair moved points (state[kSumsStale]); it refreshes S.  The
+// single-rank repair moves S in step with acc instead (repair.cu).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
 update_mode_kernel(const double* __restrict__ acc, int k, int d, int64_t n, double frac, int force_full,

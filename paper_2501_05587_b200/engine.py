@@ -556,7 +556,7 @@ class LloydEngine(ShardSequence):
     def _repair_local(self, prev, new) -> None:
         L.call(f"pcb_repair_{self.sfx}", _p(self.P), self.n, self.d, _p(self.C), self.k, _p(self.perm),
                _p(prev), _p(new), _p(self.own), _p(self.acc), _p(self.state), _p(self.repair_scratch),
-               self.repair_scratch_bytes, _stream())
+               self.repair_scratch_bytes, _p(self.S) if self.delta_frac >= 0 else None, _stream())
 
     def _finalize(self, check_convergence: bool, tol: float) -> None:
         if self.dtype == _F32:

@@ -1,7 +1,7 @@
 """Delta centroid update (update.cu): per-cluster f64 sums maintained over the
 changed rows, objective from sum |p|^2 - 2 <c, S> + n |c|^2.  Must agree with
 the full counting-sort update to f64 rounding, on every variant, and fall
-back to the full update when rows churn, clusters empty out or a repair ran."""
+back to the full update when rows churn or clusters empty out."""
 import numpy as np
 import pytest
 
@@ -68,9 +68,10 @@ def test_delta_run_matches_reference():
     np.testing.assert_allclose(res.objective_history, ref.objective_history, rtol=1e-6)
 
 
-def test_repair_forces_full_update():
-    """Duplicate points empty clusters out: the repair moves points, marks the
-    sums stale, and the next iteration refreshes them with the full update."""
+def test_repair_keeps_delta_sums():
+    """Duplicate points empty clusters out: the repair moves points and the
+    delta update's sums S with them, so later delta iterations still match
+    the full update bit for bit (labels, repairs) and the objective."""
     from paper_2501_05587_b200.engine import LloydEngine
     rng = np.random.default_rng(4)
     base = rng.normal(size=(5, 8)).astype(np.float32)
@@ -78,6 +79,9 @@ def test_repair_forces_full_update():
     k = 12
     a, modes, _, _ = _run(P, k, "auto", "tiled", iters=10)
     b, _, _, _ = _run(P, k, "full", "tiled", iters=10)
+    rep = np.flatnonzero(np.asarray(a.repairs) > 0)
+    assert rep.size, "no repair ran"
+    assert any(modes[t] == 1 for t in range(int(rep[0]) + 1, len(modes))), modes
     np.testing.assert_array_equal(a.labels, b.labels)
     np.testing.assert_array_equal(a.repairs, b.repairs)
     np.testing.assert_allclose(a.objective_history, b.objective_history, rtol=1e-9)
