@@ -89,6 +89,8 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
   const AccLayout L{k, d};
   __shared__ int s_any;
   __shared__ unsigned int s_hist[256];
+  __shared__ unsigned long long s_glob[256];
+  __shared__ int s_wsum[8];
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
   for (int j = threadIdx.x; j < k; j += blockDim.x)
@@ -103,11 +105,22 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
     for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&sc->hist[0][0])[i] = 0ull;
   while (true) {
     grid.sync();  // counts of the previous pass are final
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      int c = 0;
-      for (int j = 0; j < k; ++j)
-        if (acc[L.counts() + j] == 0.0) sc->elist[1 + c++] = j;
-      sc->elist[0] = c;
+    if (blockIdx.x == 0) {  // ascending list of the empty clusters (block-wide ballot scan)
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      int base = 0;
+      for (int j0 = 0; j0 < k; j0 += blockDim.x) {
+        const int j = j0 + threadIdx.x;
+        const bool e = j < k && acc[L.counts() + j] == 0.0;
+        const unsigned int bal = __ballot_sync(0xffffffffu, e);
+        if (lane == 0) s_wsum[warp] = __popc(bal);
+        __syncthreads();
+        int off = base;
+        for (int w = 0; w < warp; ++w) off += s_wsum[w];
+        if (e) sc->elist[1 + off + __popc(bal & ((1u << lane) - 1u))] = j;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) base += s_wsum[w];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) sc->elist[0] = base;
     }
     grid.sync();
     const int ne = ((volatile int*)sc->elist)[0];
@@ -124,38 +137,60 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
           for (int i = threadIdx.x; i < 256; i += blockDim.x) sc->hist[nb][i] = 0ull;
         for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0u;
         __syncthreads();
-        for (int64_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
-          const unsigned long long k1 = own_key(own[q]);
-          if ((k1 & m1) != p1) continue;
-          unsigned int dig;
-          if (pass < 8) {
-            dig = (unsigned int)(k1 >> (8 * (7 - pass))) & 255u;
-          } else {
-            const unsigned int k2 = ~(unsigned int)perm[q];
-            if ((k2 & m2) != p2) continue;
-            dig = (k2 >> (8 * (11 - pass))) & 255u;
+        // 4 loads in flight per thread (the pass is a latency-bound stream over own[])
+        for (int64_t b0 = lo; b0 < hi; b0 += 4 * (int64_t)blockDim.x) {  // block-uniform trip count
+          const int64_t q0 = b0 + threadIdx.x;
+          unsigned long long kk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t q = q0 + (int64_t)u * blockDim.x;
+            kk[u] = q < hi ? own_key(own[q]) : 0ull;
           }
-          atomicAdd(&s_hist[dig], 1u);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t q = q0 + (int64_t)u * blockDim.x;
+            const unsigned long long k1 = kk[u];
+            bool hit = q < hi && (k1 & m1) == p1;
+            unsigned int dig = 0u;
+            if (hit) {
+              if (pass < 8) {
+                dig = (unsigned int)(k1 >> (8 * (7 - pass))) & 255u;
+              } else {
+                const unsigned int k2 = ~(unsigned int)perm[q];
+                hit = (k2 & m2) == p2;
+                dig = (k2 >> (8 * (11 - pass))) & 255u;
+              }
+            }
+            // warp-aggregated: the leading digits are shared by most rows
+            const unsigned int peers = __match_any_sync(0xffffffffu, hit ? dig : 0xffffffffu);
+            if (hit && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_hist[dig], (unsigned)__popc(peers));
+          }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < 256; i += blockDim.x)
           if (s_hist[i]) atomicAdd(&sc->hist[hbuf][i], (unsigned long long)s_hist[i]);
         grid.sync();
-        // every block scans the global histogram from the top (same result)
+        // every block scans the global histogram from the top (same result);
+        // one parallel load into shared memory, then a serial scan there
+        for (int i = threadIdx.x; i < 256; i += blockDim.x)
+          s_glob[i] = ((volatile unsigned long long*)sc->hist[hbuf])[i];
+        __syncthreads();
         if (threadIdx.x == 0) {
           unsigned long long cum = 0ull;
           int bsel = 0;
           for (int bb = 255; bb >= 0; --bb) {
-            const unsigned long long c = ((volatile unsigned long long*)sc->hist[hbuf])[bb];
+            const unsigned long long c = s_glob[bb];
             if (cum + c >= (unsigned long long)rem) { bsel = bb; break; }
             cum += c;
           }
           s_hist[0] = (unsigned int)bsel;
           s_hist[1] = (unsigned int)(rem - (int)cum);
+          s_hist[2] = (unsigned int)(s_glob[bsel] == (unsigned long long)(rem - (int)cum));  // whole bucket taken
         }
         __syncthreads();
         const unsigned int bsel = s_hist[0];
         rem = (int)s_hist[1];
+        const bool whole = s_hist[2] != 0u;
         __syncthreads();
         if (pass < 8) {
           p1 |= (unsigned long long)bsel << (8 * (7 - pass));
@@ -165,15 +200,17 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
           m2 |= 255u << (8 * (11 - pass));
         }
         hbuf = nb;
+        if (whole) break;  // every key of the selected bucket is among the B: prefix suffices
       }
-      // (p1, p2) is the B-th largest key (ids are unique): collect the B keys >= it
+      // the B largest keys are those whose (masked) prefix is >= (p1, p2) (ids
+      // are unique; a shorter prefix only when its whole bucket is selected)
       if (blockIdx.x == 0 && threadIdx.x == 0) sc->sel_count = 0;
       grid.sync();
       for (int64_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
         const unsigned long long k1 = own_key(own[q]);
-        if (k1 < p1) continue;
+        if ((k1 & m1) < p1) continue;
         const unsigned int k2 = ~(unsigned int)perm[q];
-        if (k1 == p1 && k2 < p2) continue;
+        if ((k1 & m1) == p1 && (k2 & m2) < p2) continue;
         const int at = atomicAdd(&sc->sel_count, 1);
         if (at < RP_BATCH) { sc->sel_k1[at] = k1; sc->sel_k2[at] = k2; sc->sel_q[at] = (int)q; }
       }
@@ -230,8 +267,8 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
   }
 }
 
-// Cooperative grid: one block per SM.
-static int repair_grid() { return sm_count(); }
+// Cooperative grid: up to 4 blocks per SM (the selection passes stream own[]).
+static int repair_grid(int per_sm) { return sm_count() * std::min(per_sm, 4); }
 
 static size_t repair_scratch(int k) { return sizeof(RepairScratch) + sizeof(int) * (size_t)(k + 1); }
 
@@ -248,7 +285,7 @@ static int repair(const T* P, int64_t n, int d, const T* C, int k, const int32_t
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
   if (e != cudaSuccess) return (int)e;
   if (per_sm < 1) return PCB_EUNSUP;
-  const int grid = repair_grid();
+  const int grid = repair_grid(per_sm);
   RepairScratch* sc = (RepairScratch*)scratch;
   void* args[] = {(void*)&P,   (void*)&n,   (void*)&d,   (void*)&C,     (void*)&k,
                   (void*)&perm, (void*)&lp, (void*)&lab, (void*)&own, (void*)&acc,

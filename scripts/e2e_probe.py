@@ -1,44 +1,36 @@
-"""Where does the host-side time of run_lloyd(host numpy) go at c3? (diagnostic)"""
-import sys, time
+"""bench.py's e2e leg with per-phase wall timers patched onto LloydEngine (diagnostic, under gpurun)."""
+import sys, os, time, functools
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
-sys.path.insert(0, '.')
-from bench import make_shard
-n, d, k = 10_000_000, 128, 1024
-P = make_shard(n, d, k, 0, 0, torch.device('cuda')).cpu().numpy()
-torch.cuda.synchronize()
-def t(label, fn):
-    t0 = time.perf_counter(); r = fn(); torch.cuda.synchronize(); print(f"{label:40s} {time.perf_counter()-t0:8.3f} s", flush=True); return r
-t("np.isfinite.all", lambda: np.isfinite(P).all())
-t("ascontiguousarray", lambda: np.ascontiguousarray(P, dtype=np.float32))
-from paper_2501_05587_b200.clustering import init_assignments
-t("init_assignments", lambda: init_assignments(n, k, 0))
-t("pageable .to(cuda)", lambda: torch.from_numpy(P).to('cuda'))
-t("pin_memory copy", lambda: torch.from_numpy(P).pin_memory())
-def reg():
-    hp = torch.from_numpy(P)
-    cudart = torch.cuda.cudart()
-    r = cudart.cudaHostRegister(hp.data_ptr(), hp.numel() * 4, 0)
-    g = hp.to('cuda', non_blocking=True); torch.cuda.synchronize()
-    cudart.cudaHostUnregister(hp.data_ptr())
-    return r
-t("hostRegister+copy+unregister", reg)
-def staged(chunk=1 << 26):
-    dst = torch.empty((n, d), dtype=torch.float32, device='cuda')
-    flat = torch.from_numpy(P).view(-1); dflat = dst.view(-1)
-    bufs = [torch.empty(chunk, dtype=torch.float32).pin_memory() for _ in range(2)]
-    evs = [torch.cuda.Event() for _ in range(2)]
-    s = torch.cuda.Stream()
-    for i, off in enumerate(range(0, flat.numel(), chunk)):
-        b = i & 1
-        evs[b].synchronize()
-        m = min(chunk, flat.numel() - off)
-        bufs[b][:m].copy_(flat[off:off + m])
-        with torch.cuda.stream(s):
-            dflat[off:off + m].copy_(bufs[b][:m], non_blocking=True)
-            evs[b].record(s)
-    s.synchronize()
-    return dst
-t("staged 2x256MB pinned", staged)
+from bench import CONFIGS, make_shard
 import paper_2501_05587_b200 as pcb
-cfg = pcb.KKMeansConfig(k=k, max_iters=30, record_label_history=False)
-t("run_lloyd total", lambda: pcb.run_lloyd(P, cfg))
+from paper_2501_05587_b200 import engine as E
+
+T = {}
+def timed(name, f):
+    @functools.wraps(f)
+    def w(*a, **kw):
+        torch.cuda.synchronize(); t = time.perf_counter()
+        r = f(*a, **kw)
+        torch.cuda.synchronize(); T[name] = T.get(name, 0) + time.perf_counter() - t
+        return r
+    return w
+for nm in ("__init__", "init_labels_device", "init_centroids_from_labels", "run", "collect"):
+    setattr(E.LloydEngine, nm, timed(nm, getattr(E.LloydEngine, nm)))
+
+cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"]
+n, d, k = cfg["n"], cfg["d"], cfg["k"]
+dev = torch.device("cuda")
+if len(sys.argv) > 2:  # simulate the main bench leg's footprint first
+    x = torch.empty(int(float(sys.argv[2]) * 2**30), dtype=torch.uint8, device=dev); del x
+P_host = make_shard(n, d, k, 0, 0, dev).cpu().numpy()
+torch.cuda.empty_cache()
+c = pcb.KKMeansConfig(k=k, max_iters=30, record_label_history=False)
+pcb.run_lloyd(P_host[:100_000], pcb.KKMeansConfig(k=k, max_iters=2))
+torch.cuda.synchronize()
+for rep in range(3):
+    T.clear()
+    t0 = time.perf_counter()
+    res = pcb.run_lloyd(P_host, c)
+    wall = time.perf_counter() - t0
+    print(f"rep {rep} wall {wall*1e3:.1f} ms", {k_: round(v * 1e3, 1) for k_, v in T.items()}, flush=True)
