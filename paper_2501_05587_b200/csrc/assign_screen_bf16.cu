@@ -38,12 +38,23 @@
 #include "pcb_common.cuh"
 #include "pcb_launch.cuh"
 #include "screen_common.cuh"
+
+#if defined(PCB_EXP) && PCB_EXP == 9
+// experiment build: no TMEM loads at all (MMA + TMA producer ceiling)
+#define SB_TMEM_LD(addr, regs) ((void)(addr))
+#else
+#define SB_TMEM_LD(addr, regs) ptx::tmem_ld_32x32b_x32_async(addr, regs)
+#endif
 #include "tc_ptx.cuh"
 
 namespace pcb {
 
 constexpr int SB_BN = 128;
+#ifdef PCB_SB_STAGES
+constexpr int SB_STAGES = PCB_SB_STAGES;  // experiment builds
+#else
 constexpr int SB_STAGES = 4;
+#endif
 constexpr int SB_THREADS = 384;
 constexpr int SB_BKE = 64;      // BF16 elements per 128-byte swizzle row
 constexpr int SB_NCAND = 64;    // candidate slots per ambiguous row (pass 2)
@@ -68,7 +79,6 @@ struct SbCfg {
   static constexpr int kRows = 128 * RT;                            // rows per "pair"
   static constexpr int kBN = W ? 256 : 128;                         // centroids per tile
   static constexpr int kChunks = kBN / 32;                          // epilogue chunks per tile
-  static constexpr int kStages = W ? 3 : SB_STAGES;
   static constexpr uint32_t kTileBytes = 128 * CB;                  // 128 rows x CB bytes
   // resident A (2 row tiles), double-buffered across row pairs when it fits
   // (the next pair's rows load while the current pair's MMAs run)
@@ -80,6 +90,8 @@ struct SbCfg {
   static constexpr uint32_t kStageB = kBBytes + kAugBytes;          // 1024-aligned
   static constexpr uint32_t kAAug = 128 * 32;                       // constant A columns [1 1 1 0 ..]
   static constexpr uint32_t kBarBytes = 1024;
+  static constexpr int kStagesFit = (int)((232448u - 1024u - kABytes - kAAug - kBarBytes) / kStageB);
+  static constexpr int kStages = W ? 3 : (SB_STAGES < kStagesFit ? SB_STAGES : kStagesFit);
   static constexpr uint32_t kSmem = 1024 + kABytes + kStages * kStageB + kAAug + kBarBytes;
   static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
   static_assert(!W || NKC <= 2, "the wide layout keeps a whole tile's chunks in the ring");
@@ -193,6 +205,14 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         const int ab = it % AS;
         uint8_t* sAp = sA + ab * Cfg::kAPair;
         if (it >= AS) ptx::mbar_wait(&aempty[ab * NKC + c], (uint32_t)((it / AS - 1) & 1));
+#if defined(PCB_EXP) && PCB_EXP == 13
+        // experiment build: A loaded for the first two pairs only (A-latency share of the pace)
+        if (it >= 2) {
+          if (ptx::elect_one()) ptx::mbar_expect_tx(&afull[ab * NKC + c], 0u);
+          __syncwarp();
+          continue;
+        }
+#endif
         if (ptx::elect_one()) {
           ptx::mbar_expect_tx(&afull[ab * NKC + c], RT * Cfg::kTileBytes);
           ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (0 * NKC + c) * Cfg::kTileBytes, c * XC,
@@ -222,11 +242,19 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           if (ptx::elect_one()) {
             uint8_t* st = sB + stage * Cfg::kStageB;
             const bool last = c + 1 == NKC;  // the tile's augmented columns ride with its last chunk
+#if defined(PCB_EXP) && PCB_EXP == 10
+            // experiment build: B streamed for the first pair only (smem-write share of the MMA pace)
+            if (pr != blockIdx.x) {
+              ptx::mbar_expect_tx(&full[stage], 0u);
+            } else
+#endif
+            {
             ptx::mbar_expect_tx(&full[stage], Cfg::kBBytes + (last ? Cfg::kAugBytes : 0u));
             ptx::tma_load_2d(&tm_b, &full[stage], st, c * XC, tile * BN, pol);
             if (last) {
               ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes, 0, tile * BN, pol);
               ptx::tma_load_2d(&tm_baug, &full[stage], st + Cfg::kBBytes + BN * 16, 8, tile * BN, pol);
+            }
             }
           }
           __syncwarp();
@@ -308,16 +336,26 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     int abuf = 0;
     uint32_t aphase = 0;
     int it = 0;
+#if defined(PCB_EXP) && PCB_EXP == 14
+    // experiment build: MMA-warp cycle accounting -> state[8..11] (tempty, afull, full, total)
+    long long w_te = 0, w_af = 0, w_fu = 0;
+    const long long w_t0 = clock64();
+#define SB_TIMED(acc, stmt) do { const long long _c = clock64(); stmt; acc += clock64() - _c; } while (0)
+#else
+#define SB_TIMED(acc, stmt) stmt
+#endif
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
       for (int nt = 0; nt < ntiles; ++nt) {
-        ptx::mbar_wait(&tempty[abuf], aphase ^ 1u);
+#if !(defined(PCB_EXP) && PCB_EXP == 12)
+        SB_TIMED(w_te, ptx::mbar_wait(&tempty[abuf], aphase ^ 1u));
+#endif
         ptx::tc_fence_after();
         const uint32_t d0 = tmem + (uint32_t)(abuf * 256);
         for (int c = 0; c < NKC; ++c) {
           const int ab = it % AS;
           uint8_t* sAp = sA + ab * Cfg::kAPair;
-          if (nt == 0) ptx::mbar_wait(&afull[ab * NKC + c], (uint32_t)((it / AS) & 1));
-          ptx::mbar_wait(&full[stage], phase);
+          if (nt == 0) SB_TIMED(w_af, ptx::mbar_wait(&afull[ab * NKC + c], (uint32_t)((it / AS) & 1)));
+          SB_TIMED(w_fu, ptx::mbar_wait(&full[stage], phase));
           ptx::tc_fence_after();
           const uint64_t a0 = sdesc(ptx::smem_u32(sAp + (0 * NKC + c) * Cfg::kTileBytes));
           const uint64_t a1 = sdesc(ptx::smem_u32(sAp + (1 * NKC + c) * Cfg::kTileBytes));
@@ -352,8 +390,30 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         if (abuf == 0) aphase ^= 1u;
       }
     }
+#if defined(PCB_EXP) && PCB_EXP == 14
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd((unsigned long long*)state + 8, (unsigned long long)w_te);
+      atomicAdd((unsigned long long*)state + 9, (unsigned long long)w_af);
+      atomicAdd((unsigned long long*)state + 10, (unsigned long long)w_fu);
+      atomicAdd((unsigned long long*)state + 11, (unsigned long long)(clock64() - w_t0));
+    }
+#endif
+#undef SB_TIMED
+#if defined(PCB_EXP) && PCB_EXP == 12
+    // experiment build: MMA pipeline without the TMEM handoff (no epilogue)
+    __shared__ uint64_t done_bar;
+    if (ptx::elect_one()) { ptx::mbar_init(&done_bar, 1); ptx::fence_barrier_init(); }
+    __syncwarp();
+    if (ptx::elect_one()) ptx::umma_commit(&done_bar);
+    __syncwarp();
+    ptx::mbar_wait(&done_bar, 0);
+#endif
     }  // !W
-  } else if (warp >= 4 && warp < 4 + 4 * RT) {
+  } else if (warp >= 4 && warp < 4 + 4 * RT
+#if defined(PCB_EXP) && PCB_EXP == 12
+             && false
+#endif
+             ) {
     // ---------------- epilogue: warp (g, h) = lanes 32g.. of row tile h ----------------
     const int g = warp & 3, h = (warp - 4) >> 2;
     const float Bmax = bstat[0], dBmax = bstat[1];
@@ -414,7 +474,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       fetch_pair_b();
       ptx::mbar_wait(&tfull[tbar()], 0);
       ptx::tc_fence_after();
-      ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * ((fc_nx % BN) / 32), vA);
+      SB_TMEM_LD(tbase() + 32 * ((fc_nx % BN) / 32), vA);
     }
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
       const int64_t row = pr * PR + r_in;
@@ -445,7 +505,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           const int qe = nt == 0 ? ((q + q0) & (CH - 1)) : q;  // chunk of the tile held by cur
           if (q < CH - 1) {
             const int qn = nt == 0 ? ((q + 1 + q0) & (CH - 1)) : q + 1;
-            ptx::tmem_ld_32x32b_x32_async(taddr + 32 * qn, nxt);
+            SB_TMEM_LD(taddr + 32 * qn, nxt);
           } else {
             // this accumulator is fully read: hand it back, prefetch the next one
             ptx::tc_fence_before();
@@ -457,13 +517,13 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
               // first chunk of the next pair: read fc_nx only here, a pair after
               // its (two dependent) loads were issued
               const int qn = nt + 1 < ntiles ? 0 : (fc_nx % BN) / 32;
-              ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * qn, nxt);
+              SB_TMEM_LD(tbase() + 32 * qn, nxt);
             }
           }
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
-#if defined(PCB_EXP) && (PCB_EXP == 2 || PCB_EXP == 8)
+#if defined(PCB_EXP) && (PCB_EXP == 2 || PCB_EXP == 8 || PCB_EXP == 9 || PCB_EXP == 10 || PCB_EXP == 13)
           // experiment build: TMEM traffic only (MMA + TMEM-load ceiling)
           R1 = fminf(R1, v[0] + v[31]);
           continue;

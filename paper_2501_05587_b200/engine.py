@@ -394,7 +394,7 @@ class LloydEngine(ShardSequence):
     # Iterations after whose update the bf16 screen's rows are re-laid out by
     # label (the counting sort of that update): labels settle within a few
     # iterations, and a stale layout only costs epilogue skips, never results.
-    RELAYOUT_AT = (1, 3)
+    RELAYOUT_AT = tuple(int(x) for x in os.environ.get("PCB_RELAYOUT_AT", "1,3").split(",") if x)
 
     def _after_update(self, t: int) -> None:
         if self.variant in ("bf16s", "fp8s") and t in self.RELAYOUT_AT:
