@@ -386,6 +386,7 @@ class LloydEngine(ShardSequence):
     # -- centroid initialisation ------------------------------------------------
     def set_centroids(self, C) -> None:
         """Fixed centroids (additive `init=`), replicated on every rank."""
+        self._cold = False
         with torch.cuda.device(self.dev):
             Ct = torch.as_tensor(np.ascontiguousarray(C, dtype=self.dtype).reshape(self.k, self.d))
             self.C.copy_(Ct.to(self.dev))
@@ -472,6 +473,9 @@ class LloydEngine(ShardSequence):
             else:
                 L.call("pcb_centroids_from_acc_f64", _p(self.acc), self.k, self.d, _p(self.C),
                        _p(self.cnorm), _stream())
+        # means of random labels all sit near the global mean: the next assignment
+        # goes straight to 3xTF32 (see _assign)
+        self._cold = self.variant in ("bf16s", "fp8s") and os.environ.get("PCB_COLD_START", "1") != "0"
 
     # -- building blocks ---------------------------------------------------------
     def _sort_and_sum(self, labels, state) -> None:
@@ -495,7 +499,28 @@ class LloydEngine(ShardSequence):
                self.k, _p(self.S), _p(self.Q), _p(self.acc), _p(self.state), _stream())
         self.sums_valid = True
 
+    _cold = False
+
     def _assign(self, prev, new, acc, state) -> None:
+        if self.variant in ("bf16s", "fp8s") and self._cold:
+            # First assignment after the random init (clustering.py:298-300): every
+            # centroid is a mean of ~n/k random rows, near the global mean, and the
+            # low-precision screen certifies almost no row (100 % ambiguous at c3),
+            # so its resolver would bypass to 3xTF32 for every row anyway.  Run that
+            # resolver on all rows directly (identity list) and skip the screen.
+            self._cold = False
+            torch.arange(self.n, dtype=torch.int32, device=self.dev, out=self.ovf_list)
+            self.ovf_count.fill_(self.n)
+            self._kmark(0)
+            L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.ovf_list),
+                   _p(self.ovf_count), self.ld, _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels),
+                   _p(self.pnorm), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(new),
+                   _p(state), _stream())
+            self._kmark(1)
+            if acc is not None:
+                L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
+                       _stream())
+            return
         if self.variant in ("bf16s", "fp8s"):
             self.amb_count.zero_()
             self.two_count.zero_()
@@ -622,7 +647,7 @@ class LloydEngine(ShardSequence):
                     hist[t].copy_(self.labels[(t + 1) % 2], non_blocking=True)
             return evs
         if graph:
-            saved = self.sums_valid
+            saved, cold = self.sums_valid, self._cold
             try:
                 g = torch.cuda.CUDAGraph()
                 cs = torch.cuda.Stream(self.dev)
@@ -634,7 +659,7 @@ class LloydEngine(ShardSequence):
                 self._graph = g  # kept alive until the next run (its nodes reference our buffers)
                 return evs
             except Exception:  # capture unsupported here: run the same kernels eagerly
-                self.sums_valid = saved
+                self.sums_valid, self._cold = saved, cold
                 torch.cuda.synchronize()
         return body(False)
 
