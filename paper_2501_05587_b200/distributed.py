@@ -83,9 +83,8 @@ def repair_protocol(ops, comm, prev, new) -> None:
     k, d = ops.k, ops.d
     kd = k * d
     counts = ops.acc[kd:kd + k]
-    if int(ops.state[1].item()) != 0:           # stopped: nothing to do
-        return
-    if not bool((counts == 0).any().item()):
+    # one host read per iteration: not stopped and some cluster globally empty
+    if not bool(((counts == 0).any() & (ops.state[1] == 0)).item()):
         return
     dev = ops.acc.device
     key = torch.empty(3, dtype=torch.float64, device=dev)
