@@ -921,7 +921,10 @@ screen_exact_wide_kernel(const float* __restrict__ P, int d, const float* __rest
 // usable candidate list (too many candidates, or the bypass) are appended to
 // the overflow list for the 3xTF32 resolver.
 template <int DQ>
-__global__ void __launch_bounds__(256, DQ <= 4 ? 4 : 2)  // latency-bound: keep >= 32 warps per SM
+#ifndef PCB_EX_MINB
+#define PCB_EX_MINB 3  // measured at c3: 3 blocks (85 regs, no spills) beat 4 (64 regs, spills) and 2
+#endif
+__global__ void __launch_bounds__(256, DQ <= 4 ? PCB_EX_MINB : 2)  // latency-bound: many warps per SM
 screen_exact_kernel(const float* __restrict__ P, int d, const float* __restrict__ C,
                     const int* __restrict__ list, const int* __restrict__ count, int64_t bypass,
                     const int* __restrict__ cand, const int* __restrict__ cand_n, int32_t* __restrict__ labels,
