@@ -364,7 +364,24 @@ count_labels_kernel(const int32_t* __restrict__ labels, const int32_t* __restric
   for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
   __syncthreads();
   long long chg = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  // 16-byte loads (4 labels per thread and trip: the pass is a stream over
+  // 8 bytes per row), scalar tail
+  const bool al = ((reinterpret_cast<uintptr_t>(labels) | reinterpret_cast<uintptr_t>(prev)) & 15u) == 0;
+  const int64_t n4 = al ? n >> 2 : 0;
+  const int4* l4 = reinterpret_cast<const int4*>(labels);
+  const int4* p4 = reinterpret_cast<const int4*>(prev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 l = l4[i];
+    atomicAdd(&hist[l.x], 1);
+    atomicAdd(&hist[l.y], 1);
+    atomicAdd(&hist[l.z], 1);
+    atomicAdd(&hist[l.w], 1);
+    if (prev) {
+      const int4 q = p4[i];
+      chg += (q.x != l.x) + (q.y != l.y) + (q.z != l.z) + (q.w != l.w);
+    }
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int l = labels[i];
     atomicAdd(&hist[l], 1);
     if (prev) chg += (prev[i] != l);
