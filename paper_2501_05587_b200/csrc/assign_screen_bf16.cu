@@ -469,6 +469,14 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       const int l = lprev != nullptr ? lprev[mid_nx] : 0;
       fc_nx = (l >= 0 && l < k) ? l : 0;
     };
+#if defined(PCB_EXP) && PCB_EXP == 15
+    // experiment build: epilogue cycle accounting -> state[12..15] (tfull waits, full-path chunks, pair ends, total)
+    long long e_wait = 0, e_full = 0, e_end = 0;
+    const long long e_t0 = clock64();
+#define SB_ET(acc, stmt) do { const long long _c = clock64(); stmt; acc += clock64() - _c; } while (0)
+#else
+#define SB_ET(acc, stmt) stmt
+#endif
     if (blockIdx.x < npairs) {
       fetch_pair(blockIdx.x);
       fetch_pair_b();
@@ -512,7 +520,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             ptx::mbar_arrive(&tempty[tbar()]);
             tnext();
             if (nt + 1 < ntiles || !last_pair) {
-              ptx::mbar_wait(&tfull[tbar()], tphase());
+              SB_ET(e_wait, ptx::mbar_wait(&tfull[tbar()], tphase()));
               ptx::tc_fence_after();
               // first chunk of the next pair: read fc_nx only here, a pair after
               // its (two dependent) loads were issued
@@ -562,7 +570,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             if (__any_sync(0xffffffffu, mm <= thr_skip)) R1 = fminf(R1, mm);
 #else
             if (__any_sync(0xffffffffu, mm <= thr_skip)) {
-              screen_chunk_top2(km, msk, c0 + 32 * qe, twoE, R1, r1, R2, r2, cnt);
+              SB_ET(e_full, screen_chunk_top2(km, msk, c0 + 32 * qe, twoE, R1, r1, R2, r2, cnt));
 #if defined(PCB_EXP) && PCB_EXP == 6
               // experiment build: count full-path chunks per position (q + 4 * nt) in state[8..]
               if (lane == 0) atomicAdd((unsigned long long*)state + 8 + (nt < 8 ? nt * 4 + (q & 3) : 32), 1ull);
@@ -572,6 +580,9 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           }
         }
       }
+#if defined(PCB_EXP) && PCB_EXP == 15
+      const long long e_c0 = clock64();
+#endif
       if (CAND) {
         if (row < n) cand_n[row] = nc;
       } else {
@@ -609,7 +620,19 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           }
         }
       }
+#if defined(PCB_EXP) && PCB_EXP == 15
+      e_end += clock64() - e_c0;
+#endif
     }
+#if defined(PCB_EXP) && PCB_EXP == 15
+    if (lane == 0 && !CAND) {
+      atomicAdd((unsigned long long*)state + 12, (unsigned long long)e_wait);
+      atomicAdd((unsigned long long*)state + 13, (unsigned long long)e_full);
+      atomicAdd((unsigned long long*)state + 14, (unsigned long long)e_end);
+      atomicAdd((unsigned long long*)state + 15, (unsigned long long)(clock64() - e_t0));
+    }
+#endif
+#undef SB_ET
   }
   ptx::tc_fence_before();
   __syncthreads();
