@@ -151,9 +151,9 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
   uint64_t* aempty = afull + AS * NKC;                       // [AS][NKC]
   uint64_t* full = aempty + AS * NKC;                        // [STAGES]
   uint64_t* empty = full + STAGES;                           // [STAGES]
-  uint64_t* tfull = empty + STAGES;                          // [2] (W: per row tile)
-  uint64_t* tempty = tfull + 2;                              // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + STAGES;                          // [2 buffers][2 row tiles] (W: [row tile])
+  uint64_t* tempty = tfull + 4;                              // [2][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (k + BN - 1) / BN;
@@ -183,9 +183,9 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 4; ++b) {  // one row tile's accumulator each: its 4 epilogue warps release it
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], W ? 128 : 128 * RT);
+      ptx::mbar_init(&tempty[b], 128);
     }
     ptx::fence_barrier_init();
   }
@@ -344,48 +344,63 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
 #else
 #define SB_TIMED(acc, stmt) stmt
 #endif
+    // Per centroid tile: all K steps of row tile 0, handed to its 4 epilogue
+    // warps, then row tile 1 — each row tile's accumulator is released by its
+    // own warps, and row tile 0's epilogue starts while row tile 1's MMAs run.
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
+      const int ab = it % AS;
+      uint8_t* sAp = sA + ab * Cfg::kAPair;
       for (int nt = 0; nt < ntiles; ++nt) {
-#if !(defined(PCB_EXP) && PCB_EXP == 12)
-        SB_TIMED(w_te, ptx::mbar_wait(&tempty[abuf], aphase ^ 1u));
-#endif
-        ptx::tc_fence_after();
-        const uint32_t d0 = tmem + (uint32_t)(abuf * 256);
-        for (int c = 0; c < NKC; ++c) {
-          const int ab = it % AS;
-          uint8_t* sAp = sA + ab * Cfg::kAPair;
-          if (nt == 0) SB_TIMED(w_af, ptx::mbar_wait(&afull[ab * NKC + c], (uint32_t)((it / AS) & 1)));
-          SB_TIMED(w_fu, ptx::mbar_wait(&full[stage], phase));
-          ptx::tc_fence_after();
-          const uint64_t a0 = sdesc(ptx::smem_u32(sAp + (0 * NKC + c) * Cfg::kTileBytes));
-          const uint64_t a1 = sdesc(ptx::smem_u32(sAp + (1 * NKC + c) * Cfg::kTileBytes));
-          const uint64_t bd = sdesc(ptx::smem_u32(sB + stage * Cfg::kStageB));
-          if (ptx::elect_one()) {
+        int stc[NKC];
+        uint32_t phc[NKC];
 #pragma unroll
-            for (int ks = 0; ks < Cfg::kKSteps; ++ks) {  // 32 bytes of each row per MMA
-              const uint64_t off = (uint64_t)(ks * 32) >> 4;
-              mma_main(d0, a0 + off, bd + off, (c | ks) != 0);
-              if (RT == 2) mma_main(d0 + 128, a1 + off, bd + off, (c | ks) != 0);
-            }
-#if defined(PCB_EXP) && PCB_EXP == 8
-            if (false) {  // experiment build: no augmented step (keys wrong, timing only)
-#else
-            if (c + 1 == NKC) {  // augmented K step: + (|c|^2 + OFF) in three BF16 pieces
-#endif
-              const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
-              const uint64_t ba = ptx::sdesc_k_none(ptx::smem_u32(sB + stage * Cfg::kStageB + Cfg::kBBytes),
-                                                    BN * 16, 128);
-              ptx::umma_f16(d0, aa, ba, idesc, 1u);
-              if (RT == 2) ptx::umma_f16(d0 + 128, aa, ba, idesc, 1u);
-            }
-            ptx::umma_commit(&empty[stage]);
-            if (nt + 1 == ntiles) ptx::umma_commit(&aempty[ab * NKC + c]);  // A chunk free again
-          }
-          __syncwarp();
+        for (int c = 0; c < NKC; ++c) {
+          stc[c] = stage;
+          phc[c] = phase;
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
-        if (ptx::elect_one()) ptx::umma_commit(&tfull[abuf]);
-        __syncwarp();
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt) {
+#if !(defined(PCB_EXP) && PCB_EXP == 12)
+          SB_TIMED(w_te, ptx::mbar_wait(&tempty[abuf * 2 + rt], aphase ^ 1u));
+#endif
+          ptx::tc_fence_after();
+          const uint32_t d0 = tmem + (uint32_t)(abuf * 256 + rt * 128);
+#pragma unroll
+          for (int c = 0; c < NKC; ++c) {
+            if (rt == 0) {
+              if (nt == 0) SB_TIMED(w_af, ptx::mbar_wait(&afull[ab * NKC + c], (uint32_t)((it / AS) & 1)));
+              SB_TIMED(w_fu, ptx::mbar_wait(&full[stc[c]], phc[c]));
+              ptx::tc_fence_after();
+            }
+            const uint64_t a0 = sdesc(ptx::smem_u32(sAp + (rt * NKC + c) * Cfg::kTileBytes));
+            const uint64_t bd = sdesc(ptx::smem_u32(sB + stc[c] * Cfg::kStageB));
+            if (ptx::elect_one()) {
+#pragma unroll
+              for (int ks = 0; ks < Cfg::kKSteps; ++ks) {  // 32 bytes of each row per MMA
+                const uint64_t off = (uint64_t)(ks * 32) >> 4;
+                mma_main(d0, a0 + off, bd + off, (c | ks) != 0);
+              }
+#if defined(PCB_EXP) && PCB_EXP == 8
+              if (false) {  // experiment build: no augmented step (keys wrong, timing only)
+#else
+              if (c + 1 == NKC) {  // augmented K step: + (|c|^2 + OFF) in three BF16 pieces
+#endif
+                const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
+                const uint64_t ba = ptx::sdesc_k_none(ptx::smem_u32(sB + stc[c] * Cfg::kStageB + Cfg::kBBytes),
+                                                      BN * 16, 128);
+                ptx::umma_f16(d0, aa, ba, idesc, 1u);
+              }
+              if (rt + 1 == RT) {
+                ptx::umma_commit(&empty[stc[c]]);
+                if (nt + 1 == ntiles) ptx::umma_commit(&aempty[ab * NKC + c]);  // A chunk free again
+              }
+            }
+            __syncwarp();
+          }
+          if (ptx::elect_one()) ptx::umma_commit(&tfull[abuf * 2 + rt]);
+          __syncwarp();
+        }
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1u;
       }
@@ -429,7 +444,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     // accumulator; otherwise buffer b at columns b * 256 + h * 128
     const uint32_t tlane = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * (W ? 256 : 128));
     uint32_t tph = 0;  // W: phase of this row tile's accumulator
-    auto tbar = [&]() { return W ? h : abuf; };
+    auto tbar = [&]() { return W ? h : abuf * 2 + h; };
     auto tphase = [&]() { return W ? tph : aphase; };
     auto tbase = [&]() { return tlane + (uint32_t)(W ? 0 : abuf * 256); };
     auto tnext = [&]() {
