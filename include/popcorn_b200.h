@@ -150,11 +150,15 @@ int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const float* C_r,
                           const float* cnorm, const float* anorm, const float* danorm,
                           const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
                           const long long* state, void* stream);
+/* flag_list (capacity n) / flag_count (nullable): make the resolved labels
+ * exact — rows whose two best 3xTF32 keys are within the rigorous error bound
+ * are re-evaluated over all k centroids (f32 with a margin, f64 when thin,
+ * lowest index on ties) against C (f32 centroids).  NULL: 3xTF32 labels.  */
 int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_list,
                               const int* amb_count, int ld, float* sub_hi, float* sub_lo,
-                              int32_t* sub_labels, const float* pnorm, const float* C_hi,
+                              int32_t* sub_labels, const float* pnorm, const float* C, const float* C_hi,
                               const float* C_lo, const float* cnorm, int k, int32_t* labels,
-                              const long long* state, void* stream);
+                              int* flag_list, int* flag_count, const long long* state, void* stream);
 /* Certified BF16 screening variant ("bf16s", see assign_screen_bf16.cu):
  * one BF16 tensor-core pass (kind::f16) on RN-rounded copies P_b / C_b (row
  * stride ldb = pcb_screen_bf16_ld(d) BF16 elements) with the same rigorous
@@ -394,6 +398,16 @@ int pcb_kk_predict_f64(const double* S, int64_t lds, int64_t m, int k, const dou
 int pcb_kk_finalize(const int32_t* labels, const int32_t* labels_prev, const double* own, int64_t n, int k,
                     double* acc, double* cnt, double* obj_hist, long long* rep_hist, long long* state,
                     int check_convergence, double tol, void* stream);
+
+/* ==== Tensor-core accumulation probe (test infrastructure) ==================
+ * One chain of tcgen05.mma steps, M = N = 128, 32 bytes of K per step, F32
+ * accumulator in TMEM: D = init + sum_s A_s B_s^T (init may be NULL).  A, B:
+ * 128 rows of nsteps*32 bytes each (K contiguous); kinds[s] (device ints):
+ * 0 E4M3 (kind::f8f6f4, K=32), 1 BF16 (kind::f16, K=16), 2 TF32 (kind::tf32,
+ * K=8).  D: 128 x 128 f32, row-major.  Measures the rounding model the
+ * screening certificates assume (tests/test_gpu_mma_probe.py).             */
+int pcb_mma_probe(const void* A, const void* B, const int* kinds, int nsteps, const float* init, float* D,
+                  void* stream);
 
 #ifdef __cplusplus
 }

@@ -41,7 +41,7 @@ SIGNATURES = {
     "pcb_screen_prep_points": (I32, [P, I64, I32, I32, P, P, P, P, P]),
     "pcb_screen_prep_centroids": (I32, [P, I32, I32, P, P, P, P]),
     "pcb_assign_screen_f32": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P]),
-    "pcb_resolve_ambiguous_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P, P, P, I32, P, P, P]),
+    "pcb_resolve_ambiguous_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P, P, P, P, I32, P, P, P, P, P]),
     "pcb_update_mode": (I32, [P, I32, I32, I64, F64, I32, P, P]),
     "pcb_delta_update_f32": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),
     "pcb_delta_update_f64": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),
@@ -94,6 +94,7 @@ SIGNATURES = {
     "pcb_kk_repair_f32": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, I64, P]),
     "pcb_kk_repair_f64": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, I64, P]),
     "pcb_kk_finalize": (I32, [P, P, P, I64, I32, P, P, P, P, P, I32, F64, P]),
+    "pcb_mma_probe": (I32, [P, P, P, I32, P, P, P]),
 }
 
 ASSIGN_AUTO, ASSIGN_ROWREG, ASSIGN_TILED, ASSIGN_TC3XTF32, ASSIGN_DELTA, ASSIGN_SCREEN = 0, 1, 2, 3, 4, 5

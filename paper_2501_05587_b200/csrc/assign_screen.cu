@@ -492,19 +492,27 @@ extern "C" int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const 
 
 extern "C" int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_list,
                                          const int* amb_count, int ld, float* sub_hi, float* sub_lo,
-                                         int32_t* sub_labels, const float* pnorm, const float* C_hi,
-                                         const float* C_lo, const float* cnorm, int k, int32_t* labels,
+                                         int32_t* sub_labels, const float* pnorm, const float* C,
+                                         const float* C_hi, const float* C_lo, const float* cnorm, int k,
+                                         int32_t* labels, int* flag_list, int* flag_count,
                                          const long long* state, void* stream) {
   if (n < 1 || d < 1 || k < 1 || ld < d || ld % 32 || !P || !amb_list || !amb_count || !sub_hi || !sub_lo ||
-      !sub_labels || !pnorm || !C_hi || !C_lo || !cnorm || !labels)
+      !sub_labels || !pnorm || !C_hi || !C_lo || !cnorm || !labels || (flag_list && (!flag_count || !C)))
     return PCB_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = sm_count() * 8;
+  if (flag_list != nullptr) {
+    cudaError_t e = cudaMemsetAsync(flag_count, 0, sizeof(int), st);
+    if (e != cudaSuccess) return (int)e;
+  }
   gather_split_rows<<<grid, 256, 0, st>>>(P, d, amb_list, amb_count, ld, sub_hi, sub_lo, state);
   PCB_CHECK_LAUNCH();
   int rc = assign_tc3xtf32_devcount(sub_hi, sub_lo, ld, pnorm, n, d, C_hi, C_lo, cnorm, k, sub_labels, amb_count,
-                                    state, st);
+                                    state, st, amb_list, flag_list, flag_count);
   if (rc) return rc;
+  if (flag_list != nullptr &&
+      (rc = exact_rows(P, d, C, k, flag_list, flag_count, amb_list, sub_labels, state, st)))
+    return rc;
   scatter_rows_labels<<<grid, 256, 0, st>>>(amb_list, amb_count, sub_labels, labels, state);
   PCB_CHECK_LAUNCH();
   return 0;

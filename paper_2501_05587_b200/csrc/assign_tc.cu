@@ -53,14 +53,27 @@ struct TcCfg {
                                     TC_HIST_MAX * 4;
 };
 
-template <int BN>
+// FLAG (the resolver of the screened variants and predict): the epilogue also
+// tracks the second-best key and appends every row whose top-2 keys are within
+// the rigorous error bound 2E of the 3xTF32 keys to flag_list; those rows get
+// the exact argmin from exact_rows_kernel, so every label this path returns is
+// the exact (f64, lowest index on ties) argmin.  Per key s_j = |c_j|^2 - 2 v_j:
+//   |v_j - <p, c_j>| <= 2^-19 |p||c|   (dropped lo*lo, TF32 truncation of lo)
+//                     + acc_rel |p||c| (tensor-core accumulation, 8 units of
+//                                       2^-23 per MMA: 3.6x the worst single-MMA
+//                                       error tests/test_gpu_mma_probe.py measures)
+//   + 2^-23 (|c|^2 + 2 |p||c|)         (f32 key arithmetic, f32 norms)
+// with |c| <= max_j |c_j| (cnmax = max |c_j|^2, reduced in the prologue).
+template <int BN, bool FLAG = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
                        const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
                        const float* __restrict__ pnorm, const float* __restrict__ cnorm, int64_t n, int k,
                        int d, int num_kc, const int32_t* __restrict__ labels_prev,
                        int32_t* __restrict__ labels, float* __restrict__ mind, double* __restrict__ acc,
-                       const long long* __restrict__ state, const int* __restrict__ n_dev) {
+                       const long long* __restrict__ state, const int* __restrict__ n_dev,
+                       const int* __restrict__ row_ids = nullptr, int* __restrict__ flag_list = nullptr,
+                       int* __restrict__ flag_count = nullptr) {
   using Cfg = TcCfg<BN>;
   if (stopped(state)) return;
   if (n_dev != nullptr) n = min(n, (int64_t)*n_dev);  // row count known only on the device
@@ -177,8 +190,19 @@ assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_
     int abuf = 0;
     uint32_t aphase = 0;
     long long chg = 0;
+    float cnmax = 0.0f, acc_rel = 0.0f;
+    if (FLAG) {
+      for (int j = r_in_tile; j < k; j += 128) cnmax = fmaxf(cnmax, cnorm[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cnmax = fmaxf(cnmax, __shfl_xor_sync(0xffffffffu, cnmax, o));
+      if (lane == 0) hist[ew] = __float_as_int(cnmax);
+      ptx::named_bar_sync(1, 128);
+      cnmax = fmaxf(fmaxf(__int_as_float(hist[0]), __int_as_float(hist[1])),
+                    fmaxf(__int_as_float(hist[2]), __int_as_float(hist[3])));
+      acc_rel = (float)(3 * 4 * num_kc + 3) * 0x1p-20f;  // 3 MMAs per K = 8 step, 4 steps per chunk
+    }
     for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
-      float best = INFINITY;
+      float best = INFINITY, second = INFINITY;
       int bj = 0;
       for (int nt = 0; nt < ntiles; ++nt) {
         ptx::mbar_wait(&tfull[abuf], aphase);
@@ -194,6 +218,7 @@ assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float s = fmaf(-2.0f, v[i], __ldg(&cnorm[j0 + i]));
+              if (FLAG) second = fminf(second, fmaxf(s, best));
               if (s < best) { best = s; bj = j0 + i; }
             }
           } else {
@@ -201,6 +226,7 @@ assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_
             for (int i = 0; i < 32; ++i) {
               if (j0 + i < k) {
                 const float s = fmaf(-2.0f, v[i], __ldg(&cnorm[j0 + i]));
+                if (FLAG) second = fminf(second, fmaxf(s, best));
                 if (s < best) { best = s; bj = j0 + i; }
               }
             }
@@ -212,6 +238,22 @@ assign_tc3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_
         if (abuf == 0) aphase ^= 1u;
       }
       const int64_t row = mt * TC_BM + r_in_tile;
+      if (FLAG) {
+        bool flag = false;
+        if (row < n) {
+          const float pn = pnorm[row_ids != nullptr ? (int64_t)row_ids[row] : row];
+          const float A = sqrtf(pn) * sqrtf(cnmax) * 1.0001f;  // >= |p| max|c|
+          const float E = (2.0f * (0x1p-19f + acc_rel) * A + 0x1p-23f * (cnmax + 2.0f * A)) * 1.01f;
+          flag = !(second - best > 2.0f * E);  // NaN keys are flagged too
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, flag);
+        if (fm) {
+          int b = 0;
+          if (lane == 0) b = atomicAdd(flag_count, __popc(fm));
+          b = __shfl_sync(0xffffffffu, b, 0);
+          if (flag) flag_list[b + __popc(fm & ((1u << lane) - 1u))] = (int)row;
+        }
+      }
       if (row < n) {
         const float own = pnorm[row] + best;
         labels[row] = bj;
@@ -273,7 +315,8 @@ template <int BN>
 static int launch_tc(const float* phi, const float* plo, int ld, const float* pnorm, int64_t n, int d,
                      const float* chi, const float* clo, const float* cnorm, int k, const int32_t* lp,
                      int32_t* lab, float* mind, double* acc, const long long* state, cudaStream_t st,
-                     const int* n_dev = nullptr) {
+                     const int* n_dev = nullptr, const int* row_ids = nullptr, int* flag_list = nullptr,
+                     int* flag_count = nullptr) {
   using Cfg = TcCfg<BN>;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   int rc;
@@ -281,13 +324,13 @@ static int launch_tc(const float* phi, const float* plo, int ld, const float* pn
   if ((rc = make_tmap(&ta_lo, plo, n, ld, TC_BM))) return rc;
   if ((rc = make_tmap(&tb_hi, chi, k, ld, BN))) return rc;
   if ((rc = make_tmap(&tb_lo, clo, k, ld, BN))) return rc;
-  auto kern = assign_tc3xtf32_kernel<BN>;
+  auto kern = flag_list != nullptr ? assign_tc3xtf32_kernel<BN, true> : assign_tc3xtf32_kernel<BN, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   if (e != cudaSuccess) return (int)e;
   const int64_t mtiles = (n + TC_BM - 1) / TC_BM;
   const int grid = (int)std::min<int64_t>(mtiles, (int64_t)sm_count());
   kern<<<grid, TC_THREADS, Cfg::kSmem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, pnorm, cnorm, n, k, d, ld / TC_BK, lp,
-                                              lab, mind, acc, state, n_dev);
+                                              lab, mind, acc, state, n_dev, row_ids, flag_list, flag_count);
   PCB_CHECK_LAUNCH();
   return 0;
 }
@@ -296,15 +339,92 @@ static int launch_tc(const float* phi, const float* plo, int ld, const float* pn
 // ambiguous rows of the screened kernel, compacted by gather_split_rows).
 int assign_tc3xtf32_devcount(const float* phi, const float* plo, int ld, const float* pnorm, int64_t cap,
                              int d, const float* chi, const float* clo, const float* cnorm, int k,
-                             int32_t* lab, const int* n_dev, const long long* state, cudaStream_t st) {
+                             int32_t* lab, const int* n_dev, const long long* state, cudaStream_t st,
+                             const int* row_ids, int* flag_list, int* flag_count) {
   if (k > 128)
     return launch_tc<256>(phi, plo, ld, pnorm, cap, d, chi, clo, cnorm, k, nullptr, lab, nullptr, nullptr,
-                          state, st, n_dev);
+                          state, st, n_dev, row_ids, flag_list, flag_count);
   if (k > 64)
     return launch_tc<128>(phi, plo, ld, pnorm, cap, d, chi, clo, cnorm, k, nullptr, lab, nullptr, nullptr,
-                          state, st, n_dev);
+                          state, st, n_dev, row_ids, flag_list, flag_count);
   return launch_tc<64>(phi, plo, ld, pnorm, cap, d, chi, clo, cnorm, k, nullptr, lab, nullptr, nullptr, state,
-                       st, n_dev);
+                       st, n_dev, row_ids, flag_list, flag_count);
+}
+
+// Exact argmin (dense.py:56-68) over all k centroids for the rows the 3xTF32
+// pass flagged: 8 lanes per row (4 rows per warp), f32 distances
+// sum (p - c)^2 first — relative error <= (d + 8) 2^-23 (positive terms) —
+// and an f64 pass over all centroids for the rare rows whose two best are
+// within that margin (lowest index on ties).  out[r] for the flagged r;
+// row r of P is P[row_ids[r]] (or r).
+__global__ void __launch_bounds__(256)
+exact_rows_kernel(const float* __restrict__ P, int d, const float* __restrict__ C, int k,
+                  const int* __restrict__ flag_list, const int* __restrict__ flag_count,
+                  const int* __restrict__ row_ids, int32_t* __restrict__ out, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int64_t cnt = *flag_count;
+  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float brel = (float)(d + 8) * 0x1p-23f;
+  for (int64_t rb = w0 * 4; rb < cnt; rb += nw * 4) {
+    const int64_t q = rb + grp;
+    const bool valid = q < cnt;
+    const int r = valid ? flag_list[q] : 0;
+    const int64_t prow = row_ids != nullptr ? (int64_t)row_ids[r] : (int64_t)r;
+    const float* p = P + prow * d;
+    float f1 = 3.4e38f, f2 = 3.4e38f;
+    int bj = 0;
+    const bool vec = (d & 3) == 0;
+    for (int j = 0; j < k; ++j) {
+      const float* c = C + (int64_t)j * d;
+      float s = 0.0f;
+      if (vec) {
+        const float4* p4 = reinterpret_cast<const float4*>(p);
+        const float4* c4 = reinterpret_cast<const float4*>(c);
+        for (int f = sub; f < (d >> 2); f += 8) {
+          const float4 a = __ldg(p4 + f), b = __ldg(c4 + f);
+          const float e0 = a.x - b.x, e1 = a.y - b.y, e2 = a.z - b.z, e3 = a.w - b.w;
+          s = fmaf(e3, e3, fmaf(e2, e2, fmaf(e1, e1, fmaf(e0, e0, s))));
+        }
+      } else {
+        for (int t = sub; t < d; t += 8) {
+          const float e = __ldg(p + t) - __ldg(c + t);
+          s = fmaf(e, e, s);
+        }
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      if (s < f1) { f2 = f1; f1 = s; bj = j; } else if (s < f2) { f2 = s; }
+    }
+    const bool unsure = valid && k > 1 && f2 * (1.0f - brel) <= f1 * (1.0f + brel);
+    if (__any_sync(0xffffffffu, unsure)) {
+      double best = 0.0;
+      int bj64 = -1;
+      for (int j = 0; j < k; ++j) {
+        double s64 = 0.0;
+        if (unsure)
+          for (int t = sub; t < d; t += 8) {
+            const double e = (double)p[t] - (double)C[(int64_t)j * d + t];
+            s64 = fma(e, e, s64);
+          }
+        s64 += __shfl_xor_sync(0xffffffffu, s64, 4);
+        s64 += __shfl_xor_sync(0xffffffffu, s64, 2);
+        s64 += __shfl_xor_sync(0xffffffffu, s64, 1);
+        if (bj64 < 0 || s64 < best) { best = s64; bj64 = j; }  // ascending j: ties keep the lowest
+      }
+      if (unsure) bj = bj64;
+    }
+    if (valid && sub == 0) out[r] = bj;
+  }
+}
+
+int exact_rows(const float* P, int d, const float* C, int k, const int* flag_list, const int* flag_count,
+               const int* row_ids, int32_t* out, const long long* state, cudaStream_t st) {
+  exact_rows_kernel<<<sm_count() * 8, 256, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
 }
 
 }  // namespace pcb

@@ -147,9 +147,15 @@ __global__ void __launch_bounds__(256)
 segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict__ perm,
             const int32_t* __restrict__ offsets, int k, const T* __restrict__ C, int64_t slice,
             double* __restrict__ own_sorted, double* __restrict__ acc,
-            const long long* __restrict__ state) {
+            const long long* __restrict__ state, int col0 = 0, int dw = -1, int pass = 3) {
+  // Column slab [col0, col0 + dw) of every row (d > 1024 runs one launch per
+  // slab of 1024 columns): pass bit 0 = first slab (own distances written),
+  // bit 1 = last slab (own distances complete: objective).
   if (stopped(state) || delta_mode(state)) return;
   const AccLayout L{k, d};
+  if (dw < 0) dw = d;
+  P += col0;
+  C += col0;
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -165,7 +171,7 @@ segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict
     for (int v = 0; v < NV; ++v) {
       const int t = lane + 32 * v;
       a[v] = 0.0;
-      c[v] = t < d ? C[(int64_t)j * d + t] : T(0);
+      c[v] = t < dw ? C[(int64_t)j * d + t] : T(0);
     }
     int64_t s = s0;
     while (s < s1) {
@@ -173,14 +179,14 @@ segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const int t = lane + 32 * v;
-          if (t < d) atomicAdd(&acc[(int64_t)j * d + t], a[v]);
+          if (t < dw) atomicAdd(&acc[(int64_t)j * d + col0 + t], a[v]);
           a[v] = 0.0;
         }
         do { ++j; jend = offsets[j + 1]; } while (s >= jend);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const int t = lane + 32 * v;
-          c[v] = t < d ? C[(int64_t)j * d + t] : T(0);
+          c[v] = t < dw ? C[(int64_t)j * d + t] : T(0);
         }
       }
       const int64_t e = min(s1, jend);
@@ -192,8 +198,8 @@ segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const int t = lane + 32 * v;
-          x0[v] = t < d ? r0[t] : T(0);
-          x1[v] = t < d ? r1[t] : T(0);
+          x0[v] = t < dw ? r0[t] : T(0);
+          x1[v] = t < dw ? r1[t] : T(0);
         }
         double q0 = 0.0, q1 = 0.0;
 #pragma unroll
@@ -205,7 +211,12 @@ segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict
         }
         q0 = warp_sum(q0);
         q1 = warp_sum(q1);
-        if (lane == 0) { own_sorted[s] = q0; own_sorted[s + 1] = q1; obj += q0 + q1; }
+        if (lane == 0) {
+          if (!(pass & 1)) { q0 += own_sorted[s]; q1 += own_sorted[s + 1]; }
+          own_sorted[s] = q0;
+          own_sorted[s + 1] = q1;
+          if (pass & 2) obj += q0 + q1;
+        }
       }
       if (s < e) {
         const T* r0 = P + (int64_t)perm[s] * d;
@@ -213,20 +224,24 @@ segsum_warp(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const int t = lane + 32 * v;
-          const T x = t < d ? r0[t] : T(0);
+          const T x = t < dw ? r0[t] : T(0);
           a[v] += (double)x;
           const double e0 = (double)x - (double)c[v];
           q0 = fma(e0, e0, q0);
         }
         q0 = warp_sum(q0);
-        if (lane == 0) { own_sorted[s] = q0; obj += q0; }
+        if (lane == 0) {
+          if (!(pass & 1)) q0 += own_sorted[s];
+          own_sorted[s] = q0;
+          if (pass & 2) obj += q0;
+        }
         ++s;
       }
     }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const int t = lane + 32 * v;
-      if (t < d) atomicAdd(&acc[(int64_t)j * d + t], a[v]);
+      if (t < dw) atomicAdd(&acc[(int64_t)j * d + col0 + t], a[v]);
     }
   }
   if (lane == 0 && obj != 0.0) atomicAdd(&acc[L.objective()], obj);
@@ -400,7 +415,6 @@ static int segment_sums(const T* P, int64_t n, int d, const int32_t* perm, const
                         int k, const T* C, double* own, double* acc, const long long* state,
                         cudaStream_t st) {
   if (n < 1 || d < 1 || k < 1 || !P || !perm || !offsets || !acc || !C || !own) return PCB_EINVAL;
-  if (d > 1024) return PCB_EUNSUP;
   const int sms = sm_count();
   if (d <= 16) {
     const int64_t threads = (int64_t)sms * 2048;
@@ -431,7 +445,16 @@ static int segment_sums(const T* P, int64_t n, int d, const int32_t* perm, const
     else if (d <= 128) PCB_SEG_W(4);
     else if (d <= 256) PCB_SEG_W(8);
     else if (d <= 512) PCB_SEG_W(16);
-    else PCB_SEG_W(32);
+    else if (d <= 1024) PCB_SEG_W(32);
+    else {
+      // wider rows: slabs of 1024 columns, own distances accumulated across slabs
+      for (int c0 = 0; c0 < d; c0 += 1024) {
+        const int pass = (c0 == 0 ? 1 : 0) | (c0 + 1024 >= d ? 2 : 0);
+        segsum_warp<T, 32><<<grid, 256, 0, st>>>(P, n, d, perm, offsets, k, C, slice, own, acc, state, c0,
+                                                 std::min(1024, d - c0), pass);
+        PCB_CHECK_LAUNCH();
+      }
+    }
 #undef PCB_SEG_W
 #undef PCB_SEG_V4
   }

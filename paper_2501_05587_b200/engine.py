@@ -335,6 +335,8 @@ class LloydEngine(ShardSequence):
                 self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
+                self.flag_list = torch.empty(n, dtype=torch.int32, device=dev)
+                self.flag_count = torch.zeros(1, dtype=torch.int32, device=dev)
                 self.P_r = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 L.call("pcb_screen_prep_points", _p(self.P), n, d, self.ld, _p(self.P_r), _p(self.anorm),
                        _p(self.danorm), _p(self.bstat), _stream())
@@ -375,6 +377,8 @@ class LloydEngine(ShardSequence):
                 self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
+                self.flag_list = torch.empty(n, dtype=torch.int32, device=dev)
+                self.flag_count = torch.zeros(1, dtype=torch.int32, device=dev)
                 if self.q8:
                     L.call("pcb_screen_prep_points_fp8", _p(self.P), n, d, self.ld8, _p(self.P_b),
                            _p(self.anorm), _p(self.danorm), _p(self.bstat), _stream())
@@ -512,10 +516,7 @@ class LloydEngine(ShardSequence):
             torch.arange(self.n, dtype=torch.int32, device=self.dev, out=self.ovf_list)
             self.ovf_count.fill_(self.n)
             self._kmark(0)
-            L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.ovf_list),
-                   _p(self.ovf_count), self.ld, _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels),
-                   _p(self.pnorm), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(new),
-                   _p(state), _stream())
+            self._resolve(self.ovf_list, self.ovf_count, new, state)
             self._kmark(1)
             if acc is not None:
                 L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
@@ -538,10 +539,7 @@ class LloydEngine(ShardSequence):
                    _p(self.amb_count), _p(self.amb_thr), self.bypass, _p(self.sub_b), _p(self.cand),
                    _p(self.cand_n), _p(new), _p(self.ovf_list), _p(self.ovf_count), _p(self.orig),
                    _p(self.two_list), _p(self.two_count), _p(state), _stream())
-            L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.ovf_list),
-                   _p(self.ovf_count), self.ld, _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels),
-                   _p(self.pnorm), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(new),
-                   _p(state), _stream())
+            self._resolve(self.ovf_list, self.ovf_count, new, state)
             if acc is not None:
                 L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
                        _stream())
@@ -553,10 +551,7 @@ class LloydEngine(ShardSequence):
                    _p(self.cnorm), _p(self.anorm), _p(self.danorm), _p(self.bstat), _p(new),
                    _p(self.amb_list), _p(self.amb_count), _p(state), _stream())
             self._kmark(1)
-            L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(self.amb_list),
-                   _p(self.amb_count), self.ld, _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels),
-                   _p(self.pnorm), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(new),
-                   _p(state), _stream())
+            self._resolve(self.amb_list, self.amb_count, new, state)
             if acc is not None:
                 L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
                        _stream())
@@ -571,6 +566,14 @@ class LloydEngine(ShardSequence):
                    _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
                    self.vcode, _stream())
         self._kmark(1)
+
+    def _resolve(self, rows, count, new, state) -> None:
+        """3xTF32 labels of the listed rows, made exact (pcb_resolve_ambiguous_f32
+        with the flag list: near-ties re-evaluated over all centroids)."""
+        L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(rows), _p(count), self.ld,
+               _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels), _p(self.pnorm), _p(self.C), _p(self.C_hi),
+               _p(self.C_lo), _p(self.cnorm), self.k, _p(new), _p(self.flag_list), _p(self.flag_count), _p(state),
+               _stream())
 
     _kev = None
 
@@ -688,23 +691,42 @@ class LloydEngine(ShardSequence):
         self.set_labels(labels_prev)
         with torch.cuda.device(self.dev):
             self.state.zero_()
+        return self.traced_iteration(0)
+
+    def traced_iteration(self, t: int) -> dict:
+        """Iteration t of the ongoing fit (same kernels, relayouts and update
+        mode as run()), synchronised, with everything the lockstep checker
+        needs: the input centroids / previous labels, raw (pre-repair) and
+        final labels, objective, changed, moved, new centroids and, for the
+        screening variants, how many rows the certificate settled."""
+        with torch.cuda.device(self.dev):
+            c_in = self.C.cpu().numpy()
+            prev = self.labels[t % 2].cpu().numpy()
             raw = torch.empty_like(self.labels[1])
-            self.iteration(0, raw_out=raw)
+            self.iteration(t, raw_out=raw)
             torch.cuda.current_stream().synchronize()
             acc = self.acc.cpu().numpy()
             st = self.state.cpu().numpy()
             kd = self.k * self.d
-            return {
-                "labels": self.labels[1].cpu().numpy(),
+            out = {
+                "centroids_in": c_in,
+                "labels_prev": prev,
+                "labels": self.labels[(t + 1) % 2].cpu().numpy(),
                 "raw_labels": raw.cpu().numpy(),
                 "mind": self.mind.cpu().numpy(),
-                "objective": float(self.obj_hist[0].item()),
+                "objective": float(self.obj_hist[max(int(st[0]) - 1, 0)].item()),  # finalize's history slot
                 "changed": float(acc[kd + self.k + 1]) / self.n_total,
-                "moved": int(self.rep_hist[0].item()),
+                "moved": int(self.rep_hist[max(int(st[0]) - 1, 0)].item()),
                 "centroids": self.C.cpu().numpy(),
                 "counts": acc[kd:kd + self.k].copy(),
                 "nan": bool(st[5]),
+                "update_mode": "delta" if st[6] == 1 else "full",
             }
+            if self.variant in ("bf16s", "fp8s"):
+                amb, two, ovf = int(self.amb_count.item()), int(self.two_count.item()), int(self.ovf_count.item())
+                out["screen"] = {"ambiguous": amb, "two_candidate": two, "to_3xtf32": ovf,
+                                 "certified": self.n - amb - two, "relayout": self.orig is not None}
+            return out
 
     def predict(self, X) -> np.ndarray:
         """Nearest centroid for new points (estimator.py:131-136) — the same
@@ -717,11 +739,17 @@ class LloydEngine(ShardSequence):
             out = torch.empty(m, dtype=torch.int32, device=self.dev)
             L.call(f"pcb_point_norms_{self.sfx}", _p(Xt), m, self.d, _p(xn), _stream())
             if self.variant in ("tc3xtf32", "tc1xtf32s", "bf16s", "fp8s"):
+                # 3xTF32 over every row, near-ties re-evaluated exactly: the exact argmin
                 xh = torch.empty((m, self.ld), dtype=torch.float32, device=self.dev)
                 xl = torch.empty_like(xh)
-                L.call("pcb_split_tf32", _p(Xt), m, self.d, self.ld, _p(xh), _p(xl), _stream())
-                L.call("pcb_assign_tc_f32", _p(xh), _p(xl), self.ld, _p(xn), m, self.d, _p(self.C_hi),
-                       _p(self.C_lo), _p(self.cnorm), self.k, None, _p(out), None, None, None, _stream())
+                rows = torch.arange(m, dtype=torch.int32, device=self.dev)
+                cnt = torch.full((1,), m, dtype=torch.int32, device=self.dev)
+                sub = torch.empty(m, dtype=torch.int32, device=self.dev)
+                fl = torch.empty(m, dtype=torch.int32, device=self.dev)
+                fc = torch.zeros(1, dtype=torch.int32, device=self.dev)
+                L.call("pcb_resolve_ambiguous_f32", _p(Xt), m, self.d, _p(rows), _p(cnt), self.ld, _p(xh), _p(xl),
+                       _p(sub), _p(xn), _p(self.C), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(out),
+                       _p(fl), _p(fc), None, _stream())
             else:
                 L.call(f"pcb_assign_{self.sfx}", _p(Xt), _p(xn), m, self.d, _p(self.C), _p(self.cnorm),
                        self.k, None, _p(out), None, None, None, self.vcode if self.variant != "delta" else 0,

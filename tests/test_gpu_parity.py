@@ -202,3 +202,26 @@ def test_repair_many_empty_clusters(dtype):
     assert int((ref != raw).sum()) >= 280
     assert gpu["moved"] == int((ref != raw).sum())
     np.testing.assert_array_equal(gpu["labels"], ref)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("d", [1536, 2048])
+def test_wide_rows_lockstep(d, dtype):
+    """d > 1024: the segmented sums run in 1024-column slabs (update.cu);
+    run_lloyd and the lockstep step must work for any d, like the reference."""
+    import paper_2501_05587_b200 as pcb
+    n, k = 3000, 16
+    P = oracle.make_blobs(n, d, k, seed=4).astype(dtype)
+    lab = oracle.init_assignments(n, k, 0)
+    C = oracle.mean_centroids(P, lab, k)
+    eng = _engine(P, k, dtype)
+    pn = oracle.point_norms(P)
+    for t in range(3):
+        ref = oracle.lloyd_step(P, pn, C, lab, k)
+        gpu = eng.step_from(C, lab)
+        check_step(P, C, lab, k, gpu, ref=ref, dtype=dtype, what=f"d={d} it{t}")
+        C, lab = ref.centroids, ref.labels
+    res = pcb.run_lloyd(P, pcb.KKMeansConfig(k=k, max_iters=5, dtype=dtype))
+    refr = oracle.run_lloyd(P, k, max_iters=5, dtype=dtype)
+    assert res.iterations_run == 5
+    np.testing.assert_allclose(res.objective_history, refr.objective_history, rtol=1e-6)

@@ -1,0 +1,90 @@
+"""Steady-state lockstep parity at the benchmark shapes, strict north-star bar.
+
+The benchmark times iterations 3-22 of a fit, where the default E4M3 screen
+certifies ~96 % of rows, the rows are re-laid out by label, the centroid update
+runs in delta mode and two-candidate rows skip pass 2.  These tests put the
+engine into exactly that regime and check every step against the reference's
+own loop body (oracle.lloyd_step = clustering.py:309-317) on identical inputs:
+
+1. the oracle (pinned bit-for-bit to the reference) runs the fit from the
+   reference's init (init_assignments, seed 0) to iteration T0 = 10;
+2. the engine takes the oracle's centroids C_T0 and labels_{T0-1} and runs
+   iterations T0 .. T0+3 as a fit (relayout after T0, delta updates after);
+3. each GPU step is compared with oracle.lloyd_step from the same
+   (centroids, previous labels) under tests/parity.check_step_strict:
+   labels equal except rows with f64 top-2 relative gap < 1e-5 (the only
+   other admissible mismatch is a row the reference's f32 expansion mis-ranks,
+   where the GPU label is the exact argmin — counted), objective within 1e-6
+   relative (no allowance), centroids within 1e-5.
+
+Also asserted: the screen certified >= 90 % of the rows (the benchmarked path
+is the one exercised) and the iterations after T0 ran the delta update (at least one).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from parity import check_step_strict
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+SHAPES = {
+    "c3_shape": (200_000, 128, 1024),
+    "c5_shape": (100_000, 64, 4096),
+    "c4_shape": (50_000, 784, 256),
+}
+T0, STEPS = 10, 4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _report(name, rows):
+    out = os.environ.get("PCB_REPORT_DIR")
+    if out:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, f"steady_state_{name}.json"), "w") as f:
+            json.dump(rows, f, indent=1)
+
+
+@pytest.mark.parametrize("shape", sorted(SHAPES))
+def test_steady_state_lockstep_fp8s(shape):
+    from paper_2501_05587_b200.engine import LloydEngine
+    n, d, k = SHAPES[shape]
+    P = oracle.make_blobs(n, d, k, seed=0)
+    pn = oracle.point_norms(P)
+    # 1. the reference loop to iteration T0
+    lab = oracle.init_assignments(n, k, 0)
+    C = oracle.mean_centroids(P, lab, k)
+    for _ in range(T0):
+        st = oracle.lloyd_step(P, pn, C, lab, k)
+        C, lab = st.centroids, st.labels
+    # 2. the engine continues the fit from the same state, benchmark regime
+    eng = LloydEngine(P, k, variant="fp8s", max_iters=T0 + STEPS + 1)
+    eng.RELAYOUT_AT = (T0,)
+    eng.set_centroids(C)
+    eng.set_labels(lab)
+    eng.state.zero_()
+    rows = []
+    for t in range(T0, T0 + STEPS):
+        gpu = eng.traced_iteration(t)
+        ref = oracle.lloyd_step(P, pn, gpu["centroids_in"], gpu["labels_prev"], k)
+        r = check_step_strict(P, k, gpu, ref, what=f"{shape} it{t}")
+        r.update(iteration=t, update_mode=gpu["update_mode"], **gpu["screen"])
+        r["certified_frac"] = gpu["screen"]["certified"] / n
+        rows.append(r)
+    _report(shape, rows)
+    steady = rows[1:]  # after the relayout
+    assert all(r["relayout"] for r in steady)
+    assert any(r["update_mode"] == "delta" for r in steady), rows
+    assert min(r["certified_frac"] for r in steady) >= 0.90, rows
+    # a reference f32 mis-rank is rare at these gaps; more would mean a bug
+    assert sum(r["ref_f32_flips"] for r in rows) <= max(2, n // 100_000), rows
