@@ -140,13 +140,25 @@ def blas_threads() -> int:
     return os.cpu_count() or 1
 
 
+def config_keys(args, cfg, variant: str, world: int, launch: str) -> dict:
+    """The `config` object both arms print (same keys)."""
+    n, d, k = cfg["n"], cfg["d"], cfg["k"]
+    return {"workload": f"{args.config}: n={n} d={d} k={k}", "n": n, "d": d, "k": k, "variant": variant,
+            "parallelism": f"dp{world} row-sharded" if variant != "reference" else "host threads (numpy/OpenBLAS)",
+            "launch": launch,
+            "l2": "inputs larger than L2" if n * d * 4 > 126e6 else "inputs fit in L2 (no flush)"}
+
+
 def run_reference(args, cfg):
+    """The reference's CPU algorithm (oracle port of popcorn.run_lloyd, golden-
+    pinned to the unmodified reference) on the box's host cores, one Lloyd
+    iteration over a bounded row sample per step, extrapolated linearly in n;
+    the linearity is shown by timing three sample sizes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     n, d, k = cfg["n"], cfg["d"], cfg["k"]
     ns = _sample_rows(n, d, k, budget_s=args.ref_budget)
-    import torch
     # same synthetic recipe as the GPU arm, generated on the CPU for the sample
     centers = np.random.Generator(np.random.PCG64(args.seed)).uniform(-10, 10, size=(k, d))
     g = np.random.Generator(np.random.PCG64(args.seed + 17))
@@ -167,20 +179,64 @@ def run_reference(args, cfg):
     t_sample = float(np.mean(times))
     t_full = t_sample * n / ns
     value = 1.0 / t_full
+    # linearity: one iteration (same centroids) at 1/4 and 1/2 of the sample
+    lin = []
+    for frac in (0.25, 0.5, 1.0):
+        m = max(1000, int(ns * frac))
+        t0 = time.perf_counter()
+        oracle.lloyd_step(P[:m], pn[:m], C, lab[:m], k)
+        dt = time.perf_counter() - t0 if frac < 1.0 else t_sample
+        lin.append({"rows": m, "s_per_iter": dt, "ns_per_row": dt / m * 1e9})
     sample = f"{ns} of {n} rows, one Lloyd iteration per step, extrapolated x{n / ns:.1f} in n"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic blobs (host, PCG64)",
-        "config": {"workload": args.config, **cfg},
+        "config": config_keys(args, cfg, "reference", 1, "host"),
         "dists_per_sec": n * k / t_full,
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "linearity": lin},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` without torchrun: launch N ranks on this node
+    (torch.distributed.run, 127.0.0.1 rendezvous) and relay rank 0's line."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench: --gpus {args.gpus} needs {args.gpus} visible GPUs, this node has {have}", file=sys.stderr)
+        return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def nccl_summary(pattern: str):
+    """Rank count seen by NCCL's own INIT log lines (NCCL_DEBUG=INFO)."""
+    import glob
+    import re
+    ranks, lines = set(), []
+    for f in glob.glob(pattern):
+        try:
+            for ln in open(f, errors="replace"):
+                m = re.search(r"comm 0x[0-9a-f]+ rank (\d+) nRanks (\d+)", ln)
+                if m:
+                    ranks.add((int(m.group(1)), int(m.group(2))))
+                    if len(lines) < 8:
+                        lines.append(ln.strip()[-120:])
+        except OSError:
+            pass
+    nr = sorted({r[1] for r in ranks})
+    return {"nranks": nr, "ranks_seen": len({r[0] for r in ranks}), "init_lines": lines, "log": pattern}
 
 
 def main():
@@ -204,15 +260,23 @@ def main():
         cfg["n"] = args.n_override
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)
 
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        # NCCL's own INIT lines (rank / nRanks per communicator) go to a file
+        # per process so stdout keeps the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/pcb_bench_nccl.{os.environ.get('MASTER_PORT', '0')}.%p.log")
     import torch
     import torch.distributed as dist
     from paper_2501_05587_b200 import _lib
     from paper_2501_05587_b200.distributed import Comm, init_from_env, shard_range
     from paper_2501_05587_b200.engine import LloydEngine
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
     if world > 1:
         init_from_env("nccl")
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -229,8 +293,12 @@ def main():
         comm.offset = lo
     eng.init_labels_device(0, lo)  # init_assignments(n, k, 0), drawn on the device
     eng.init_centroids_from_labels()
-    for t in range(W):
-        eng.iteration(t)
+    eng.state.zero_()
+    if world > 1:
+        eng.run_multi(W)  # warm-up: empty-cluster repairs (iterations 0-2) run through the host protocol
+    else:
+        for t in range(W):
+            eng.iteration(t)
     torch.cuda.synchronize()
     if comm is not None:
         comm.barrier()
@@ -239,11 +307,14 @@ def main():
     sampler.start()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    # single rank: the K timed iterations are one captured CUDA graph (every
-    # decision is on the device; external event nodes time each iteration and
-    # the dominant kernel inside it); multi-rank: eager (host repair check)
-    use_graph = world == 1 and not args.no_graph
+    # the K timed iterations are one captured CUDA graph on every rank (every
+    # decision is on the device; multi-rank: the NCCL all-reduce is captured
+    # too and a repair, which steady state does not need, would park the
+    # iteration — checked below); external event nodes time each iteration
+    # and the dominant kernel inside it
+    use_graph = not args.no_graph
     evs = None
+    launches0 = int(_lib.load().pcb_launch_count())
     if use_graph:
         try:
             g = torch.cuda.CUDAGraph()
@@ -251,23 +322,32 @@ def main():
             cs.wait_stream(torch.cuda.current_stream())
             evs = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(5)] for _ in range(K)]
             with torch.cuda.stream(cs), torch.cuda.graph(g, stream=cs):
-                for s in range(K):
-                    eng.iteration(W + s, events=evs[s])
+                for s_ in range(K):
+                    eng.iteration(W + s_, events=evs[s_])
             torch.cuda.current_stream().wait_stream(cs)
         except Exception as exc:  # eager fallback, same kernels
             print(f"bench: graph capture failed ({exc!r}); timing eagerly", file=sys.stderr)
             use_graph = False
+            torch.cuda.synchronize()
+            launches0 = int(_lib.load().pcb_launch_count())
     if not use_graph:
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
     torch.cuda.synchronize()
+    if comm is not None:
+        comm.barrier()
     start.record()
     if use_graph:
         g.replay()
+    elif world > 1:
+        ed = eng.run_multi(W + K, make_events=lambda: [torch.cuda.Event(enable_timing=True) for _ in range(5)],
+                           t0=W)
+        evs = [ed[t] for t in sorted(ed)]
     else:
-        for s in range(K):
-            eng.iteration(W + s, events=evs[s])
+        for s_ in range(K):
+            eng.iteration(W + s_, events=evs[s_])
     end.record()
     torch.cuda.synchronize()
+    gpu_launches = int(_lib.load().pcb_launch_count()) - launches0
     clocks = sampler.stop()
     if comm is not None:
         comm.barrier()
@@ -275,13 +355,16 @@ def main():
     assign_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     upd_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
     kern_ms = float(np.mean([e[3].elapsed_time(e[4]) for e in evs]))
-    t = torch.tensor([ms, assign_ms, upd_ms, kern_ms], dtype=torch.float64, device=dev)
+    st = eng.state.cpu().numpy()
+    parked = int(st[1]) == eng.PENDING
+    t = torch.tensor([ms, assign_ms, upd_ms, kern_ms, float(parked)], dtype=torch.float64, device=dev)
     if comm is not None:
         comm.all_reduce_max(t)
-    ms, assign_ms, upd_ms, kern_ms = (float(x) for x in t.cpu())
-    st = eng.state.cpu().numpy()
+    ms, assign_ms, upd_ms, kern_ms, parked = (float(x) for x in t.cpu())
     if st[5] != 0:
         raise SystemExit("non-finite distances during the bench")
+    if parked:
+        raise SystemExit("an empty-cluster repair fell inside the timed iterations; rerun with more --warmup")
     amb = int(eng.amb_count.item()) if getattr(eng, "amb_count", None) is not None else None
     if amb is not None and getattr(eng, "two_count", None) is not None:
         amb += int(eng.two_count.item())  # two-candidate rows resolved without the second pass
@@ -291,15 +374,19 @@ def main():
     peaks, peak_src = _peaks()
     n_local = hi - lo
     flops = 2.0 * n_local * k * d  # algorithmic: one dot product per point-centroid pair
-    if d <= 32 and eng.variant not in ("tc3xtf32", "tc1xtf32s", "bf16s", "fp8s"):
-        # small-d FFMA path: report against HBM (bytes of P read + labels)
+    ffma_path = d <= 32 and eng.variant not in ("tc3xtf32", "tc1xtf32s", "bf16s", "fp8s")
+    if ffma_path:
+        # small-d FFMA path: SURVEY 8(d) puts it on the FFMA roof (AI ~28 flop/B > ridge);
+        # peak = 148 SMs x 128 FP32 lanes x 2 flop x the SM clock sampled under load
+        mhz = (clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        ffma_peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+        roof = {"bound": "ffma", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": ffma_peak,
+                "unit": "TFLOP/s", "traffic": None,
+                "peak_source": f"FFMA = 148 SM x 128 lanes x 2 flop x {mhz:.0f} MHz (sampled SM clock)"}
         traffic_alg = n_local * (4 * d + 8 + 4) + k * d * 4
-        roof = {"bound": "hbm", "achieved": traffic_alg / (kern_ms * 1e-3) / 1e9,
-                "peak": peaks["hbm_gbs"], "unit": "GB/s", "traffic": None,
-                "peak_source": f"{peak_src} copy bandwidth"}
+        roof["hbm_gbs_alg"] = traffic_alg / (kern_ms * 1e-3) / 1e9
+        roof["hbm_frac_alg"] = roof["hbm_gbs_alg"] / peaks["hbm_gbs"]
     else:
-        # kind::tf32 issues at half the bf16 rate; the burst bf16 figure is used
-        # (the kernel runs near max clocks, see "clocks"), i.e. the larger peak.
         tf32 = peaks["bf16_tflops"] / 2.0
         if eng.variant == "tc3xtf32":  # three TF32 products per dot product
             peak, src = tf32 / 3.0, "3xTF32 effective = bf16 burst / 6"
@@ -312,48 +399,46 @@ def main():
         roof = {"bound": "tensor", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": peak,
                 "unit": "TFLOP/s", "traffic": None, "peak_source": f"{peak_src} {src}"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    scr = {"res": "assign_screen_res_kernel", "pair": "assign_screen_2sm_kernel",
-           "stream": "assign_screen_kernel"}.get(os.environ.get("PCB_SCREEN_IMPL", "res"), "assign_screen_res_kernel")
-    roof["kernel"] = {"tc1xtf32s": scr, "tc3xtf32": "assign_tc3xtf32_kernel",
+    roof["kernel"] = {"tc1xtf32s": "assign_screen_res_kernel", "tc3xtf32": "assign_tc3xtf32_kernel",
                       "bf16s": "assign_screen_bf16_kernel", "fp8s": "assign_screen_bf16_kernel<F8>"}.get(
         eng.variant, f"assign[{eng.variant}]")
     roof["kernel_ms"] = kern_ms
-    roof["algorithmic_per_launch"] = f"2*n*k*d = {flops:.4g} flop" if roof["unit"] == "TFLOP/s" else \
-        f"{traffic_alg:.4g} bytes"
+    roof["algorithmic_per_launch"] = f"2*n*k*d = {flops:.4g} flop (per rank)"
     roof["assign_ms"] = assign_ms
     roof["update_ms"] = upd_ms
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{eng.variant}.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and world == 1:
         try:
             roof["traffic"] = json.load(open(prof)).get("bytes_per_launch")
         except Exception:
             pass
 
+    launch = ("cuda graph (K iterations" + (", NCCL all-reduce captured)" if world > 1 else ")")) if use_graph \
+        else "eager" + (" (lagged repair check)" if world > 1 else "")
     line = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32",  # inputs/results f32; the screen's operands are bf16/e4m3, certified exact
         "data": "synthetic blobs generated on device (centers U(-10,10), N(0,1) noise)",
-        "config": {"workload": f"{args.config}: n={n} d={d} k={k}", "n": n, "d": d, "k": k,
-                   "variant": eng.variant, "parallelism": f"dp{world} row-sharded",
-                   "launch": "cuda graph (K iterations)" if use_graph else "eager",
-                   "l2": "inputs larger than L2" if n * d * 4 > 126e6 else "inputs fit in L2 (no flush)"},
+        "config": config_keys(args, cfg, eng.variant, world, launch),
         "dists_per_sec": n * k / (ms_per_step * 1e-3),
         "roofline": roof,
-        # library kernels per steady-state iteration (counted from the ncu launch
-        # lists in profiles/), plus the relayouts that fall inside the window
-        "gpu_launches": {"fp8s": 21, "bf16s": 19, "tc1xtf32s": 15}.get(eng.variant, 9) * K
-                        + sum(1 for t in getattr(eng, "RELAYOUT_AT", ()) if W <= t < W + K
-                              and eng.variant in ("fp8s", "bf16s")),
+        # this library's kernels in the timed region: counted by the library
+        # itself (pcb_launch_count, one per launch or captured graph node)
+        "gpu_launches": gpu_launches,
         "screen_ambiguous_rows_last_iter": amb,
         "clocks": clocks,
     }
+    if world > 1:
+        line["nccl"] = nccl_summary(os.environ["NCCL_DEBUG_FILE"].replace("%p", "*").replace("%h", "*"))
     del eng, P
-    if n * d * 4 > 20e9:  # very large shards (c5): return the cache before the e2e fit
+    if (n // world) * d * 4 > 20e9:  # very large shards (c5): return the cache before the e2e fit
         torch.cuda.empty_cache()
 
-    if rank == 0 and world == 1 and not args.no_e2e:
-        line["e2e"] = e2e_run(args, cfg, dev)
+    if not args.no_e2e:
+        e2e = e2e_run(args, cfg, dev, comm, lo, hi)
+        if rank == 0:
+            line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ns = _sample_rows(n, d, k, budget_s=args.ref_budget)
         Ps = make_shard(ns, d, k, 0, args.seed, dev).cpu().numpy()
@@ -368,28 +453,89 @@ def main():
     return 0
 
 
-def e2e_run(args, cfg, dev):
-    """Through the public drop-in API with host buffers: run_lloyd(P_host, cfg)."""
+def e2e_run(args, cfg, dev, comm=None, lo=0, hi=None):
+    """Through the public drop-in API with host buffers: run_lloyd(P_host, cfg)
+    (one rank) or run_lloyd_sharded(P_host_shard, ...) on every rank (N > 1,
+    time = max over ranks).  Timed: validation, staged H2D of the points, prep,
+    device init, the max_iters iterations, D2H of labels / history / centroids.
+    Reported next to it: the same call with the reference's default contract
+    (label_history on: one n-label D2H per iteration) and, on one rank, a
+    phase breakdown of the first call (scripts-free, synchronised phases)."""
     import torch
     import paper_2501_05587_b200 as pcb
+    from paper_2501_05587_b200.distributed import run_lloyd_sharded
     n, d, k = cfg["n"], cfg["d"], cfg["k"]
-    P_host = make_shard(n, d, k, 0, args.seed, dev).cpu().numpy()
+    world = comm.world_size if comm is not None else 1
+    hi = n if hi is None else hi
+    P_host = make_shard(hi - lo, d, k, comm.rank if comm is not None else 0, args.seed, dev).cpu().numpy()
     if n * d * 4 > 20e9:
         torch.cuda.empty_cache()
-    # otherwise the allocator keeps the blocks of the timed leg's fit (same
-    # sizes), as in a process that has fitted before
     it = args.e2e_iters
-    c = pcb.KKMeansConfig(k=k, max_iters=it, record_label_history=False)
-    pcb.run_lloyd(P_host[: min(n, 100_000)], pcb.KKMeansConfig(k=k, max_iters=2))  # warm libs + staging buffers
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    res = pcb.run_lloyd(P_host, c)
-    wall = time.perf_counter() - t0
-    h2d = n * d * 4 + n * 4
+
+    def fit(history: bool):
+        c = pcb.KKMeansConfig(k=k, max_iters=it, record_label_history=history)
+        if comm is not None:
+            comm.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = run_lloyd_sharded(P_host, c, n, lo, comm) if world > 1 else pcb.run_lloyd(P_host, c)
+        wall = time.perf_counter() - t0
+        if comm is not None:
+            w = torch.tensor([wall], dtype=torch.float64, device=dev)
+            comm.all_reduce_max(w)
+            wall = float(w.item())
+        return res, wall
+
+    # warm the libraries and the pinned staging buffers (a process that has fitted before)
+    if world == 1:
+        pcb.run_lloyd(P_host[: min(n, 100_000)], pcb.KKMeansConfig(k=k, max_iters=2))
+    res, wall = fit(False)
+    res_h, wall_h = fit(True)
+    h2d = n * d * 4
     d2h = n * 4 + it * 16 + k * d * 4
-    return {"value": res.iterations_run / wall, "unit": "iters/s",
-            "h2d_bytes_per_step": h2d // it, "d2h_bytes_per_step": d2h // it,
-            "step": f"one run_lloyd(host numpy, max_iters={it}) call = {it} steps", "wall_s": wall}
+    out = {"value": res.iterations_run / wall, "unit": "iters/s",
+           "h2d_bytes_per_step": h2d // it, "d2h_bytes_per_step": d2h // it,
+           "step": f"one run_lloyd(host numpy, max_iters={it}, record_label_history=False) call = {it} steps"
+                   + (f" on each of {world} ranks (run_lloyd_sharded), max over ranks" if world > 1 else ""),
+           "wall_s": wall,
+           "default_contract": {"value": res_h.iterations_run / wall_h, "unit": "iters/s", "wall_s": wall_h,
+                                "label_history": True,
+                                "d2h_bytes_per_step": (d2h + it * n * 4) // it}}
+    if world == 1:
+        out["phases_ms"] = e2e_phases(P_host, k, it, dev)
+    return out
+
+
+def e2e_phases(P_host, k, it, dev):
+    """Where one run_lloyd call's time goes (synchronised after each phase;
+    same sequence as clustering.run_lloyd)."""
+    import torch
+    from paper_2501_05587_b200.engine import LloydEngine, h2d_staged
+    ph = {}
+
+    def mark(name, t0):
+        torch.cuda.synchronize()
+        ph[name] = (time.perf_counter() - t0) * 1e3
+        return time.perf_counter()
+
+    t = time.perf_counter()
+    Pd = h2d_staged(P_host, dev)
+    t = mark("h2d", t)
+    eng = LloydEngine(Pd, k, max_iters=it)
+    t = mark("prep", t)
+    eng.init_labels_device(0)
+    eng.init_centroids_from_labels()
+    eng.state.zero_()
+    t = mark("init", t)
+    for s_ in range(min(4, it)):
+        eng.iteration(s_)
+    t = mark("iterations_0_3", t)
+    for s_ in range(4, it):
+        eng.iteration(s_)
+    t = mark(f"iterations_4_{it - 1}", t)
+    eng.collect(None, ())
+    mark("collect", t)
+    return ph
 
 
 if __name__ == "__main__":

@@ -48,6 +48,9 @@ extern "C" {
 #define PCB_ASSIGN_SCREEN_FP8  7 /* same with E4M3 operands (kind::f8f6f4), scaled keys (f32, d <= 256) */
 
 int         pcb_abi_version(void);
+/* Kernels launched by this library so far in this process (launches recorded
+ * into a CUDA graph count once, at capture). */
+long long   pcb_launch_count(void);
 const char* pcb_error_string(int code);
 /* sm count / compute capability of `device`; returns PCB_ENODEV if not sm_100. */
 int pcb_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
@@ -291,23 +294,34 @@ int pcb_repair_f64(const double* P, int64_t n, int d, const double* C, int k, co
                    long long* state, void* scratch, int64_t scratch_bytes, double* sums,
                    void* stream);
 
-/* Multi-rank repair (host-orchestrated).  argmax_own writes
- * [own distance, global point index, local sorted position] of this rank's
- * best unmoved point (ties -> lowest index).  repair_apply moves the donor
- * (sorted position pos) on its owner rank and writes a delta record (f64,
- * d+4 words: p_donor | old label | d_objective | d_changed | valid=1);
- * non-owners zero it; after an all-reduce SUM every rank calls repair_commit
- * to patch its (already identical) accumulator.                           */
-int pcb_argmax_own(const double* own_sorted, const int32_t* perm, int64_t n, int64_t offset,
-                   double* out3, void* stream);
-int pcb_repair_apply_f32(const float* P, int d, const float* C, const int32_t* perm,
-                         const int32_t* labels_prev, int32_t* labels, double* own_sorted,
-                         int64_t pos, int j, double* delta, void* stream);
-int pcb_repair_apply_f64(const double* P, int d, const double* C, const int32_t* perm,
-                         const int32_t* labels_prev, int32_t* labels, double* own_sorted,
-                         int64_t pos, int j, double* delta, void* stream);
-int pcb_repair_commit(double* acc, int k, int d, int j, const double* delta, long long* state,
-                      void* stream);
+/* Batched multi-rank repair (one round per pass of clustering.py:126-138,
+ * distributed.repair_protocol):
+ *   pcb_repair_select:   this shard's E (<= 4096) unmoved points with the
+ *                        largest own distance, ranked (own desc, global id
+ *                        asc): out3E = E x [own, offset + id, sorted position]
+ *                        (padding -inf, 9e18, -1); scratch as pcb_repair_*.
+ *   pcb_repair_apply_batch_*: moves m of this rank (sorted positions pos[],
+ *                        target clusters j_list[], record slots[]): labels,
+ *                        own = -inf, delta records (d+4 words each, layout of
+ *                        pcb_repair_apply_*) into deltas (E records, zeroed
+ *                        by the caller, all-reduced SUM afterwards).
+ *   pcb_repair_commit_batch: every rank applies the E records in slot order
+ *                        (j_list[e] = cluster of slot e) to acc / state.
+ *   pcb_flag_global_empty: after the all-reduce: if a cluster is globally
+ *                        empty, saved <- acc and state[1] = 2 (repair pending:
+ *                        later kernels return; the host restores acc, runs the
+ *                        protocol, finalizes and clears the flag).          */
+int pcb_repair_select(const double* own_sorted, const int32_t* perm, int64_t n, int64_t offset, int E,
+                      double* out3E, void* scratch, int64_t scratch_bytes, void* stream);
+int pcb_repair_apply_batch_f32(const float* P, int d, const float* C, const int32_t* perm,
+                               const int32_t* labels_prev, int32_t* labels, double* own_sorted, const int* pos,
+                               const int* j_list, const int* slots, int m, double* deltas, void* stream);
+int pcb_repair_apply_batch_f64(const double* P, int d, const double* C, const int32_t* perm,
+                               const int32_t* labels_prev, int32_t* labels, double* own_sorted, const int* pos,
+                               const int* j_list, const int* slots, int m, double* deltas, void* stream);
+int pcb_repair_commit_batch(double* acc, int k, int d, int E, const int* j_list, const double* deltas,
+                            long long* state, void* stream);
+int pcb_flag_global_empty(const double* acc, int k, int d, double* saved, long long* state, void* stream);
 
 /* ---- finalize: c_j = sums_j / counts_j (empty -> 0, clustering.py:286-287),
  *      cnorm, optional TF32 hi/lo split of C (row stride ld), history

@@ -21,6 +21,7 @@ F64 = ctypes.c_double
 # name -> (restype, argtypes); kept in sync with include/popcorn_b200.h
 SIGNATURES = {
     "pcb_abi_version": (I32, []),
+    "pcb_launch_count": (ctypes.c_longlong, []),
     "pcb_error_string": (ctypes.c_char_p, [I32]),
     "pcb_device_info": (I32, [I32, P, P, P]),
     "pcb_count_nonfinite_f32": (I32, [P, I64, P, P]),
@@ -70,10 +71,11 @@ SIGNATURES = {
     "pcb_repair_scratch_bytes": (I64, [I32]),
     "pcb_repair_f32": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, I64, P, P]),
     "pcb_repair_f64": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, I64, P, P]),
-    "pcb_argmax_own": (I32, [P, P, I64, I64, P, P]),
-    "pcb_repair_apply_f32": (I32, [P, I32, P, P, P, P, P, I64, I32, P, P]),
-    "pcb_repair_apply_f64": (I32, [P, I32, P, P, P, P, P, I64, I32, P, P]),
-    "pcb_repair_commit": (I32, [P, I32, I32, I32, P, P, P]),
+    "pcb_repair_select": (I32, [P, P, I64, I64, I32, P, P, I64, P]),
+    "pcb_repair_apply_batch_f32": (I32, [P, I32, P, P, P, P, P, P, P, P, I32, P, P]),
+    "pcb_repair_apply_batch_f64": (I32, [P, I32, P, P, P, P, P, P, P, P, I32, P, P]),
+    "pcb_repair_commit_batch": (I32, [P, I32, I32, I32, P, P, P, P]),
+    "pcb_flag_global_empty": (I32, [P, I32, I32, P, P, P]),
     "pcb_finalize_f32": (I32, [P, I32, I32, I64, P, P, P, P, I32, P, P, P, I32, F64, P]),
     "pcb_finalize_f64": (I32, [P, I32, I32, I64, P, P, P, P, P, I32, F64, P]),
     "pcb_centroids_from_acc_f32": (I32, [P, I32, I32, P, P, P, P, I32, P]),

@@ -354,9 +354,12 @@ int assign_tc3xtf32_devcount(const float* phi, const float* plo, int ld, const f
 // Exact argmin (dense.py:56-68) over all k centroids for the rows the 3xTF32
 // pass flagged: 8 lanes per row (4 rows per warp), f32 distances
 // sum (p - c)^2 first — relative error <= (d + 8) 2^-23 (positive terms) —
-// and an f64 pass over all centroids for the rare rows whose two best are
-// within that margin (lowest index on ties).  out[r] for the flagged r;
-// row r of P is P[row_ids[r]] (or r).
+// and an f64 pass for the rare rows whose two best are within that margin
+// (f64 only for the centroids inside the margin; lowest index on ties).
+// out[r] for the flagged r; row r of P is P[row_ids[r]] (or r).
+// DQ > 0: d % 4 == 0 and d <= 32 DQ: the row's float4s stay in registers and
+// four centroids are in flight per step; DQ = 0: generic.
+template <int DQ>
 __global__ void __launch_bounds__(256)
 exact_rows_kernel(const float* __restrict__ P, int d, const float* __restrict__ C, int k,
                   const int* __restrict__ flag_list, const int* __restrict__ flag_count,
@@ -367,44 +370,74 @@ exact_rows_kernel(const float* __restrict__ P, int d, const float* __restrict__ 
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const float brel = (float)(d + 8) * 0x1p-23f;
+  const int d4 = d >> 2;
   for (int64_t rb = w0 * 4; rb < cnt; rb += nw * 4) {
     const int64_t q = rb + grp;
     const bool valid = q < cnt;
     const int r = valid ? flag_list[q] : 0;
     const int64_t prow = row_ids != nullptr ? (int64_t)row_ids[r] : (int64_t)r;
     const float* p = P + prow * d;
-    float f1 = 3.4e38f, f2 = 3.4e38f;
-    int bj = 0;
-    const bool vec = (d & 3) == 0;
-    for (int j = 0; j < k; ++j) {
+    auto dist32 = [&](int j) -> float {  // partial over this lane's columns
       const float* c = C + (int64_t)j * d;
       float s = 0.0f;
-      if (vec) {
-        const float4* p4 = reinterpret_cast<const float4*>(p);
-        const float4* c4 = reinterpret_cast<const float4*>(c);
-        for (int f = sub; f < (d >> 2); f += 8) {
-          const float4 a = __ldg(p4 + f), b = __ldg(c4 + f);
-          const float e0 = a.x - b.x, e1 = a.y - b.y, e2 = a.z - b.z, e3 = a.w - b.w;
-          s = fmaf(e3, e3, fmaf(e2, e2, fmaf(e1, e1, fmaf(e0, e0, s))));
-        }
-      } else {
-        for (int t = sub; t < d; t += 8) {
-          const float e = __ldg(p + t) - __ldg(c + t);
-          s = fmaf(e, e, s);
-        }
+      for (int t = sub; t < d; t += 8) {
+        const float e = __ldg(p + t) - __ldg(c + t);
+        s = fmaf(e, e, s);
       }
+      return s;
+    };
+    float f1 = 3.4e38f, f2 = 3.4e38f;
+    int bj = 0;
+    auto take = [&](float s, int j) {
       s += __shfl_xor_sync(0xffffffffu, s, 4);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       if (s < f1) { f2 = f1; f1 = s; bj = j; } else if (s < f2) { f2 = s; }
+    };
+    if constexpr (DQ > 0) {
+      float4 x[DQ];
+#pragma unroll
+      for (int u = 0; u < DQ; ++u) {
+        const int f = sub + 8 * u;
+        x[u] = f < d4 ? __ldg(reinterpret_cast<const float4*>(p) + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      int j = 0;
+      for (; j + 4 <= k; j += 4) {
+        float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int u = 0; u < DQ; ++u) {
+          const int f = sub + 8 * u;
+          if (f < d4) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const float4 c = __ldg(reinterpret_cast<const float4*>(C + (int64_t)(j + v) * d) + f);
+              const float e0 = x[u].x - c.x, e1 = x[u].y - c.y, e2 = x[u].z - c.z, e3 = x[u].w - c.w;
+              s[v] = fmaf(e3, e3, fmaf(e2, e2, fmaf(e1, e1, fmaf(e0, e0, s[v]))));
+            }
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) take(s[v], j + v);
+      }
+      for (; j < k; ++j) take(dist32(j), j);
+    } else {
+      for (int j = 0; j < k; ++j) take(dist32(j), j);
     }
-    const bool unsure = valid && k > 1 && f2 * (1.0f - brel) <= f1 * (1.0f + brel);
+    const float lim = f1 * (1.0f + brel) / (1.0f - brel);
+    const bool unsure = valid && k > 1 && f2 <= lim;
     if (__any_sync(0xffffffffu, unsure)) {
+      // f64 over the centroids whose f32 distance is within the margin of f1
       double best = 0.0;
       int bj64 = -1;
       for (int j = 0; j < k; ++j) {
+        float s = dist32(j);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        const bool cand = unsure && s <= lim;
+        if (!__any_sync(0xffffffffu, cand)) continue;
         double s64 = 0.0;
-        if (unsure)
+        if (cand)
           for (int t = sub; t < d; t += 8) {
             const double e = (double)p[t] - (double)C[(int64_t)j * d + t];
             s64 = fma(e, e, s64);
@@ -412,7 +445,7 @@ exact_rows_kernel(const float* __restrict__ P, int d, const float* __restrict__ 
         s64 += __shfl_xor_sync(0xffffffffu, s64, 4);
         s64 += __shfl_xor_sync(0xffffffffu, s64, 2);
         s64 += __shfl_xor_sync(0xffffffffu, s64, 1);
-        if (bj64 < 0 || s64 < best) { best = s64; bj64 = j; }  // ascending j: ties keep the lowest
+        if (cand && (bj64 < 0 || s64 < best)) { best = s64; bj64 = j; }  // ascending j: ties keep the lowest
       }
       if (unsure) bj = bj64;
     }
@@ -422,7 +455,14 @@ exact_rows_kernel(const float* __restrict__ P, int d, const float* __restrict__ 
 
 int exact_rows(const float* P, int d, const float* C, int k, const int* flag_list, const int* flag_count,
                const int* row_ids, int32_t* out, const long long* state, cudaStream_t st) {
-  exact_rows_kernel<<<sm_count() * 8, 256, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out, state);
+  const int grid = sm_count() * 8;
+#define PCB_XR(DQV) exact_rows_kernel<DQV><<<grid, 256, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out, state)
+  if (d % 4 != 0 || d > 256) PCB_XR(0);
+  else if (d <= 32) PCB_XR(1);
+  else if (d <= 64) PCB_XR(2);
+  else if (d <= 128) PCB_XR(4);
+  else PCB_XR(8);
+#undef PCB_XR
   PCB_CHECK_LAUNCH();
   return 0;
 }

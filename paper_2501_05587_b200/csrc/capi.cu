@@ -1,10 +1,15 @@
 // ABI plumbing: version, error strings, device query.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "pcb_common.cuh"
 #include "pcb_launch.cuh"
 
 namespace pcb {
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 int sm_count() {
   static int cached[64] = {0};
   int dev = 0;
@@ -44,3 +49,5 @@ extern "C" int pcb_device_info(int device, int* sm, int* major, int* minor) {
   if (minor) *minor = mn;
   return mj == 10 ? 0 : PCB_ENODEV;
 }
+
+extern "C" long long pcb_launch_count(void) { return pcb::g_launches.load(std::memory_order_relaxed); }

@@ -11,7 +11,15 @@
 #error "popcorn_b200 targets sm_100a only"
 #endif
 
-#define PCB_CHECK_LAUNCH() do { cudaError_t e__ = cudaGetLastError(); if (e__ != cudaSuccess) return (int)e__; } while (0)
+namespace pcb {
+// Host-side count of the kernels this library has launched (or recorded into
+// a CUDA graph being captured); pcb_launch_count() reads it.
+void count_launch();
+}  // namespace pcb
+
+// After every kernel launch: count it, then surface a launch error.
+#define PCB_CHECK_LAUNCH() do { pcb::count_launch(); cudaError_t e__ = cudaGetLastError(); \
+                                if (e__ != cudaSuccess) return (int)e__; } while (0)
 
 namespace pcb {
 

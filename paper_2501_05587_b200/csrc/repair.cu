@@ -26,16 +26,6 @@ namespace cg = cooperative_groups;
 
 namespace pcb {
 
-struct DonorKey {
-  double v;     // own distance
-  long long i;  // point id (global on multi-rank)
-  long long s;  // position in the label-sorted order (local)
-};
-
-__device__ __forceinline__ void argmax_merge(DonorKey& a, const DonorKey& b) {
-  if (b.v > a.v || (b.v == a.v && b.i < a.i)) a = b;
-}
-
 // Exact own distance (same evaluation as the update kernel): sum (p - c)^2 in f64.
 template <typename T>
 __device__ double pair_distance(const T* P, const T* C, int d, int64_t i, int j) {
@@ -47,10 +37,6 @@ __device__ double pair_distance(const T* P, const T* C, int d, int64_t i, int j)
   return q;
 }
 
-__device__ __forceinline__ DonorKey shfl_key(const DonorKey& k, int o) {
-  return DonorKey{__shfl_xor_sync(0xffffffffu, k.v, o), __shfl_xor_sync(0xffffffffu, k.i, o),
-                  __shfl_xor_sync(0xffffffffu, k.s, o)};
-}
 
 // Donors of one pass are the top-E unmoved points in (own distance desc,
 // point id asc) order: every argmax of the reference's loop excludes the points
@@ -78,23 +64,29 @@ __device__ __forceinline__ unsigned long long own_key(double v) {
   return (unsigned long long)ordered_bits(v);  // total order, -inf (taken) smallest
 }
 
+// Select mode (sel_out != nullptr; multi-rank repair, see pcb_repair_select):
+// no accumulator, no moves — one batch of B = sel_E selections whose ranked
+// keys (own distance, offset + point id, sorted position) go to sel_out.
 template <typename T>
 __global__ void __launch_bounds__(256)
 repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C, int k,
               const int32_t* __restrict__ perm, const int32_t* __restrict__ labels_prev,
               int32_t* __restrict__ labels, double* __restrict__ own, double* __restrict__ acc,
-              long long* __restrict__ state, RepairScratch* __restrict__ sc, double* __restrict__ S) {
-  if (stopped(state)) return;
+              long long* __restrict__ state, RepairScratch* __restrict__ sc, double* __restrict__ S,
+              int sel_E = 0, double* __restrict__ sel_out = nullptr, long long offset = 0) {
+  const bool select = sel_out != nullptr;
+  if (!select && stopped(state)) return;
   cg::grid_group grid = cg::this_grid();
   const AccLayout L{k, d};
   __shared__ int s_any;
   __shared__ unsigned int s_hist[256];
   __shared__ unsigned long long s_glob[256];
   __shared__ int s_wsum[8];
-  if (threadIdx.x == 0) s_any = 0;
+  if (threadIdx.x == 0) s_any = select ? 1 : 0;
   __syncthreads();
-  for (int j = threadIdx.x; j < k; j += blockDim.x)
-    if (acc[L.counts() + j] == 0.0) s_any = 1;
+  if (!select)
+    for (int j = threadIdx.x; j < k; j += blockDim.x)
+      if (acc[L.counts() + j] == 0.0) s_any = 1;
   __syncthreads();
   if (!s_any) return;  // identical decision in every block: no barrier reached
 
@@ -105,7 +97,9 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
     for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&sc->hist[0][0])[i] = 0ull;
   while (true) {
     grid.sync();  // counts of the previous pass are final
-    if (blockIdx.x == 0) {  // ascending list of the empty clusters (block-wide ballot scan)
+    if (select) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) sc->elist[0] = min(sel_E, RP_BATCH);
+    } else if (blockIdx.x == 0) {  // ascending list of the empty clusters (block-wide ballot scan)
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       int base = 0;
       for (int j0 = 0; j0 < k; j0 += blockDim.x) {
@@ -230,6 +224,18 @@ repair_kernel(const T* __restrict__ P, int64_t n, int d, const T* __restrict__ C
         }
       }
       grid.sync();
+      if (select) {  // ranked keys out, nothing moved
+        const int cnt = min(((volatile int*)&sc->sel_count)[0], B);
+        if (blockIdx.x == 0)
+          for (int e = threadIdx.x; e < B; e += blockDim.x) {
+            const bool ok = e < cnt;
+            const int q = ok ? sc->move_q[e] : -1;
+            sel_out[3 * e + 0] = ok ? own[q] : -INFINITY;
+            sel_out[3 * e + 1] = ok ? (double)(offset + perm[q]) : 9.0e18;
+            sel_out[3 * e + 2] = (double)q;
+          }
+        return;
+      }
       // apply the B moves, one warp per move
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       const int cntm = min(((volatile int*)&sc->sel_count)[0], B);
@@ -290,6 +296,40 @@ static int repair(const T* P, int64_t n, int d, const T* C, int k, const int32_t
   void* args[] = {(void*)&P,   (void*)&n,   (void*)&d,   (void*)&C,     (void*)&k,
                   (void*)&perm, (void*)&lp, (void*)&lab, (void*)&own, (void*)&acc,
                   (void*)&state, (void*)&sc, (void*)&S};
+  pcb::count_launch();
+  e = cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(256), args, 0, st);
+  return (int)e;
+}
+
+// Select mode launch: the E (<= RP_BATCH) unmoved points of this shard with
+// the largest own distance, ranked (own desc, global id asc), as
+// [own, offset + id, sorted position] triplets; padding (-inf, 9e18, -1).
+static int repair_select(const double* own, const int32_t* perm, int64_t n, int64_t offset, int E, double* out,
+                         void* scratch, int64_t scratch_bytes, cudaStream_t st) {
+  if (n < 1 || E < 1 || E > RP_BATCH || !own || !perm || !out || !scratch) return PCB_EINVAL;
+  if (n > INT32_MAX) return PCB_EUNSUP;
+  if (scratch_bytes < (int64_t)repair_scratch(1)) return PCB_EINVAL;
+  auto kern = repair_kernel<float>;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+  if (e != cudaSuccess) return (int)e;
+  if (per_sm < 1) return PCB_EUNSUP;
+  const int grid = repair_grid(per_sm);
+  RepairScratch* sc = (RepairScratch*)scratch;
+  const float* P = nullptr;
+  const float* C = nullptr;
+  int d = 1, k = 1;
+  const int32_t* lp = nullptr;
+  int32_t* lab = nullptr;
+  double* ownp = const_cast<double*>(own);
+  double* acc = nullptr;
+  long long* state = nullptr;
+  double* S = nullptr;
+  long long off = offset;
+  void* args[] = {(void*)&P,    (void*)&n,   (void*)&d,     (void*)&C,  (void*)&k,  (void*)&perm,
+                  (void*)&lp,   (void*)&lab, (void*)&ownp,  (void*)&acc, (void*)&state, (void*)&sc,
+                  (void*)&S,    (void*)&E,   (void*)&out,   (void*)&off};
+  pcb::count_launch();
   e = cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(256), args, 0, st);
   return (int)e;
 }
@@ -297,6 +337,11 @@ static int repair(const T* P, int64_t n, int d, const T* C, int k, const int32_t
 }  // namespace pcb
 
 extern "C" int64_t pcb_repair_scratch_bytes(int k) { return (int64_t)pcb::repair_scratch(k); }
+
+extern "C" int pcb_repair_select(const double* own_sorted, const int32_t* perm, int64_t n, int64_t offset, int E,
+                                 double* out3E, void* scratch, int64_t scratch_bytes, void* stream) {
+  return pcb::repair_select(own_sorted, perm, n, offset, E, out3E, scratch, scratch_bytes, (cudaStream_t)stream);
+}
 
 extern "C" int pcb_repair_f32(const float* P, int64_t n, int d, const float* C, int k,
                               const int32_t* perm, const int32_t* labels_prev, int32_t* labels,
@@ -315,109 +360,136 @@ extern "C" int pcb_repair_f64(const double* P, int64_t n, int d, const double* C
 }
 
 // ---------------------------------------------------------------------------
-// Multi-rank repair building blocks (host-orchestrated, rare path).  The
-// driver all-gathers the per-rank argmax keys, the owner rank applies the
-// donation locally and publishes a delta record that every rank commits to
-// its (already all-reduced, hence identical) accumulator.
-//   delta layout (f64, d+4 words): [ p_donor (d) | old label | d_objective |
-//                                    d_changed | valid ]
+// Multi-rank repair building blocks (host-orchestrated, rare path; see
+// distributed.repair_protocol).  Delta record of one move (f64, d+4 words):
+//   [ p_donor (d) | old label | d_objective | d_changed | valid ]
 // ---------------------------------------------------------------------------
 namespace pcb {
 
-__global__ void __launch_bounds__(1024)
-argmax_own_kernel(const double* __restrict__ own, const int32_t* __restrict__ perm, int64_t n,
-                  int64_t offset, double* __restrict__ out) {
-  __shared__ DonorKey s_warp[32];
-  DonorKey best{-INFINITY, offset + n, 0};
-  for (int64_t q = threadIdx.x; q < n; q += blockDim.x) {
-    DonorKey c{own[q], offset + (long long)perm[q], q};
-    argmax_merge(best, c);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) argmax_merge(best, shfl_key(best, o));
-  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = best;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) argmax_merge(best, s_warp[w]);
-    out[0] = best.v;
-    out[1] = (double)best.i;
-    out[2] = (double)best.s;
-  }
-}
-
+// Batched multi-rank moves: move m (one warp each) takes the donor at sorted
+// position pos[m] to cluster jl[m] and writes its delta record to slot sl[m]
+// of `deltas` (E records of d+4 words; the caller zeroes them, so after the
+// all-reduce every slot holds its owner's record).
 template <typename T>
-__global__ void repair_apply_kernel(const T* __restrict__ P, int d, const T* __restrict__ C,
-                                    const int32_t* __restrict__ perm,
-                                    const int32_t* __restrict__ labels_prev,
-                                    int32_t* __restrict__ labels, double* __restrict__ own,
-                                    int64_t pos, int j, double* __restrict__ delta) {
-  const int64_t donor = perm[pos];
-  for (int t = threadIdx.x; t < d; t += blockDim.x) delta[t] = (double)P[donor * d + t];
-  if (threadIdx.x == 0) {
-    const int old = labels[donor];
-    const double dnew = pair_distance(P, C, d, donor, j);
-    delta[d] = (double)old;
-    delta[d + 1] = dnew - own[pos];
-    delta[d + 2] = labels_prev ? (double)((j != labels_prev[donor]) - (old != labels_prev[donor])) : 0.0;
-    delta[d + 3] = 1.0;
-    labels[donor] = j;
-    own[pos] = -INFINITY;
+__global__ void repair_apply_batch_kernel(const T* __restrict__ P, int d, const T* __restrict__ C,
+                                          const int32_t* __restrict__ perm, const int32_t* __restrict__ labels_prev,
+                                          int32_t* __restrict__ labels, double* __restrict__ own,
+                                          const int* __restrict__ pos, const int* __restrict__ jl,
+                                          const int* __restrict__ sl, int m, double* __restrict__ deltas) {
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = w0; e < m; e += nw) {
+    const int64_t q = pos[e];
+    const int j = jl[e];
+    const int64_t donor = perm[q];
+    double* rec = deltas + (int64_t)sl[e] * (d + 4);
+    double part = 0.0;
+    for (int t = lane; t < d; t += 32) {
+      const double p = (double)P[donor * d + t];
+      rec[t] = p;
+      const double df = p - (double)C[(int64_t)j * d + t];
+      part = fma(df, df, part);
+    }
+    part = warp_sum(part);
+    if (lane == 0) {
+      const int old = labels[donor];
+      rec[d] = (double)old;
+      rec[d + 1] = part - own[q];
+      rec[d + 2] = labels_prev ? (double)((j != labels_prev[donor]) - (old != labels_prev[donor])) : 0.0;
+      rec[d + 3] = 1.0;
+      labels[donor] = j;
+      own[q] = -INFINITY;
+    }
   }
 }
 
-__global__ void repair_commit_kernel(double* __restrict__ acc, int k, int d, int j,
-                                     const double* __restrict__ delta, long long* __restrict__ state) {
+// Every rank applies the E all-reduced records in slot order (one block, so
+// every rank rounds the same way and the accumulators stay identical).
+__global__ void repair_commit_batch_kernel(double* __restrict__ acc, int k, int d, int E, const int* __restrict__ jl,
+                                           const double* __restrict__ deltas, long long* __restrict__ state) {
   const AccLayout L{k, d};
-  if (delta[d + 3] != 1.0) return;
-  const int old = (int)delta[d];
-  for (int t = threadIdx.x; t < d; t += blockDim.x) {
-    acc[(int64_t)old * d + t] -= delta[t];
-    acc[(int64_t)j * d + t] += delta[t];
+  for (int e = 0; e < E; ++e) {
+    const double* rec = deltas + (int64_t)e * (d + 4);
+    if (rec[d + 3] != 1.0) continue;
+    const int old = (int)rec[d], j = jl[e];
+    for (int t = threadIdx.x; t < d; t += blockDim.x) {
+      acc[(int64_t)old * d + t] -= rec[t];
+      acc[(int64_t)j * d + t] += rec[t];
+    }
+    if (threadIdx.x == 0) {
+      acc[L.counts() + old] -= 1.0;
+      acc[L.counts() + j] += 1.0;
+      acc[L.objective()] += rec[d + 1];
+      acc[L.changed()] += rec[d + 2];
+      state[kMoved] += 1;
+      state[kSumsStale] = 1;
+    }
+    __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    acc[L.counts() + old] -= 1.0;
-    acc[L.counts() + j] += 1.0;
-    acc[L.objective()] += delta[d + 1];
-    acc[L.changed()] += delta[d + 2];
-    state[kMoved] += 1;
-    state[kSumsStale] = 1;
-  }
+}
+
+// Multi-rank: after the all-reduce, a globally empty cluster makes this
+// iteration wait for the host's repair protocol — the accumulator is saved
+// and state[kStop] = 2 (every later kernel of the iteration and of the
+// iterations already enqueued returns at once; the host restores the
+// accumulator, repairs, finalizes and resumes; engine.ShardSequence).
+__global__ void __launch_bounds__(1024)
+flag_global_empty_kernel(const double* __restrict__ acc, int k, int d, double* __restrict__ saved,
+                         long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const AccLayout L{k, d};
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x)
+    if (acc[L.counts() + j] == 0.0) any = 1;
+  __syncthreads();
+  if (!any) return;
+  for (int64_t i = threadIdx.x; i < L.size(); i += blockDim.x) saved[i] = acc[i];
+  __syncthreads();
+  if (threadIdx.x == 0) state[kStop] = 2;
 }
 
 }  // namespace pcb
 
-extern "C" int pcb_argmax_own(const double* own_sorted, const int32_t* perm, int64_t n, int64_t offset,
-                              double* out3, void* stream) {
-  if (n < 1 || !own_sorted || !perm || !out3) return PCB_EINVAL;
-  pcb::argmax_own_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(own_sorted, perm, n, offset, out3);
+extern "C" int pcb_repair_apply_batch_f32(const float* P, int d, const float* C, const int32_t* perm,
+                                          const int32_t* labels_prev, int32_t* labels, double* own_sorted,
+                                          const int* pos, const int* j_list, const int* slots, int m, double* deltas,
+                                          void* stream) {
+  if (d < 1 || m < 0 || !P || !C || !perm || !labels || !own_sorted || !deltas || (m && (!pos || !j_list || !slots)))
+    return PCB_EINVAL;
+  if (m == 0) return 0;
+  pcb::repair_apply_batch_kernel<float><<<std::min(1024, (m + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
+      P, d, C, perm, labels_prev, labels, own_sorted, pos, j_list, slots, m, deltas);
   PCB_CHECK_LAUNCH();
   return 0;
 }
 
-extern "C" int pcb_repair_apply_f32(const float* P, int d, const float* C, const int32_t* perm,
-                                    const int32_t* labels_prev, int32_t* labels, double* own_sorted,
-                                    int64_t pos, int j, double* delta, void* stream) {
-  if (d < 1 || !P || !C || !perm || !labels || !own_sorted || !delta || pos < 0) return PCB_EINVAL;
-  pcb::repair_apply_kernel<float><<<1, 128, 0, (cudaStream_t)stream>>>(P, d, C, perm, labels_prev, labels,
-                                                                      own_sorted, pos, j, delta);
+extern "C" int pcb_repair_apply_batch_f64(const double* P, int d, const double* C, const int32_t* perm,
+                                          const int32_t* labels_prev, int32_t* labels, double* own_sorted,
+                                          const int* pos, const int* j_list, const int* slots, int m, double* deltas,
+                                          void* stream) {
+  if (d < 1 || m < 0 || !P || !C || !perm || !labels || !own_sorted || !deltas || (m && (!pos || !j_list || !slots)))
+    return PCB_EINVAL;
+  if (m == 0) return 0;
+  pcb::repair_apply_batch_kernel<double><<<std::min(1024, (m + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
+      P, d, C, perm, labels_prev, labels, own_sorted, pos, j_list, slots, m, deltas);
   PCB_CHECK_LAUNCH();
   return 0;
 }
 
-extern "C" int pcb_repair_apply_f64(const double* P, int d, const double* C, const int32_t* perm,
-                                    const int32_t* labels_prev, int32_t* labels, double* own_sorted,
-                                    int64_t pos, int j, double* delta, void* stream) {
-  if (d < 1 || !P || !C || !perm || !labels || !own_sorted || !delta || pos < 0) return PCB_EINVAL;
-  pcb::repair_apply_kernel<double><<<1, 128, 0, (cudaStream_t)stream>>>(P, d, C, perm, labels_prev, labels,
-                                                                       own_sorted, pos, j, delta);
+extern "C" int pcb_repair_commit_batch(double* acc, int k, int d, int E, const int* j_list, const double* deltas,
+                                       long long* state, void* stream) {
+  if (k < 1 || d < 1 || E < 1 || !acc || !j_list || !deltas || !state) return PCB_EINVAL;
+  pcb::repair_commit_batch_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(acc, k, d, E, j_list, deltas, state);
   PCB_CHECK_LAUNCH();
   return 0;
 }
 
-extern "C" int pcb_repair_commit(double* acc, int k, int d, int j, const double* delta,
-                                 long long* state, void* stream) {
-  if (k < 1 || d < 1 || !acc || !delta || !state) return PCB_EINVAL;
-  pcb::repair_commit_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(acc, k, d, j, delta, state);
+extern "C" int pcb_flag_global_empty(const double* acc, int k, int d, double* saved, long long* state,
+                                     void* stream) {
+  if (k < 1 || d < 1 || !acc || !saved || !state) return PCB_EINVAL;
+  pcb::flag_global_empty_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(acc, k, d, saved, state);
   PCB_CHECK_LAUNCH();
   return 0;
 }

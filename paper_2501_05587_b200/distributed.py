@@ -9,10 +9,12 @@ fused f64 accumulator [sums k*d | counts k | objective | changed]
 centroids stay bitwise identical across ranks.
 
 Empty-cluster repair (clustering.py:111-139) needs global decisions; it is
-rare and host-orchestrated: one host read of the global counts per iteration
-decides whether it runs; per donor, each rank's best unmoved point
-(argmax_own) is all-gathered, the owner applies the move and publishes a
-delta that every rank commits after an all_reduce.
+rare (the first iterations) and host-orchestrated without costing the common
+case a host round trip: after the all-reduce a device flag parks an
+iteration whose global counts show an empty cluster, the host notices it a
+couple of iterations later (ShardSequence.run_multi reads the state with a
+lag), and the batched protocol below runs one all_gather + one all_reduce per
+pass of the reference's repair loop.
 """
 from __future__ import annotations
 
@@ -68,41 +70,49 @@ class Comm:
 
 
 
-def repair_protocol(ops, comm, prev, new) -> None:
-    """Global empty-cluster repair across ranks (clustering.py:111-139).
+REPAIR_BATCH = 4096  # repair.cu RP_BATCH: selections per round
 
-    Same semantics as the single-rank kernel: passes over the clusters empty at
-    the start of each pass, ascending; donor = unmoved point with the largest
-    own distance, lowest *global* index on ties.  Every rank holds the same
-    all-reduced accumulator, so every rank sees the same empty set; per donor
-    the ranks all-gather their best (own, global index, local position) key,
-    the owner applies the move and publishes a delta record that all ranks
-    commit after an all-reduce.  Only runs (one host read of the counts per
-    iteration) when a cluster is globally empty.
+
+def repair_protocol(ops, comm, prev, new) -> None:
+    """Global empty-cluster repair across ranks (clustering.py:111-139), batched.
+
+    Same semantics as the single-rank kernel (repair.cu): passes over the
+    clusters empty at the start of each pass, ascending; the e-th of them
+    receives the e-th unmoved point in (own distance desc, global index asc)
+    order.  Every rank holds the same all-reduced accumulator, hence the same
+    empty set.  One round per pass (per 4096 empties): each rank ranks its E
+    best unmoved points on the device (pcb_repair_select), the keys are
+    all-gathered and merged on the host (the global top-E is among the
+    per-rank top-E lists), each owner applies its moves and writes their delta
+    records into its slots of a zeroed E x (d+4) buffer, one all-reduce
+    completes the buffer, and every rank commits all E records in slot order.
+    Runs only when a cluster is globally empty (the iteration parked itself,
+    ShardSequence.run_multi).
     """
     k, d = ops.k, ops.d
     kd = k * d
-    counts = ops.acc[kd:kd + k]
-    # one host read per iteration: not stopped and some cluster globally empty
-    if not bool(((counts == 0).any() & (ops.state[1] == 0)).item()):
+    if int(ops.state[1]) != 0:  # stopped (converged): nothing to repair
         return
-    dev = ops.acc.device
-    key = torch.empty(3, dtype=torch.float64, device=dev)
-    delta = torch.empty(d + 4, dtype=torch.float64, device=dev)
     while True:
-        empties = torch.nonzero(counts == 0).flatten().tolist()
+        counts = ops.acc[kd:kd + k]
+        empties = torch.nonzero(counts == 0).flatten().tolist()  # host read, rare path
         if not empties:
             return
-        for j in empties:
-            ops.argmax_own(comm.offset, key)
-            keys = torch.stack(comm.all_gather(key)).cpu().numpy()
-            order = np.lexsort((keys[:, 1], -keys[:, 0]))   # max own, then min global index
-            win = int(order[0])
-            delta.zero_()
-            if win == comm.rank:
-                ops.repair_apply(prev, new, int(keys[win, 2]), int(j), delta)
-            comm.all_reduce_sum(delta)
-            ops.repair_commit(int(j), delta)
+        for c0 in range(0, len(empties), REPAIR_BATCH):
+            J = empties[c0:c0 + REPAIR_BATCH]
+            E = len(J)
+            keys = ops.repair_select(comm.offset, E)                      # (E, 3) on the device
+            allk = torch.stack(comm.all_gather(keys)).cpu().numpy()       # (world, E, 3)
+            flat = allk.reshape(-1, 3)
+            owner = np.repeat(np.arange(allk.shape[0]), E)
+            order = np.lexsort((flat[:, 1], -flat[:, 0]))[:E]             # own desc, global index asc
+            mine = [(e, int(flat[i, 2])) for e, i in enumerate(order) if owner[i] == comm.rank]
+            deltas = ops.new_deltas(E)
+            if mine:
+                ops.repair_apply_batch(prev, new, [q for _, q in mine], [J[e] for e, _ in mine],
+                                       [e for e, _ in mine], deltas)
+            comm.all_reduce_sum(deltas)
+            ops.repair_commit_batch(J, deltas)
 
 
 def run_lloyd_sharded(points_local, cfg: KKMeansConfig, n_total: int, offset: int,

@@ -199,9 +199,11 @@ class ShardSequence:
     """The per-rank Lloyd iteration, independent of where the numbers live.
 
     Subclasses provide the numeric steps (`_assign`, `_sort_and_sum`,
-    `_repair_local`, `_finalize`) and the multi-rank repair primitives
-    (`argmax_own`, `repair_apply`, `repair_commit`); the order of operations,
-    the single all-reduce of the fused accumulator and the global repair
+    `_repair_local`, `_finalize`) and the multi-rank primitives
+    (`flag_pending`, `restore_pending`, `snapshot_state` / `read_snapshot`,
+    `repair_select`, `new_deltas`, `repair_apply_batch`,
+    `repair_commit_batch`); the order of operations, the single all-reduce of
+    the fused accumulator, the lagged multi-rank loop and the global repair
     protocol live here once, shared by the CUDA engine and the CPU test
     double used by the gloo tests.
     Attributes used: labels[2], acc, state, k, d, comm.
@@ -230,10 +232,66 @@ class ShardSequence:
         self._allreduce(self.acc)                               # the one collective per iteration
         if raw_out is not None:
             raw_out.copy_(new)
-        self._repair(prev, new)                                 # clustering.py:111-139
+        if self._multi():
+            # a globally empty cluster parks the iteration (state[1] = 2) for the
+            # host's repair protocol; no host round trip when none is empty
+            self.flag_pending()
+        else:
+            self._repair_local(prev, new)                       # clustering.py:111-139
         self._finalize(check_convergence, tol)                  # clustering.py:316-324
         if events is not None:
             events[2].record()
+
+    def _multi(self) -> bool:
+        return self.comm is not None and self.comm.world_size > 1
+
+    # -- multi-rank fit: enqueue ahead, check the repair flag with a lag -----------
+    PENDING = 2  # state[1] value of an iteration parked for the host repair
+
+    def run_multi(self, max_iters: int, check_convergence: bool = False, tol: float = 0.0,
+                  make_events=None, hist=None, lag: int = 2, t0: int = 0) -> dict:
+        """Iterations 0 .. max_iters-1 across ranks with no host synchronisation
+        per iteration: each iteration is enqueued, then the device state of the
+        iteration `lag` back is read (pinned copy + event).  Empty clusters are
+        rare (the first iterations); an iteration that needs the repair parks
+        itself on the device, every iteration enqueued after it returns at once,
+        and when the host sees the flag it restores the accumulator, runs the
+        batched protocol (distributed.repair_protocol) and the finalize, and
+        resumes from the next iteration.  Every rank holds the same all-reduced
+        accumulator, so every rank takes the same branch at the same iteration.
+        Iterations t0 .. max_iters-1; returns {t: events}."""
+        from collections import deque
+        evs = {}
+        queue = deque()
+        t = t0
+        while t < max_iters:
+            ev = make_events() if make_events is not None else None
+            self.iteration(t, check_convergence, tol, ev)
+            if hist is not None:
+                hist[t].copy_(self.labels[(t + 1) % 2], non_blocking=True)
+            evs[t] = ev
+            queue.append((t, self.snapshot_state()))
+            t += 1
+            while queue and (len(queue) > lag or t >= max_iters):
+                tq, snap = queue.popleft()
+                flag = int(self.read_snapshot(snap)[1])
+                if flag == self.PENDING:
+                    self.resume_after_repair(tq, check_convergence, tol)
+                    if hist is not None:
+                        hist[tq].copy_(self.labels[(tq + 1) % 2], non_blocking=True)
+                    t = tq + 1
+                    queue.clear()
+                elif flag != 0:  # converged: the rest are no-ops
+                    t = max_iters
+                    queue.clear()
+        return evs
+
+    def resume_after_repair(self, t: int, check_convergence: bool, tol: float) -> None:
+        from .distributed import repair_protocol
+        prev, new = self.labels[t % 2], self.labels[(t + 1) % 2]
+        self.restore_pending()
+        repair_protocol(self, self.comm, prev, new)
+        self._finalize(check_convergence, tol)
 
     def _update(self, prev, new) -> None:
         self._sort_and_sum(new, self.state)
@@ -244,13 +302,6 @@ class ShardSequence:
     def _allreduce(self, t) -> None:
         if self.comm is not None and self.comm.world_size > 1:
             self.comm.all_reduce_sum(t)
-
-    def _repair(self, prev, new) -> None:
-        if self.comm is not None and self.comm.world_size > 1:
-            from .distributed import repair_protocol
-            repair_protocol(self, self.comm, prev, new)
-        else:
-            self._repair_local(prev, new)
 
 
 class LloydEngine(ShardSequence):
@@ -293,6 +344,8 @@ class LloydEngine(ShardSequence):
             self.mind = torch.empty(n, dtype=td, device=dev)
             self.acc_size = kk * d + kk + 2
             self.acc = torch.zeros(self.acc_size, dtype=torch.float64, device=dev)
+            # multi-rank: the accumulator of an iteration parked for the host repair
+            self.acc_saved = torch.zeros_like(self.acc) if comm is not None and comm.world_size > 1 else None
             self.perm = torch.empty(n, dtype=torch.int32, device=dev)
             self.own = torch.empty(n, dtype=torch.float64, device=dev)  # own distances, sorted order
             self.offsets = torch.empty(kk + 1, dtype=torch.int32, device=dev)
@@ -598,16 +651,50 @@ class LloydEngine(ShardSequence):
                    int(check_convergence), float(tol), _stream())
 
     # -- multi-rank repair primitives (distributed.repair_protocol) ---------------
-    def argmax_own(self, offset: int, key_out) -> None:
-        L.call("pcb_argmax_own", _p(self.own), _p(self.perm), self.n, offset, _p(key_out), _stream())
-
-    def repair_apply(self, prev, new, pos: int, j: int, delta) -> None:
-        L.call(f"pcb_repair_apply_{self.sfx}", _p(self.P), self.d, _p(self.C), _p(self.perm), _p(prev),
-               _p(new), _p(self.own), int(pos), int(j), _p(delta), _stream())
-
-    def repair_commit(self, j: int, delta) -> None:
-        L.call("pcb_repair_commit", _p(self.acc), self.k, self.d, int(j), _p(delta), _p(self.state),
+    def flag_pending(self) -> None:
+        L.call("pcb_flag_global_empty", _p(self.acc), self.k, self.d, _p(self.acc_saved), _p(self.state),
                _stream())
+
+    def restore_pending(self) -> None:
+        self.acc.copy_(self.acc_saved)
+        self.state[1] = 0
+
+    def snapshot_state(self):
+        """Asynchronous copy of the loop state words (pinned) + its event."""
+        if not hasattr(self, "_snap_ring"):
+            self._snap_ring = torch.zeros((8, 2), dtype=torch.int64, pin_memory=True)
+            self._snap_i = 0
+        slot = self._snap_ring[self._snap_i % 8]
+        self._snap_i += 1
+        slot.copy_(self.state[:2], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return slot, ev
+
+    @staticmethod
+    def read_snapshot(snap):
+        slot, ev = snap
+        ev.synchronize()
+        return slot.numpy().copy()
+
+    def repair_select(self, offset: int, E: int):
+        out = torch.empty((E, 3), dtype=torch.float64, device=self.dev)
+        L.call("pcb_repair_select", _p(self.own), _p(self.perm), self.n, int(offset), int(E), _p(out),
+               _p(self.repair_scratch), self.repair_scratch_bytes, _stream())
+        return out
+
+    def new_deltas(self, E: int):
+        return torch.zeros((E, self.d + 4), dtype=torch.float64, device=self.dev)
+
+    def repair_apply_batch(self, prev, new, pos, js, slots, deltas) -> None:
+        t = torch.tensor([pos, js, slots], dtype=torch.int32).to(self.dev)
+        L.call(f"pcb_repair_apply_batch_{self.sfx}", _p(self.P), self.d, _p(self.C), _p(self.perm), _p(prev),
+               _p(new), _p(self.own), _p(t[0]), _p(t[1]), _p(t[2]), len(pos), _p(deltas), _stream())
+
+    def repair_commit_batch(self, js, deltas) -> None:
+        t = torch.tensor(js, dtype=torch.int32).to(self.dev)
+        L.call("pcb_repair_commit_batch", _p(self.acc), self.k, self.d, len(js), _p(t), _p(deltas),
+               _p(self.state), _stream())
 
     # -- whole fit -----------------------------------------------------------------
     def run(self, max_iters: int, tol: float = 0.0, check_convergence: bool = False,
@@ -617,8 +704,8 @@ class LloydEngine(ShardSequence):
         device, and the host-side schedule — full update at the start,
         relayouts — is known in advance), which removes the launch gaps between
         the ~30 small kernels of an iteration; large fits are GPU-bound and run
-        eagerly, as do multi-rank fits (the repair protocol reads the global
-        counts on the host)."""
+        eagerly.  Multi-rank fits are enqueued ahead with a lagged check of the
+        repair flag (run_multi): no host synchronisation per iteration."""
         if max_iters > self.max_iters:
             raise ValueError("max_iters exceeds the engine's history capacity")
         with torch.cuda.device(self.dev):
@@ -626,10 +713,15 @@ class LloydEngine(ShardSequence):
             hist = None
             if record_history:
                 hist = torch.empty((max_iters, self.n), dtype=torch.int32, pin_memory=True)
+            if self._multi():
+                mk = (lambda: [torch.cuda.Event(enable_timing=True) for _ in range(3)]) if timing else None
+                evd = self.run_multi(max_iters, check_convergence, tol, mk, hist)
+                torch.cuda.current_stream().synchronize()
+                return self.collect(hist, [evd[t] for t in sorted(evd)] if timing else ())
             # graphs pay off where launches dominate (small n k d); a large fit
             # is GPU-bound and instantiating ~1000 nodes would only add latency
             small = 2.0 * self.n * self.k * self.d < 1e11
-            use_graph = graph and small and (self.comm is None or self.comm.world_size == 1)
+            use_graph = graph and small
             evs = self.iterations(0, max_iters, check_convergence, tol, timing, hist, use_graph)
             torch.cuda.current_stream().synchronize()
             return self.collect(hist, evs)

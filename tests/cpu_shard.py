@@ -95,46 +95,74 @@ class NumpyShard(ShardSequence):
             self.state[1] = 1
             self.state[2] = 1
 
-    # -- multi-rank repair primitives -------------------------------------------------
-    def argmax_own(self, offset, key_out):
-        own = self.own
-        best = np.max(own)
-        pos = np.flatnonzero(own == best)
-        gidx = offset + self.perm[pos]
-        q = pos[np.argmin(gidx)]
-        key_out.copy_(torch.tensor([best, float(offset + self.perm[q]), float(q)], dtype=torch.float64))
-
-    def repair_apply(self, prev, new, pos, j, delta):
-        donor = int(self.perm[pos])
-        lab = new.numpy()
-        old = int(lab[donor])
-        dnew = float(((self.P64[donor] - self.C.astype(np.float64)[j]) ** 2).sum())
-        p = int(prev.numpy()[donor])
-        vals = np.concatenate([self.P64[donor], [old, dnew - self.own[pos],
-                                                 float((j != p) - (old != p)), 1.0]])
-        delta.copy_(torch.from_numpy(vals))
-        lab[donor] = j
-        self.own[pos] = -np.inf
-
-    def repair_commit(self, j, delta):
-        dl = delta.numpy()
-        d, k = self.d, self.k
-        if dl[d + 3] != 1.0:
+    # -- multi-rank primitives (same contract as the CUDA engine's) ----------------
+    def flag_pending(self):
+        if self._stopped():
             return
-        old = int(dl[d])
+        kd = self.k * self.d
+        if (self.acc[kd:kd + self.k] == 0).any():
+            self.acc_saved = self.acc.clone()
+            self.state[1] = 2
+
+    def restore_pending(self):
+        self.acc.copy_(self.acc_saved)
+        self.state[1] = 0
+
+    def snapshot_state(self):
+        return self.state[:2].clone()
+
+    @staticmethod
+    def read_snapshot(snap):
+        return snap.numpy()
+
+    def repair_select(self, offset, E):
+        gidx = offset + self.perm
+        order = np.lexsort((gidx, -self.own))[:E]
+        out = np.full((E, 3), [-np.inf, 9.0e18, -1.0])
+        out[:order.size, 0] = self.own[order]
+        out[:order.size, 1] = gidx[order]
+        out[:order.size, 2] = order
+        return torch.from_numpy(out)
+
+    def new_deltas(self, E):
+        return torch.zeros((E, self.d + 4), dtype=torch.float64)
+
+    def repair_apply_batch(self, prev, new, pos, js, slots, deltas):
+        lab = new.numpy()
+        C64 = self.C.astype(np.float64)
+        for q, j, e in zip(pos, js, slots):
+            donor = int(self.perm[q])
+            old = int(lab[donor])
+            dnew = float(((self.P64[donor] - C64[j]) ** 2).sum())
+            p = int(prev.numpy()[donor])
+            deltas[e] = torch.from_numpy(np.concatenate([self.P64[donor], [old, dnew - self.own[q],
+                                                                           float((j != p) - (old != p)), 1.0]]))
+            lab[donor] = j
+            self.own[q] = -np.inf
+
+    def repair_commit_batch(self, js, deltas):
+        dl = deltas.numpy()
+        d, k = self.d, self.k
         acc = self.acc.numpy()
-        acc[old * d:(old + 1) * d] -= dl[:d]
-        acc[j * d:(j + 1) * d] += dl[:d]
-        acc[k * d + old] -= 1.0
-        acc[k * d + j] += 1.0
-        acc[k * d + k] += dl[d + 1]
-        acc[k * d + k + 1] += dl[d + 2]
-        self.state[3] += 1
+        for e, j in enumerate(js):
+            if dl[e, d + 3] != 1.0:
+                continue
+            old = int(dl[e, d])
+            acc[old * d:(old + 1) * d] -= dl[e, :d]
+            acc[j * d:(j + 1) * d] += dl[e, :d]
+            acc[k * d + old] -= 1.0
+            acc[k * d + j] += 1.0
+            acc[k * d + k] += dl[e, d + 1]
+            acc[k * d + k + 1] += dl[e, d + 2]
+            self.state[3] += 1
 
     # -- whole fit ------------------------------------------------------------------
     def fit(self, max_iters, check_convergence=False, tol=0.0):
-        for t in range(max_iters):
-            self.iteration(t, check_convergence, tol)
+        if self._multi():
+            self.run_multi(max_iters, check_convergence, tol)
+        else:
+            for t in range(max_iters):
+                self.iteration(t, check_convergence, tol)
         iters = int(self.state[0])
         return {"labels": self.labels[iters % 2].numpy().copy(), "iters": iters,
                 "objective": self.obj_hist[:iters].copy(), "repairs": self.rep_hist[:iters].copy(),

@@ -103,8 +103,14 @@ def check_step(P, C_in, labels_prev, k, gpu, ref=None, *, dtype=np.float32, what
     if not diff.any():
         assert gpu["moved"] == ref.moved, f"{what}: moved {gpu['moved']} vs {ref.moved}"
         assert abs(gpu["changed"] - ref.changed) <= 1e-12, f"{what}: changed"
+        # the reference's mean is an f32 running sum (clustering.py:287); on
+        # adversarial inputs (thousands of identical rows) its own error vs the
+        # exact mean exceeds CEN_RTOL — ours is within CEN_RTOL of the exact
+        # mean (above), so the distance to the reference may add the reference's
         err_ref = centroid_rel_err(gpu["centroids"], ref.centroids)
-        assert err_ref <= CEN_RTOL, f"{what}: centroids vs reference rel err {err_ref:.3e}"
+        ref_self = centroid_rel_err(ref.centroids, exact)
+        assert err_ref <= CEN_RTOL + ref_self, (f"{what}: centroids vs reference rel err {err_ref:.3e} "
+                                                f"(reference vs exact means {ref_self:.3e})")
     return {"mismatches": int(diff.sum()), "exempt": int(exempt.sum()),
             "obj_rel": dobj / max(abs(ref_obj), 1e-300), "cen_rel": err}
 
@@ -161,9 +167,11 @@ def check_step_strict(P, k, gpu, ref, *, what=""):
         touched[ref.labels[diff]] = True
     keep = ~touched
     cen_ref = centroid_rel_err(gpu["centroids"][keep], ref.centroids[keep]) if keep.any() else 0.0
-    assert cen_ref <= CEN_RTOL, f"{what}: centroids vs reference rel err {cen_ref:.3e}"
+    ref_self = centroid_rel_err(ref.centroids[keep], exact[keep]) if keep.any() else 0.0
+    assert cen_ref <= CEN_RTOL + ref_self, (f"{what}: centroids vs reference rel err {cen_ref:.3e} "
+                                            f"(reference vs exact means {ref_self:.3e})")
     if not diff.any():
         assert gpu["moved"] == ref.moved, f"{what}: moved {gpu['moved']} vs {ref.moved}"
         assert abs(gpu["changed"] - ref.changed) <= 1e-12, f"{what}: changed"
     return {"mismatches": int(diff.sum()), "gap_exempt": int(gap_ex.sum()), "ref_f32_flips": flips,
-            "obj_rel": obj_rel, "cen_rel": cen_rel, "cen_ref_rel": cen_ref}
+            "obj_rel": obj_rel, "cen_rel": cen_rel, "cen_ref_rel": cen_ref, "ref_mean_self_err": ref_self}
