@@ -293,9 +293,12 @@ static int repair(const T* P, int64_t n, int d, const T* C, int k, const int32_t
   if (per_sm < 1) return PCB_EUNSUP;
   const int grid = repair_grid(per_sm);
   RepairScratch* sc = (RepairScratch*)scratch;
+  int sel_E = 0;
+  double* sel_out = nullptr;
+  long long offset = 0;
   void* args[] = {(void*)&P,   (void*)&n,   (void*)&d,   (void*)&C,     (void*)&k,
                   (void*)&perm, (void*)&lp, (void*)&lab, (void*)&own, (void*)&acc,
-                  (void*)&state, (void*)&sc, (void*)&S};
+                  (void*)&state, (void*)&sc, (void*)&S, (void*)&sel_E, (void*)&sel_out, (void*)&offset};
   pcb::count_launch();
   e = cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(256), args, 0, st);
   return (int)e;
