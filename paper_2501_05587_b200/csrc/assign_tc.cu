@@ -453,10 +453,122 @@ exact_rows_kernel(const float* __restrict__ P, int d, const float* __restrict__ 
   }
 }
 
+// Tiled f32 pass over the flagged rows (the common case): 32 rows per block,
+// centroids in tiles of 64 and columns in chunks of 32 staged in shared
+// memory, each thread 4 rows x 4 centroids of sum (p - c)^2 (sequential
+// per pair: relative error <= (d + 8) 2^-23, positive terms).  Rows whose
+// runner-up is within that margin go to `thin` for exact_rows_kernel (f64).
+constexpr int XR_R = 32, XR_C = 64, XR_K = 32;
+
+__global__ void __launch_bounds__(128)
+exact_rows_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__ C, int k,
+                        const int* __restrict__ flag_list, const int* __restrict__ flag_count,
+                        const int* __restrict__ row_ids, int32_t* __restrict__ out, int* __restrict__ thin,
+                        int* __restrict__ thin_count, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  __shared__ __align__(16) float sP[XR_K][XR_R];
+  __shared__ __align__(16) float sC[XR_K][XR_C];
+  __shared__ int64_t srow[XR_R];
+  __shared__ int sidx[XR_R];
+  const int cnt = *flag_count;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const float brel = (float)(d + 8) * 0x1p-23f;
+  for (int rb = blockIdx.x * XR_R; rb < cnt; rb += gridDim.x * XR_R) {
+    __syncthreads();
+    if (tid < XR_R) {
+      const int q = rb + tid;
+      const int r = q < cnt ? flag_list[q] : -1;
+      sidx[tid] = r;
+      srow[tid] = r < 0 ? -1 : (row_ids != nullptr ? (int64_t)row_ids[r] : (int64_t)r);
+    }
+    float f1[4], f2[4];
+    int bj[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { f1[i] = 3.4e38f; f2[i] = 3.4e38f; bj[i] = 0; }
+    for (int c0 = 0; c0 < k; c0 += XR_C) {
+      float acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+      for (int k0 = 0; k0 < d; k0 += XR_K) {
+        __syncthreads();
+        for (int e = tid; e < XR_R * XR_K; e += 128) {  // row-contiguous reads
+          const int r = e / XR_K, kk = e % XR_K;
+          const int64_t pr = srow[r];
+          sP[kk][r] = (pr >= 0 && k0 + kk < d) ? __ldg(P + pr * d + k0 + kk) : 0.0f;
+        }
+        for (int e = tid; e < XR_C * XR_K; e += 128) {
+          const int c = e / XR_K, kk = e % XR_K;
+          sC[kk][c] = (c0 + c < k && k0 + kk < d) ? __ldg(C + (int64_t)(c0 + c) * d + k0 + kk) : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < XR_K; ++kk) {
+          const float4 a = *reinterpret_cast<const float4*>(&sP[kk][ty * 4]);
+          const float4 b = *reinterpret_cast<const float4*>(&sC[kk][tx * 4]);
+          const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float e = av[i] - bv[j];
+              acc[i][j] = fmaf(e, e, acc[i][j]);
+            }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int cj = c0 + tx * 4 + j;
+        if (cj < k) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float s = acc[i][j];
+            if (s < f1[i]) { f2[i] = f1[i]; f1[i] = s; bj[i] = cj; } else if (s < f2[i]) { f2[i] = s; }
+          }
+        }
+      }
+    }
+    // merge over the 16 threads of each row group (lanes ty*16 .. ty*16+15 of a warp)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        const float g1 = __shfl_xor_sync(0xffffffffu, f1[i], o);
+        const float g2 = __shfl_xor_sync(0xffffffffu, f2[i], o);
+        const int gj = __shfl_xor_sync(0xffffffffu, bj[i], o);
+        if (g1 < f1[i] || (g1 == f1[i] && gj < bj[i])) {
+          f2[i] = fminf(f1[i], g2);
+          f1[i] = g1;
+          bj[i] = gj;
+        } else {
+          f2[i] = fminf(f2[i], g1);
+        }
+      }
+    }
+    if (tx == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = sidx[ty * 4 + i];
+        if (r < 0) continue;
+        const bool unsure = k > 1 && f2[i] <= f1[i] * (1.0f + brel) / (1.0f - brel);
+        if (unsure) thin[atomicAdd(thin_count, 1)] = r;
+        else out[r] = bj[i];
+      }
+    }
+  }
+}
+
 int exact_rows(const float* P, int d, const float* C, int k, const int* flag_list, const int* flag_count,
-               const int* row_ids, int32_t* out, const long long* state, cudaStream_t st) {
-  const int grid = sm_count() * 8;
-#define PCB_XR(DQV) exact_rows_kernel<DQV><<<grid, 256, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out, state)
+                int* thin_list, int* thin_count, const int* row_ids, int32_t* out, const long long* state,
+                cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(thin_count, 0, sizeof(int), st);
+  if (e != cudaSuccess) return (int)e;
+  exact_rows_tiled_kernel<<<sm_count() * 4, 128, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out,
+                                                          thin_list, thin_count, state);
+  PCB_CHECK_LAUNCH();
+  const int grid = sm_count() * 2;
+#define PCB_XR(DQV) exact_rows_kernel<DQV><<<grid, 256, 0, st>>>(P, d, C, k, thin_list, thin_count, row_ids, out, state)
   if (d % 4 != 0 || d > 256) PCB_XR(0);
   else if (d <= 32) PCB_XR(1);
   else if (d <= 64) PCB_XR(2);

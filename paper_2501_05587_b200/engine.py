@@ -388,8 +388,8 @@ class LloydEngine(ShardSequence):
                 self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
-                self.flag_list = torch.empty(n, dtype=torch.int32, device=dev)
-                self.flag_count = torch.zeros(1, dtype=torch.int32, device=dev)
+                self.flag_list = torch.empty(2 * n, dtype=torch.int32, device=dev)  # flagged | thin margin
+                self.flag_count = torch.zeros(2, dtype=torch.int32, device=dev)
                 self.P_r = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 L.call("pcb_screen_prep_points", _p(self.P), n, d, self.ld, _p(self.P_r), _p(self.anorm),
                        _p(self.danorm), _p(self.bstat), _stream())
@@ -430,8 +430,8 @@ class LloydEngine(ShardSequence):
                 self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
-                self.flag_list = torch.empty(n, dtype=torch.int32, device=dev)
-                self.flag_count = torch.zeros(1, dtype=torch.int32, device=dev)
+                self.flag_list = torch.empty(2 * n, dtype=torch.int32, device=dev)  # flagged | thin margin
+                self.flag_count = torch.zeros(2, dtype=torch.int32, device=dev)
                 if self.q8:
                     L.call("pcb_screen_prep_points_fp8", _p(self.P), n, d, self.ld8, _p(self.P_b),
                            _p(self.anorm), _p(self.danorm), _p(self.bstat), _stream())
@@ -837,8 +837,8 @@ class LloydEngine(ShardSequence):
                 rows = torch.arange(m, dtype=torch.int32, device=self.dev)
                 cnt = torch.full((1,), m, dtype=torch.int32, device=self.dev)
                 sub = torch.empty(m, dtype=torch.int32, device=self.dev)
-                fl = torch.empty(m, dtype=torch.int32, device=self.dev)
-                fc = torch.zeros(1, dtype=torch.int32, device=self.dev)
+                fl = torch.empty(2 * m, dtype=torch.int32, device=self.dev)
+                fc = torch.zeros(2, dtype=torch.int32, device=self.dev)
                 L.call("pcb_resolve_ambiguous_f32", _p(Xt), m, self.d, _p(rows), _p(cnt), self.ld, _p(xh), _p(xl),
                        _p(sub), _p(xn), _p(self.C), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(out),
                        _p(fl), _p(fc), None, _stream())
