@@ -157,12 +157,14 @@ int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const float* C_r,
  * resolved labels exact — rows whose two best 3xTF32 keys are within the
  * rigorous error bound are re-evaluated over all k centroids (tiled f32 with
  * a margin, f64 when it is thin, lowest index on ties) against C (f32
- * centroids).  NULL: 3xTF32 labels.                                         */
+ * centroids; scratch: pcb_exact_scratch_bytes()).  NULL: 3xTF32 labels.    */
 int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_list,
                               const int* amb_count, int ld, float* sub_hi, float* sub_lo,
                               int32_t* sub_labels, const float* pnorm, const float* C, const float* C_hi,
                               const float* C_lo, const float* cnorm, int k, int32_t* labels,
-                              int* flag_list, int* flag_count, const long long* state, void* stream);
+                              int* flag_list, int* flag_count, void* scratch, int64_t scratch_bytes,
+                              const long long* state, void* stream);
+int64_t pcb_exact_scratch_bytes(void);   /* `scratch` of pcb_resolve_ambiguous_f32 (flag list given) */
 /* Certified BF16 screening variant ("bf16s", see assign_screen_bf16.cu):
  * one BF16 tensor-core pass (kind::f16) on RN-rounded copies P_b / C_b (row
  * stride ldb = pcb_screen_bf16_ld(d) BF16 elements) with the same rigorous

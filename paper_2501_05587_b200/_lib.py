@@ -42,7 +42,9 @@ SIGNATURES = {
     "pcb_screen_prep_points": (I32, [P, I64, I32, I32, P, P, P, P, P]),
     "pcb_screen_prep_centroids": (I32, [P, I32, I32, P, P, P, P]),
     "pcb_assign_screen_f32": (I32, [P, I64, I32, P, I32, P, P, P, P, P, P, P, P, P]),
-    "pcb_resolve_ambiguous_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P, P, P, P, I32, P, P, P, P, P]),
+    "pcb_resolve_ambiguous_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P, P, P, P, I32, P, P, P, P, I64, P,
+                                        P]),
+    "pcb_exact_scratch_bytes": (I64, []),
     "pcb_update_mode": (I32, [P, I32, I32, I64, F64, I32, P, P]),
     "pcb_delta_update_f32": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),
     "pcb_delta_update_f64": (I32, [P, I64, I32, P, P, P, I32, P, P, P, P, P]),

@@ -494,10 +494,11 @@ extern "C" int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const
                                          const int* amb_count, int ld, float* sub_hi, float* sub_lo,
                                          int32_t* sub_labels, const float* pnorm, const float* C,
                                          const float* C_hi, const float* C_lo, const float* cnorm, int k,
-                                         int32_t* labels, int* flag_list, int* flag_count,
-                                         const long long* state, void* stream) {
+                                         int32_t* labels, int* flag_list, int* flag_count, void* scratch,
+                                         int64_t scratch_bytes, const long long* state, void* stream) {
   if (n < 1 || d < 1 || k < 1 || ld < d || ld % 32 || !P || !amb_list || !amb_count || !sub_hi || !sub_lo ||
-      !sub_labels || !pnorm || !C_hi || !C_lo || !cnorm || !labels || (flag_list && (!flag_count || !C)))
+      !sub_labels || !pnorm || !C_hi || !C_lo || !cnorm || !labels ||
+      (flag_list && (!flag_count || !C || !scratch || scratch_bytes < exact_scratch_bytes())))
     return PCB_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = sm_count() * 8;
@@ -512,12 +513,14 @@ extern "C" int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const
   if (rc) return rc;
   if (flag_list != nullptr &&
       (rc = exact_rows(P, d, C, k, flag_list, flag_count, flag_list + n, flag_count + 1, amb_list, sub_labels,
-                       state, st)))
+                       scratch, state, st)))
     return rc;
   scatter_rows_labels<<<grid, 256, 0, st>>>(amb_list, amb_count, sub_labels, labels, state);
   PCB_CHECK_LAUNCH();
   return 0;
 }
+
+extern "C" int64_t pcb_exact_scratch_bytes(void) { return exact_scratch_bytes(); }
 
 extern "C" int pcb_count_labels(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
                                 double* acc, const long long* state, void* stream) {

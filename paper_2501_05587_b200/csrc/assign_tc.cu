@@ -39,6 +39,7 @@ constexpr int TC_BM = 128;     // rows per tile (UMMA M)
 constexpr int TC_BK = 32;      // f32 per 128-byte swizzle row
 constexpr int TC_THREADS = 256;
 constexpr int TC_HIST_MAX = 4096;
+constexpr int XR_SCRATCH_ROWS = 32768;  // flagged rows whose exact pass may split the centroid range
 
 template <int BN>
 struct TcCfg {
@@ -351,128 +352,72 @@ int assign_tc3xtf32_devcount(const float* phi, const float* plo, int ld, const f
                        st, n_dev, row_ids, flag_list, flag_count);
 }
 
+// ---------------------------------------------------------------------------
 // Exact argmin (dense.py:56-68) over all k centroids for the rows the 3xTF32
-// pass flagged: 8 lanes per row (4 rows per warp), f32 distances
-// sum (p - c)^2 first — relative error <= (d + 8) 2^-23 (positive terms) —
-// and an f64 pass for the rare rows whose two best are within that margin
-// (f64 only for the centroids inside the margin; lowest index on ties).
-// out[r] for the flagged r; row r of P is P[row_ids[r]] (or r).
-// DQ > 0: d % 4 == 0 and d <= 32 DQ: the row's float4s stay in registers and
-// four centroids are in flight per step; DQ = 0: generic.
-template <int DQ>
-__global__ void __launch_bounds__(256)
-exact_rows_kernel(const float* __restrict__ P, int d, const float* __restrict__ C, int k,
-                  const int* __restrict__ flag_list, const int* __restrict__ flag_count,
-                  const int* __restrict__ row_ids, int32_t* __restrict__ out, const long long* __restrict__ state) {
-  if (stopped(state)) return;
-  const int64_t cnt = *flag_count;
-  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
-  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const float brel = (float)(d + 8) * 0x1p-23f;
-  const int d4 = d >> 2;
-  for (int64_t rb = w0 * 4; rb < cnt; rb += nw * 4) {
-    const int64_t q = rb + grp;
-    const bool valid = q < cnt;
-    const int r = valid ? flag_list[q] : 0;
-    const int64_t prow = row_ids != nullptr ? (int64_t)row_ids[r] : (int64_t)r;
-    const float* p = P + prow * d;
-    auto dist32 = [&](int j) -> float {  // partial over this lane's columns
-      const float* c = C + (int64_t)j * d;
-      float s = 0.0f;
-      for (int t = sub; t < d; t += 8) {
-        const float e = __ldg(p + t) - __ldg(c + t);
-        s = fmaf(e, e, s);
-      }
-      return s;
-    };
-    float f1 = 3.4e38f, f2 = 3.4e38f;
-    int bj = 0;
-    auto take = [&](float s, int j) {
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      if (s < f1) { f2 = f1; f1 = s; bj = j; } else if (s < f2) { f2 = s; }
-    };
-    if constexpr (DQ > 0) {
-      float4 x[DQ];
-#pragma unroll
-      for (int u = 0; u < DQ; ++u) {
-        const int f = sub + 8 * u;
-        x[u] = f < d4 ? __ldg(reinterpret_cast<const float4*>(p) + f) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      int j = 0;
-      for (; j + 4 <= k; j += 4) {
-        float s[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int u = 0; u < DQ; ++u) {
-          const int f = sub + 8 * u;
-          if (f < d4) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const float4 c = __ldg(reinterpret_cast<const float4*>(C + (int64_t)(j + v) * d) + f);
-              const float e0 = x[u].x - c.x, e1 = x[u].y - c.y, e2 = x[u].z - c.z, e3 = x[u].w - c.w;
-              s[v] = fmaf(e3, e3, fmaf(e2, e2, fmaf(e1, e1, fmaf(e0, e0, s[v]))));
-            }
-          }
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) take(s[v], j + v);
-      }
-      for (; j < k; ++j) take(dist32(j), j);
-    } else {
-      for (int j = 0; j < k; ++j) take(dist32(j), j);
-    }
-    const float lim = f1 * (1.0f + brel) / (1.0f - brel);
-    const bool unsure = valid && k > 1 && f2 <= lim;
-    if (__any_sync(0xffffffffu, unsure)) {
-      // f64 over the centroids whose f32 distance is within the margin of f1
-      double best = 0.0;
-      int bj64 = -1;
-      for (int j = 0; j < k; ++j) {
-        float s = dist32(j);
-        s += __shfl_xor_sync(0xffffffffu, s, 4);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        const bool cand = unsure && s <= lim;
-        if (!__any_sync(0xffffffffu, cand)) continue;
-        double s64 = 0.0;
-        if (cand)
-          for (int t = sub; t < d; t += 8) {
-            const double e = (double)p[t] - (double)C[(int64_t)j * d + t];
-            s64 = fma(e, e, s64);
-          }
-        s64 += __shfl_xor_sync(0xffffffffu, s64, 4);
-        s64 += __shfl_xor_sync(0xffffffffu, s64, 2);
-        s64 += __shfl_xor_sync(0xffffffffu, s64, 1);
-        if (cand && (bj64 < 0 || s64 < best)) { best = s64; bj64 = j; }  // ascending j: ties keep the lowest
-      }
-      if (unsure) bj = bj64;
-    }
-    if (valid && sub == 0) out[r] = bj;
+// pass flagged (flag_list; row r of P is P[row_ids[r]], label -> out[r]).
+//
+// exact_tiled_kernel: f32 sum (p - c)^2 per pair (sequential, positive terms:
+//   relative error <= (d + 8) 2^-23), 32 rows per block, centroids in tiles
+//   of 64 and columns in chunks of 32 staged in shared memory, each thread
+//   4 rows x 4 centroids.  Few flagged rows (steady state: ~1e3) would leave
+//   most SMs idle, so the centroid range is split over gridDim.y segments
+//   (chosen on the device from the row count) whose partial top-2 the merge
+//   kernel combines; one segment writes its result directly.
+// The row's label is certain unless the runner-up is within the f32 margin;
+// those rows (rare: near-ties) go to exact_thin_kernel, one block per row,
+// f64 over the centroids inside the margin, lowest index on ties.
+// ---------------------------------------------------------------------------
+constexpr int XR_R = 32, XR_C = 64, XR_K = 32, XR_SEG = 16;
+
+struct ExactScratch {
+  int seg;                         // centroid segments of this launch
+  int pad;
+  float f1[XR_SEG * XR_SCRATCH_ROWS];
+  float f2[XR_SEG * XR_SCRATCH_ROWS];
+  int bj[XR_SEG * XR_SCRATCH_ROWS];
+};
+
+__device__ __forceinline__ int exact_segments(int cnt, int nblk_x, int k) {
+  const int nrb = (cnt + XR_R - 1) / XR_R;
+  if (nrb == 0 || nrb * XR_R > XR_SCRATCH_ROWS) return 1;
+  int seg = (nblk_x * 2) / nrb;  // ~2 blocks per SM in flight
+  seg = seg < 1 ? 1 : (seg > XR_SEG ? XR_SEG : seg);
+  const int maxseg = (k + XR_C - 1) / XR_C;
+  return seg < maxseg ? seg : maxseg;
+}
+
+__device__ __forceinline__ void top2_merge(float& f1, float& f2, int& bj, float g1, float g2, int gj) {
+  if (g1 < f1 || (g1 == f1 && gj < bj)) {
+    f2 = fminf(f1, g2);
+    f1 = g1;
+    bj = gj;
+  } else {
+    f2 = fminf(f2, g1);
   }
 }
 
-// Tiled f32 pass over the flagged rows (the common case): 32 rows per block,
-// centroids in tiles of 64 and columns in chunks of 32 staged in shared
-// memory, each thread 4 rows x 4 centroids of sum (p - c)^2 (sequential
-// per pair: relative error <= (d + 8) 2^-23, positive terms).  Rows whose
-// runner-up is within that margin go to `thin` for exact_rows_kernel (f64).
-constexpr int XR_R = 32, XR_C = 64, XR_K = 32;
+__device__ __forceinline__ bool thin_margin(float f1, float f2, int d, int k) {
+  const float brel = (float)(d + 8) * 0x1p-23f;
+  return k > 1 && f2 <= f1 * (1.0f + brel) / (1.0f - brel);
+}
 
 __global__ void __launch_bounds__(128)
-exact_rows_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__ C, int k,
-                        const int* __restrict__ flag_list, const int* __restrict__ flag_count,
-                        const int* __restrict__ row_ids, int32_t* __restrict__ out, int* __restrict__ thin,
-                        int* __restrict__ thin_count, const long long* __restrict__ state) {
+exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__ C, int k,
+                   const int* __restrict__ flag_list, const int* __restrict__ flag_count,
+                   const int* __restrict__ row_ids, int32_t* __restrict__ out, int* __restrict__ thin,
+                   int* __restrict__ thin_count, ExactScratch* __restrict__ sc, const long long* __restrict__ state) {
   if (stopped(state)) return;
   __shared__ __align__(16) float sP[XR_K][XR_R];
   __shared__ __align__(16) float sC[XR_K][XR_C];
   __shared__ int64_t srow[XR_R];
   __shared__ int sidx[XR_R];
   const int cnt = *flag_count;
+  const int seg = exact_segments(cnt, gridDim.x, k);
+  if ((int)blockIdx.y >= seg) return;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) sc->seg = seg;
+  const int ctiles = (k + XR_C - 1) / XR_C;
+  const int t_lo = (int)((int64_t)ctiles * blockIdx.y / seg), t_hi = (int)((int64_t)ctiles * (blockIdx.y + 1) / seg);
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const float brel = (float)(d + 8) * 0x1p-23f;
   for (int rb = blockIdx.x * XR_R; rb < cnt; rb += gridDim.x * XR_R) {
     __syncthreads();
     if (tid < XR_R) {
@@ -484,8 +429,9 @@ exact_rows_tiled_kernel(const float* __restrict__ P, int d, const float* __restr
     float f1[4], f2[4];
     int bj[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) { f1[i] = 3.4e38f; f2[i] = 3.4e38f; bj[i] = 0; }
-    for (int c0 = 0; c0 < k; c0 += XR_C) {
+    for (int i = 0; i < 4; ++i) { f1[i] = 3.4e38f; f2[i] = 3.4e38f; bj[i] = 0x7fffffff; }
+    for (int ct = t_lo; ct < t_hi; ++ct) {
+      const int c0 = ct * XR_C;
       float acc[4][4];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -537,47 +483,135 @@ exact_rows_tiled_kernel(const float* __restrict__ P, int d, const float* __restr
         const float g1 = __shfl_xor_sync(0xffffffffu, f1[i], o);
         const float g2 = __shfl_xor_sync(0xffffffffu, f2[i], o);
         const int gj = __shfl_xor_sync(0xffffffffu, bj[i], o);
-        if (g1 < f1[i] || (g1 == f1[i] && gj < bj[i])) {
-          f2[i] = fminf(f1[i], g2);
-          f1[i] = g1;
-          bj[i] = gj;
-        } else {
-          f2[i] = fminf(f2[i], g1);
-        }
+        top2_merge(f1[i], f2[i], bj[i], g1, g2, gj);
       }
     }
     if (tx == 0) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
+        const int q = rb + ty * 4 + i;
         const int r = sidx[ty * 4 + i];
         if (r < 0) continue;
-        const bool unsure = k > 1 && f2[i] <= f1[i] * (1.0f + brel) / (1.0f - brel);
-        if (unsure) thin[atomicAdd(thin_count, 1)] = r;
-        else out[r] = bj[i];
+        if (seg > 1) {
+          sc->f1[blockIdx.y * XR_SCRATCH_ROWS + q] = f1[i];
+          sc->f2[blockIdx.y * XR_SCRATCH_ROWS + q] = f2[i];
+          sc->bj[blockIdx.y * XR_SCRATCH_ROWS + q] = bj[i];
+        } else if (thin_margin(f1[i], f2[i], d, k)) {
+          thin[atomicAdd(thin_count, 1)] = r;
+        } else {
+          out[r] = bj[i];
+        }
       }
     }
   }
 }
 
+// Several centroid segments: combine their partial top-2 per flagged row.
+__global__ void __launch_bounds__(256)
+exact_merge_kernel(int d, int k, const int* __restrict__ flag_list, const int* __restrict__ flag_count,
+                   int32_t* __restrict__ out, int* __restrict__ thin, int* __restrict__ thin_count,
+                   const ExactScratch* __restrict__ sc, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  const int cnt = *flag_count;
+  const int seg = ((volatile const ExactScratch*)sc)->seg;
+  if (seg <= 1) return;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
+    float f1 = sc->f1[q], f2 = sc->f2[q];
+    int bj = sc->bj[q];
+    for (int s = 1; s < seg; ++s)
+      top2_merge(f1, f2, bj, sc->f1[s * XR_SCRATCH_ROWS + q], sc->f2[s * XR_SCRATCH_ROWS + q],
+                 sc->bj[s * XR_SCRATCH_ROWS + q]);
+    const int r = flag_list[q];
+    if (thin_margin(f1, f2, d, k)) thin[atomicAdd(thin_count, 1)] = r;
+    else out[r] = bj;
+  }
+}
+
+// Rows with a thin f32 margin: one block per row; f32 distances to every
+// centroid (the row in shared memory), then f64 for those within the margin
+// of the smallest; block argmin with the lowest index on ties.
+__global__ void __launch_bounds__(256)
+exact_thin_kernel(const float* __restrict__ P, int d, const float* __restrict__ C, int k,
+                  const int* __restrict__ thin, const int* __restrict__ thin_count, const int* __restrict__ row_ids,
+                  int32_t* __restrict__ out, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  extern __shared__ float sp[];  // d floats
+  __shared__ float wf[8];
+  __shared__ double wd[8];
+  __shared__ int wj[8];
+  const int cnt = *thin_count;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float brel = (float)(d + 8) * 0x1p-23f;
+  for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
+    const int r = thin[q];
+    const int64_t prow = row_ids != nullptr ? (int64_t)row_ids[r] : (int64_t)r;
+    __syncthreads();
+    for (int t = threadIdx.x; t < d; t += blockDim.x) sp[t] = P[prow * d + t];
+    __syncthreads();
+    auto d32 = [&](int j) {
+      const float* c = C + (int64_t)j * d;
+      float s = 0.0f;
+      for (int t = 0; t < d; ++t) {
+        const float e = sp[t] - __ldg(c + t);
+        s = fmaf(e, e, s);
+      }
+      return s;
+    };
+    float m = 3.4e38f;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) m = fminf(m, d32(j));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) wf[warp] = m;
+    __syncthreads();
+    float f1 = wf[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) f1 = fminf(f1, wf[w]);
+    const float lim = f1 * (1.0f + brel) / (1.0f - brel);
+    double best = 1.0e308;
+    int bj = 0x7fffffff;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      if (d32(j) > lim) continue;
+      double s64 = 0.0;
+      for (int t = 0; t < d; ++t) {
+        const double e = (double)sp[t] - (double)C[(int64_t)j * d + t];
+        s64 = fma(e, e, s64);
+      }
+      if (s64 < best || (s64 == best && j < bj)) { best = s64; bj = j; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (b2 < best || (b2 == best && j2 < bj)) { best = b2; bj = j2; }
+    }
+    if (lane == 0) { wd[warp] = best; wj[warp] = bj; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (wd[w] < best || (wd[w] == best && wj[w] < bj)) { best = wd[w]; bj = wj[w]; }
+      out[r] = bj;
+    }
+  }
+}
+
 int exact_rows(const float* P, int d, const float* C, int k, const int* flag_list, const int* flag_count,
-                int* thin_list, int* thin_count, const int* row_ids, int32_t* out, const long long* state,
-                cudaStream_t st) {
+               int* thin_list, int* thin_count, const int* row_ids, int32_t* out, void* scratch,
+               const long long* state, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(thin_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return (int)e;
-  exact_rows_tiled_kernel<<<sm_count() * 4, 128, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out,
-                                                          thin_list, thin_count, state);
+  ExactScratch* sc = (ExactScratch*)scratch;
+  const int gx = sm_count() * 4;
+  exact_tiled_kernel<<<dim3(gx, XR_SEG), 128, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out, thin_list,
+                                                       thin_count, sc, state);
   PCB_CHECK_LAUNCH();
-  const int grid = sm_count() * 2;
-#define PCB_XR(DQV) exact_rows_kernel<DQV><<<grid, 256, 0, st>>>(P, d, C, k, thin_list, thin_count, row_ids, out, state)
-  if (d % 4 != 0 || d > 256) PCB_XR(0);
-  else if (d <= 32) PCB_XR(1);
-  else if (d <= 64) PCB_XR(2);
-  else if (d <= 128) PCB_XR(4);
-  else PCB_XR(8);
-#undef PCB_XR
+  exact_merge_kernel<<<sm_count(), 256, 0, st>>>(d, k, flag_list, flag_count, out, thin_list, thin_count, sc, state);
+  PCB_CHECK_LAUNCH();
+  exact_thin_kernel<<<sm_count() * 2, 256, (size_t)d * sizeof(float), st>>>(P, d, C, k, thin_list, thin_count,
+                                                                           row_ids, out, state);
   PCB_CHECK_LAUNCH();
   return 0;
 }
+
+int64_t exact_scratch_bytes() { return (int64_t)sizeof(ExactScratch); }
 
 }  // namespace pcb
 

@@ -390,6 +390,8 @@ class LloydEngine(ShardSequence):
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
                 self.flag_list = torch.empty(2 * n, dtype=torch.int32, device=dev)  # flagged | thin margin
                 self.flag_count = torch.zeros(2, dtype=torch.int32, device=dev)
+                self.exact_scratch = torch.empty(int(L.load().pcb_exact_scratch_bytes()), dtype=torch.uint8,
+                                                 device=dev)
                 self.P_r = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 L.call("pcb_screen_prep_points", _p(self.P), n, d, self.ld, _p(self.P_r), _p(self.anorm),
                        _p(self.danorm), _p(self.bstat), _stream())
@@ -432,6 +434,8 @@ class LloydEngine(ShardSequence):
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
                 self.flag_list = torch.empty(2 * n, dtype=torch.int32, device=dev)  # flagged | thin margin
                 self.flag_count = torch.zeros(2, dtype=torch.int32, device=dev)
+                self.exact_scratch = torch.empty(int(L.load().pcb_exact_scratch_bytes()), dtype=torch.uint8,
+                                                 device=dev)
                 if self.q8:
                     L.call("pcb_screen_prep_points_fp8", _p(self.P), n, d, self.ld8, _p(self.P_b),
                            _p(self.anorm), _p(self.danorm), _p(self.bstat), _stream())
@@ -625,8 +629,8 @@ class LloydEngine(ShardSequence):
         with the flag list: near-ties re-evaluated over all centroids)."""
         L.call("pcb_resolve_ambiguous_f32", _p(self.P), self.n, self.d, _p(rows), _p(count), self.ld,
                _p(self.sub_hi), _p(self.sub_lo), _p(self.sub_labels), _p(self.pnorm), _p(self.C), _p(self.C_hi),
-               _p(self.C_lo), _p(self.cnorm), self.k, _p(new), _p(self.flag_list), _p(self.flag_count), _p(state),
-               _stream())
+               _p(self.C_lo), _p(self.cnorm), self.k, _p(new), _p(self.flag_list), _p(self.flag_count),
+               _p(self.exact_scratch), self.exact_scratch.numel(), _p(state), _stream())
 
     _kev = None
 
@@ -839,9 +843,10 @@ class LloydEngine(ShardSequence):
                 sub = torch.empty(m, dtype=torch.int32, device=self.dev)
                 fl = torch.empty(2 * m, dtype=torch.int32, device=self.dev)
                 fc = torch.zeros(2, dtype=torch.int32, device=self.dev)
+                xs = torch.empty(int(L.load().pcb_exact_scratch_bytes()), dtype=torch.uint8, device=self.dev)
                 L.call("pcb_resolve_ambiguous_f32", _p(Xt), m, self.d, _p(rows), _p(cnt), self.ld, _p(xh), _p(xl),
                        _p(sub), _p(xn), _p(self.C), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(out),
-                       _p(fl), _p(fc), None, _stream())
+                       _p(fl), _p(fc), _p(xs), xs.numel(), None, _stream())
             else:
                 L.call(f"pcb_assign_{self.sfx}", _p(Xt), _p(xn), m, self.d, _p(self.C), _p(self.cnorm),
                        self.k, None, _p(out), None, None, None, self.vcode if self.variant != "delta" else 0,
