@@ -153,11 +153,11 @@ int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const float* C_r,
                           const float* cnorm, const float* anorm, const float* danorm,
                           const float* bstat, int32_t* labels, int* amb_list, int* amb_count,
                           const long long* state, void* stream);
-/* flag_list (capacity 2n) / flag_count (2 ints) (nullable): make the
- * resolved labels exact — rows whose two best 3xTF32 keys are within the
- * rigorous error bound are re-evaluated over all k centroids (tiled f32 with
- * a margin, f64 when it is thin, lowest index on ties) against C (f32
- * centroids; scratch: pcb_exact_scratch_bytes()).  NULL: 3xTF32 labels.    */
+/* flag_list (capacity n) / flag_count (nullable): make the resolved labels
+ * exact — rows whose two best 3xTF32 keys are within the rigorous error
+ * bound are re-evaluated over all k centroids (f64 sums of squares, lowest
+ * index on ties) against C (f32 centroids; scratch:
+ * pcb_exact_scratch_bytes()).  NULL: 3xTF32 labels.                         */
 int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const int* amb_list,
                               const int* amb_count, int ld, float* sub_hi, float* sub_lo,
                               int32_t* sub_labels, const float* pnorm, const float* C, const float* C_hi,

@@ -503,7 +503,7 @@ extern "C" int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = sm_count() * 8;
   if (flag_list != nullptr) {
-    cudaError_t e = cudaMemsetAsync(flag_count, 0, 2 * sizeof(int), st);
+    cudaError_t e = cudaMemsetAsync(flag_count, 0, sizeof(int), st);
     if (e != cudaSuccess) return (int)e;
   }
   gather_split_rows<<<grid, 256, 0, st>>>(P, d, amb_list, amb_count, ld, sub_hi, sub_lo, state);
@@ -512,8 +512,7 @@ extern "C" int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const
                                     state, st, amb_list, flag_list, flag_count);
   if (rc) return rc;
   if (flag_list != nullptr &&
-      (rc = exact_rows(P, d, C, k, flag_list, flag_count, flag_list + n, flag_count + 1, amb_list, sub_labels,
-                       scratch, state, st)))
+      (rc = exact_rows(P, d, C, k, flag_list, flag_count, amb_list, sub_labels, scratch, state, st)))
     return rc;
   scatter_rows_labels<<<grid, 256, 0, st>>>(amb_list, amb_count, sub_labels, labels, state);
   PCB_CHECK_LAUNCH();

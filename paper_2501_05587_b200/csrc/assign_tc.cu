@@ -354,26 +354,24 @@ int assign_tc3xtf32_devcount(const float* phi, const float* plo, int ld, const f
 
 // ---------------------------------------------------------------------------
 // Exact argmin (dense.py:56-68) over all k centroids for the rows the 3xTF32
-// pass flagged (flag_list; row r of P is P[row_ids[r]], label -> out[r]).
-//
-// exact_tiled_kernel: f32 sum (p - c)^2 per pair (sequential, positive terms:
-//   relative error <= (d + 8) 2^-23), 32 rows per block, centroids in tiles
-//   of 64 and columns in chunks of 32 staged in shared memory, each thread
-//   4 rows x 4 centroids.  Few flagged rows (steady state: ~1e3) would leave
-//   most SMs idle, so the centroid range is split over gridDim.y segments
-//   (chosen on the device from the row count) whose partial top-2 the merge
-//   kernel combines; one segment writes its result directly.
-// The row's label is certain unless the runner-up is within the f32 margin;
-// those rows (rare: near-ties) go to exact_thin_kernel, one block per row,
-// f64 over the centroids inside the margin, lowest index on ties.
+// pass flagged (flag_list; row r of P is P[row_ids[r]], label -> out[r]):
+// sum_t (p_t - c_t)^2 in f64 for every (row, centroid) pair, lowest index on
+// ties.  32 rows per block, centroids in tiles of 64 and columns in chunks of
+// 32 staged in shared memory (f32, converted exactly), each thread 4 rows x
+// 4 centroids with sequential f64 sums.  Few flagged rows (steady state:
+// ~1e3) would leave most SMs idle, so the centroid range is split over
+// gridDim.y segments (chosen on the device from the row count) whose partial
+// argmins exact_merge_kernel combines; with one segment the block writes the
+// labels itself.  (f32 sums with a rigorous margin were tried first: at the
+// cold start every flagged row's margin is thinner than the f32 error of
+// distances ~4e3, so everything fell through to an f64 pass anyway.)
 // ---------------------------------------------------------------------------
 constexpr int XR_R = 32, XR_C = 64, XR_K = 32, XR_SEG = 16;
 
 struct ExactScratch {
   int seg;                         // centroid segments of this launch
   int pad;
-  float f1[XR_SEG * XR_SCRATCH_ROWS];
-  float f2[XR_SEG * XR_SCRATCH_ROWS];
+  double dmin[XR_SEG * XR_SCRATCH_ROWS];
   int bj[XR_SEG * XR_SCRATCH_ROWS];
 };
 
@@ -386,26 +384,15 @@ __device__ __forceinline__ int exact_segments(int cnt, int nblk_x, int k) {
   return seg < maxseg ? seg : maxseg;
 }
 
-__device__ __forceinline__ void top2_merge(float& f1, float& f2, int& bj, float g1, float g2, int gj) {
-  if (g1 < f1 || (g1 == f1 && gj < bj)) {
-    f2 = fminf(f1, g2);
-    f1 = g1;
-    bj = gj;
-  } else {
-    f2 = fminf(f2, g1);
-  }
-}
-
-__device__ __forceinline__ bool thin_margin(float f1, float f2, int d, int k) {
-  const float brel = (float)(d + 8) * 0x1p-23f;
-  return k > 1 && f2 <= f1 * (1.0f + brel) / (1.0f - brel);
+__device__ __forceinline__ void argmin_take(double& v, int& j, double v2, int j2) {
+  if (v2 < v || (v2 == v && j2 < j)) { v = v2; j = j2; }
 }
 
 __global__ void __launch_bounds__(128)
 exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__ C, int k,
                    const int* __restrict__ flag_list, const int* __restrict__ flag_count,
-                   const int* __restrict__ row_ids, int32_t* __restrict__ out, int* __restrict__ thin,
-                   int* __restrict__ thin_count, ExactScratch* __restrict__ sc, const long long* __restrict__ state) {
+                   const int* __restrict__ row_ids, int32_t* __restrict__ out, ExactScratch* __restrict__ sc,
+                   const long long* __restrict__ state) {
   if (stopped(state)) return;
   __shared__ __align__(16) float sP[XR_K][XR_R];
   __shared__ __align__(16) float sC[XR_K][XR_C];
@@ -426,17 +413,17 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
       sidx[tid] = r;
       srow[tid] = r < 0 ? -1 : (row_ids != nullptr ? (int64_t)row_ids[r] : (int64_t)r);
     }
-    float f1[4], f2[4];
+    double best[4];
     int bj[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) { f1[i] = 3.4e38f; f2[i] = 3.4e38f; bj[i] = 0x7fffffff; }
+    for (int i = 0; i < 4; ++i) { best[i] = 1.0e308; bj[i] = 0x7fffffff; }
     for (int ct = t_lo; ct < t_hi; ++ct) {
       const int c0 = ct * XR_C;
-      float acc[4][4];
+      double acc[4][4];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
       for (int k0 = 0; k0 < d; k0 += XR_K) {
         __syncthreads();
         for (int e = tid; e < XR_R * XR_K; e += 128) {  // row-contiguous reads
@@ -449,17 +436,17 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
           sC[kk][c] = (c0 + c < k && k0 + kk < d) ? __ldg(C + (int64_t)(c0 + c) * d + k0 + kk) : 0.0f;
         }
         __syncthreads();
-#pragma unroll 8
+#pragma unroll 4
         for (int kk = 0; kk < XR_K; ++kk) {
           const float4 a = *reinterpret_cast<const float4*>(&sP[kk][ty * 4]);
           const float4 b = *reinterpret_cast<const float4*>(&sC[kk][tx * 4]);
-          const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+          const double av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float e = av[i] - bv[j];
-              acc[i][j] = fmaf(e, e, acc[i][j]);
+              const double e = av[i] - bv[j];
+              acc[i][j] = fma(e, e, acc[i][j]);
             }
         }
       }
@@ -468,10 +455,8 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
         const int cj = c0 + tx * 4 + j;
         if (cj < k) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float s = acc[i][j];
-            if (s < f1[i]) { f2[i] = f1[i]; f1[i] = s; bj[i] = cj; } else if (s < f2[i]) { f2[i] = s; }
-          }
+          for (int i = 0; i < 4; ++i)
+            if (acc[i][j] < best[i]) { best[i] = acc[i][j]; bj[i] = cj; }  // ascending cj: ties keep the lowest
         }
       }
     }
@@ -480,10 +465,9 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
     for (int i = 0; i < 4; ++i) {
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) {
-        const float g1 = __shfl_xor_sync(0xffffffffu, f1[i], o);
-        const float g2 = __shfl_xor_sync(0xffffffffu, f2[i], o);
-        const int gj = __shfl_xor_sync(0xffffffffu, bj[i], o);
-        top2_merge(f1[i], f2[i], bj[i], g1, g2, gj);
+        const double v2 = __shfl_xor_sync(0xffffffffu, best[i], o);
+        const int j2 = __shfl_xor_sync(0xffffffffu, bj[i], o);
+        argmin_take(best[i], bj[i], v2, j2);
       }
     }
     if (tx == 0) {
@@ -493,11 +477,8 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
         const int r = sidx[ty * 4 + i];
         if (r < 0) continue;
         if (seg > 1) {
-          sc->f1[blockIdx.y * XR_SCRATCH_ROWS + q] = f1[i];
-          sc->f2[blockIdx.y * XR_SCRATCH_ROWS + q] = f2[i];
+          sc->dmin[blockIdx.y * XR_SCRATCH_ROWS + q] = best[i];
           sc->bj[blockIdx.y * XR_SCRATCH_ROWS + q] = bj[i];
-        } else if (thin_margin(f1[i], f2[i], d, k)) {
-          thin[atomicAdd(thin_count, 1)] = r;
         } else {
           out[r] = bj[i];
         }
@@ -506,107 +487,29 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
   }
 }
 
-// Several centroid segments: combine their partial top-2 per flagged row.
+// Several centroid segments: combine their partial argmins per flagged row.
 __global__ void __launch_bounds__(256)
-exact_merge_kernel(int d, int k, const int* __restrict__ flag_list, const int* __restrict__ flag_count,
-                   int32_t* __restrict__ out, int* __restrict__ thin, int* __restrict__ thin_count,
+exact_merge_kernel(const int* __restrict__ flag_list, const int* __restrict__ flag_count, int32_t* __restrict__ out,
                    const ExactScratch* __restrict__ sc, const long long* __restrict__ state) {
   if (stopped(state)) return;
   const int cnt = *flag_count;
   const int seg = ((volatile const ExactScratch*)sc)->seg;
   if (seg <= 1) return;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
-    float f1 = sc->f1[q], f2 = sc->f2[q];
-    int bj = sc->bj[q];
-    for (int s = 1; s < seg; ++s)
-      top2_merge(f1, f2, bj, sc->f1[s * XR_SCRATCH_ROWS + q], sc->f2[s * XR_SCRATCH_ROWS + q],
-                 sc->bj[s * XR_SCRATCH_ROWS + q]);
-    const int r = flag_list[q];
-    if (thin_margin(f1, f2, d, k)) thin[atomicAdd(thin_count, 1)] = r;
-    else out[r] = bj;
-  }
-}
-
-// Rows with a thin f32 margin: one block per row; f32 distances to every
-// centroid (the row in shared memory), then f64 for those within the margin
-// of the smallest; block argmin with the lowest index on ties.
-__global__ void __launch_bounds__(256)
-exact_thin_kernel(const float* __restrict__ P, int d, const float* __restrict__ C, int k,
-                  const int* __restrict__ thin, const int* __restrict__ thin_count, const int* __restrict__ row_ids,
-                  int32_t* __restrict__ out, const long long* __restrict__ state) {
-  if (stopped(state)) return;
-  extern __shared__ float sp[];  // d floats
-  __shared__ float wf[8];
-  __shared__ double wd[8];
-  __shared__ int wj[8];
-  const int cnt = *thin_count;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float brel = (float)(d + 8) * 0x1p-23f;
-  for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
-    const int r = thin[q];
-    const int64_t prow = row_ids != nullptr ? (int64_t)row_ids[r] : (int64_t)r;
-    __syncthreads();
-    for (int t = threadIdx.x; t < d; t += blockDim.x) sp[t] = P[prow * d + t];
-    __syncthreads();
-    auto d32 = [&](int j) {
-      const float* c = C + (int64_t)j * d;
-      float s = 0.0f;
-      for (int t = 0; t < d; ++t) {
-        const float e = sp[t] - __ldg(c + t);
-        s = fmaf(e, e, s);
-      }
-      return s;
-    };
-    float m = 3.4e38f;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) m = fminf(m, d32(j));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) wf[warp] = m;
-    __syncthreads();
-    float f1 = wf[0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) f1 = fminf(f1, wf[w]);
-    const float lim = f1 * (1.0f + brel) / (1.0f - brel);
-    double best = 1.0e308;
-    int bj = 0x7fffffff;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
-      if (d32(j) > lim) continue;
-      double s64 = 0.0;
-      for (int t = 0; t < d; ++t) {
-        const double e = (double)sp[t] - (double)C[(int64_t)j * d + t];
-        s64 = fma(e, e, s64);
-      }
-      if (s64 < best || (s64 == best && j < bj)) { best = s64; bj = j; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
-      const int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
-      if (b2 < best || (b2 == best && j2 < bj)) { best = b2; bj = j2; }
-    }
-    if (lane == 0) { wd[warp] = best; wj[warp] = bj; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-        if (wd[w] < best || (wd[w] == best && wj[w] < bj)) { best = wd[w]; bj = wj[w]; }
-      out[r] = bj;
-    }
+    double v = sc->dmin[q];
+    int j = sc->bj[q];
+    for (int s = 1; s < seg; ++s) argmin_take(v, j, sc->dmin[s * XR_SCRATCH_ROWS + q], sc->bj[s * XR_SCRATCH_ROWS + q]);
+    out[flag_list[q]] = j;
   }
 }
 
 int exact_rows(const float* P, int d, const float* C, int k, const int* flag_list, const int* flag_count,
-               int* thin_list, int* thin_count, const int* row_ids, int32_t* out, void* scratch,
-               const long long* state, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(thin_count, 0, sizeof(int), st);
-  if (e != cudaSuccess) return (int)e;
+               const int* row_ids, int32_t* out, void* scratch, const long long* state, cudaStream_t st) {
   ExactScratch* sc = (ExactScratch*)scratch;
   const int gx = sm_count() * 4;
-  exact_tiled_kernel<<<dim3(gx, XR_SEG), 128, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out, thin_list,
-                                                       thin_count, sc, state);
+  exact_tiled_kernel<<<dim3(gx, XR_SEG), 128, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out, sc, state);
   PCB_CHECK_LAUNCH();
-  exact_merge_kernel<<<sm_count(), 256, 0, st>>>(d, k, flag_list, flag_count, out, thin_list, thin_count, sc, state);
-  PCB_CHECK_LAUNCH();
-  exact_thin_kernel<<<sm_count() * 2, 256, (size_t)d * sizeof(float), st>>>(P, d, C, k, thin_list, thin_count,
-                                                                           row_ids, out, state);
+  exact_merge_kernel<<<sm_count(), 256, 0, st>>>(flag_list, flag_count, out, sc, state);
   PCB_CHECK_LAUNCH();
   return 0;
 }

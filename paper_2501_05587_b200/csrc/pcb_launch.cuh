@@ -29,11 +29,10 @@ int assign_tc3xtf32_devcount(const float* phi, const float* plo, int ld, const f
                              const int* row_ids = nullptr, int* flag_list = nullptr, int* flag_count = nullptr);
 
 // Exact argmin over all centroids of the rows flag_list[0 : *flag_count)
-// (row r of P = P[row_ids[r]], or r); out[r] = label.  thin_list /
-// thin_count: scratch for the rows the f32 pass leaves to the f64 pass.
+// (row r of P = P[row_ids[r]], or r); out[r] = label.  scratch:
+// exact_scratch_bytes().
 int exact_rows(const float* P, int d, const float* C, int k, const int* flag_list, const int* flag_count,
-               int* thin_list, int* thin_count, const int* row_ids, int32_t* out, void* scratch,
-               const long long* state, cudaStream_t st);
+               const int* row_ids, int32_t* out, void* scratch, const long long* state, cudaStream_t st);
 int64_t exact_scratch_bytes();
 
 int assign_screen_resident(const float* P_r, int64_t n, int ld, const float* C_r, int k, const float* cnorm,

@@ -388,8 +388,8 @@ class LloydEngine(ShardSequence):
                 self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
-                self.flag_list = torch.empty(2 * n, dtype=torch.int32, device=dev)  # flagged | thin margin
-                self.flag_count = torch.zeros(2, dtype=torch.int32, device=dev)
+                self.flag_list = torch.empty(n, dtype=torch.int32, device=dev)
+                self.flag_count = torch.zeros(1, dtype=torch.int32, device=dev)
                 self.exact_scratch = torch.empty(int(L.load().pcb_exact_scratch_bytes()), dtype=torch.uint8,
                                                  device=dev)
                 self.P_r = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
@@ -432,8 +432,8 @@ class LloydEngine(ShardSequence):
                 self.sub_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.sub_labels = torch.empty(n, dtype=torch.int32, device=dev)
-                self.flag_list = torch.empty(2 * n, dtype=torch.int32, device=dev)  # flagged | thin margin
-                self.flag_count = torch.zeros(2, dtype=torch.int32, device=dev)
+                self.flag_list = torch.empty(n, dtype=torch.int32, device=dev)
+                self.flag_count = torch.zeros(1, dtype=torch.int32, device=dev)
                 self.exact_scratch = torch.empty(int(L.load().pcb_exact_scratch_bytes()), dtype=torch.uint8,
                                                  device=dev)
                 if self.q8:
@@ -841,8 +841,8 @@ class LloydEngine(ShardSequence):
                 rows = torch.arange(m, dtype=torch.int32, device=self.dev)
                 cnt = torch.full((1,), m, dtype=torch.int32, device=self.dev)
                 sub = torch.empty(m, dtype=torch.int32, device=self.dev)
-                fl = torch.empty(2 * m, dtype=torch.int32, device=self.dev)
-                fc = torch.zeros(2, dtype=torch.int32, device=self.dev)
+                fl = torch.empty(m, dtype=torch.int32, device=self.dev)
+                fc = torch.zeros(1, dtype=torch.int32, device=self.dev)
                 xs = torch.empty(int(L.load().pcb_exact_scratch_bytes()), dtype=torch.uint8, device=self.dev)
                 L.call("pcb_resolve_ambiguous_f32", _p(Xt), m, self.d, _p(rows), _p(cnt), self.ld, _p(xh), _p(xl),
                        _p(sub), _p(xn), _p(self.C), _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(out),
