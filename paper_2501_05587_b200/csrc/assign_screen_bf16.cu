@@ -39,21 +39,14 @@
 #include "pcb_launch.cuh"
 #include "screen_common.cuh"
 
-#if defined(PCB_EXP) && PCB_EXP == 9
-// experiment build: no TMEM loads at all (MMA + TMA producer ceiling)
-#define SB_TMEM_LD(addr, regs) ((void)(addr))
-#else
-#define SB_TMEM_LD(addr, regs) ptx::tmem_ld_32x32b_x32_async(addr, regs)
-#endif
 #include "tc_ptx.cuh"
 
 namespace pcb {
 
 constexpr int SB_BN = 128;
-#ifdef PCB_SB_STAGES
-constexpr int SB_STAGES = PCB_SB_STAGES;  // experiment builds
-#else
 constexpr int SB_STAGES = 4;
+#ifndef PCB_REGS_LOW
+#define PCB_REGS_LOW 96
 #endif
 constexpr int SB_THREADS = 384;
 constexpr int SB_BKE = 64;      // BF16 elements per 128-byte swizzle row
@@ -94,6 +87,13 @@ struct SbCfg {
   static constexpr int kStages = W ? 3 : (SB_STAGES < kStagesFit ? SB_STAGES : kStagesFit);
   static constexpr uint32_t kSmem = 1024 + kABytes + kStages * kStageB + kAAug + kBarBytes;
   static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
+  // setmaxnreg split of the CTA's registers: producer / MMA warpgroup
+  // (kRegsLow) and the two epilogue warpgroups (kRegsHigh).  setmaxnreg.inc
+  // only draws on what the CTA was launched with (384 x 168, the
+  // __launch_bounds__ cap; checked at launch): 128 low + 256 high <= 64512.
+  static constexpr int kLaunchRegs = 168;
+  static constexpr int kRegsLow = PCB_REGS_LOW;
+  static constexpr int kRegsHigh = (SB_THREADS * kLaunchRegs - 128 * kRegsLow) / 256 / 8 * 8;
   static_assert(!W || NKC <= 2, "the wide layout keeps a whole tile's chunks in the ring");
   static_assert(!W || RT == 2, "the wide layout alternates two row tiles");
 };
@@ -120,6 +120,47 @@ __device__ __forceinline__ int64_t sb_rows(int64_t n, const int* amb_count, int6
   if (amb_count == nullptr) return n;
   const int64_t c = *(volatile const int*)amb_count;
   return c > bypass ? 0 : c;
+}
+
+// Minimum of a 32-key chunk: a depth-4 tree of 3-input mins (16 FMNMX3).
+__device__ __forceinline__ float sb_chunk_min(const uint32_t (&c)[32]) {
+  float t[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i)
+    t[i] = fmin3(__uint_as_float(c[3 * i]), __uint_as_float(c[3 * i + 1]), __uint_as_float(c[3 * i + 2]));
+  t[10] = fminf(__uint_as_float(c[30]), __uint_as_float(c[31]));
+  return fminf(fmin3(fmin3(t[0], t[1], t[2]), fmin3(t[3], t[4], t[5]), fmin3(t[6], t[7], t[8])), fminf(t[9], t[10]));
+}
+
+// Pass 2 (candidate emission) on one 32-key chunk (columns col ..): the
+// candidate mask (FSETP + SEL per key), then a short loop over its set bits
+// (2-3 candidates per row in total).
+__device__ __forceinline__ void sb_chunk_cand(const uint32_t (&cur)[32], int col, float thr, int64_t row, int64_t n,
+                                              int64_t rc, int* __restrict__ cand, int& nc) {
+  uint32_t bits = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) bits |= (__uint_as_float(cur[i]) <= thr ? 1u : 0u) << i;
+  while (bits) {
+    const int i = __ffs(bits) - 1;
+    bits &= bits - 1;
+    if (row < n && nc < SB_NCAND) cand[rc * SB_NCAND + nc] = col + i;
+    ++nc;
+  }
+}
+
+// Full update of one chunk (running best two packed keys, exact count).
+__device__ __forceinline__ void sb_chunk_full(const uint32_t (&cur)[32], int col, float twoE, uint32_t msk,
+                                              float& R1, int& r1, float& R2, int& r2, float& cnt) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
+  screen_chunk_top2(v, msk, col, twoE, R1, r1, R2, r2, cnt);
+}
+
+// Chunk skip threshold of the running minimum: a chunk whose smallest key is
+// above it for every row of the warp leaves (R1, r1, R2, r2, cnt) unchanged.
+__device__ __forceinline__ float sb_skip_thr(float R1, float twoE) {
+  return (R1 + twoE + 0x1p-16f * fabsf(R1)) * (1.0f + 0x1p-16f);
 }
 
 template <int NKC, bool CAND, bool W, bool F8, int RT, int CB>
@@ -155,7 +196,9 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
   uint64_t* tempty = tfull + 4;                              // [2][2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so role branches and the
+  // MMA loop's bookkeeping stay in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int ntiles = (k + BN - 1) / BN;
   const float OFF = bstat[2];
   // constant A columns of the augmented K step, no-swizzle K-major layout
@@ -195,7 +238,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t npairs = (n + PR - 1) / PR;
-
+  // registers: the producer / MMA warpgroup needs few, the two epilogue
+  // warpgroups hold two chunk pairs of keys (128 registers) in flight
+  if (warp < 4) {
+  ptx::regs_dec<SbCfg<NKC, W, RT, CB>::kRegsLow>();
   if (warp == 0) {
     // ---------------- A producer: both row tiles, chunk by chunk ----------------
     const uint64_t pol = ptx::policy_evict_first();
@@ -205,14 +251,6 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         const int ab = it % AS;
         uint8_t* sAp = sA + ab * Cfg::kAPair;
         if (it >= AS) ptx::mbar_wait(&aempty[ab * NKC + c], (uint32_t)((it / AS - 1) & 1));
-#if defined(PCB_EXP) && PCB_EXP == 13
-        // experiment build: A loaded for the first two pairs only (A-latency share of the pace)
-        if (it >= 2) {
-          if (ptx::elect_one()) ptx::mbar_expect_tx(&afull[ab * NKC + c], 0u);
-          __syncwarp();
-          continue;
-        }
-#endif
         if (ptx::elect_one()) {
           ptx::mbar_expect_tx(&afull[ab * NKC + c], RT * Cfg::kTileBytes);
           ptx::tma_load_2d(&tm_a, &afull[ab * NKC + c], sAp + (0 * NKC + c) * Cfg::kTileBytes, c * XC,
@@ -242,12 +280,6 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           if (ptx::elect_one()) {
             uint8_t* st = sB + stage * Cfg::kStageB;
             const bool last = c + 1 == NKC;  // the tile's augmented columns ride with its last chunk
-#if defined(PCB_EXP) && PCB_EXP == 10
-            // experiment build: B streamed for the first pair only (smem-write share of the MMA pace)
-            if (pr != blockIdx.x) {
-              ptx::mbar_expect_tx(&full[stage], 0u);
-            } else
-#endif
             {
             ptx::mbar_expect_tx(&full[stage], Cfg::kBBytes + (last ? Cfg::kAugBytes : 0u));
             ptx::tma_load_2d(&tm_b, &full[stage], st, c * XC, tile * BN, pol);
@@ -336,14 +368,6 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     int abuf = 0;
     uint32_t aphase = 0;
     int it = 0;
-#if defined(PCB_EXP) && PCB_EXP == 14
-    // experiment build: MMA-warp cycle accounting -> state[8..11] (tempty, afull, full, total)
-    long long w_te = 0, w_af = 0, w_fu = 0;
-    const long long w_t0 = clock64();
-#define SB_TIMED(acc, stmt) do { const long long _c = clock64(); stmt; acc += clock64() - _c; } while (0)
-#else
-#define SB_TIMED(acc, stmt) stmt
-#endif
     // Per centroid tile: all K steps of row tile 0, handed to its 4 epilogue
     // warps, then row tile 1 — each row tile's accumulator is released by its
     // own warps, and row tile 0's epilogue starts while row tile 1's MMAs run.
@@ -361,16 +385,14 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         }
 #pragma unroll
         for (int rt = 0; rt < RT; ++rt) {
-#if !(defined(PCB_EXP) && PCB_EXP == 12)
-          SB_TIMED(w_te, ptx::mbar_wait(&tempty[abuf * 2 + rt], aphase ^ 1u));
-#endif
+          ptx::mbar_wait(&tempty[abuf * 2 + rt], aphase ^ 1u);
           ptx::tc_fence_after();
           const uint32_t d0 = tmem + (uint32_t)(abuf * 256 + rt * 128);
 #pragma unroll
           for (int c = 0; c < NKC; ++c) {
             if (rt == 0) {
-              if (nt == 0) SB_TIMED(w_af, ptx::mbar_wait(&afull[ab * NKC + c], (uint32_t)((it / AS) & 1)));
-              SB_TIMED(w_fu, ptx::mbar_wait(&full[stc[c]], phc[c]));
+              if (nt == 0) ptx::mbar_wait(&afull[ab * NKC + c], (uint32_t)((it / AS) & 1));
+              ptx::mbar_wait(&full[stc[c]], phc[c]);
               ptx::tc_fence_after();
             }
             const uint64_t a0 = sdesc(ptx::smem_u32(sAp + (rt * NKC + c) * Cfg::kTileBytes));
@@ -381,11 +403,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
                 const uint64_t off = (uint64_t)(ks * 32) >> 4;
                 mma_main(d0, a0 + off, bd + off, (c | ks) != 0);
               }
-#if defined(PCB_EXP) && PCB_EXP == 8
-              if (false) {  // experiment build: no augmented step (keys wrong, timing only)
-#else
               if (c + 1 == NKC) {  // augmented K step: + (|c|^2 + OFF) in three BF16 pieces
-#endif
                 const uint64_t aa = ptx::sdesc_k_none(ptx::smem_u32(sAaug), 128 * 16, 128);
                 const uint64_t ba = ptx::sdesc_k_none(ptx::smem_u32(sB + stc[c] * Cfg::kStageB + Cfg::kBBytes),
                                                       BN * 16, 128);
@@ -405,30 +423,11 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         if (abuf == 0) aphase ^= 1u;
       }
     }
-#if defined(PCB_EXP) && PCB_EXP == 14
-    if ((threadIdx.x & 31) == 0) {
-      atomicAdd((unsigned long long*)state + 8, (unsigned long long)w_te);
-      atomicAdd((unsigned long long*)state + 9, (unsigned long long)w_af);
-      atomicAdd((unsigned long long*)state + 10, (unsigned long long)w_fu);
-      atomicAdd((unsigned long long*)state + 11, (unsigned long long)(clock64() - w_t0));
-    }
-#endif
-#undef SB_TIMED
-#if defined(PCB_EXP) && PCB_EXP == 12
-    // experiment build: MMA pipeline without the TMEM handoff (no epilogue)
-    __shared__ uint64_t done_bar;
-    if (ptx::elect_one()) { ptx::mbar_init(&done_bar, 1); ptx::fence_barrier_init(); }
-    __syncwarp();
-    if (ptx::elect_one()) ptx::umma_commit(&done_bar);
-    __syncwarp();
-    ptx::mbar_wait(&done_bar, 0);
-#endif
     }  // !W
-  } else if (warp >= 4 && warp < 4 + 4 * RT
-#if defined(PCB_EXP) && PCB_EXP == 12
-             && false
-#endif
-             ) {
+  }
+  } else {
+  ptx::regs_inc<SbCfg<NKC, W, RT, CB>::kRegsHigh>();
+  if (warp < 4 + 4 * RT) {
     // ---------------- epilogue: warp (g, h) = lanes 32g.. of row tile h ----------------
     const int g = warp & 3, h = (warp - 4) >> 2;
     const float Bmax = bstat[0], dBmax = bstat[1];
@@ -455,9 +454,15 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         if (abuf == 0) aphase ^= 1u;
       }
     };
-    // TMEM loads run one 32-column chunk ahead of the arithmetic (vA / vB by
-    // chunk parity; 4 chunks per tile), across tile and pair boundaries
-    uint32_t vA[32], vB[32];
+    // TMEM loads run one chunk PAIR ahead of the arithmetic: two 32-column
+    // loads are issued back to back and covered by one tcgen05.wait::ld (which
+    // waits for every outstanding load), so each wait's latency is paid once
+    // per 64 columns.  Buffers (vA0, vA1) / (vB0, vB1) alternate by pair
+    // parity (CH / 2 pairs per tile, an even count), across tile and pair
+    // boundaries.  The epilogue warpgroups run at 224 registers (setmaxnreg).
+    constexpr int CP = CH / 2;
+    static_assert(CH % 4 == 0, "chunk pairs alternate buffers across tiles");
+    uint32_t vA0[32], vA1[32], vB0[32], vB1[32];
     // per-row inputs of the next pair are fetched one pair ahead: their DRAM
     // latency would otherwise hold both TMEM buffers (and the MMAs) at every
     // pair boundary
@@ -466,7 +471,8 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     // first column (orig -> previous label) is a dependent pair of loads: the
     // second one is issued a chunk later (fetch_pair_b).
     float an_nx = 0.0f, dan_nx = 0.0f;
-    int fc_nx = 0, out_nx = 0, mid_nx = 0;
+    unsigned fc_nx = 0;  // first column of the next pair (unsigned: / and % are shifts)
+    int out_nx = 0, mid_nx = 0;
     auto fetch_pair = [&](int64_t p) {
       const int64_t rr = p * PR + r_in < n ? p * PR + r_in : n - 1;
       out_nx = (!CAND && orig != nullptr) ? orig[rr] : (int)rr;
@@ -482,22 +488,16 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
     };
     auto fetch_pair_b = [&]() {
       const int l = lprev != nullptr ? lprev[mid_nx] : 0;
-      fc_nx = (l >= 0 && l < k) ? l : 0;
+      fc_nx = (l >= 0 && l < k) ? (unsigned)l : 0u;
     };
-#if defined(PCB_EXP) && PCB_EXP == 15
-    // experiment build: epilogue cycle accounting -> state[12..15] (tfull waits, full-path chunks, pair ends, total)
-    long long e_wait = 0, e_full = 0, e_end = 0;
-    const long long e_t0 = clock64();
-#define SB_ET(acc, stmt) do { const long long _c = clock64(); stmt; acc += clock64() - _c; } while (0)
-#else
-#define SB_ET(acc, stmt) stmt
-#endif
     if (blockIdx.x < npairs) {
       fetch_pair(blockIdx.x);
       fetch_pair_b();
       ptx::mbar_wait(&tfull[tbar()], 0);
       ptx::tc_fence_after();
-      SB_TMEM_LD(tbase() + 32 * ((fc_nx % BN) / 32), vA);
+      const int q0 = (int)((fc_nx % BN) / 32);
+      ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * q0, vA0);
+      ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * ((q0 + 1) & (CH - 1)), vA1);
     }
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
       const int64_t row = pr * PR + r_in;
@@ -511,93 +511,66 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         twoE = kscale * screen_two_e_aug(an_nx, dan_nx, Bmax, dBmax, OFF, acc_rel);
         big = 64.0f / twoE;
       }
-      const int t0 = fc_nx / BN, q0 = (fc_nx % BN) / 32;
+      (void)big;
+      const int t0 = (int)(fc_nx / BN), q0 = (int)((fc_nx % BN) / 32);
       const int out_row = out_nx;  // original row id (label store)
       if (!last_pair) fetch_pair(pr + gridDim.x);
       float R1 = 3.4e38f, R2 = 3.4e38f, cnt = 0.0f;
       int r1 = 0, r2 = 0;
+      float thr_skip = 3.4e38f;  // sb_skip_thr(R1, twoE), refreshed when R1 changes
       for (int nt = 0; nt < ntiles; ++nt) {
         const uint32_t taddr = tbase();
         const int c0 = (nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles) * BN;
 #pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          uint32_t (&cur)[32] = (q & 1) ? vB : vA;
-          uint32_t (&nxt)[32] = (q & 1) ? vA : vB;
-          ptx::tmem_wait_ld(cur);
-          if (nt == 0 && q == CH - 1 && !last_pair) fetch_pair_b();  // its first load was issued a tile ago
-          const int qe = nt == 0 ? ((q + q0) & (CH - 1)) : q;  // chunk of the tile held by cur
-          if (q < CH - 1) {
-            const int qn = nt == 0 ? ((q + 1 + q0) & (CH - 1)) : q + 1;
-            SB_TMEM_LD(taddr + 32 * qn, nxt);
+        for (int p = 0; p < CP; ++p) {
+          uint32_t (&cur0)[32] = (p & 1) ? vB0 : vA0;
+          uint32_t (&cur1)[32] = (p & 1) ? vB1 : vA1;
+          uint32_t (&nxt0)[32] = (p & 1) ? vA0 : vB0;
+          uint32_t (&nxt1)[32] = (p & 1) ? vA1 : vB1;
+          ptx::tmem_wait_ld(cur0);
+          ptx::tie_regs(cur1);
+          if (nt == 0 && p == CP - 1 && !last_pair) fetch_pair_b();  // its first load was issued a tile ago
+          // chunks of the tile held by cur0 / cur1 (the first tile starts at the previous label's chunk)
+          const int qa = nt == 0 ? ((2 * p + q0) & (CH - 1)) : 2 * p;
+          const int qb = nt == 0 ? ((2 * p + 1 + q0) & (CH - 1)) : 2 * p + 1;
+          if (p < CP - 1) {
+            const int qn = nt == 0 ? ((2 * p + 2 + q0) & (CH - 1)) : 2 * p + 2;
+            const int qm = nt == 0 ? ((2 * p + 3 + q0) & (CH - 1)) : 2 * p + 3;
+            ptx::tmem_ld_32x32b_x32_async(taddr + 32 * qn, nxt0);
+            ptx::tmem_ld_32x32b_x32_async(taddr + 32 * qm, nxt1);
           } else {
             // this accumulator is fully read: hand it back, prefetch the next one
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[tbar()]);
             tnext();
             if (nt + 1 < ntiles || !last_pair) {
-              SB_ET(e_wait, ptx::mbar_wait(&tfull[tbar()], tphase()));
+              ptx::mbar_wait(&tfull[tbar()], tphase());
               ptx::tc_fence_after();
-              // first chunk of the next pair: read fc_nx only here, a pair after
+              // first chunks of the next pair: read fc_nx only here, a pair after
               // its (two dependent) loads were issued
-              const int qn = nt + 1 < ntiles ? 0 : (fc_nx % BN) / 32;
-              SB_TMEM_LD(tbase() + 32 * qn, nxt);
+              const int qn = nt + 1 < ntiles ? 0 : (int)((fc_nx % BN) / 32);
+              ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * qn, nxt0);
+              ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * ((qn + 1) & (CH - 1)), nxt1);
             }
           }
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]);
-#if defined(PCB_EXP) && (PCB_EXP == 2 || PCB_EXP == 8 || PCB_EXP == 9 || PCB_EXP == 10 || PCB_EXP == 13)
-          // experiment build: TMEM traffic only (MMA + TMEM-load ceiling)
-          R1 = fminf(R1, v[0] + v[31]);
-          continue;
-#endif
           if (CAND) {
-            // candidate mask of the chunk (FSETP + SEL per key), then a short
-            // loop over its set bits (2-3 candidates per row in total)
-            uint32_t bits = 0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) bits |= (v[i] <= thr ? 1u : 0u) << i;
-            while (bits) {
-              const int i = __ffs(bits) - 1;
-              bits &= bits - 1;
-              if (row < n && nc < SB_NCAND) cand[rc * SB_NCAND + nc] = c0 + 32 * qe + i;
-              ++nc;
-            }
+            sb_chunk_cand(cur0, c0 + 32 * qa, thr, row, n, rc, cand, nc);
+            sb_chunk_cand(cur1, c0 + 32 * qb, thr, row, n, rc, cand, nc);
           } else {
-            // chunk skip: when no key of the chunk is within the running
-            // threshold for any row of the warp, processing it would leave
-            // (R1, r1, cnt) unchanged — the full update below is skipped.
-            // Rows are laid out by label (pcb_screen_relayout_bf16), so the
-            // rows of a warp see their minima in the same chunks and most
-            // chunks of most warps take this path.
-            const float thr_skip = (R1 + twoE + 0x1p-16f * fabsf(R1)) * (1.0f + 0x1p-16f);
-            const float (&km)[32] = v;  // the MMA produced the keys (augmented K step)
-            // minimum of the chunk as a depth-4 tree of 3-input mins (a chain
-            // of 16 dependent FMNMX3 sits on every chunk's critical path)
-            float t[11];
-#pragma unroll
-            for (int i = 0; i < 10; ++i) t[i] = fmin3(km[3 * i], km[3 * i + 1], km[3 * i + 2]);
-            t[10] = fminf(km[30], km[31]);
-            const float mm = fminf(fmin3(fmin3(t[0], t[1], t[2]), fmin3(t[3], t[4], t[5]), fmin3(t[6], t[7], t[8])),
-                                   fminf(t[9], t[10]));
-#if defined(PCB_EXP) && PCB_EXP == 5
-            // experiment build: skip-path cost only (results invalid)
-            if (__any_sync(0xffffffffu, mm <= thr_skip)) R1 = fminf(R1, mm);
-#else
-            if (__any_sync(0xffffffffu, mm <= thr_skip)) {
-              SB_ET(e_full, screen_chunk_top2(km, msk, c0 + 32 * qe, twoE, R1, r1, R2, r2, cnt));
-#if defined(PCB_EXP) && PCB_EXP == 6
-              // experiment build: count full-path chunks per position (q + 4 * nt) in state[8..]
-              if (lane == 0) atomicAdd((unsigned long long*)state + 8 + (nt < 8 ? nt * 4 + (q & 3) : 32), 1ull);
-#endif
+            // chunk skip, decided per pair: rows are laid out by label
+            // (pcb_screen_relayout_bf16), so the rows of a warp see their
+            // minima in the same chunks and most pairs of most warps skip
+            const float m0 = sb_chunk_min(cur0), m1 = sb_chunk_min(cur1);
+            if (__any_sync(0xffffffffu, fminf(m0, m1) <= thr_skip)) {
+              if (__any_sync(0xffffffffu, m0 <= thr_skip))
+                sb_chunk_full(cur0, c0 + 32 * qa, twoE, msk, R1, r1, R2, r2, cnt);
+              if (__any_sync(0xffffffffu, m1 <= sb_skip_thr(R1, twoE)))
+                sb_chunk_full(cur1, c0 + 32 * qb, twoE, msk, R1, r1, R2, r2, cnt);
+              thr_skip = sb_skip_thr(R1, twoE);
             }
-#endif
           }
         }
       }
-#if defined(PCB_EXP) && PCB_EXP == 15
-      const long long e_c0 = clock64();
-#endif
       if (CAND) {
         if (row < n) cand_n[row] = nc;
       } else {
@@ -617,11 +590,7 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
             two_list[3 * pos + 2] = r2;
           }
         }
-#if defined(PCB_EXP) && PCB_EXP == 7
-        const bool amb = false;  // experiment build: no ambiguous-row append
-#else
         const bool amb = row < n && cnt > 2.0f;
-#endif
         const unsigned m = __ballot_sync(0xffffffffu, amb);
         if (m) {
           int base = 0;
@@ -635,20 +604,9 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
           }
         }
       }
-#if defined(PCB_EXP) && PCB_EXP == 15
-      e_end += clock64() - e_c0;
-#endif
     }
-#if defined(PCB_EXP) && PCB_EXP == 15
-    if (lane == 0 && !CAND) {
-      atomicAdd((unsigned long long*)state + 12, (unsigned long long)e_wait);
-      atomicAdd((unsigned long long*)state + 13, (unsigned long long)e_full);
-      atomicAdd((unsigned long long*)state + 14, (unsigned long long)e_end);
-      atomicAdd((unsigned long long*)state + 15, (unsigned long long)(clock64() - e_t0));
-    }
-#endif
-#undef SB_ET
   }
+  }  // epilogue warpgroups
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -694,6 +652,16 @@ static int launch_screen_bf16(const __nv_bfloat16* A, int64_t n, const __nv_bflo
   auto kern = assign_screen_bf16_kernel<NKC, CAND, W, F8, RT, CB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   if (e != cudaSuccess) return (int)e;
+  {
+    // the setmaxnreg split assumes the launch allocation ptxas was given
+    static int regs = -1;
+    if (regs < 0) {
+      cudaFuncAttributes fa;
+      if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return PCB_ENODEV;
+      regs = fa.numRegs;
+    }
+    if (regs != Cfg::kLaunchRegs) return PCB_EUNSUP;
+  }
   const int64_t npairs = (n + Cfg::kRows - 1) / Cfg::kRows;
   const int grid = (int)std::min<int64_t>(npairs, (int64_t)sm_count());
   kern<<<grid, SB_THREADS, Cfg::kSmem, st>>>(ta, tb, tg, an, dan, bstat, n, k, labels, amb_list, amb_count,
