@@ -374,7 +374,7 @@ def main():
     peaks, peak_src = _peaks()
     n_local = hi - lo
     flops = 2.0 * n_local * k * d  # algorithmic: one dot product per point-centroid pair
-    ffma_path = d <= 32 and eng.variant not in ("tc3xtf32", "tc1xtf32s", "bf16s", "fp8s")
+    ffma_path = d <= 32 and eng.variant not in ("tc3xtf32", "tc1xtf32s", "bf16s", "fp8s", "deltatc")
     if ffma_path:
         # small-d FFMA path: SURVEY 8(d) puts it on the FFMA roof (AI ~28 flop/B > ridge);
         # peak = 148 SMs x 128 FP32 lanes x 2 flop x the SM clock sampled under load
@@ -394,13 +394,28 @@ def main():
             peak, src = peaks["bf16_tflops"], "bf16 burst (dense)"
         elif eng.variant == "fp8s":  # one E4M3 (kind::f8f6f4) pass: twice the BF16 rate
             peak, src = 2.0 * peaks["bf16_tflops"], "fp8 = 2 x bf16 burst (dense, derived)"
+        elif eng.variant == "deltatc":
+            # the chunked scheme issues 3 x 3xTF32 block products per (pair, block), not one
+            # dot product: its own roof is 3xTF32 on the algorithmic 2nkd basis; the MMA
+            # work it actually issues is reported beside it against plain TF32
+            peak, src = tf32 / 3.0, "3xTF32 effective = bf16 burst / 6"
         else:
             peak, src = tf32, "TF32 = bf16 burst / 2"
         roof = {"bound": "tensor", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": peak,
                 "unit": "TFLOP/s", "traffic": None, "peak_source": f"{peak_src} {src}"}
+        if eng.variant == "deltatc":
+            nb = (d + 1 + 7) // 8  # delta = 8 blocks of the augmented row
+            kpad = (k + 15) // 16 * 16
+            npad = (n_local + 127) // 128 * 128
+            # per (point, centroid): T_0 3 MMAs x nb blocks + T_b 5 MMAs x (nb - 1), 8x8 MACs each
+            mma_flops = 2.0 * npad * kpad * 64 * (3 * nb + 5 * (nb - 1))
+            roof["mma_flops_per_launch"] = mma_flops
+            roof["mma_tflops"] = mma_flops / (kern_ms * 1e-3) / 1e12
+            roof["mma_frac_of_tf32"] = roof["mma_tflops"] / tf32
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["kernel"] = {"tc1xtf32s": "assign_screen_res_kernel", "tc3xtf32": "assign_tc3xtf32_kernel",
-                      "bf16s": "assign_screen_bf16_kernel", "fp8s": "assign_screen_bf16_kernel<F8>"}.get(
+                      "bf16s": "assign_screen_bf16_kernel", "fp8s": "assign_screen_bf16_kernel<F8>",
+                      "deltatc": "assign_delta_tc_kernel", "delta": "assign_delta_kernel"}.get(
         eng.variant, f"assign[{eng.variant}]")
     roof["kernel_ms"] = kern_ms
     roof["algorithmic_per_launch"] = f"2*n*k*d = {flops:.4g} flop (per rank)"

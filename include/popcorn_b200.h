@@ -46,6 +46,7 @@ extern "C" {
 #define PCB_ASSIGN_SCREEN    5  /* tcgen05 1xTF32 certified screening (f32) */
 #define PCB_ASSIGN_SCREEN_BF16 6 /* tcgen05 BF16 certified screening + exact candidates (f32, d <= 256) */
 #define PCB_ASSIGN_SCREEN_FP8  7 /* same with E4M3 operands (kind::f8f6f4), scaled keys (f32, d <= 256) */
+#define PCB_ASSIGN_DELTA_TC    8 /* delta-chunked P.C.P^T ablation on tcgen05 (3xTF32 block MMAs, f32) */
 
 int         pcb_abi_version(void);
 /* Kernels launched by this library so far in this process (launches recorded
@@ -133,6 +134,25 @@ int pcb_assign_tc_f32(const float* P_hi, const float* P_lo, int ld, const float*
                       int d, const float* C_hi, const float* C_lo, const float* cnorm, int k,
                       const int32_t* labels_prev, int32_t* labels, float* mind, double* acc,
                       const long long* state, void* stream);
+
+/* delta-chunked P.C.P^T on the tensor cores (PCB_ASSIGN_DELTA_TC, the
+ * tensor-core form of the attachment's scheme; see
+ * assign_delta_tc.cu).  delta = 8; the augmented operands are
+ *   Q   = [1, p, 0..]             n x ld          (pcb_delta_tc_prep_points, once per fit)
+ *   F,G = C_j's first block column / first block row, 8 rows per centroid,
+ *         (8 * pcb_delta_tc_kpad(k)) x ld    (pcb_delta_tc_prep_centroids, per iteration)
+ * each split into TF32 hi + exact remainder lo; ld = pcb_delta_tc_ld(d).
+ * Outputs and bookkeeping as pcb_assign_f32, with mind[i] = D[i, labels[i]]
+ * (the full bilinear form, |p|^2 included).                                */
+int pcb_delta_tc_ld(int d);
+int pcb_delta_tc_kpad(int k);
+int pcb_delta_tc_prep_points(const float* P, int64_t n, int d, int ld, float* Q_hi, float* Q_lo, void* stream);
+int pcb_delta_tc_prep_centroids(const float* C, const float* cnorm, int k, int d, int ld, float* F_hi,
+                                float* F_lo, float* G_hi, float* G_lo, void* stream);
+int pcb_assign_delta_tc_f32(const float* Q_hi, const float* Q_lo, int ld, int64_t n, int d,
+                            const float* F_hi, const float* F_lo, const float* G_hi, const float* G_lo,
+                            int k, const int32_t* labels_prev, int32_t* labels, float* mind,
+                            double* acc, const long long* state, void* stream);
 
 /* Certified 1xTF32 screening variant ("tc1xtf32s", see assign_screen.cu):
  * one TF32 tensor-core pass on TF32-rounded operands (P_r = rna(P), C_r =

@@ -99,14 +99,21 @@ SIGNATURES = {
     "pcb_kk_repair_f64": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, I64, P]),
     "pcb_kk_finalize": (I32, [P, P, P, I64, I32, P, P, P, P, P, I32, F64, P]),
     "pcb_mma_probe": (I32, [P, P, P, I32, P, P, P]),
+    "pcb_delta_tc_ld": (I32, [I32]),
+    "pcb_delta_tc_kpad": (I32, [I32]),
+    "pcb_delta_tc_prep_points": (I32, [P, I64, I32, I32, P, P, P]),
+    "pcb_delta_tc_prep_centroids": (I32, [P, P, I32, I32, I32, P, P, P, P, P]),
+    "pcb_assign_delta_tc_f32": (I32, [P, P, I32, I64, I32, P, P, P, P, I32, P, P, P, P, P, P]),
 }
 
 ASSIGN_AUTO, ASSIGN_ROWREG, ASSIGN_TILED, ASSIGN_TC3XTF32, ASSIGN_DELTA, ASSIGN_SCREEN = 0, 1, 2, 3, 4, 5
 ASSIGN_SCREEN_BF16 = 6
 ASSIGN_SCREEN_FP8 = 7
+ASSIGN_DELTA_TC = 8
 VARIANTS = {"auto": ASSIGN_AUTO, "rowreg": ASSIGN_ROWREG, "tiled": ASSIGN_TILED,
             "tc3xtf32": ASSIGN_TC3XTF32, "delta": ASSIGN_DELTA, "tc1xtf32s": ASSIGN_SCREEN,
-            "bf16s": ASSIGN_SCREEN_BF16, "fp8s": ASSIGN_SCREEN_FP8}
+            "bf16s": ASSIGN_SCREEN_BF16, "fp8s": ASSIGN_SCREEN_FP8,
+            "deltatc": ASSIGN_DELTA_TC}
 STATE_WORDS = 8
 
 _lib = None

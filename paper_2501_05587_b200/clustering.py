@@ -54,7 +54,8 @@ class KKMeansConfig:
       init                 None -> random labels + means (clustering.py:298-300);
                            an array (k, d) -> fixed initial centroids.
       record_label_history keep per-iteration labels (4n bytes D2H per iteration).
-      variant              assignment kernel: 'auto', 'rowreg', 'tiled', 'tc3xtf32', 'tc1xtf32s', 'bf16s'.
+      variant              assignment kernel: 'auto', 'rowreg', 'tiled', 'tc3xtf32', 'tc1xtf32s', 'bf16s',
+                           'fp8s', or the delta-chunked ablations 'delta' (FFMA) / 'deltatc' (tcgen05).
       device               CUDA device index (None = current).
     """
 

@@ -134,7 +134,7 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
     if variant not in L.VARIANTS:
         raise ValueError(f"unknown assign variant {variant!r}; expected one of {tuple(L.VARIANTS)}")
     if variant != "auto":
-        if dtype == _F64 and variant in ("tc3xtf32", "delta", "tc1xtf32s", "bf16s", "fp8s"):
+        if dtype == _F64 and variant in ("tc3xtf32", "delta", "deltatc", "tc1xtf32s", "bf16s", "fp8s"):
             raise ValueError(f"variant {variant!r} is float32-only")
         dmax = 1024 if variant == "fp8s" else 512  # 8 operand chunks of 128 bytes
         if variant in ("bf16s", "fp8s") and (d > dmax or k > SCREEN_KMAX):
@@ -371,6 +371,16 @@ class LloydEngine(ShardSequence):
                 self.ld = (d + 31) // 32 * 32
                 self.C_hi = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
                 self.C_lo = torch.zeros((kk, self.ld), dtype=torch.float32, device=dev)
+            if self.variant == "deltatc":
+                # delta-chunked ablation on the tensor cores: augmented Q = [1, p] and the
+                # centroids' first block column / row (F, G), all split hi/lo (assign_delta_tc.cu)
+                self.ldq = int(L.load().pcb_delta_tc_ld(d))
+                self.Q_hi = torch.empty((n, self.ldq), dtype=torch.float32, device=dev)
+                self.Q_lo = torch.empty((n, self.ldq), dtype=torch.float32, device=dev)
+                brows = 8 * int(L.load().pcb_delta_tc_kpad(kk))
+                self.FG = [torch.zeros((brows, self.ldq), dtype=torch.float32, device=dev) for _ in range(4)]
+                L.call("pcb_delta_tc_prep_points", _p(self.P), n, d, self.ldq, _p(self.Q_hi), _p(self.Q_lo),
+                       _stream())
             if self.variant == "tc3xtf32":
                 self.P_hi = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
                 self.P_lo = torch.empty((n, self.ld), dtype=torch.float32, device=dev)
@@ -479,6 +489,9 @@ class LloydEngine(ShardSequence):
             L.call("pcb_screen_prep_centroids_fp8" if self.q8 else "pcb_screen_prep_centroids_bf16", _p(self.C),
                    _p(self.cnorm), self.k, self.d, self.ld8 if self.q8 else self.ldb, _p(self.C_b), _p(self.C_aug),
                    _p(self.bnorm), _p(self.dbnorm), _p(self.bstat), _stream())
+        if self.variant == "deltatc":
+            L.call("pcb_delta_tc_prep_centroids", _p(self.C), _p(self.cnorm), self.k, self.d, self.ldq,
+                   *[_p(t) for t in self.FG], _stream())
         if self.variant == "tc1xtf32s":
             L.call("pcb_screen_prep_centroids", _p(self.C), self.k, self.d, _p(self.bnorm),
                    _p(self.dbnorm), _p(self.bstat), _stream())
@@ -614,7 +627,11 @@ class LloydEngine(ShardSequence):
                        _stream())
             return
         self._kmark(0)
-        if self.variant == "tc3xtf32":
+        if self.variant == "deltatc":
+            L.call("pcb_assign_delta_tc_f32", _p(self.Q_hi), _p(self.Q_lo), self.ldq, self.n, self.d,
+                   *[_p(t) for t in self.FG], self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
+                   _stream())
+        elif self.variant == "tc3xtf32":
             L.call("pcb_assign_tc_f32", _p(self.P_hi), _p(self.P_lo), self.ld, _p(self.pnorm), self.n,
                    self.d, _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(prev), _p(new),
                    _p(self.mind), _p(acc), _p(state), _stream())
@@ -849,6 +866,6 @@ class LloydEngine(ShardSequence):
                        _p(fl), _p(fc), _p(xs), xs.numel(), None, _stream())
             else:
                 L.call(f"pcb_assign_{self.sfx}", _p(Xt), _p(xn), m, self.d, _p(self.C), _p(self.cnorm),
-                       self.k, None, _p(out), None, None, None, self.vcode if self.variant != "delta" else 0,
+                       self.k, None, _p(out), None, None, None, self.vcode if self.variant not in ("delta", "deltatc") else 0,
                        _stream())
             return out.cpu().numpy()

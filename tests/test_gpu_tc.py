@@ -176,29 +176,59 @@ def test_screen_full_run_matches_reference():
 # ---------------------------------------------------------------------------
 # delta-chunked P.C.P^T ablation
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("n,d,k", [(500, 2, 7), (1000, 16, 40), (1500, 100, 33), (600, 784, 20)])
-def test_delta_chunked_lockstep(n, d, k):
+@pytest.mark.parametrize("variant", ["delta", "deltatc"])
+@pytest.mark.parametrize("n,d,k", [(500, 2, 7), (1000, 16, 40), (1500, 100, 33), (600, 784, 20), (700, 7, 17),
+                                   (300, 8, 16), (1000, 31, 129)])
+def test_delta_chunked_lockstep(variant, n, d, k):
     from paper_2501_05587_b200.engine import LloydEngine
     P = oracle.make_blobs(n, d, k, seed=d)
     lab = oracle.init_assignments(n, k, 2)
     C = oracle.mean_centroids(P, lab, k)
-    eng = LloydEngine(P, k, variant="delta", max_iters=1)
+    eng = LloydEngine(P, k, variant=variant, max_iters=1)
     pn = oracle.point_norms(P)
     for t in range(3):
         ref = oracle.lloyd_step(P, pn, C, lab, k)
         gpu = eng.step_from(C, lab)
-        check_step(P, C, lab, k, gpu, ref=ref, what=f"delta n={n} d={d} k={k} it{t}")
+        check_step(P, C, lab, k, gpu, ref=ref, what=f"{variant} n={n} d={d} k={k} it{t}")
         C, lab = ref.centroids, ref.labels
 
 
-def test_delta_chunked_worked_examples():
+@pytest.mark.parametrize("variant", ["delta", "deltatc"])
+def test_delta_chunked_worked_examples(variant):
     """The attachment's worked values via the chunked kernel (analysis.py oracle)."""
     from paper_2501_05587_b200.engine import LloydEngine
     for p, c, want in (([3.0], [7.0], 16.0), ([1.0], [7.0], 36.0), ([5.0, 2.0], [1.0, 4.0], 20.0),
                        ([4.0, 3.0, 2.0], [5.0, 2.0, 3.0], 3.0)):
         P = np.array([p], dtype=np.float32)
-        eng = LloydEngine(P, 1, variant="delta", max_iters=1)
+        eng = LloydEngine(P, 1, variant=variant, max_iters=1)
         eng.set_centroids(np.array([c], dtype=np.float32))
         out = eng.step_from(np.array([c], dtype=np.float32), np.zeros(1, dtype=np.int32))
         assert out["mind"][0] == pytest.approx(want, abs=1e-5)
         assert out["mind"][0] == pytest.approx(oracle.augmented_distance(p, c), abs=1e-5)
+
+
+def test_delta_tc_full_distances():
+    """Every (point, centroid) value of the tensor-core chunked form against the
+    f64 distance, through predict-free single-centroid runs: k = 1 makes mind the
+    chunked D of that centroid, for d spanning partial blocks and chunks."""
+    from paper_2501_05587_b200.engine import LloydEngine
+    rng = np.random.default_rng(5)
+    for d in (1, 7, 8, 9, 31, 32, 33, 100):
+        P = rng.normal(size=(300, d)).astype(np.float32) * 3
+        c = rng.normal(size=(1, d)).astype(np.float32)
+        eng = LloydEngine(P, 1, variant="deltatc", max_iters=1)
+        out = eng.step_from(c, np.zeros(300, dtype=np.int32))
+        exact = ((P.astype(np.float64) - c.astype(np.float64)) ** 2).sum(1)
+        scale = (P.astype(np.float64) ** 2).sum(1) + (c.astype(np.float64) ** 2).sum()
+        assert np.all(np.abs(out["mind"] - exact) <= 1e-5 * scale + 1e-6), d
+
+
+def test_delta_tc_ablation_matches_fused():
+    """The chunked tensor-core form and the fused 3xTF32 GEMM agree on a fit
+    (both exact up to the f32 expansion's near-ties)."""
+    import paper_2501_05587_b200 as pcb
+    P = oracle.make_blobs(20000, 64, 48, seed=3)
+    a = pcb.run_lloyd(P, pcb.KKMeansConfig(k=48, max_iters=6, variant="deltatc"))
+    ref = oracle.run_lloyd(P, 48, max_iters=6)
+    np.testing.assert_allclose(a.objective_history, ref.objective_history, rtol=1e-6)
+    np.testing.assert_array_equal(a.labels, ref.labels)
