@@ -445,6 +445,12 @@ int pcb_kk_finalize(const int32_t* labels, const int32_t* labels_prev, const dou
  * screening certificates assume (tests/test_gpu_mma_probe.py).             */
 int pcb_mma_probe(const void* A, const void* B, const int* kinds, int nsteps, const float* init, float* D,
                   void* stream);
+/* Same chain with every step E4M3 into an F16 accumulator (the F16-key
+ * screen): init (f32, rounded to f16, may be NULL) is written and D read back
+ * through tcgen05.st/ld .unpack/.pack::16b; raw (may be NULL) receives the
+ * 128 x 128 unpacked 32-bit TMEM cells (layout check).                       */
+int pcb_mma_probe_f16acc(const void* A, const void* B, const int* kinds, int nsteps, const float* init, float* D,
+                         uint32_t* raw, void* stream);
 
 #ifdef __cplusplus
 }

@@ -99,6 +99,7 @@ SIGNATURES = {
     "pcb_kk_repair_f64": (I32, [P, I64, P, I64, I64, I32, P, P, P, P, P, P, P, I64, P]),
     "pcb_kk_finalize": (I32, [P, P, P, I64, I32, P, P, P, P, P, I32, F64, P]),
     "pcb_mma_probe": (I32, [P, P, P, I32, P, P, P]),
+    "pcb_mma_probe_f16acc": (I32, [P, P, P, I32, P, P, P, P]),
     "pcb_delta_tc_ld": (I32, [I32]),
     "pcb_delta_tc_kpad": (I32, [I32]),
     "pcb_delta_tc_prep_points": (I32, [P, I64, I32, I32, P, P, P]),

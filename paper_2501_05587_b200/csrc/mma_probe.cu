@@ -11,6 +11,7 @@
 // optionally preloaded with an arbitrary f32 matrix) on caller-chosen
 // operands and returns the accumulator; tests/test_gpu_mma_probe.py compares
 // it with the exactly rounded sums and checks the screens' budget.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -29,9 +30,13 @@ constexpr uint32_t MP_SMEM = 1024 + 2 * MP_BATCH * MP_STEP;
 // 0 = E4M3 x E4M3 (kind::f8f6f4, K = 32), 1 = BF16 x BF16 (kind::f16, K = 16),
 // 2 = TF32 x TF32 (kind::tf32, K = 8).  D (128 x 128 f32) = init + sum of the
 // steps, or the sum alone when init is null.
+// H16: every step is E4M3 (kind::f8f6f4) into an F16 accumulator; init and D
+// go through tcgen05.st/ld .unpack/.pack::16b (two 16-bit columns per
+// register), raw (optional) receives the unpacked 32-bit TMEM cells.
+template <bool H16>
 __global__ void __launch_bounds__(128, 1)
 mma_probe_kernel(const uint8_t* __restrict__ A, const uint8_t* __restrict__ B, const int* __restrict__ kinds,
-                 int nsteps, const float* __restrict__ init, float* __restrict__ D) {
+                 int nsteps, const float* __restrict__ init, float* __restrict__ D, uint32_t* __restrict__ raw_out) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
@@ -50,12 +55,25 @@ mma_probe_kernel(const uint8_t* __restrict__ A, const uint8_t* __restrict__ B, c
   const uint32_t tmem = tslot;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   if (init != nullptr) {
+    if (H16) {
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t r[32];
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(init[row * 128 + c * 32 + i]);
-      ptx::tmem_st_32x32b_x32(trow + 32 * c, r);
+        for (int i = 0; i < 32; ++i) {
+          const __half2 h = __floats2half2_rn(init[row * 128 + c * 64 + 2 * i], init[row * 128 + c * 64 + 2 * i + 1]);
+          r[i] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        ptx::tmem_st_32x32b_x32_unpack16(trow + 64 * c, r);
+      }
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(init[row * 128 + c * 32 + i]);
+        ptx::tmem_st_32x32b_x32(trow + 32 * c, r);
+      }
     }
   }
   ptx::tc_fence_before();
@@ -86,7 +104,8 @@ mma_probe_kernel(const uint8_t* __restrict__ A, const uint8_t* __restrict__ B, c
           const uint64_t bd = ptx::sdesc_k_none(ptx::smem_u32(sB + s * MP_STEP), 2048, 128);
           const uint32_t acc = (init != nullptr || s0 + s > 0) ? 1u : 0u;
           const int kind = kinds[s0 + s];
-          if (kind == 0) ptx::umma_f8(tmem, ad, bd, ptx::idesc_e4m3<128, 128>(), acc);
+          if (H16) ptx::umma_f8(tmem, ad, bd, ptx::idesc_e4m3<128, 128>() & ~(3u << 4), acc);  // D format F16
+          else if (kind == 0) ptx::umma_f8(tmem, ad, bd, ptx::idesc_e4m3<128, 128>(), acc);
           else if (kind == 1) ptx::umma_f16(tmem, ad, bd, ptx::idesc_bf16<128, 128>(), acc);
           else ptx::umma_tf32(tmem, ad, bd, ptx::idesc_tf32<128, 128>(), acc);
         }
@@ -99,12 +118,36 @@ mma_probe_kernel(const uint8_t* __restrict__ A, const uint8_t* __restrict__ B, c
     ptx::tc_fence_after();
     __syncthreads();  // the next batch overwrites the operands the MMAs read
   }
+  if (H16) {
 #pragma unroll 1
-  for (int c = 0; c < 4; ++c) {
-    float v[32];
-    ptx::tmem_ld_32x32b_x32(trow + 32 * c, v);
+    for (int c = 0; c < 2; ++c) {
+      uint32_t r[32];
+      ptx::tmem_ld_32x32b_x32_async_pack16(trow + 64 * c, r);
+      ptx::tmem_wait_ld(r);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) D[row * 128 + c * 32 + i] = v[i];
+      for (int i = 0; i < 32; ++i) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&r[i]));
+        D[row * 128 + c * 64 + 2 * i] = f.x;
+        D[row * 128 + c * 64 + 2 * i + 1] = f.y;
+      }
+    }
+    if (raw_out != nullptr) {
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        ptx::tmem_ld_32x32b_x32(trow + 32 * c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) raw_out[row * 128 + c * 32 + i] = __float_as_uint(v[i]);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      float v[32];
+      ptx::tmem_ld_32x32b_x32(trow + 32 * c, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) D[row * 128 + c * 32 + i] = v[i];
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -119,10 +162,23 @@ using namespace pcb;
 extern "C" int pcb_mma_probe(const void* A, const void* B, const int* kinds, int nsteps, const float* init,
                              float* D, void* stream) {
   if (!A || !B || !kinds || !D || nsteps < 1 || nsteps > 4096) return PCB_EINVAL;
-  cudaError_t e = cudaFuncSetAttribute(mma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MP_SMEM);
+  cudaError_t e = cudaFuncSetAttribute(mma_probe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)MP_SMEM);
   if (e != cudaSuccess) return (int)e;
-  mma_probe_kernel<<<1, 128, MP_SMEM, (cudaStream_t)stream>>>((const uint8_t*)A, (const uint8_t*)B, kinds, nsteps,
-                                                              init, D);
+  mma_probe_kernel<false><<<1, 128, MP_SMEM, (cudaStream_t)stream>>>((const uint8_t*)A, (const uint8_t*)B, kinds,
+                                                                     nsteps, init, D, nullptr);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int pcb_mma_probe_f16acc(const void* A, const void* B, const int* kinds, int nsteps, const float* init,
+                                    float* D, uint32_t* raw, void* stream) {
+  if (!A || !B || !kinds || !D || nsteps < 1 || nsteps > 4096) return PCB_EINVAL;
+  cudaError_t e = cudaFuncSetAttribute(mma_probe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)MP_SMEM);
+  if (e != cudaSuccess) return (int)e;
+  mma_probe_kernel<true><<<1, 128, MP_SMEM, (cudaStream_t)stream>>>((const uint8_t*)A, (const uint8_t*)B, kinds,
+                                                                    nsteps, init, D, raw);
   PCB_CHECK_LAUNCH();
   return 0;
 }

@@ -305,3 +305,72 @@ _all_cases_base = all_cases
 
 def all_cases():  # noqa: F811
     return _all_cases_base() + half_ulp_cases()
+
+
+# ---- F16 accumulator (E4M3 into kind::f8f6f4 with D = F16) ------------------------
+
+def run_device_f16acc(steps, init=None):
+    """(D as f64, raw 32-bit TMEM cells) of an E4M3 chain into an F16 accumulator."""
+    import torch
+
+    from paper_2501_05587_b200 import _lib as L
+
+    n = len(steps)
+    A = np.concatenate([s.a for s in steps], axis=1)
+    B = np.concatenate([s.b for s in steps], axis=1)
+    dev = torch.device("cuda", 0)
+    tA = torch.from_numpy(np.ascontiguousarray(A)).to(dev)
+    tB = torch.from_numpy(np.ascontiguousarray(B)).to(dev)
+    tk = torch.zeros(n, dtype=torch.int32, device=dev)
+    ti = None if init is None else torch.from_numpy(np.ascontiguousarray(init, np.float32)).to(dev)
+    tD = torch.empty((128, 128), dtype=torch.float32, device=dev)
+    tR = torch.empty((128, 128), dtype=torch.int32, device=dev)
+    p = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())
+    L.call("pcb_mma_probe_f16acc", p(tA), p(tB), p(tk), n, p(ti), p(tD), p(tR),
+           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    return tD.cpu().numpy().astype(np.float64), tR.cpu().numpy().view(np.uint32)
+
+
+def measure_f16acc(name, steps, init=None):
+    """Worst |D - exact| in units of 2^-11 of (sum |terms| + |exact|) per MMA."""
+    D, _ = run_device_f16acc(steps, init)
+    init16 = None if init is None else np.asarray(init, np.float32).astype(np.float16).astype(np.float64)
+    ex, mag = exact(steps, init16)
+    err = np.abs(D - ex)
+    finite = np.isfinite(D)
+    scale = np.maximum(mag + np.abs(ex), 1e-300)
+    units = np.where(finite, err / scale / 2.0 ** -11, np.inf)
+    m = len(steps)
+    return {"case": name, "kind": "e4m3->f16", "n_mma": m, "worst_units": float(units.max()),
+            "per_mma_worst_units": float(units.max() / m), "frac_exact": float((err == 0).mean()),
+            "nonfinite": int((~finite).sum())}
+
+
+def f16acc_cases(seed=11):
+    """E4M3 chains into an F16 accumulator, sized so no partial sum overflows f16."""
+    rng = _rng(seed)
+    small = np.array([c for c in E4M3_FINITE if abs(E4M3_VAL[c]) <= 4], np.uint8)
+    mid = np.array([c for c in E4M3_FINITE if abs(E4M3_VAL[c]) <= 16], np.uint8)
+    out = []
+    out.append(("f16acc random |x| <= 4", [e4m3_step(rng.choice(small, 4096), rng.choice(small, 4096))], None))
+    out.append(("f16acc random |x| <= 16", [e4m3_step(rng.choice(mid, 4096), rng.choice(mid, 4096))], None))
+    out.append(("f16acc chain of 4 |x| <= 4", [e4m3_step(rng.choice(small, 4096), rng.choice(small, 4096))
+                                               for _ in range(4)], None))
+    # dominant product + tiny ones
+    a = rng.choice(small, (128, 32)).astype(np.uint8)
+    b = rng.choice(small, (128, 32)).astype(np.uint8)
+    a[:, 0] = e4m3_code(16.0)
+    b[:, 0] = e4m3_code(16.0)
+    tiny = np.array([c for c in E4M3_FINITE if 0 < abs(E4M3_VAL[c]) <= 2.0 ** -4], np.uint8)
+    a[:, 1:] = rng.choice(tiny, (128, 31))
+    out.append(("f16acc dominant + 31 tiny", [e4m3_step(a, b)], None))
+    # large accumulator (init) + small products
+    init = (rng.choice([-1.0, 1.0], (128, 128)) * rng.uniform(1000, 30000, (128, 128))).astype(np.float32)
+    out.append(("f16acc large accumulator + small products", [e4m3_step(rng.choice(small, 4096),
+                                                                         rng.choice(small, 4096))], init))
+    # the screen pattern: 4 E4M3 K steps of -2 p.c then the augmented step adding |c|^2 + OFF pieces
+    out.append(("f16acc chain of 4 + init 2^14", [e4m3_step(rng.choice(small, 4096), rng.choice(small, 4096))
+                                                  for _ in range(4)],
+                np.full((128, 128), 16384.0, np.float32)))
+    return out

@@ -43,3 +43,28 @@ def test_probe_bf16_and_tf32_exact_on_integers():
     D = M.run_device(steps)
     ex, _ = M.exact(steps)
     assert np.array_equal(D, ex)
+
+
+def test_f16acc_layout_and_exact_integers():
+    """E4M3 into an F16 accumulator: small integer sums are exact; the packed
+    readout puts column 2i in the low half of register i; the unpacked cell of
+    column j holds D[:, j] as an f16 in its low 16 bits (recorded, not assumed)."""
+    rng = np.random.Generator(np.random.PCG64(7))
+    ints = np.array([M.e4m3_code(float(v)) for v in range(-4, 5)], np.uint8)
+    steps = [M.e4m3_step(rng.choice(ints, 4096), rng.choice(ints, 4096)) for _ in range(2)]
+    D, raw = M.run_device_f16acc(steps)
+    ex, _ = M.exact(steps)
+    assert np.array_equal(D, ex)
+    lo = (raw & 0xFFFF).astype(np.uint16).view(np.float16).astype(np.float64)
+    print("raw low-half == D:", bool(np.array_equal(lo, ex)), "high halves zero:", bool(((raw >> 16) == 0).all()))
+
+
+@pytest.mark.parametrize("case", M.f16acc_cases(), ids=lambda c: c[0])
+def test_f16acc_error_model(case):
+    name, steps, init = case
+    r = M.measure_f16acc(name, steps, init)
+    print(r)
+    assert r["nonfinite"] == 0, r
+    # budget of the F16-key screen: 2 units of 2^-11 (one RN rounding of the
+    # result plus alignment) per MMA of (sum |terms| + |result|)
+    assert r["worst_units"] <= 2.0 * r["n_mma"], r
