@@ -413,7 +413,7 @@ def main():
             roof["mma_tflops"] = mma_flops / (kern_ms * 1e-3) / 1e12
             roof["mma_frac_of_tf32"] = roof["mma_tflops"] / tf32
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["kernel"] = {"tc1xtf32s": "assign_screen_res_kernel", "tc3xtf32": "assign_tc3xtf32_kernel",
+    roof["kernel"] = {"tc1xtf32s": "assign_screen_kernel", "tc3xtf32": "assign_tc3xtf32_kernel",
                       "bf16s": "assign_screen_bf16_kernel", "fp8s": "assign_screen_bf16_kernel<F8>",
                       "deltatc": "assign_delta_tc_kernel", "delta": "assign_delta_kernel"}.get(
         eng.variant, f"assign[{eng.variant}]")

@@ -28,8 +28,6 @@
 // pipe), which is equivalent to the top-2 test (see the update rule in the
 // chunk loop) at less than half the ALU work.
 #include <cudaTypedefs.h>
-#include <cstdlib>
-#include <cstring>
 
 #include "pcb_common.cuh"
 #include "pcb_launch.cuh"
@@ -470,19 +468,6 @@ extern "C" int pcb_assign_screen_f32(const float* P_r, int64_t n, int ld, const 
   if (n > INT32_MAX) return PCB_EUNSUP;
   if (k > SC_KMAX) return PCB_EUNSUP;
   cudaStream_t st = (cudaStream_t)stream;
-  // d <= 128: A-resident kernels; PCB_SCREEN_IMPL = res (default: one SM,
-  // assign_screen_res.cu; measured fastest at c3, profiles/r01_screen_ab.md) |
-  // pair (CTA pairs, cta_group::2, assign_screen_2sm.cu) | stream (this file)
-  const char* impl = getenv("PCB_SCREEN_IMPL");
-  const bool want_stream = impl != nullptr && strcmp(impl, "stream") == 0;
-  const bool want_pair = impl != nullptr && strcmp(impl, "pair") == 0;
-  if (ld <= 4 * SC_BK && !want_stream) {
-    if (want_pair)
-      return assign_screen_pair(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count, state,
-                                st);
-    return assign_screen_resident(P_r, n, ld, C_r, k, cnorm, anorm, danorm, bstat, labels, amb_list, amb_count,
-                                  state, st);
-  }
   if (k > 128)
     return launch_screen<256>(P_r, n, ld, C_r, k, anorm, danorm, cnorm, bstat, labels, amb_list, amb_count, state,
                               st);

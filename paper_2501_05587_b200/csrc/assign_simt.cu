@@ -19,6 +19,8 @@
 //  * assign_tiled<T>: register-tiled SIMT GEMM (64x64x16 tiles, 4x4 per thread)
 //    with the argmin fused in the epilogue; any d.  Used for f64 and as the
 //    non-tensor-core fallback for large d.
+#include <cstdlib>
+
 #include "pcb_common.cuh"
 #include "pcb_launch.cuh"
 
@@ -247,6 +249,166 @@ assign_tiled(const T* __restrict__ P, const T* __restrict__ pnorm, int64_t n, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small-d f32, packed: the same per-pair arithmetic as assign_rowreg (dot =
+// fma over t in order, s = fma(-2, dot, cnorm), strict '<' in ascending j), two
+// points per f32x2 register pair so that every FFMA2 advances two dot
+// products.  Each thread holds NPAIR point pairs (2 NPAIR points) and walks the
+// centroids two at a time (4 NPAIR independent FMA chains); centroid values
+// come from shared memory duplicated as (c, c) pairs, so one LDS.128 feeds
+// two k-steps of every pair.  Results are bit-identical to assign_rowreg.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long rp_pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void rp_unpack(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long rp_ffma2(unsigned long long a, unsigned long long b,
+                                                       unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+template <int DP, int NPAIR>
+__global__ void __launch_bounds__(256)
+assign_rowpair(const float* __restrict__ P, const float* __restrict__ pnorm, int64_t n, int d,
+               const float* __restrict__ C, const float* __restrict__ cnorm, int k, int kc,
+               const int32_t* __restrict__ labels_prev, int32_t* __restrict__ labels,
+               float* __restrict__ mind, double* __restrict__ acc, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  constexpr int PPT = 2 * NPAIR;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* sC = reinterpret_cast<float2*>(smem_raw);          // [kc2][DP] (c, c) pairs
+  const int kc2 = (kc + 1) & ~1;                             // even: centroids in steps of two
+  float* sN = reinterpret_cast<float*>(sC + (size_t)kc2 * DP);  // [kc2]
+  int* hist = reinterpret_cast<int*>(sN + kc2);
+  const AccLayout L{k, d};
+  BlockBook book{(acc != nullptr && k <= kHistMax) ? hist : nullptr, 0};
+  if (book.hist) for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
+
+  auto load_chunk = [&](int c0) {
+    const int cnt = min(kc, k - c0);
+    for (int e = threadIdx.x; e < kc2 * DP; e += blockDim.x) {
+      const int jj = e / DP, t = e - jj * DP;
+      const float v = (jj < cnt && t < d) ? C[(int64_t)(c0 + jj) * d + t] : 0.0f;
+      sC[e] = make_float2(v, v);
+    }
+    // padding centroid of an odd chunk: s = +inf never beats a real key
+    for (int jj = threadIdx.x; jj < kc2; jj += blockDim.x) sN[jj] = jj < cnt ? cnorm[c0 + jj] : INFINITY;
+  };
+  const bool single_chunk = (k <= kc);
+  if (single_chunk) load_chunk(0);
+  __syncthreads();
+
+  const unsigned long long m2 = rp_pack(-2.0f, -2.0f);
+  const int64_t group = (int64_t)blockDim.x * PPT;
+  for (int64_t base = (int64_t)blockIdx.x * group; base < n; base += (int64_t)gridDim.x * group) {
+    unsigned long long pp[NPAIR][DP];
+    int64_t idx[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) idx[r] = base + threadIdx.x + (int64_t)r * blockDim.x;
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q) {
+      const int64_t ia = idx[2 * q] < n ? idx[2 * q] : n - 1, ib = idx[2 * q + 1] < n ? idx[2 * q + 1] : n - 1;
+#pragma unroll
+      for (int t = 0; t < DP; ++t)
+        pp[q][t] = rp_pack(t < d ? P[ia * d + t] : 0.0f, t < d ? P[ib * d + t] : 0.0f);
+    }
+    float bv[PPT];
+    int bj[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) { bv[r] = INFINITY; bj[r] = 0; }
+
+    for (int c0 = 0; c0 < k; c0 += kc) {
+      if (!single_chunk) { __syncthreads(); load_chunk(c0); __syncthreads(); }
+      const int cnt2 = (min(kc, k - c0) + 1) & ~1;
+      for (int jj = 0; jj < cnt2; jj += 2) {
+        unsigned long long dot[NPAIR][2];
+#pragma unroll
+        for (int q = 0; q < NPAIR; ++q) dot[q][0] = dot[q][1] = 0ull;
+        const float4* ca = reinterpret_cast<const float4*>(sC + (size_t)jj * DP);
+        const float4* cb = reinterpret_cast<const float4*>(sC + (size_t)(jj + 1) * DP);
+#pragma unroll
+        for (int t2 = 0; t2 < (DP + 1) / 2; ++t2) {
+          float4 va, vb;
+          if (DP == 1) {
+            const float2 a1 = sC[(size_t)jj * DP], b1 = sC[(size_t)(jj + 1) * DP];
+            va = make_float4(a1.x, a1.y, 0.0f, 0.0f);
+            vb = make_float4(b1.x, b1.y, 0.0f, 0.0f);
+          } else {
+            va = ca[t2];
+            vb = cb[t2];
+          }
+          const unsigned long long a0 = rp_pack(va.x, va.y), b0 = rp_pack(vb.x, vb.y);
+#pragma unroll
+          for (int q = 0; q < NPAIR; ++q) {
+            dot[q][0] = rp_ffma2(pp[q][2 * t2], a0, dot[q][0]);
+            dot[q][1] = rp_ffma2(pp[q][2 * t2], b0, dot[q][1]);
+          }
+          if (2 * t2 + 1 < DP) {
+            const unsigned long long a1 = rp_pack(va.z, va.w), b1 = rp_pack(vb.z, vb.w);
+#pragma unroll
+            for (int q = 0; q < NPAIR; ++q) {
+              dot[q][0] = rp_ffma2(pp[q][2 * t2 + 1], a1, dot[q][0]);
+              dot[q][1] = rp_ffma2(pp[q][2 * t2 + 1], b1, dot[q][1]);
+            }
+          }
+        }
+        const unsigned long long na = rp_pack(sN[jj], sN[jj]), nb = rp_pack(sN[jj + 1], sN[jj + 1]);
+#pragma unroll
+        for (int q = 0; q < NPAIR; ++q) {
+          float s0, s1, s2, s3;
+          rp_unpack(rp_ffma2(dot[q][0], m2, na), s0, s1);  // centroid jj, points 2q, 2q+1
+          rp_unpack(rp_ffma2(dot[q][1], m2, nb), s2, s3);  // centroid jj+1
+          if (s0 < bv[2 * q]) { bv[2 * q] = s0; bj[2 * q] = c0 + jj; }
+          if (s1 < bv[2 * q + 1]) { bv[2 * q + 1] = s1; bj[2 * q + 1] = c0 + jj; }
+          if (s2 < bv[2 * q]) { bv[2 * q] = s2; bj[2 * q] = c0 + jj + 1; }
+          if (s3 < bv[2 * q + 1]) { bv[2 * q + 1] = s3; bj[2 * q + 1] = c0 + jj + 1; }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+      if (idx[r] < n) {
+        const float own = pnorm[idx[r]] + bv[r];
+        labels[idx[r]] = bj[r];
+        if (mind) mind[idx[r]] = own;
+        if (acc) book_point(book, acc, L, bj[r], labels_prev, idx[r]);
+        flag_nonfinite(state, (double)own);
+      }
+    }
+  }
+  if (acc) {
+    __syncthreads();
+    book_flush(book, acc, L, k);
+  }
+}
+
+template <int DP, int NPAIR>
+static int launch_rowpair(const float* P, const float* pnorm, int64_t n, int d, const float* C, const float* cnorm,
+                          int k, const int32_t* lp, int32_t* lab, float* mind, double* acc, const long long* state,
+                          cudaStream_t st) {
+  const int per = (2 * DP + 1) * (int)sizeof(float);
+  int kc = (32768 / per) & ~1;
+  if (kc > k) kc = k;
+  const int kc2 = (kc + 1) & ~1;
+  size_t smem = (size_t)kc2 * per + ((acc != nullptr && k <= kHistMax) ? (size_t)k * sizeof(int) : 0);
+  auto kern = assign_rowpair<DP, NPAIR>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  const int64_t groups = (n + 256 * 2 * NPAIR - 1) / (256 * 2 * NPAIR);
+  const int grid = (int)std::min<int64_t>(groups, (int64_t)persistent_grid(kern, 256, smem));
+  kern<<<grid, 256, smem, st>>>(P, pnorm, n, d, C, cnorm, k, kc, lp, lab, mind, acc, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
 template <typename T, int DP, int PPT>
 static int launch_rowreg(const T* P, const T* pnorm, int64_t n, int d, const T* C, const T* cnorm,
                          int k, const int32_t* lp, int32_t* lab, T* mind, double* acc,
@@ -273,6 +435,21 @@ static int assign_dispatch(const T* P, const T* pnorm, int64_t n, int d, const T
                            const long long* state, int variant, cudaStream_t st) {
   if (n < 1 || d < 1 || k < 1 || !P || !pnorm || !C || !cnorm || !lab) return PCB_EINVAL;
   if (variant == PCB_ASSIGN_AUTO) variant = (d <= 32) ? PCB_ASSIGN_ROWREG : PCB_ASSIGN_TILED;
+  if (variant == PCB_ASSIGN_ROWREG && sizeof(T) == 4 && getenv("PCB_ROWREG_SCALAR") == nullptr) {
+    // f32: packed two-points-per-FFMA2 kernel (bit-identical to assign_rowreg)
+    const float* Pf = reinterpret_cast<const float*>(P);
+    const float* pn = reinterpret_cast<const float*>(pnorm);
+    const float* Cf = reinterpret_cast<const float*>(C);
+    const float* cn = reinterpret_cast<const float*>(cnorm);
+    float* md = reinterpret_cast<float*>(mind);
+    if (d <= 1) return launch_rowpair<1, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
+    if (d <= 2) return launch_rowpair<2, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
+    if (d <= 4) return launch_rowpair<4, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
+    if (d <= 8) return launch_rowpair<8, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
+    if (d <= 16) return launch_rowpair<16, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
+    if (d <= 32) return launch_rowpair<32, 1>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
+    return PCB_EUNSUP;
+  }
   if (variant == PCB_ASSIGN_ROWREG) {
     if (d <= 1) return launch_rowreg<T, 1, 4>(P, pnorm, n, d, C, cnorm, k, lp, lab, mind, acc, state, st);
     if (d <= 2) return launch_rowreg<T, 2, 4>(P, pnorm, n, d, C, cnorm, k, lp, lab, mind, acc, state, st);

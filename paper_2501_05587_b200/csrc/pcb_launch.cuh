@@ -35,12 +35,4 @@ int exact_rows(const float* P, int d, const float* C, int k, const int* flag_lis
                const int* row_ids, int32_t* out, void* scratch, const long long* state, cudaStream_t st);
 int64_t exact_scratch_bytes();
 
-int assign_screen_resident(const float* P_r, int64_t n, int ld, const float* C_r, int k, const float* cnorm,
-                           const float* anorm, const float* danorm, const float* bstat, int32_t* labels,
-                           int* amb_list, int* amb_count, const long long* state, cudaStream_t st);
-
-int assign_screen_pair(const float* P_r, int64_t n, int ld, const float* C_r, int k, const float* cnorm,
-                       const float* anorm, const float* danorm, const float* bstat, int32_t* labels, int* amb_list,
-                       int* amb_count, const long long* state, cudaStream_t st);
-
 }  // namespace pcb
