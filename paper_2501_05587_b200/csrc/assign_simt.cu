@@ -273,7 +273,7 @@ __device__ __forceinline__ unsigned long long rp_ffma2(unsigned long long a, uns
   return r;
 }
 
-template <int DP, int NPAIR>
+template <int DP, int NPAIR, int CJ>
 __global__ void __launch_bounds__(256)
 assign_rowpair(const float* __restrict__ P, const float* __restrict__ pnorm, int64_t n, int d,
                const float* __restrict__ C, const float* __restrict__ cnorm, int k, int kc,
@@ -281,11 +281,13 @@ assign_rowpair(const float* __restrict__ P, const float* __restrict__ pnorm, int
                float* __restrict__ mind, double* __restrict__ acc, const long long* __restrict__ state) {
   if (stopped(state)) return;
   constexpr int PPT = 2 * NPAIR;
+  constexpr int SPR = DP + 1;                                // padded row stride of the point stage
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* sC = reinterpret_cast<float2*>(smem_raw);          // [kc2][DP] (c, c) pairs
-  const int kc2 = (kc + 1) & ~1;                             // even: centroids in steps of two
+  const int kc2 = (kc + CJ - 1) / CJ * CJ;                   // centroids in steps of CJ
   float* sN = reinterpret_cast<float*>(sC + (size_t)kc2 * DP);  // [kc2]
-  int* hist = reinterpret_cast<int*>(sN + kc2);
+  float* sP = sN + kc2;                                      // [warps][32][SPR] point stage
+  int* hist = reinterpret_cast<int*>(sP + (blockDim.x >> 5) * 32 * SPR);
   const AccLayout L{k, d};
   BlockBook book{(acc != nullptr && k <= kHistMax) ? hist : nullptr, 0};
   if (book.hist) for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
@@ -297,7 +299,7 @@ assign_rowpair(const float* __restrict__ P, const float* __restrict__ pnorm, int
       const float v = (jj < cnt && t < d) ? C[(int64_t)(c0 + jj) * d + t] : 0.0f;
       sC[e] = make_float2(v, v);
     }
-    // padding centroid of an odd chunk: s = +inf never beats a real key
+    // padding centroids of a ragged chunk: s = +inf never beats a real key
     for (int jj = threadIdx.x; jj < kc2; jj += blockDim.x) sN[jj] = jj < cnt ? cnorm[c0 + jj] : INFINITY;
   };
   const bool single_chunk = (k <= kc);
@@ -306,18 +308,61 @@ assign_rowpair(const float* __restrict__ P, const float* __restrict__ pnorm, int
 
   const unsigned long long m2 = rp_pack(-2.0f, -2.0f);
   const int64_t group = (int64_t)blockDim.x * PPT;
+  const int lane = threadIdx.x & 31;
+  float* wP = sP + (threadIdx.x >> 5) * 32 * SPR;
   for (int64_t base = (int64_t)blockIdx.x * group; base < n; base += (int64_t)gridDim.x * group) {
     unsigned long long pp[NPAIR][DP];
     int64_t idx[PPT];
 #pragma unroll
     for (int r = 0; r < PPT; ++r) idx[r] = base + threadIdx.x + (int64_t)r * blockDim.x;
+    // per-row inputs of the epilogue, fetched now so their latency overlaps the distances
+    float pn_r[PPT];
+    int lp_r[PPT];
 #pragma unroll
-    for (int q = 0; q < NPAIR; ++q) {
-      const int64_t ia = idx[2 * q] < n ? idx[2 * q] : n - 1, ib = idx[2 * q + 1] < n ? idx[2 * q + 1] : n - 1;
-#pragma unroll
-      for (int t = 0; t < DP; ++t)
-        pp[q][t] = rp_pack(t < d ? P[ia * d + t] : 0.0f, t < d ? P[ib * d + t] : 0.0f);
+    for (int r = 0; r < PPT; ++r) {
+      const int64_t ii = idx[r] < n ? idx[r] : n - 1;
+      pn_r[r] = pnorm[ii];
+      lp_r[r] = labels_prev != nullptr ? labels_prev[ii] : 0;
     }
+    // The 32 rows of a warp for point slot r are contiguous in P: read them
+    // coalesced (lane-strided over 32 d floats, every load of the round in
+    // flight at once) into the warp's padded stage, then every lane takes its
+    // own row (row-per-lane reads of P would cost one L1 wavefront per lane per
+    // column).  (A register prefetch of the next round was tried: the extra
+    // registers cost more occupancy than the hidden latency gained.)
+    float tmp[PPT][DP];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+      const int64_t row0 = idx[r] - lane;
+      const int64_t avail = n - row0 < 32 ? n - row0 : 32;  // rows of this warp slot inside P
+      const float* src = P + row0 * d;
+      const int lim = (int)avail * d;
+#pragma unroll
+      for (int i = 0; i < DP; ++i) {
+        const int e = lane + 32 * i;
+        tmp[r][i] = (i < d && e < lim) ? __ldg(src + e) : 0.0f;
+      }
+    }
+    float pv[PPT][DP];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < DP; ++i) {
+        const int e = lane + 32 * i;
+        if (i < d) {
+          const int rr = e / d, t = e - rr * d;
+          wP[rr * SPR + t] = tmp[r][i];
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < DP; ++t) pv[r][t] = t < d ? wP[lane * SPR + t] : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q)
+#pragma unroll
+      for (int t = 0; t < DP; ++t) pp[q][t] = rp_pack(pv[2 * q][t], pv[2 * q + 1][t]);
     float bv[PPT];
     int bj[PPT];
 #pragma unroll
@@ -325,59 +370,65 @@ assign_rowpair(const float* __restrict__ P, const float* __restrict__ pnorm, int
 
     for (int c0 = 0; c0 < k; c0 += kc) {
       if (!single_chunk) { __syncthreads(); load_chunk(c0); __syncthreads(); }
-      const int cnt2 = (min(kc, k - c0) + 1) & ~1;
-      for (int jj = 0; jj < cnt2; jj += 2) {
-        unsigned long long dot[NPAIR][2];
+      const int cnt2 = (min(kc, k - c0) + CJ - 1) / CJ * CJ;
+      for (int jj = 0; jj < cnt2; jj += CJ) {
+        unsigned long long dot[NPAIR][CJ];
 #pragma unroll
-        for (int q = 0; q < NPAIR; ++q) dot[q][0] = dot[q][1] = 0ull;
-        const float4* ca = reinterpret_cast<const float4*>(sC + (size_t)jj * DP);
-        const float4* cb = reinterpret_cast<const float4*>(sC + (size_t)(jj + 1) * DP);
+        for (int q = 0; q < NPAIR; ++q)
+#pragma unroll
+          for (int u = 0; u < CJ; ++u) dot[q][u] = 0ull;
 #pragma unroll
         for (int t2 = 0; t2 < (DP + 1) / 2; ++t2) {
-          float4 va, vb;
-          if (DP == 1) {
-            const float2 a1 = sC[(size_t)jj * DP], b1 = sC[(size_t)(jj + 1) * DP];
-            va = make_float4(a1.x, a1.y, 0.0f, 0.0f);
-            vb = make_float4(b1.x, b1.y, 0.0f, 0.0f);
-          } else {
-            va = ca[t2];
-            vb = cb[t2];
-          }
-          const unsigned long long a0 = rp_pack(va.x, va.y), b0 = rp_pack(vb.x, vb.y);
+          float4 v[CJ];
 #pragma unroll
-          for (int q = 0; q < NPAIR; ++q) {
-            dot[q][0] = rp_ffma2(pp[q][2 * t2], a0, dot[q][0]);
-            dot[q][1] = rp_ffma2(pp[q][2 * t2], b0, dot[q][1]);
+          for (int u = 0; u < CJ; ++u) {
+            if (DP == 1) {
+              const float2 a1 = sC[(size_t)(jj + u) * DP];
+              v[u] = make_float4(a1.x, a1.y, 0.0f, 0.0f);
+            } else {
+              v[u] = reinterpret_cast<const float4*>(sC + (size_t)(jj + u) * DP)[t2];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < CJ; ++u) {
+            const unsigned long long c0v = rp_pack(v[u].x, v[u].y);
+#pragma unroll
+            for (int q = 0; q < NPAIR; ++q) dot[q][u] = rp_ffma2(pp[q][2 * t2], c0v, dot[q][u]);
           }
           if (2 * t2 + 1 < DP) {
-            const unsigned long long a1 = rp_pack(va.z, va.w), b1 = rp_pack(vb.z, vb.w);
 #pragma unroll
-            for (int q = 0; q < NPAIR; ++q) {
-              dot[q][0] = rp_ffma2(pp[q][2 * t2 + 1], a1, dot[q][0]);
-              dot[q][1] = rp_ffma2(pp[q][2 * t2 + 1], b1, dot[q][1]);
+            for (int u = 0; u < CJ; ++u) {
+              const unsigned long long c1v = rp_pack(v[u].z, v[u].w);
+#pragma unroll
+              for (int q = 0; q < NPAIR; ++q) dot[q][u] = rp_ffma2(pp[q][2 * t2 + 1], c1v, dot[q][u]);
             }
           }
         }
-        const unsigned long long na = rp_pack(sN[jj], sN[jj]), nb = rp_pack(sN[jj + 1], sN[jj + 1]);
+        // keys and the running argmin in ascending centroid order (strict '<')
 #pragma unroll
-        for (int q = 0; q < NPAIR; ++q) {
-          float s0, s1, s2, s3;
-          rp_unpack(rp_ffma2(dot[q][0], m2, na), s0, s1);  // centroid jj, points 2q, 2q+1
-          rp_unpack(rp_ffma2(dot[q][1], m2, nb), s2, s3);  // centroid jj+1
-          if (s0 < bv[2 * q]) { bv[2 * q] = s0; bj[2 * q] = c0 + jj; }
-          if (s1 < bv[2 * q + 1]) { bv[2 * q + 1] = s1; bj[2 * q + 1] = c0 + jj; }
-          if (s2 < bv[2 * q]) { bv[2 * q] = s2; bj[2 * q] = c0 + jj + 1; }
-          if (s3 < bv[2 * q + 1]) { bv[2 * q + 1] = s3; bj[2 * q + 1] = c0 + jj + 1; }
+        for (int u = 0; u < CJ; ++u) {
+          const unsigned long long nu = rp_pack(sN[jj + u], sN[jj + u]);
+#pragma unroll
+          for (int q = 0; q < NPAIR; ++q) {
+            float s0, s1;
+            rp_unpack(rp_ffma2(dot[q][u], m2, nu), s0, s1);  // centroid jj + u, points 2q, 2q + 1
+            if (s0 < bv[2 * q]) { bv[2 * q] = s0; bj[2 * q] = c0 + jj + u; }
+            if (s1 < bv[2 * q + 1]) { bv[2 * q + 1] = s1; bj[2 * q + 1] = c0 + jj + u; }
+          }
         }
       }
     }
 #pragma unroll
     for (int r = 0; r < PPT; ++r) {
       if (idx[r] < n) {
-        const float own = pnorm[idx[r]] + bv[r];
+        const float own = pn_r[r] + bv[r];
         labels[idx[r]] = bj[r];
         if (mind) mind[idx[r]] = own;
-        if (acc) book_point(book, acc, L, bj[r], labels_prev, idx[r]);
+        if (acc) {
+          if (labels_prev != nullptr) book.changed += (lp_r[r] != bj[r]);
+          if (book.hist != nullptr) atomicAdd(&book.hist[bj[r]], 1);
+          else atomicAdd(&acc[L.counts() + bj[r]], 1.0);
+        }
         flag_nonfinite(state, (double)own);
       }
     }
@@ -388,16 +439,17 @@ assign_rowpair(const float* __restrict__ P, const float* __restrict__ pnorm, int
   }
 }
 
-template <int DP, int NPAIR>
+template <int DP, int NPAIR, int CJ = 2>
 static int launch_rowpair(const float* P, const float* pnorm, int64_t n, int d, const float* C, const float* cnorm,
                           int k, const int32_t* lp, int32_t* lab, float* mind, double* acc, const long long* state,
                           cudaStream_t st) {
   const int per = (2 * DP + 1) * (int)sizeof(float);
-  int kc = (32768 / per) & ~1;
+  int kc = (32768 / per) & ~(CJ - 1);
   if (kc > k) kc = k;
-  const int kc2 = (kc + 1) & ~1;
-  size_t smem = (size_t)kc2 * per + ((acc != nullptr && k <= kHistMax) ? (size_t)k * sizeof(int) : 0);
-  auto kern = assign_rowpair<DP, NPAIR>;
+  const int kc2 = (kc + CJ - 1) / CJ * CJ;
+  size_t smem = (size_t)kc2 * per + (size_t)8 * 32 * (DP + 1) * sizeof(float) +
+                ((acc != nullptr && k <= kHistMax) ? (size_t)k * sizeof(int) : 0);
+  auto kern = assign_rowpair<DP, NPAIR, CJ>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
@@ -446,7 +498,7 @@ static int assign_dispatch(const T* P, const T* pnorm, int64_t n, int d, const T
     if (d <= 2) return launch_rowpair<2, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
     if (d <= 4) return launch_rowpair<4, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
     if (d <= 8) return launch_rowpair<8, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
-    if (d <= 16) return launch_rowpair<16, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
+    if (d <= 16) return launch_rowpair<16, 2, 4>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
     if (d <= 32) return launch_rowpair<32, 1>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
     return PCB_EUNSUP;
   }
