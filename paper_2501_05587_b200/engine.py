@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -472,6 +473,9 @@ class LloydEngine(ShardSequence):
         if self.variant in ("bf16s", "fp8s") and t in self.RELAYOUT_AT:
             self.relayout()
 
+    # the screen's row layout state (relayout swaps these)
+    _LAYOUT_ATTRS = ("orig", "P_b", "anorm", "danorm", "P_b0", "an0", "dan0")
+
     def relayout(self) -> None:
         """Rebuild P_b / anorm / danorm in the label order of the last update's
         counting sort (self.perm); see pcb_screen_relayout_bf16."""
@@ -764,6 +768,9 @@ class LloydEngine(ShardSequence):
             return evs
         if graph:
             saved, cold = self.sums_valid, self._cold
+            # relayout() (captured at t in RELAYOUT_AT) swaps in new operand buffers whose
+            # fill kernels only run on replay: keep the current ones to restore on failure
+            layout = {a: getattr(self, a, None) for a in self._LAYOUT_ATTRS}
             try:
                 g = torch.cuda.CUDAGraph()
                 cs = torch.cuda.Stream(self.dev)
@@ -774,8 +781,12 @@ class LloydEngine(ShardSequence):
                 g.replay()
                 self._graph = g  # kept alive until the next run (its nodes reference our buffers)
                 return evs
-            except Exception:  # capture unsupported here: run the same kernels eagerly
+            except RuntimeError as e:  # capture unsupported here: run the same kernels eagerly
+                warnings.warn(f"CUDA graph capture failed ({e}); running the iterations eagerly")
                 self.sums_valid, self._cold = saved, cold
+                for a, v in layout.items():
+                    setattr(self, a, v)
+                self._graph = None
                 torch.cuda.synchronize()
         return body(False)
 

@@ -92,3 +92,25 @@ def test_steady_state_lockstep_fp8s(shape):
     assert min(r["certified_frac"] for r in steady) >= min_cert, rows
     # a reference f32 mis-rank is rare at these gaps; more would mean a bug
     assert sum(r["ref_f32_flips"] for r in rows) <= max(2, n // 100_000), rows
+
+
+def test_graph_capture_failure_restores_relayout(monkeypatch):
+    """A capture that fails after the relayout was recorded (its fill kernels
+    never ran) falls back to eager iterations on the pre-capture row layout and
+    returns the same fit (engine.iterations)."""
+    import warnings
+
+    import paper_2501_05587_b200 as pcb
+    P = oracle.make_blobs(20000, 64, 24, seed=9)
+    cfg = pcb.KKMeansConfig(k=24, max_iters=6, variant="fp8s")
+    good = pcb.run_lloyd(P, cfg)
+
+    def boom(self):
+        raise RuntimeError("forced replay failure")
+    monkeypatch.setattr(torch.cuda.CUDAGraph, "replay", boom)
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        bad = pcb.run_lloyd(P, cfg)
+    assert any("graph capture failed" in str(x.message) for x in w)
+    np.testing.assert_array_equal(good.labels, bad.labels)
+    np.testing.assert_allclose(good.objective_history, bad.objective_history, rtol=0, atol=0)
