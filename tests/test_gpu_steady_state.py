@@ -113,4 +113,4 @@ def test_graph_capture_failure_restores_relayout(monkeypatch):
         bad = pcb.run_lloyd(P, cfg)
     assert any("graph capture failed" in str(x.message) for x in w)
     np.testing.assert_array_equal(good.labels, bad.labels)
-    np.testing.assert_allclose(good.objective_history, bad.objective_history, rtol=0, atol=0)
+    np.testing.assert_allclose(good.objective_history, bad.objective_history, rtol=1e-12)  # f64 atomics order
