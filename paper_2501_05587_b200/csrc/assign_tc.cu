@@ -394,8 +394,11 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
                    const int* __restrict__ row_ids, int32_t* __restrict__ out, ExactScratch* __restrict__ sc,
                    const long long* __restrict__ state) {
   if (stopped(state)) return;
-  __shared__ __align__(16) float sP[XR_K][XR_R];
-  __shared__ __align__(16) float sC[XR_K][XR_C];
+  // f64 tiles, converted once per element at staging (not once per use in the
+  // inner loop); rows padded by 2 doubles against bank conflicts of the
+  // transposing stores, 16-byte aligned for the double2 reads
+  __shared__ __align__(16) double sP[XR_K][XR_R + 2];
+  __shared__ __align__(16) double sC[XR_K][XR_C + 2];
   __shared__ int64_t srow[XR_R];
   __shared__ int sidx[XR_R];
   const int cnt = *flag_count;
@@ -429,18 +432,20 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
         for (int e = tid; e < XR_R * XR_K; e += 128) {  // row-contiguous reads
           const int r = e / XR_K, kk = e % XR_K;
           const int64_t pr = srow[r];
-          sP[kk][r] = (pr >= 0 && k0 + kk < d) ? __ldg(P + pr * d + k0 + kk) : 0.0f;
+          sP[kk][r] = (pr >= 0 && k0 + kk < d) ? (double)__ldg(P + pr * d + k0 + kk) : 0.0;
         }
         for (int e = tid; e < XR_C * XR_K; e += 128) {
           const int c = e / XR_K, kk = e % XR_K;
-          sC[kk][c] = (c0 + c < k && k0 + kk < d) ? __ldg(C + (int64_t)(c0 + c) * d + k0 + kk) : 0.0f;
+          sC[kk][c] = (c0 + c < k && k0 + kk < d) ? (double)__ldg(C + (int64_t)(c0 + c) * d + k0 + kk) : 0.0;
         }
         __syncthreads();
 #pragma unroll 4
         for (int kk = 0; kk < XR_K; ++kk) {
-          const float4 a = *reinterpret_cast<const float4*>(&sP[kk][ty * 4]);
-          const float4 b = *reinterpret_cast<const float4*>(&sC[kk][tx * 4]);
-          const double av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+          const double2 a0 = *reinterpret_cast<const double2*>(&sP[kk][ty * 4]);
+          const double2 a1 = *reinterpret_cast<const double2*>(&sP[kk][ty * 4 + 2]);
+          const double2 b0 = *reinterpret_cast<const double2*>(&sC[kk][tx * 4]);
+          const double2 b1 = *reinterpret_cast<const double2*>(&sC[kk][tx * 4 + 2]);
+          const double av[4] = {a0.x, a0.y, a1.x, a1.y}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll

@@ -18,6 +18,14 @@ __global__ void __launch_bounds__(1024, 1) fma_loop(int iters, float a, float b,
       if (MODE == 0) x[i] = fmaf(x[i], y[i], a);             // 3 registers (a in a register via asm below)
       if (MODE == 1) x[i] = fmaf(x[i], 0.999f, 1e-7f);        // immediate operands
     }
+    if (MODE == 3) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double xd = (double)x[i];
+        xd = fma(xd, (double)y[i], 1e-7);
+        x[i] = (float)xd;
+      }
+    }
     if (MODE == 2) {
 #pragma unroll
       for (int i = 0; i < 8; i += 2) {
@@ -39,8 +47,38 @@ __global__ void __launch_bounds__(1024, 1) fma_loop(int iters, float a, float b,
   if (threadIdx.x == 0) atomicAdd(cyc, t1 - t0);
 }
 
+__global__ void __launch_bounds__(1024, 1) dfma_loop(int iters, double a, double* out, unsigned long long* cyc) {
+  double x[8], y[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { x[i] = threadIdx.x * 1e-7 + i; y[i] = 0.999 + i * 1e-3; }
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], y[i], a);
+  }
+  unsigned long long t1 = clock64();
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.0) out[0] = s;
+  if (threadIdx.x == 0) atomicAdd(cyc, t1 - t0);
+}
+
 template <int MODE>
 static void run(int iters) {
+  if (MODE == 4) {
+    double* o;
+    unsigned long long* c;
+    cudaMalloc(&o, 8);
+    cudaMalloc(&c, 8);
+    cudaMemset(c, 0, 8);
+    dfma_loop<<<148, 1024>>>(iters, 1e-7, o, c);
+    cudaDeviceSynchronize();
+    unsigned long long h;
+    cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+    printf("{\"mode\": \"dfma\", \"dfma_per_clk_per_sm\": %.2f}\n", (double)iters * 8 * 1024 / ((double)h / 148));
+    return;
+  }
   float* o;
   unsigned long long* c;
   cudaMalloc(&o, 4);
@@ -62,5 +100,6 @@ int main() {
   run<0>(20000);
   run<1>(20000);
   run<2>(20000);
+  run<4>(2000);
   return 0;
 }

@@ -1,0 +1,21 @@
+#!/bin/bash
+# Steady-state launch list (cold, serialised) of the c3 default: 12 warm-up
+# iterations skipped, then ~3 iterations of launches.
+cfg=${1:-c3}; tag=${2:-steady_$cfg}
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 330 -c 75 --csv \
+  --log-file gpurun_out/launches_$tag.csv python bench.py --config $cfg --steps 4 --warmup 12 --no-graph \
+  --no-e2e --no-cpu-baseline > gpurun_out/launches_$tag.log 2>&1
+echo "ncu rc=$?"
+python - "$tag" <<'PY'
+import csv, sys, collections
+rows = list(csv.reader(l for l in open(f"gpurun_out/launches_{sys.argv[1]}.csv") if not l.startswith("==")))
+hdr = rows[0]; ki = hdr.index("Kernel Name"); vi = hdr.index("Metric Value")
+seq = [(r[ki][:70], float(r[vi].replace(",", ""))) for r in rows[1:] if len(r) > vi]
+t = collections.defaultdict(list)
+for k, v in seq: t[k].append(v)
+tot = sum(v for _, v in seq)
+for k, v in sorted(t.items(), key=lambda x: -sum(x[1])):
+    print(f"{sum(v)/len(v)/1e3:9.3f} us x{len(v):3d}  {100*sum(v)/tot:5.1f}%  {k}")
+print("sequence:")
+for k, v in seq[:40]: print(f"   {v/1e3:9.3f}  {k}")
+PY
