@@ -257,6 +257,13 @@ int pcb_resolve_screen_fp8(const float* P, int64_t n, int d, const void* P_q, in
                            const int* two_count, const long long* state, void* stream);
 int pcb_count_labels(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
                      double* acc, const long long* state, void* stream);
+/* The same pass fused with the delta update's changed-row sums: when the
+ * previous iteration took the delta update (state[6] odd) it also applies
+ * S[new] += p, S[prev] -= p for every changed row (f64 atomics) and sets
+ * state[8]; pcb_update_mode then records mode 3 (delta, sums applied) or a full
+ * update overwrites S.  P: n x d f32, S: k x d f64 (the S of pcb_delta_update_f32). */
+int pcb_count_labels_delta_f32(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
+                               double* acc, const long long* state, const float* P, double* S, void* stream);
 
 /* ---- centroid update (clustering.py:282-288): counting sort of point ids by
  *      label, then a segmented f64 sum of point rows per cluster into acc.  */

@@ -67,6 +67,7 @@ SIGNATURES = {
                                       P, P]),
     "pcb_screen_relayout_bf16": (I32, [P, P, P, I64, I32, P, P, P, P, P, P]),
     "pcb_count_labels": (I32, [P, P, I64, I32, I32, P, P, P]),
+    "pcb_count_labels_delta_f32": (I32, [P, P, I64, I32, I32, P, P, P, P, P]),
     "pcb_sort_by_label": (I32, [P, I64, I32, P, P, P, P, P, P]),
     "pcb_segment_sums_f32": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P]),
     "pcb_segment_sums_f64": (I32, [P, I64, I32, P, P, I32, P, P, P, P, P]),
@@ -115,7 +116,7 @@ VARIANTS = {"auto": ASSIGN_AUTO, "rowreg": ASSIGN_ROWREG, "tiled": ASSIGN_TILED,
             "tc3xtf32": ASSIGN_TC3XTF32, "delta": ASSIGN_DELTA, "tc1xtf32s": ASSIGN_SCREEN,
             "bf16s": ASSIGN_SCREEN_BF16, "fp8s": ASSIGN_SCREEN_FP8,
             "deltatc": ASSIGN_DELTA_TC}
-STATE_WORDS = 8
+STATE_WORDS = 9
 
 _lib = None
 _load_error = None

@@ -353,12 +353,38 @@ scatter_rows_labels(const int* __restrict__ list, const int* __restrict__ count,
 
 // counts and changed of the final labels (clustering.py:146-149) — used by the
 // screened variant, whose assignment kernel only produces labels.
+//
+// With P and S (the delta update's persistent per-cluster f64 sums): when the
+// previous iteration took the delta update (so this one most likely does too)
+// the pass also applies the changed rows to S (S[new] += p, S[prev] -= p), the
+// work of delta_sums_kernel, in the same stream over both label arrays;
+// state[kSpec] tells pcb_update_mode, which then marks the mode 3 (delta sums
+// done) or, if this iteration needs the full update, lets it overwrite S.
 __global__ void __launch_bounds__(256)
 count_labels_kernel(const int32_t* __restrict__ labels, const int32_t* __restrict__ prev, int64_t n, int k,
-                    int d, double* __restrict__ acc, const long long* __restrict__ state) {
+                    int d, double* __restrict__ acc, const long long* __restrict__ state,
+                    const float* __restrict__ P = nullptr, double* __restrict__ S = nullptr) {
   if (stopped(state)) return;
   extern __shared__ int hist[];
   const AccLayout L{k, d};
+  // every block reads the previous iteration's mode (nobody writes it before pcb_update_mode)
+  const bool spec = S != nullptr && prev != nullptr && delta_mode(state);
+  if (spec && blockIdx.x == 0 && threadIdx.x == 0) const_cast<long long*>(state)[kSpec] = 1;
+  const int lane = threadIdx.x & 31;
+  // changed rows of the warp's 32 x 4 labels, applied cooperatively (lanes over d)
+  auto apply = [&](unsigned m, int64_t i0, int stride, int a, int b) {
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t r = i0 + (int64_t)src * stride;
+      const int ja = __shfl_sync(0xffffffffu, a, src), jb = __shfl_sync(0xffffffffu, b, src);
+      for (int t = lane; t < d; t += 32) {
+        const double x = (double)P[r * d + t];
+        atomicAdd(&S[(int64_t)jb * d + t], x);
+        atomicAdd(&S[(int64_t)ja * d + t], -x);
+      }
+    }
+  };
   for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
   __syncthreads();
   long long chg = 0;
@@ -368,21 +394,39 @@ count_labels_kernel(const int32_t* __restrict__ labels, const int32_t* __restric
   const int64_t n4 = al ? n >> 2 : 0;
   const int4* l4 = reinterpret_cast<const int4*>(labels);
   const int4* p4 = reinterpret_cast<const int4*>(prev);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    const int4 l = l4[i];
-    atomicAdd(&hist[l.x], 1);
-    atomicAdd(&hist[l.y], 1);
-    atomicAdd(&hist[l.z], 1);
-    atomicAdd(&hist[l.w], 1);
+  // warp-uniform trip counts (the changed-row ballots need the whole warp)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n4; i0 += stride) {
+    const int64_t i = i0 + lane;
+    const bool in = i < n4;
+    const int4 l = in ? l4[i] : make_int4(0, 0, 0, 0);
+    if (in) {
+      atomicAdd(&hist[l.x], 1);
+      atomicAdd(&hist[l.y], 1);
+      atomicAdd(&hist[l.z], 1);
+      atomicAdd(&hist[l.w], 1);
+    }
     if (prev) {
-      const int4 q = p4[i];
+      const int4 q = in ? p4[i] : l;
       chg += (q.x != l.x) + (q.y != l.y) + (q.z != l.z) + (q.w != l.w);
+      if (spec) {
+        apply(__ballot_sync(0xffffffffu, q.x != l.x), 4 * i0 + 0, 4, q.x, l.x);
+        apply(__ballot_sync(0xffffffffu, q.y != l.y), 4 * i0 + 1, 4, q.y, l.y);
+        apply(__ballot_sync(0xffffffffu, q.z != l.z), 4 * i0 + 2, 4, q.z, l.z);
+        apply(__ballot_sync(0xffffffffu, q.w != l.w), 4 * i0 + 3, 4, q.w, l.w);
+      }
     }
   }
-  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int l = labels[i];
-    atomicAdd(&hist[l], 1);
-    if (prev) chg += (prev[i] != l);
+  for (int64_t i0 = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+    const int64_t i = i0 + lane;
+    const bool in = i < n;
+    const int l = in ? labels[i] : 0;
+    if (in) atomicAdd(&hist[l], 1);
+    if (prev) {
+      const int q = in ? prev[i] : l;
+      chg += (q != l);
+      if (spec) apply(__ballot_sync(0xffffffffu, q != l), i0, 1, q, l);
+    }
   }
   chg = warp_sum(chg);
   if ((threadIdx.x & 31) == 0 && chg) atomicAdd(&acc[L.changed()], (double)chg);
@@ -505,6 +549,18 @@ extern "C" int pcb_resolve_ambiguous_f32(const float* P, int64_t n, int d, const
 }
 
 extern "C" int64_t pcb_exact_scratch_bytes(void) { return exact_scratch_bytes(); }
+
+extern "C" int pcb_count_labels_delta_f32(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k,
+                                          int d, double* acc, const long long* state, const float* P, double* S,
+                                          void* stream) {
+  if (n < 1 || k < 1 || !labels || !labels_prev || !acc || !state || !P || !S) return PCB_EINVAL;
+  if (k > 12288) return pcb_count_labels(labels, labels_prev, n, k, d, acc, state, stream);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 4);
+  count_labels_kernel<<<grid, 256, k * sizeof(int), (cudaStream_t)stream>>>(labels, labels_prev, n, k, d, acc,
+                                                                          state, P, S);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
 
 extern "C" int pcb_count_labels(const int32_t* labels, const int32_t* labels_prev, int64_t n, int k, int d,
                                 double* acc, const long long* state, void* stream) {

@@ -40,10 +40,13 @@ struct AccLayout {
 //   [0] iterations recorded, [1] stop flag, [2] converged flag,
 //   [3] repairs (moved points) of the current iteration,
 //   [4] finalize block ticket, [5] non-finite distance seen,
-//   [6] centroid-update mode of the iteration (0 full, 1 delta; update.cu),
-//   [7] persistent per-cluster sums stale (a repair moved points)
+//   [6] centroid-update mode of the iteration (0 full, 1 delta, 3 delta whose
+//       changed-row sums the count pass already applied; update.cu),
+//   [7] persistent per-cluster sums stale (a repair moved points),
+//   [8] the count pass applied the changed-row sums speculatively (the
+//       previous iteration was a delta one)
 enum StateWord { kIters = 0, kStop = 1, kConverged = 2, kMoved = 3, kTicket = 4, kNanFlag = 5, kMode = 6,
-                 kSumsStale = 7, kStateWords = 8 };
+                 kSumsStale = 7, kSpec = 8, kStateWords = 9 };
 
 __device__ __forceinline__ bool stopped(const long long* state) {
   return state != nullptr && ((volatile const long long*)state)[kStop] != 0;
@@ -52,7 +55,7 @@ __device__ __forceinline__ bool stopped(const long long* state) {
 // Delta centroid update this iteration: the counting sort / segmented sums of
 // the full update are skipped (they exit at once).
 __device__ __forceinline__ bool delta_mode(const long long* state) {
-  return state != nullptr && ((volatile const long long*)state)[kMode] == 1;
+  return state != nullptr && (((volatile const long long*)state)[kMode] & 1) != 0;
 }
 
 template <typename T>

@@ -488,8 +488,11 @@ update_mode_kernel(const double* __restrict__ acc, int k, int d, int64_t n, doub
   __syncthreads();
   if (threadIdx.x == 0) {
     const bool full = force_full || any_empty || state[kSumsStale] != 0 || acc[L.changed()] > frac * (double)n;
-    state[kMode] = full ? 0 : 1;
+    // delta with the count pass's speculative changed-row sums already in S: 3
+    // (a full update overwrites S from the full sums, discarding them)
+    state[kMode] = full ? 0 : (state[kSpec] != 0 ? 3 : 1);
     state[kSumsStale] = 0;
+    state[kSpec] = 0;
   }
 }
 
@@ -498,7 +501,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 delta_sums_kernel(const T* __restrict__ P, int64_t n, int d, const int32_t* __restrict__ prev,
                   const int32_t* __restrict__ labels, double* __restrict__ S, const long long* __restrict__ state) {
-  if (stopped(state) || !delta_mode(state)) return;
+  if (stopped(state) || !delta_mode(state) || ((volatile const long long*)state)[kMode] == 3) return;
   const int lane = threadIdx.x & 31;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;

@@ -593,8 +593,7 @@ class LloydEngine(ShardSequence):
             self._resolve(self.ovf_list, self.ovf_count, new, state)
             self._kmark(1)
             if acc is not None:
-                L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
-                       _stream())
+                self._count_labels(new, prev, acc, state)
             return
         if self.variant in ("bf16s", "fp8s"):
             self.amb_count.zero_()
@@ -615,8 +614,7 @@ class LloydEngine(ShardSequence):
                    _p(self.two_list), _p(self.two_count), _p(state), _stream())
             self._resolve(self.ovf_list, self.ovf_count, new, state)
             if acc is not None:
-                L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
-                       _stream())
+                self._count_labels(new, prev, acc, state)
             return
         if self.variant == "tc1xtf32s":
             self.amb_count.zero_()
@@ -627,8 +625,7 @@ class LloydEngine(ShardSequence):
             self._kmark(1)
             self._resolve(self.amb_list, self.amb_count, new, state)
             if acc is not None:
-                L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
-                       _stream())
+                self._count_labels(new, prev, acc, state)
             return
         self._kmark(0)
         if self.variant == "deltatc":
@@ -644,6 +641,16 @@ class LloydEngine(ShardSequence):
                    _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
                    self.vcode, _stream())
         self._kmark(1)
+
+    def _count_labels(self, new, prev, acc, state) -> None:
+        """counts / changed of the new labels (clustering.py:146-149); with the delta
+        update on, fused with its changed-row sums when the previous iteration was a
+        delta one (pcb_count_labels_delta_f32; delta_sums then has nothing left to do)."""
+        if self.delta_frac >= 0 and self.dtype == _F32:
+            L.call("pcb_count_labels_delta_f32", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state),
+                   _p(self.P), _p(self.S), _stream())
+        else:
+            L.call("pcb_count_labels", _p(new), _p(prev), self.n, self.k, self.d, _p(acc), _p(state), _stream())
 
     def _resolve(self, rows, count, new, state) -> None:
         """3xTF32 labels of the listed rows, made exact (pcb_resolve_ambiguous_f32
@@ -844,7 +851,7 @@ class LloydEngine(ShardSequence):
                 "centroids": self.C.cpu().numpy(),
                 "counts": acc[kd:kd + self.k].copy(),
                 "nan": bool(st[5]),
-                "update_mode": "delta" if st[6] == 1 else "full",
+                "update_mode": "delta" if int(st[6]) & 1 else "full",
             }
             if self.variant in ("bf16s", "fp8s"):
                 amb, two, ovf = int(self.amb_count.item()), int(self.two_count.item()), int(self.ovf_count.item())

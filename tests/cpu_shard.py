@@ -39,7 +39,7 @@ class NumpyShard(ShardSequence):
         self.labels = [torch.from_numpy(np.asarray(labels0_local, dtype=np.int32).copy()),
                        torch.zeros(self.n, dtype=torch.int32)]
         self.acc = torch.zeros(k * self.d + k + 2, dtype=torch.float64)
-        self.state = torch.zeros(8, dtype=torch.int64)
+        self.state = torch.zeros(9, dtype=torch.int64)
         self.C = np.asarray(C0, dtype=dtype).copy()
         self.obj_hist = np.zeros(max_iters)
         self.rep_hist = np.zeros(max_iters, dtype=np.int64)

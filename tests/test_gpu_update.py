@@ -39,8 +39,11 @@ def test_delta_matches_full_update(variant, n, d, k):
     P = oracle.make_blobs(n, d, k, seed=3)
     a, modes, ca, _ = _run(P, k, "auto", variant)
     b, _, cb, _ = _run(P, k, "full", variant)
-    assert 1 in modes, "the delta update never ran"
+    assert any(m & 1 for m in modes), "the delta update never ran"
     assert modes[0] == 0  # sums not valid yet: full
+    if variant in ("fp8s", "bf16s"):
+        # delta after delta: the count pass applied the changed-row sums (mode 3)
+        assert 3 in modes, modes
     np.testing.assert_array_equal(a.labels, b.labels)
     np.testing.assert_allclose(a.objective_history, b.objective_history, rtol=1e-10)
     for x, y in zip(ca, cb):
@@ -51,7 +54,7 @@ def test_delta_matches_full_update_f64():
     P = oracle.make_blobs(20000, 24, 30, seed=8).astype(np.float64)
     a, modes, _, _ = _run(P, 30, "auto", dtype=np.float64)
     b, _, _, _ = _run(P, 30, "full", dtype=np.float64)
-    assert 1 in modes
+    assert any(m & 1 for m in modes)
     np.testing.assert_array_equal(a.labels, b.labels)
     np.testing.assert_allclose(a.objective_history, b.objective_history, rtol=1e-10)
     np.testing.assert_allclose(a.centroids, b.centroids, rtol=1e-12, atol=1e-12)
