@@ -1156,7 +1156,7 @@ static int resolve_screen(const float* P, int64_t n, int d, const void* P_b, int
                                state, st);
   if (rc) return rc;
   const int DQ = (d + 31) / 32;  // float4 per lane (8 lanes per row)
-  const int xgrid = sm_count() * 16;
+  const int xgrid = sm_count() * 4;  // ~one resident wave (grid-stride over the rows)
 #define PCB_EX_CASE(N)                                                                                          \
   if (DQ <= N) {                                                                                              \
     screen_exact_kernel<N><<<xgrid, 256, 0, st>>>(P, d, C, amb_list, amb_count, bypass, cand, cand_n, labels, \

@@ -403,12 +403,15 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
   __shared__ int sidx[XR_R];
   const int cnt = *flag_count;
   const int seg = exact_segments(cnt, gridDim.x, k);
-  if ((int)blockIdx.y >= seg) return;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) sc->seg = seg;
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->seg = seg;
   const int ctiles = (k + XR_C - 1) / XR_C;
-  const int t_lo = (int)((int64_t)ctiles * blockIdx.y / seg), t_hi = (int)((int64_t)ctiles * (blockIdx.y + 1) / seg);
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  for (int rb = blockIdx.x * XR_R; rb < cnt; rb += gridDim.x * XR_R) {
+  // work items (row block, centroid segment) over a 1-D grid: a launch sized for
+  // the cold start's ~1e5 flagged rows costs little when only ~1e2 are flagged
+  const int nrb = (cnt + XR_R - 1) / XR_R;
+  for (int item = blockIdx.x; item < nrb * seg; item += gridDim.x) {
+    const int sg = item % seg, rb = (item / seg) * XR_R;
+    const int t_lo = (int)((int64_t)ctiles * sg / seg), t_hi = (int)((int64_t)ctiles * (sg + 1) / seg);
     __syncthreads();
     if (tid < XR_R) {
       const int q = rb + tid;
@@ -482,8 +485,8 @@ exact_tiled_kernel(const float* __restrict__ P, int d, const float* __restrict__
         const int r = sidx[ty * 4 + i];
         if (r < 0) continue;
         if (seg > 1) {
-          sc->dmin[blockIdx.y * XR_SCRATCH_ROWS + q] = best[i];
-          sc->bj[blockIdx.y * XR_SCRATCH_ROWS + q] = bj[i];
+          sc->dmin[sg * XR_SCRATCH_ROWS + q] = best[i];
+          sc->bj[sg * XR_SCRATCH_ROWS + q] = bj[i];
         } else {
           out[r] = bj[i];
         }
@@ -512,7 +515,7 @@ int exact_rows(const float* P, int d, const float* C, int k, const int* flag_lis
                const int* row_ids, int32_t* out, void* scratch, const long long* state, cudaStream_t st) {
   ExactScratch* sc = (ExactScratch*)scratch;
   const int gx = sm_count() * 4;
-  exact_tiled_kernel<<<dim3(gx, XR_SEG), 128, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out, sc, state);
+  exact_tiled_kernel<<<gx, 128, 0, st>>>(P, d, C, k, flag_list, flag_count, row_ids, out, sc, state);
   PCB_CHECK_LAUNCH();
   exact_merge_kernel<<<sm_count(), 256, 0, st>>>(flag_list, flag_count, out, sc, state);
   PCB_CHECK_LAUNCH();
