@@ -505,6 +505,10 @@ def e2e_run(args, cfg, dev, comm=None, lo=0, hi=None):
     if world == 1:
         pcb.run_lloyd(P_host[: min(n, 100_000)], pcb.KKMeansConfig(k=k, max_iters=2))
     res, wall = fit(False)
+    # default contract: the first call pins the n x max_iters history staging
+    # buffer (cudaHostAlloc, ~0.7 s per GB), later calls reuse it from torch's
+    # pinned-memory cache; both are reported
+    res_h, wall_h_cold = fit(True)
     res_h, wall_h = fit(True)
     h2d = n * d * 4
     d2h = n * 4 + it * 16 + k * d * 4
@@ -514,7 +518,7 @@ def e2e_run(args, cfg, dev, comm=None, lo=0, hi=None):
                    + (f" on each of {world} ranks (run_lloyd_sharded), max over ranks" if world > 1 else ""),
            "wall_s": wall,
            "default_contract": {"value": res_h.iterations_run / wall_h, "unit": "iters/s", "wall_s": wall_h,
-                                "label_history": True,
+                                "first_call_wall_s": wall_h_cold, "label_history": True,
                                 "d2h_bytes_per_step": (d2h + it * n * 4) // it}}
     if world == 1:
         out["phases_ms"] = e2e_phases(P_host, k, it, dev)

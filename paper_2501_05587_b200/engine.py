@@ -797,6 +797,17 @@ class LloydEngine(ShardSequence):
                 torch.cuda.synchronize()
         return body(False)
 
+    @staticmethod
+    def _history_arrays(hist, iters: int) -> list:
+        """label_history (clustering.py:320): one int32[n] array per iteration, as
+        rows of one host array filled by a single (multi-threaded) copy out of the
+        pinned staging rows — 30 separate single-threaded copies cost ~10x more."""
+        if hist is None or iters == 0:
+            return []
+        out = np.empty((iters, hist.shape[1]), dtype=np.int32)
+        torch.from_numpy(out).copy_(hist[:iters])
+        return list(out)
+
     def collect(self, hist=None, evs=()) -> RunOutput:
         st = self.state.cpu().numpy()
         if st[5] != 0:
@@ -812,7 +823,7 @@ class LloydEngine(ShardSequence):
             objective_history=self.obj_hist[:iters].cpu().numpy().astype(np.float64),
             repairs=self.rep_hist[:iters].cpu().numpy().astype(np.int64),
             labels=labels,
-            label_history=[hist[t].numpy().copy() for t in range(iters)] if hist is not None else [],
+            label_history=self._history_arrays(hist, iters),
             centroids=self.C.cpu().numpy(), distance_seconds=dist_s, update_seconds=upd_s)
 
     # -- lockstep / predict -----------------------------------------------------------
