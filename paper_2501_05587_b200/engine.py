@@ -161,6 +161,42 @@ def resolve_variant(variant: str, dtype: np.dtype, d: int, k: int = 1) -> str:
 SCREEN_KMAX = 6144  # assign_screen.cu SC_KMAX
 
 
+class HistoryRing:
+    """label_history of an eager single-rank fit (clustering.py:320): iteration
+    t's labels go D2H into pinned slot t % R and the host copies that slot into
+    the result array R iterations later, while the GPU runs ahead, so only R
+    rows are pinned — pinning the whole (max_iters x n) staging buffer costs
+    ~0.7 s per GB the first time (c3: 1.2 GB)."""
+
+    def __init__(self, n: int, max_iters: int, slots: int = 4):
+        self.out = np.empty((max_iters, n), dtype=np.int32)
+        self.pin = torch.empty((slots, n), dtype=torch.int32, pin_memory=True)
+        self.ev = [None] * slots
+        self.pending: list = []
+
+    def push(self, t: int, labels: torch.Tensor) -> None:
+        s = t % len(self.ev)
+        if self.ev[s] is not None:
+            self._drain()
+        self.pin[s].copy_(labels, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.ev[s] = ev
+        self.pending.append(t)
+
+    def _drain(self) -> None:
+        t = self.pending.pop(0)
+        s = t % len(self.ev)
+        self.ev[s].synchronize()
+        torch.from_numpy(self.out[t]).copy_(self.pin[s])
+        self.ev[s] = None
+
+    def finish(self, iters: int) -> list:
+        while self.pending:
+            self._drain()
+        return list(self.out[:iters])
+
+
 @dataclass
 class RunOutput:
     iterations_run: int
@@ -742,18 +778,20 @@ class LloydEngine(ShardSequence):
             raise ValueError("max_iters exceeds the engine's history capacity")
         with torch.cuda.device(self.dev):
             self.state.zero_()
+            # graphs pay off where launches dominate (small n k d); a large fit
+            # is GPU-bound and instantiating ~1000 nodes would only add latency
+            small = 2.0 * self.n * self.k * self.d < 1e11
+            use_graph = graph and small and not self._multi()
             hist = None
             if record_history:
-                hist = torch.empty((max_iters, self.n), dtype=torch.int32, pin_memory=True)
+                # eager single-rank fits stream the history through a few pinned slots
+                hist = (HistoryRing(self.n, max_iters) if not use_graph and not self._multi() else
+                        torch.empty((max_iters, self.n), dtype=torch.int32, pin_memory=True))
             if self._multi():
                 mk = (lambda: [torch.cuda.Event(enable_timing=True) for _ in range(3)]) if timing else None
                 evd = self.run_multi(max_iters, check_convergence, tol, mk, hist)
                 torch.cuda.current_stream().synchronize()
                 return self.collect(hist, [evd[t] for t in sorted(evd)] if timing else ())
-            # graphs pay off where launches dominate (small n k d); a large fit
-            # is GPU-bound and instantiating ~1000 nodes would only add latency
-            small = 2.0 * self.n * self.k * self.d < 1e11
-            use_graph = graph and small
             evs = self.iterations(0, max_iters, check_convergence, tol, timing, hist, use_graph)
             torch.cuda.current_stream().synchronize()
             return self.collect(hist, evs)
@@ -770,10 +808,12 @@ class LloydEngine(ShardSequence):
                 self.iteration(t, check_convergence, tol, ev)
                 if ev is not None:
                     evs.append(ev)
-                if hist is not None:
+                if isinstance(hist, HistoryRing):
+                    hist.push(t, self.labels[(t + 1) % 2])
+                elif hist is not None:
                     hist[t].copy_(self.labels[(t + 1) % 2], non_blocking=True)
             return evs
-        if graph:
+        if graph and not isinstance(hist, HistoryRing):
             saved, cold = self.sums_valid, self._cold
             # relayout() (captured at t in RELAYOUT_AT) swaps in new operand buffers whose
             # fill kernels only run on replay: keep the current ones to restore on failure
@@ -802,6 +842,8 @@ class LloydEngine(ShardSequence):
         """label_history (clustering.py:320): one int32[n] array per iteration, as
         rows of one host array filled by a single (multi-threaded) copy out of the
         pinned staging rows — 30 separate single-threaded copies cost ~10x more."""
+        if isinstance(hist, HistoryRing):
+            return hist.finish(iters)
         if hist is None or iters == 0:
             return []
         out = np.empty((iters, hist.shape[1]), dtype=np.int32)

@@ -90,3 +90,22 @@ def test_repair_keeps_delta_sums():
     np.testing.assert_allclose(a.objective_history, b.objective_history, rtol=1e-9)
     ref = oracle.run_lloyd(P, k, max_iters=10)
     np.testing.assert_array_equal(a.repairs, ref.repairs)
+
+
+def test_history_ring_matches_pinned_history():
+    """label_history of an eager fit (streamed through the pinned slot ring)
+    equals the graph-replayed fit's (one pinned buffer), iteration by iteration,
+    including a fit that converges early (the ring drops the no-op iterations)."""
+    from paper_2501_05587_b200.engine import LloydEngine
+    P = oracle.make_blobs(30000, 48, 20, seed=12)
+    outs = []
+    for graph in (True, False):
+        eng = LloydEngine(P, 20, max_iters=12)
+        eng.init_labels_device(0)
+        eng.init_centroids_from_labels()
+        outs.append(eng.run(12, check_convergence=True, tol=0.0, record_history=True, graph=graph))
+    a, b = outs
+    assert a.iterations_run == b.iterations_run and len(a.label_history) == a.iterations_run
+    for x, y in zip(a.label_history, b.label_history):
+        np.testing.assert_array_equal(x, y)
+    np.testing.assert_array_equal(a.labels, b.labels)
