@@ -237,8 +237,9 @@ int pcb_screen_relayout_bf16(const void* Pb0, const float* an0, const float* dan
                              void* stream);
 /* E4M3 screening variant ("fp8s"): the same kernels and contract as the BF16
  * one with E4M3 operand rows of ld8 = pcb_screen_fp8_ld(d) bytes (power-of-two
- * scales chosen on the device, bstat of 16 floats; the keys are scaled by
- * S = bstat[4] and so are amb_thr).                                          */
+ * scales chosen on the device by pcb_screen_prep_points_fp8 — the points' from
+ * max |p|, the centroids' from 2 max |p|, fixed for the fit; bstat of 16
+ * floats; the keys are scaled by S = bstat[4] and so are amb_thr).           */
 int pcb_screen_fp8_ld(int d);
 int pcb_screen_prep_points_fp8(const float* P, int64_t n, int d, int ld8, void* P_q, float* anorm,
                                float* danorm, float* bstat /* 16 */, void* stream);

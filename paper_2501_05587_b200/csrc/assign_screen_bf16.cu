@@ -1253,18 +1253,81 @@ __global__ void maxabs_kernel(const float* __restrict__ X, int64_t count, float*
   if ((threadIdx.x & 31) == 0) atomic_max_pos_f(out, m);
 }
 
-// power-of-two scale with maxabs * mult * scale <= 448 (E4M3 max finite)
-__global__ void e4m3_scale_kernel(const float* __restrict__ maxabs, float mult, float* __restrict__ scale,
-                                  float* __restrict__ S, const float* __restrict__ other) {
-  const float m = *maxabs * mult;
+// the largest power-of-two scale with m * scale <= 448 (E4M3 max finite)
+__device__ __forceinline__ float e4m3_pow2_scale(float m) {
   float sc = 1.0f;
   if (m > 0.0f && isfinite(m)) {
     sc = exp2f(floorf(log2f(448.0f / m)));
     while (m * sc > 448.0f) sc *= 0.5f;
     while (m * sc * 2.0f <= 448.0f) sc *= 2.0f;
   }
+  return sc;
+}
+
+// power-of-two scale with maxabs * mult * scale <= 448 (E4M3 max finite)
+__global__ void e4m3_scale_kernel(const float* __restrict__ maxabs, float mult, float* __restrict__ scale,
+                                  float* __restrict__ S, const float* __restrict__ other) {
+  const float sc = e4m3_pow2_scale(*maxabs * mult);
   *scale = sc;
   if (S != nullptr) *S = sc * *other;
+}
+
+// The centroids' E4M3 scale, fixed for the fit: every coordinate of a mean of
+// rows is within max |p| (bstat[6]), so sc = scale of 2 max |p| never
+// saturates the rows e4m3(-2 c sc); centroids given by the caller that exceed
+// it saturate (satfinite), which the exact residual norms |c - c~| charge to
+// the bound.  S = sp sc.
+__global__ void e4m3_centroid_scale_kernel(float* __restrict__ bstat) {
+  const float sc = e4m3_pow2_scale(2.0f * bstat[6]);
+  bstat[8] = sc;
+  bstat[4] = sc * bstat[5];
+}
+
+// max |c~|, max |dc| over the centroids (bstat[0], bstat[1]) and the augmented
+// columns S (|c|^2 + OFF) in three BF16 pieces (padding rows j >= k: huge key),
+// one block: the tail of the per-iteration E4M3 centroid prep.
+__global__ void __launch_bounds__(1024) centroid_max_aug_kernel(const float* __restrict__ bnorm,
+                                                                const float* __restrict__ dbnorm,
+                                                                const float* __restrict__ cnorm,
+                                                                float* __restrict__ bstat, int k, int kpad,
+                                                                __nv_bfloat16* __restrict__ aug) {
+  __shared__ float red[32][2];
+  float a = 0.0f, b = 0.0f;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) { a = fmaxf(a, bnorm[j]); b = fmaxf(b, dbnorm[j]); }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5][0] = a; red[threadIdx.x >> 5][1] = b; }
+  const float off = bstat[2], S = bstat[4];
+  for (int j = threadIdx.x; j < kpad; j += blockDim.x) {
+    uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = make_uint4(0u, 0u, 0u, 0u);
+    __nv_bfloat16 h1, h2, h3;
+    if (j < k) {
+      const float cp = (cnorm[j] + off) * S;
+      h1 = __float2bfloat16_rn(cp);
+      const float r1 = cp - __bfloat162float(h1);  // exact
+      h2 = __float2bfloat16_rn(r1);
+      h3 = __float2bfloat16_rn(r1 - __bfloat162float(h2));
+    } else {
+      h1 = __float2bfloat16_rn(3.0e38f);
+      h2 = h3 = __float2bfloat16_rn(0.0f);
+    }
+    lo.x = (uint32_t)__bfloat16_as_ushort(h1) | ((uint32_t)__bfloat16_as_ushort(h2) << 16);
+    lo.y = (uint32_t)__bfloat16_as_ushort(h3);
+    uint4* dst = reinterpret_cast<uint4*>(aug + (int64_t)j * SB_AUG);
+    dst[0] = lo;
+    dst[1] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { a = fmaxf(a, red[w][0]); b = fmaxf(b, red[w][1]); }
+    a = fmaxf(a, red[0][0]);
+    b = fmaxf(b, red[0][1]);
+    bstat[0] = a;
+    bstat[1] = b;
+  }
 }
 
 // Per row: E4M3 copy of mult * scale * x (row stride ld8 bytes, zero padded),
@@ -1305,7 +1368,7 @@ row_e4m3_norms_kernel(const float* __restrict__ X, int64_t rows, int d, float* _
 extern "C" int pcb_screen_fp8_ld(int d) { return d <= 64 ? 64 : (d + 127) / 128 * 128; }
 
 // bstat (16 floats): [0] max|c~| [1] max|dc| [2] OFF [3] scratch [4] S = sp sc
-// [5] sp [6] max|p| [7] max|c| [8] sc
+// [5] sp [6] max|p| [7] (unused) [8] sc (the centroids' scale, fixed per fit from max|p|)
 extern "C" int pcb_screen_prep_points_fp8(const float* P, int64_t n, int d, int ld8, void* P_q, float* anorm,
                                           float* danorm, float* bstat, void* stream) {
   if (n < 1 || d < 1 || ld8 < d || (ld8 % 128 && ld8 != 64) || !P || !P_q || !anorm || !danorm || !bstat)
@@ -1323,6 +1386,8 @@ extern "C" int pcb_screen_prep_points_fp8(const float* P, int64_t n, int d, int 
   PCB_CHECK_LAUNCH();
   screen_off_kernel<<<1, 1, 0, st>>>(bstat, bstat + 3);
   PCB_CHECK_LAUNCH();
+  e4m3_centroid_scale_kernel<<<1, 1, 0, st>>>(bstat);
+  PCB_CHECK_LAUNCH();
   return 0;
 }
 
@@ -1332,22 +1397,13 @@ extern "C" int pcb_screen_prep_centroids_fp8(const float* C, const float* cnorm,
       !bstat)
     return PCB_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(bstat, 0, 2 * sizeof(float), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(bstat + 7, 0, sizeof(float), st);
-  if (e != cudaSuccess) return (int)e;
-  const int g1 = (int)std::min<int64_t>(((int64_t)k * d + 255) / 256, (int64_t)sm_count() * 4);
-  maxabs_kernel<<<g1, 256, 0, st>>>(C, (int64_t)k * d, bstat + 7);
-  PCB_CHECK_LAUNCH();
-  // B rows are e4m3(-2 c sc): the factor -2 is part of the scaled value
-  e4m3_scale_kernel<<<1, 1, 0, st>>>(bstat + 7, 2.0f, bstat + 8, bstat + 4, bstat + 5);
-  PCB_CHECK_LAUNCH();
+  // sc (bstat[8]) and S (bstat[4]) were fixed by pcb_screen_prep_points_fp8
   row_e4m3_norms_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(C, k, d, bnorm, dbnorm, nullptr, (uint8_t*)C_q, ld8,
                                                              bstat + 8, -2.0f);
   PCB_CHECK_LAUNCH();
-  max2_bf16_kernel<<<1, 256, 0, st>>>(bnorm, dbnorm, k, bstat);
-  PCB_CHECK_LAUNCH();
   const int kpad = (k + SB_KPAD - 1) / SB_KPAD * SB_KPAD;
-  centroid_aug_kernel<<<(kpad + 127) / 128, 128, 0, st>>>(cnorm, bstat, k, kpad, reinterpret_cast<__nv_bfloat16*>(C_aug));
+  centroid_max_aug_kernel<<<1, 1024, 0, st>>>(bnorm, dbnorm, cnorm, bstat, k, kpad,
+                                              reinterpret_cast<__nv_bfloat16*>(C_aug));
   PCB_CHECK_LAUNCH();
   return 0;
 }

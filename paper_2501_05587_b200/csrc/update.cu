@@ -636,7 +636,9 @@ static int delta_update(const T* P, int64_t n, int d, const int32_t* prev, const
                         double* S, const double* Q, double* acc, const long long* state, cudaStream_t st) {
   if (n < 1 || d < 1 || k < 1 || !P || !prev || !labels || !C || !S || !Q || !acc || !state) return PCB_EINVAL;
   const int sms = pcb::sm_count();
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+  // two blocks per SM (4 label groups in flight per warp): enough for the label
+  // scan, and a cheap launch when the count pass already applied the sums (mode 3)
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 2));
   pcb::delta_sums_kernel<T><<<grid, 256, 0, st>>>(P, n, d, prev, labels, S, state);
   PCB_CHECK_LAUNCH();
   const int64_t kd = (int64_t)k * d;

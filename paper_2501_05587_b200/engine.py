@@ -466,10 +466,11 @@ class LloydEngine(ShardSequence):
                 self.dbnorm = torch.empty(kk, dtype=torch.float32, device=dev)
                 self.bstat = torch.zeros(16, dtype=torch.float32, device=dev)
                 self.amb_list = torch.empty(n, dtype=torch.int32, device=dev)
-                self.amb_count = torch.zeros(1, dtype=torch.int32, device=dev)
+                self.ctr = torch.zeros(2, dtype=torch.int32, device=dev)  # [ambiguous, two-candidate] rows
+                self.amb_count = self.ctr[0:1]
                 self.amb_thr = torch.empty(n, dtype=torch.float32, device=dev)
                 self.two_list = torch.empty(3 * n, dtype=torch.int32, device=dev)  # (row, r1, r2)
-                self.two_count = torch.zeros(1, dtype=torch.int32, device=dev)
+                self.two_count = self.ctr[1:2]
                 self.sub_b = torch.empty((n, self.ldb), dtype=torch.bfloat16, device=dev)
                 self.bypass = max(n // 4, 1)  # more ambiguous rows: straight to 3xTF32
                 self.cand = torch.empty((self.bypass, ncand), dtype=torch.int32, device=dev)
@@ -632,8 +633,7 @@ class LloydEngine(ShardSequence):
                 self._count_labels(new, prev, acc, state)
             return
         if self.variant in ("bf16s", "fp8s"):
-            self.amb_count.zero_()
-            self.two_count.zero_()
+            self.ctr.zero_()  # both counters, one fill
             self._kmark(0)
             ldq = self.ld8 if self.q8 else self.ldb
             L.call("pcb_assign_screen_fp8" if self.q8 else "pcb_assign_screen_bf16", _p(self.P_b), self.n, ldq,

@@ -2,7 +2,7 @@
 # Steady-state launch list (cold, serialised) of the c3 default: 12 warm-up
 # iterations skipped, then ~3 iterations of launches.
 cfg=${1:-c3}; tag=${2:-steady_$cfg}
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 330 -c 75 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s ${SKIP:-330} -c ${COUNT:-75} --csv \
   --log-file gpurun_out/launches_$tag.csv python bench.py --config $cfg --steps 4 --warmup 12 --no-graph \
   --no-e2e --no-cpu-baseline > gpurun_out/launches_$tag.log 2>&1
 echo "ncu rc=$?"
