@@ -44,7 +44,10 @@
 namespace pcb {
 
 constexpr int SB_BN = 128;
-constexpr int SB_STAGES = 4;
+#ifndef PCB_SB_STAGES
+#define PCB_SB_STAGES 4
+#endif
+constexpr int SB_STAGES = PCB_SB_STAGES;  // centroid-chunk ring depth (capped by shared memory)
 #ifndef PCB_REGS_LOW
 #define PCB_REGS_LOW 96
 #endif
