@@ -1,0 +1,73 @@
+"""Parity at the benchmark size (c3: n = 10M, d = 128, k = 1024) through
+size-independent properties of a Lloyd iteration (clustering.py:308-324),
+checked on the device in f64 for the steady-state iterations the bench times:
+
+* labels: every row's label is the exact argmin of the iteration's input
+  centroids (f64, lowest index on ties; tests/audit.py) — the certified screen,
+  the candidate stage and the resolver alike;
+* counts: the per-cluster counts sum to n and match a bincount of the labels;
+* objective: objective_history[t] = sum_i |p_i - c_label(i)|^2 over the
+  iteration's input centroids (clustering.py:146-148), f64, to 1e-9 relative;
+* centroids: the new centroids are the f64 means of their rows rounded once to
+  f32 (clustering.py:282-288), to 1e-6 relative.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_c3_fullsize_steady_state_properties():
+    from audit import direct_f64, exact_argmin_device
+    from bench import CONFIGS, make_shard
+    from paper_2501_05587_b200.engine import LloydEngine
+    cfg = CONFIGS["c3"]
+    n, d, k = cfg["n"], cfg["d"], cfg["k"]
+    dev = torch.device("cuda", 0)
+    P = make_shard(n, d, k, 0, 0, dev)
+    eng = LloydEngine(P, k, max_iters=16)
+    assert eng.variant == "fp8s"
+    eng.init_labels_device(0)
+    eng.init_centroids_from_labels()
+    for t in range(10):
+        eng.iteration(t)
+    for t in (10, 11):
+        out = eng.traced_iteration(t)
+        assert out["update_mode"] == "delta" and out["screen"]["certified"] > 0.9 * n, out["screen"]
+        C_in = out["centroids_in"]
+        lab = torch.from_numpy(out["labels"]).to(dev).long()
+        assert out["moved"] == 0
+        # labels: the exact argmin of the input centroids
+        ex = exact_argmin_device(P, C_in).long()
+        mism = torch.nonzero(ex != lab).flatten()
+        if mism.numel():  # the f64 expansion itself can mis-rank a near-tie: direct f64 sums decide
+            Pr = P[mism].cpu().numpy()
+            ds = direct_f64(Pr, C_in, lab[mism].cpu().numpy())
+            dx = direct_f64(Pr, C_in, ex[mism].cpu().numpy())
+            worse = (ds > dx) | ((ds == dx) & (lab[mism].cpu().numpy() > ex[mism].cpu().numpy()))
+            assert not worse.any(), int(worse.sum())
+        # counts
+        cnt = torch.bincount(lab, minlength=k).double().cpu().numpy()
+        assert cnt.sum() == n
+        np.testing.assert_array_equal(cnt, out["counts"])
+        # objective over the input centroids, f64
+        C64 = torch.from_numpy(C_in.astype(np.float64)).to(dev)
+        obj = 0.0
+        sums = torch.zeros((k, d), dtype=torch.float64, device=dev)
+        for s in range(0, n, 2_000_000):
+            X = P[s:s + 2_000_000].double()
+            L = lab[s:s + 2_000_000]
+            obj += float(((X - C64[L]) ** 2).sum())
+            sums.index_add_(0, L, X)
+        assert abs(out["objective"] - obj) <= 1e-9 * obj, (out["objective"], obj)
+        # centroids: f64 means rounded once to f32
+        means = (sums / torch.from_numpy(cnt).to(dev)[:, None]).float().cpu().numpy()
+        rel = np.abs(out["centroids"] - means).max() / np.abs(means).max()
+        assert rel <= 1e-6, rel
