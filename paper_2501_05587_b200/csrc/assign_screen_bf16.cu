@@ -44,6 +44,9 @@
 namespace pcb {
 
 constexpr int SB_BN = 128;
+#ifndef PCB_EPI_X4
+#define PCB_EPI_X4 1
+#endif
 #ifndef PCB_SB_STAGES
 #define PCB_SB_STAGES 4
 #endif
@@ -457,12 +460,14 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
         if (abuf == 0) aphase ^= 1u;
       }
     };
-    // TMEM loads run one chunk PAIR ahead of the arithmetic: two 32-column
-    // loads are issued back to back and covered by one tcgen05.wait::ld (which
-    // waits for every outstanding load), so each wait's latency is paid once
-    // per 64 columns.  Buffers (vA0, vA1) / (vB0, vB1) alternate by pair
-    // parity (CH / 2 pairs per tile, an even count), across tile and pair
-    // boundaries.  The epilogue warpgroups run at 224 registers (setmaxnreg).
+    // N = 128 tiles (X4 below): a tile's four 32-column chunks are loaded at
+    // once into (vA0, vA1, vB0, vB1) and the accumulator is handed back after a
+    // single tcgen05.wait::ld, before any arithmetic — the MMAs wait on this
+    // release (two accumulators per row tile), not on the arithmetic.
+    // N = 256 tiles (W): loads run one chunk PAIR ahead of the arithmetic, two
+    // loads per wait, buffers (vA0, vA1) / (vB0, vB1) alternating by pair
+    // parity across tile and pair boundaries.  The epilogue warpgroups run at
+    // 200 registers (setmaxnreg).
     constexpr int CP = CH / 2;
     static_assert(CH % 4 == 0, "chunk pairs alternate buffers across tiles");
     uint32_t vA0[32], vA1[32], vB0[32], vB1[32];
@@ -493,7 +498,13 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       const int l = lprev != nullptr ? lprev[mid_nx] : 0;
       fc_nx = (l >= 0 && l < k) ? (unsigned)l : 0u;
     };
-    if (blockIdx.x < npairs) {
+    // X4: no loads run ahead across tiles.  Measured against the pair-ahead
+    // scheme (PCB_EPI_X4=0): c3 1.232 vs 1.290 ms, c5 38.1 vs 37.8 ms
+    constexpr bool X4 = PCB_EPI_X4 && !W && CH == 4;
+    if (X4 && blockIdx.x < npairs) {
+      fetch_pair(blockIdx.x);
+      fetch_pair_b();
+    } else if (blockIdx.x < npairs) {
       fetch_pair(blockIdx.x);
       fetch_pair_b();
       ptx::mbar_wait(&tfull[tbar()], 0);
@@ -521,6 +532,43 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
       float R1 = 3.4e38f, R2 = 3.4e38f, cnt = 0.0f;
       int r1 = 0, r2 = 0;
       float thr_skip = 3.4e38f;  // sb_skip_thr(R1, twoE), refreshed when R1 changes
+      auto pair_work = [&](const uint32_t (&cur0)[32], const uint32_t (&cur1)[32], int ca, int cb) {
+        if (CAND) {
+          sb_chunk_cand(cur0, ca, thr, row, n, rc, cand, nc);
+          sb_chunk_cand(cur1, cb, thr, row, n, rc, cand, nc);
+        } else {
+          const float m0 = sb_chunk_min(cur0), m1 = sb_chunk_min(cur1);
+          if (__any_sync(0xffffffffu, fminf(m0, m1) <= thr_skip)) {
+            if (__any_sync(0xffffffffu, m0 <= thr_skip)) sb_chunk_full(cur0, ca, twoE, msk, R1, r1, R2, r2, cnt);
+            if (__any_sync(0xffffffffu, m1 <= sb_skip_thr(R1, twoE)))
+              sb_chunk_full(cur1, cb, twoE, msk, R1, r1, R2, r2, cnt);
+            thr_skip = sb_skip_thr(R1, twoE);
+          }
+        }
+      };
+      if constexpr (X4) {
+        for (int nt = 0; nt < ntiles; ++nt) {
+          const int c0 = (nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles) * BN;
+          const int qr = nt == 0 ? q0 : 0;  // the first tile starts at the previous label's chunk
+          ptx::mbar_wait(&tfull[tbar()], tphase());
+          ptx::tc_fence_after();
+          const uint32_t taddr = tbase();
+          ptx::tmem_ld_32x32b_x32_async(taddr + 32 * qr, vA0);
+          ptx::tmem_ld_32x32b_x32_async(taddr + 32 * ((qr + 1) & 3), vA1);
+          ptx::tmem_ld_32x32b_x32_async(taddr + 32 * ((qr + 2) & 3), vB0);
+          ptx::tmem_ld_32x32b_x32_async(taddr + 32 * ((qr + 3) & 3), vB1);
+          ptx::tmem_wait_ld(vA0);
+          ptx::tie_regs(vA1);
+          ptx::tie_regs(vB0);
+          ptx::tie_regs(vB1);
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&tempty[tbar()]);
+          tnext();
+          if (nt == 0 && !last_pair) fetch_pair_b();
+          pair_work(vA0, vA1, c0 + 32 * qr, c0 + 32 * ((qr + 1) & 3));
+          pair_work(vB0, vB1, c0 + 32 * ((qr + 2) & 3), c0 + 32 * ((qr + 3) & 3));
+        }
+      } else
       for (int nt = 0; nt < ntiles; ++nt) {
         const uint32_t taddr = tbase();
         const int c0 = (nt + t0 < ntiles ? nt + t0 : nt + t0 - ntiles) * BN;
@@ -556,22 +604,10 @@ assign_screen_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid
               ptx::tmem_ld_32x32b_x32_async(tbase() + 32 * ((qn + 1) & (CH - 1)), nxt1);
             }
           }
-          if (CAND) {
-            sb_chunk_cand(cur0, c0 + 32 * qa, thr, row, n, rc, cand, nc);
-            sb_chunk_cand(cur1, c0 + 32 * qb, thr, row, n, rc, cand, nc);
-          } else {
-            // chunk skip, decided per pair: rows are laid out by label
-            // (pcb_screen_relayout_bf16), so the rows of a warp see their
-            // minima in the same chunks and most pairs of most warps skip
-            const float m0 = sb_chunk_min(cur0), m1 = sb_chunk_min(cur1);
-            if (__any_sync(0xffffffffu, fminf(m0, m1) <= thr_skip)) {
-              if (__any_sync(0xffffffffu, m0 <= thr_skip))
-                sb_chunk_full(cur0, c0 + 32 * qa, twoE, msk, R1, r1, R2, r2, cnt);
-              if (__any_sync(0xffffffffu, m1 <= sb_skip_thr(R1, twoE)))
-                sb_chunk_full(cur1, c0 + 32 * qb, twoE, msk, R1, r1, R2, r2, cnt);
-              thr_skip = sb_skip_thr(R1, twoE);
-            }
-          }
+          // chunk skip, decided per pair: rows are laid out by label
+          // (pcb_screen_relayout_bf16), so the rows of a warp see their
+          // minima in the same chunks and most pairs of most warps skip
+          pair_work(cur0, cur1, c0 + 32 * qa, c0 + 32 * qb);
         }
       }
       if (CAND) {
