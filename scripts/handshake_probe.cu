@@ -45,6 +45,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld_x64(uint32_t taddr, uint32_t (&r)[64]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63]) : "r"(taddr));
+}
+__device__ __forceinline__ void tie64(uint32_t (&r)[64]) {
+#pragma unroll
+  for (int i = 0; i < 64; ++i) asm volatile("" : "+r"(r[i]));
+}
+
 // TMA: centroid tiles (KS * 32 B rows + the 4 KB augmented block) streamed from
 // global memory (32 tiles, L2-resident) through a 4-stage ring by warp 3
 // ARR: arrivals per release: 128 (every thread) or 4 (one lane per warp)
@@ -168,6 +176,23 @@ __global__ void __launch_bounds__(384, 1) probe(int tiles, unsigned long long* c
       ptx::mbar_wait(&tfull[buf * 2 + h], ph);
       ptx::tc_fence_after();
       if (TMA == 6 && (SPLIT || h == 1) && g == 0 && lane == 0) ptx::mbar_arrive(&empty[t % STAGES]);
+      if (LD == 3) {
+        const uint32_t ta = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)((buf * 2 + h) * N);
+        uint32_t r0[64], r1[64];
+        tmem_ld_x64(ta, r0);
+        tmem_ld_x64(ta + 64, r1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tie64(r0);
+        tie64(r1);
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[buf * 2 + h]);
+        uint32_t x = 0;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) x ^= r0[i] ^ r1[i];
+        if (x == 0x12345678u) asm volatile("trap;");
+        if (++buf == NB) { buf = 0; ph ^= 1u; }
+        continue;
+      }
       if (LD == 2) {
         const uint32_t ta = tmem + ((uint32_t)(g * 32) << 16) + (uint32_t)((buf * 2 + h) * N);
         uint32_t r0[32], r1[32], r2[32], r3[32];
@@ -261,16 +286,10 @@ int main() {
   cudaHostGetDevicePointer(&dh, hh, 0);
   cudaMemcpyToSymbol(g_hang_host, &dh, sizeof(dh));
   for (int r = 0; r < 2; ++r) {
-    run<4, 2, 128, 128, 1, true, 6>(sms, 40000, "c3 ring, epi releases, ld pairs");
-    run<4, 2, 128, 128, 0, true, 6, true>(sms, 40000, "c3 split MMA warps");
-    run<4, 2, 128, 128, 1, true, 6, true>(sms, 40000, "c3 split, ld pairs");
-    run<4, 2, 128, 128, 2, true, 6, true>(sms, 40000, "c3 split, ld x4");
-    run<2, 2, 128, 128, 1, true, 6>(sms, 40000, "c5 ring, epi releases, ld pairs");
-    run<2, 2, 128, 128, 2, true, 6>(sms, 40000, "c5 ring, epi releases, ld x4");
-    run<2, 2, 128, 128, 0, true, 6, true>(sms, 40000, "c5 split MMA warps");
-    run<2, 2, 128, 128, 1, true, 6, true>(sms, 40000, "c5 split, ld pairs");
-    run<2, 2, 128, 128, 2, true, 6, true>(sms, 40000, "c5 split, ld x4");
-    run<2, 2, 128, 128, 0, false, 0>(sms, 40000, "c5 MMA floor (no handshake)");
+    run<2, 2, 128, 128, 2, true, 6, true>(sms, 40000, "c5 split, ld x32 x4");
+    run<2, 2, 128, 128, 3, true, 6, true>(sms, 40000, "c5 split, ld x64 x2");
+    run<4, 2, 128, 128, 2, true, 6, true>(sms, 40000, "c3 split, ld x32 x4");
+    run<4, 2, 128, 128, 3, true, 6, true>(sms, 40000, "c3 split, ld x64 x2");
   }
   for (int i = 0; i < 17; ++i) printf("%u ", hh[i]);
   printf(" <- hang codes\n");
