@@ -439,6 +439,222 @@ assign_rowpair(const float* __restrict__ P, const float* __restrict__ pnorm, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// assign_rowcst<D>: assign_rowpair's arithmetic (bit-identical labels / keys)
+// with the centroids in the constant bank instead of shared memory, for
+// d == D and k (D + 1) floats within the constant cache's 8 KB working set
+// (c2: d=16, k=64).  ncu of the shared-memory kernels at c2 put a
+// third of all warp stalls on the short scoreboard of the centroid LDS.128s;
+// from the constant bank the compiler loads two centroid values per LDCU.64
+// into uniform registers and FFMA2 takes each as a broadcast scalar operand
+// (`FFMA2 R, R.F32x2, UR.F32, R`), so no vector register or shared-memory
+// wavefront is spent on centroids and the loads hoist freely.  The centroids
+// and their norms are copied into the bank (two D2D copies on the launching
+// stream, graph-capturable) before each launch; the bank is one per process
+// and device, so launches that use it must be ordered (one stream), as every
+// launch of an engine is.
+// ---------------------------------------------------------------------------
+constexpr int kCstFloats = 2048;
+__constant__ float c_cst[kCstFloats];
+
+template <int D, int NPAIR, int U>
+__device__ __forceinline__ void rc_block(const unsigned long long (&pp)[NPAIR][D], int jj, int k,
+                                         float (&bv)[2 * NPAIR], int (&bj)[2 * NPAIR]) {
+  const unsigned long long m2 = rp_pack(-2.0f, -2.0f);
+  unsigned long long dot[NPAIR][U];
+#pragma unroll
+  for (int q = 0; q < NPAIR; ++q)
+#pragma unroll
+    for (int u = 0; u < U; ++u) dot[q][u] = 0ull;
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float c = c_cst[(jj + u) * D + t];
+      const unsigned long long cc = rp_pack(c, c);
+#pragma unroll
+      for (int q = 0; q < NPAIR; ++q) dot[q][u] = rp_ffma2(pp[q][t], cc, dot[q][u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float cn = c_cst[k * D + jj + u];
+    const unsigned long long nu = rp_pack(cn, cn);
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q) {
+      float s0, s1;
+      rp_unpack(rp_ffma2(dot[q][u], m2, nu), s0, s1);
+      if (s0 < bv[2 * q]) { bv[2 * q] = s0; bj[2 * q] = jj + u; }
+      if (s1 < bv[2 * q + 1]) { bv[2 * q + 1] = s1; bj[2 * q + 1] = jj + u; }
+    }
+  }
+}
+
+__device__ __forceinline__ void rc_cp_async4(void* dst, const void* src, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(src), "r"(src_bytes) : "memory");
+}
+
+// Prefetch one group (1024 rows: slot r of warp w = the 32 contiguous rows
+// base + 256 r + 32 w ..) into the warp's stage with cp.async, coalesced 4-byte
+// copies (a warp reads 32 consecutive floats per copy), rows past n zero-filled.
+// The stage holds the two points of each lane's pair q (slots 2q, 2q + 1)
+// interleaved: 16-byte chunk c of lane-row r = (a_2c, b_2c, a_2c+1, b_2c+1), so
+// one LDS.128 yields two packed f32x2 operands and no register ever packs a
+// pair (a packing MOV is cheap enough that ptxas rematerialises it inside the
+// centroid loop: 220 IMAD.MOVs per 136 FFMA2s).  Chunk c of lane-row r sits at
+// (c + r / R) mod CH (CH = chunks per lane-row, R = lane-rows per 128-byte
+// line): the row-per-lane LDS.128s are conflict-free.
+template <int D>
+__device__ __forceinline__ void rc_prefetch(const float* __restrict__ P, int64_t n, int64_t base, float* stage) {
+  constexpr int CH = D / 2, R = 8 / CH, RS = 32 / D;   // RS: rows per 32 consecutive floats
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = lane % D, r0 = lane / D;                 // copy i of a slot: row r0 + RS i, column t
+  float* dl = stage + (t & 1) * 2;
+#pragma unroll
+  for (int sl = 0; sl < 4; ++sl) {
+    const int64_t rb = base + 256 * sl + 32 * w;
+    float* dq = dl + (sl >> 1) * (32 * 2 * D) + (sl & 1);
+    const float* src = P + (rb + r0) * D + t;
+    if (rb + 32 <= n) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const int row = r0 + RS * i;
+        rc_cp_async4(dq + row * 2 * D + (((t >> 1) + row / R) % CH) * 4, src + (int64_t)RS * i * D, 4);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const int row = r0 + RS * i;
+        const bool in = rb + row < n;
+        rc_cp_async4(dq + row * 2 * D + (((t >> 1) + row / R) % CH) * 4, in ? src + (int64_t)RS * i * D : P,
+                     in ? 4 : 0);
+      }
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Persistent loop over 1024-row groups; each warp's next group streams into its
+// stage (cp.async) while it computes the current one, so the per-group load
+// (every warp of the GPU loading at once, ~19 MB per wave at c2) no longer
+// idles the FMA pipe.
+template <int D>
+__global__ void __launch_bounds__(256, 2)
+assign_rowcst(const float* __restrict__ P, const float* __restrict__ pnorm, int64_t n, int k,
+              const int32_t* __restrict__ labels_prev, int32_t* __restrict__ labels,
+              float* __restrict__ mind, double* __restrict__ acc, const long long* __restrict__ state) {
+  if (stopped(state)) return;
+  constexpr int NPAIR = 2, PPT = 4, CJ = 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* stage = reinterpret_cast<float*>(smem_raw) + (threadIdx.x >> 5) * (PPT * 32 * D);
+  int* hist = reinterpret_cast<int*>(reinterpret_cast<float*>(smem_raw) + (blockDim.x >> 5) * (PPT * 32 * D));
+  const AccLayout L{k, D};
+  BlockBook book{(acc != nullptr && k <= kHistMax) ? hist : nullptr, 0};
+  if (book.hist) for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int64_t group = (int64_t)blockDim.x * PPT;
+  const int64_t ng = (n + group - 1) / group;
+  int64_t g = blockIdx.x;
+  if (g < ng) rc_prefetch<D>(P, n, g * group, stage);
+  for (; g < ng; g += gridDim.x) {
+    const int64_t base = g * group;
+    int64_t idx[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) idx[r] = base + threadIdx.x + (int64_t)r * blockDim.x;
+    float pn_r[PPT];
+    int lp_r[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+      const int64_t ii = idx[r] < n ? idx[r] : n - 1;
+      pn_r[r] = pnorm[ii];
+      lp_r[r] = labels_prev != nullptr ? labels_prev[ii] : 0;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    unsigned long long pp[NPAIR][D];
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q)
+#pragma unroll
+      for (int c = 0; c < D / 2; ++c) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(
+            stage + q * (32 * 2 * D) + lane * 2 * D + ((c + lane / (16 / D)) % (D / 2)) * 4);
+        pp[q][2 * c] = v.x;
+        pp[q][2 * c + 1] = v.y;
+      }
+    __syncwarp();
+    if (g + gridDim.x < ng) rc_prefetch<D>(P, n, (g + gridDim.x) * group, stage);
+
+    float bv[PPT];
+    int bj[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) { bv[r] = INFINITY; bj[r] = 0; }
+    int jj = 0;
+    for (; jj + CJ <= k; jj += CJ) rc_block<D, NPAIR, CJ>(pp, jj, k, bv, bj);
+    for (; jj < k; ++jj) rc_block<D, NPAIR, 1>(pp, jj, k, bv, bj);
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+      if (idx[r] < n) {
+        const float own = pn_r[r] + bv[r];
+        labels[idx[r]] = bj[r];
+        if (mind) mind[idx[r]] = own;
+        if (acc) {
+          if (labels_prev != nullptr) book.changed += (lp_r[r] != bj[r]);
+          if (book.hist != nullptr) atomicAdd(&book.hist[bj[r]], 1);
+          else atomicAdd(&acc[L.counts() + bj[r]], 1.0);
+        }
+        flag_nonfinite(state, (double)own);
+      }
+    }
+  }
+  if (acc) {
+    __syncthreads();
+    book_flush(book, acc, L, k);
+  }
+}
+
+template <int D>
+static int launch_rowcst(const float* P, const float* pnorm, int64_t n, const float* C, const float* cnorm, int k,
+                         const int32_t* lp, int32_t* lab, float* mind, double* acc, const long long* state,
+                         cudaStream_t st) {
+  static float* bank = nullptr;
+  if (bank == nullptr) {
+    void* a = nullptr;
+    cudaError_t e = cudaGetSymbolAddress(&a, c_cst);
+    if (e != cudaSuccess) return (int)e;
+    bank = static_cast<float*>(a);
+  }
+  cudaError_t e = cudaMemcpyAsync(bank, C, (size_t)k * D * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(bank + (size_t)k * D, cnorm, (size_t)k * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return (int)e;
+  const size_t smem = (size_t)8 * 4 * 32 * D * sizeof(float) +
+                      ((acc != nullptr && k <= kHistMax) ? (size_t)k * sizeof(int) : 0);
+  auto kern = assign_rowcst<D>;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024 + kHistMax * 4);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  const int64_t groups = (n + 256 * 4 - 1) / (256 * 4);
+  const int grid = (int)std::min<int64_t>(groups, (int64_t)persistent_grid(kern, 256, smem));
+  kern<<<grid, 256, smem, st>>>(P, pnorm, n, k, lp, lab, mind, acc, state);
+  PCB_CHECK_LAUNCH();
+  return 0;
+}
+
+// the constant-bank kernel serves d in {8, 16} when the centroids and norms fit
+// the bank and P's rows are 16-byte aligned for cp.async (at c1's d = 2,
+// k = 10 the launch is latency-bound and the bank copies cost more than they
+// save: 8.8 vs 11.1 us); PCB_ROWCST_OFF selects the shared-memory kernel (A/B)
+static bool rowcst_fits(const float* P, int d, int k) {
+  static const bool off = getenv("PCB_ROWCST_OFF") != nullptr;
+  return !off && (d == 8 || d == 16) && (int64_t)k * (d + 1) <= kCstFloats && ((uintptr_t)P & 15) == 0;
+}
+
 template <int DP, int NPAIR, int CJ = 2>
 static int launch_rowpair(const float* P, const float* pnorm, int64_t n, int d, const float* C, const float* cnorm,
                           int k, const int32_t* lp, int32_t* lab, float* mind, double* acc, const long long* state,
@@ -494,6 +710,10 @@ static int assign_dispatch(const T* P, const T* pnorm, int64_t n, int d, const T
     const float* Cf = reinterpret_cast<const float*>(C);
     const float* cn = reinterpret_cast<const float*>(cnorm);
     float* md = reinterpret_cast<float*>(mind);
+    if (rowcst_fits(Pf, d, k)) {
+      if (d == 8) return launch_rowcst<8>(Pf, pn, n, Cf, cn, k, lp, lab, md, acc, state, st);
+      return launch_rowcst<16>(Pf, pn, n, Cf, cn, k, lp, lab, md, acc, state, st);
+    }
     if (d <= 1) return launch_rowpair<1, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
     if (d <= 2) return launch_rowpair<2, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
     if (d <= 4) return launch_rowpair<4, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
