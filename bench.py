@@ -265,7 +265,10 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1:
+    # the multi-rank path (NCCL, captured all-reduce, lagged repair protocol);
+    # PCB_FORCE_MULTI=1 runs it with one rank (diagnostics on a 1-GPU box)
+    multi = world > 1 or os.environ.get("PCB_FORCE_MULTI", "0") == "1"
+    if multi:
         # NCCL's own INIT lines (rank / nRanks per communicator) go to a file
         # per process so stdout keeps the one JSON line
         os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -277,12 +280,12 @@ def main():
     from paper_2501_05587_b200.distributed import Comm, init_from_env, shard_range
     from paper_2501_05587_b200.engine import LloydEngine
 
-    if world > 1:
+    if multi:
         init_from_env("nccl")
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    comm = Comm() if world > 1 else None
+    comm = Comm() if multi else None
 
     n, d, k = cfg["n"], cfg["d"], cfg["k"]
     lo, hi = shard_range(n, rank, world)
@@ -294,7 +297,7 @@ def main():
     eng.init_labels_device(0, lo)  # init_assignments(n, k, 0), drawn on the device
     eng.init_centroids_from_labels()
     eng.state.zero_()
-    if world > 1:
+    if multi:
         eng.run_multi(W)  # warm-up: empty-cluster repairs (iterations 0-2) run through the host protocol
     else:
         for t in range(W):
@@ -338,7 +341,7 @@ def main():
     start.record()
     if use_graph:
         g.replay()
-    elif world > 1:
+    elif multi:
         ed = eng.run_multi(W + K, make_events=lambda: [torch.cuda.Event(enable_timing=True) for _ in range(5)],
                            t0=W)
         evs = [ed[t] for t in sorted(ed)]
@@ -428,8 +431,8 @@ def main():
         except Exception:
             pass
 
-    launch = ("cuda graph (K iterations" + (", NCCL all-reduce captured)" if world > 1 else ")")) if use_graph \
-        else "eager" + (" (lagged repair check)" if world > 1 else "")
+    launch = ("cuda graph (K iterations" + (", NCCL all-reduce captured)" if multi else ")")) if use_graph \
+        else "eager" + (" (lagged repair check)" if multi else "")
     line = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -444,7 +447,7 @@ def main():
         "screen_ambiguous_rows_last_iter": amb,
         "clocks": clocks,
     }
-    if world > 1:
+    if multi:
         line["nccl"] = nccl_summary(os.environ["NCCL_DEBUG_FILE"].replace("%p", "*").replace("%h", "*"))
     del eng, P
     if (n // world) * d * 4 > 20e9:  # very large shards (c5): return the cache before the e2e fit
@@ -463,7 +466,7 @@ def main():
                                 "sample": f"{ns} of {n} rows, 2 iterations, extrapolated linearly in n"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
     return 0
 
@@ -481,6 +484,7 @@ def e2e_run(args, cfg, dev, comm=None, lo=0, hi=None):
     from paper_2501_05587_b200.distributed import run_lloyd_sharded
     n, d, k = cfg["n"], cfg["d"], cfg["k"]
     world = comm.world_size if comm is not None else 1
+    multi = comm is not None and comm.multi
     hi = n if hi is None else hi
     P_host = make_shard(hi - lo, d, k, comm.rank if comm is not None else 0, args.seed, dev).cpu().numpy()
     if n * d * 4 > 20e9:
@@ -493,7 +497,7 @@ def e2e_run(args, cfg, dev, comm=None, lo=0, hi=None):
             comm.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = run_lloyd_sharded(P_host, c, n, lo, comm) if world > 1 else pcb.run_lloyd(P_host, c)
+        res = run_lloyd_sharded(P_host, c, n, lo, comm) if multi else pcb.run_lloyd(P_host, c)
         wall = time.perf_counter() - t0
         if comm is not None:
             w = torch.tensor([wall], dtype=torch.float64, device=dev)
@@ -519,7 +523,7 @@ def e2e_run(args, cfg, dev, comm=None, lo=0, hi=None):
     out = {"value": res.iterations_run / wall, "unit": "iters/s",
            "h2d_bytes_per_step": h2d // it, "d2h_bytes_per_step": d2h // it,
            "step": f"one run_lloyd(host numpy, max_iters={it}, record_label_history=False) call = {it} steps"
-                   + (f" on each of {world} ranks (run_lloyd_sharded), max over ranks" if world > 1 else ""),
+                   + (f" on each of {world} ranks (run_lloyd_sharded), max over ranks" if multi else ""),
            "wall_s": wall, "first_call_wall_s": wall_cold,
            "default_contract": {"value": res_h.iterations_run / wall_h, "unit": "iters/s", "wall_s": wall_h,
                                 "first_call_wall_s": wall_h_cold, "label_history": True,

@@ -53,6 +53,10 @@ class Comm:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world_size = dist.get_world_size(group) if dist.is_initialized() else 1
         self.offset = 0
+        # the multi-rank protocol (collectives, device empty-cluster flags, host
+        # repair rounds) runs for world_size > 1; PCB_FORCE_MULTI=1 runs it on a
+        # single rank too (diagnostics: NCCL + graph capture on a 1-GPU box)
+        self.multi = self.world_size > 1 or os.environ.get("PCB_FORCE_MULTI", "0") == "1"
 
     def all_reduce_sum(self, t):
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)

@@ -280,7 +280,7 @@ class ShardSequence:
             events[2].record()
 
     def _multi(self) -> bool:
-        return self.comm is not None and self.comm.world_size > 1
+        return self.comm is not None and self.comm.multi
 
     # -- multi-rank fit: enqueue ahead, check the repair flag with a lag -----------
     PENDING = 2  # state[1] value of an iteration parked for the host repair
@@ -337,7 +337,7 @@ class ShardSequence:
         pass
 
     def _allreduce(self, t) -> None:
-        if self.comm is not None and self.comm.world_size > 1:
+        if self.comm is not None and self.comm.multi:
             self.comm.all_reduce_sum(t)
 
 
@@ -382,7 +382,7 @@ class LloydEngine(ShardSequence):
             self.acc_size = kk * d + kk + 2
             self.acc = torch.zeros(self.acc_size, dtype=torch.float64, device=dev)
             # multi-rank: the accumulator of an iteration parked for the host repair
-            self.acc_saved = torch.zeros_like(self.acc) if comm is not None and comm.world_size > 1 else None
+            self.acc_saved = torch.zeros_like(self.acc) if comm is not None and comm.multi else None
             self.perm = torch.empty(n, dtype=torch.int32, device=dev)
             self.own = torch.empty(n, dtype=torch.float64, device=dev)  # own distances, sorted order
             self.offsets = torch.empty(kk + 1, dtype=torch.int32, device=dev)

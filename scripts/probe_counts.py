@@ -4,6 +4,7 @@ import torch, numpy as np
 from bench import make_shard, CONFIGS
 from paper_2501_05587_b200.engine import LloydEngine
 cfg = CONFIGS["c3"]; n, d, k = cfg["n"], cfg["d"], cfg["k"]
+if len(sys.argv) > 1: n = int(sys.argv[1])
 P = make_shard(n, d, k, 0, 0, torch.device("cuda", 0))
 eng = LloydEngine(P, k, max_iters=20)
 eng.init_labels_device(0)

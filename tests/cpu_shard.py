@@ -18,6 +18,7 @@ class LocalComm:
 
     rank = 0
     world_size = 1
+    multi = False
     offset = 0
 
     def all_reduce_sum(self, t):
