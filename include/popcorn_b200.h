@@ -127,6 +127,17 @@ int pcb_assign_f64(const double* P, const double* pnorm, int64_t n, int d,
                    const int32_t* labels_prev, int32_t* labels, double* mind,
                    double* acc, const long long* state, int variant, void* stream);
 
+/* pcb_assign_f32 plus the delta update's changed-row sums: S (k x d f64, the
+ * persistent per-cluster sums of pcb_delta_update_f32) gets S[new] += p,
+ * S[prev] -= p for every row whose label changed, when the previous iteration
+ * was a delta one, and state marks it so pcb_update_mode selects "sums
+ * applied" (or discards them for a full update).  Done by the small-d
+ * constant-bank kernel; other kernels leave S to pcb_delta_update_f32. */
+int pcb_assign_spec_f32(const float* P, const float* pnorm, int64_t n, int d,
+                        const float* C, const float* cnorm, int k,
+                        const int32_t* labels_prev, int32_t* labels, float* mind,
+                        double* acc, const long long* state, double* S, int variant, void* stream);
+
 /* tcgen05 3xTF32 variant (PCB_ASSIGN_TC3XTF32): operands pre-split with
  * pcb_split_tf32 into hi/lo matrices of row stride ld (multiple of 32, >= d);
  * same outputs and bookkeeping as pcb_assign_f32.                          */

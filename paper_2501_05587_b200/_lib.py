@@ -38,6 +38,7 @@ SIGNATURES = {
     "pcb_split_tf32": (I32, [P, I64, I32, I32, P, P, P]),
     "pcb_assign_f32": (I32, [P, P, I64, I32, P, P, I32, P, P, P, P, P, I32, P]),
     "pcb_assign_f64": (I32, [P, P, I64, I32, P, P, I32, P, P, P, P, P, I32, P]),
+    "pcb_assign_spec_f32": (I32, [P, P, I64, I32, P, P, I32, P, P, P, P, P, P, I32, P]),
     "pcb_assign_tc_f32": (I32, [P, P, I32, P, I64, I32, P, P, P, I32, P, P, P, P, P, P]),
     "pcb_screen_prep_points": (I32, [P, I64, I32, I32, P, P, P, P, P]),
     "pcb_screen_prep_centroids": (I32, [P, I32, I32, P, P, P, P]),

@@ -543,8 +543,16 @@ template <int D>
 __global__ void __launch_bounds__(256, 2)
 assign_rowcst(const float* __restrict__ P, const float* __restrict__ pnorm, int64_t n, int k,
               const int32_t* __restrict__ labels_prev, int32_t* __restrict__ labels,
-              float* __restrict__ mind, double* __restrict__ acc, const long long* __restrict__ state) {
+              float* __restrict__ mind, double* __restrict__ acc, const long long* __restrict__ state,
+              double* __restrict__ S) {
   if (stopped(state)) return;
+  // With S (the delta update's persistent per-cluster f64 sums) and the
+  // previous iteration a delta one: apply each changed row to S here, from the
+  // point values already in registers (S[new] += p, S[prev] -= p), the work of
+  // delta_sums_kernel; state[kSpec] tells pcb_update_mode (as the screen
+  // path's count pass does, assign_screen.cu count_labels_kernel).
+  const bool spec = S != nullptr && labels_prev != nullptr && acc != nullptr && delta_mode(state);
+  if (spec && blockIdx.x == 0 && threadIdx.x == 0) const_cast<long long*>(state)[kSpec] = 1;
   constexpr int NPAIR = 2, PPT = 4, CJ = 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* stage = reinterpret_cast<float*>(smem_raw) + (threadIdx.x >> 5) * (PPT * 32 * D);
@@ -608,6 +616,26 @@ assign_rowcst(const float* __restrict__ P, const float* __restrict__ pnorm, int6
         flag_nonfinite(state, (double)own);
       }
     }
+    if (spec) {
+      // changed rows of the warp, one at a time with the lanes over the
+      // columns (the row was just read: an L1/L2 hit), as delta_sums_kernel
+      const int lane = threadIdx.x & 31;
+#pragma unroll
+      for (int r = 0; r < PPT; ++r) {
+        unsigned m = __ballot_sync(0xffffffffu, idx[r] < n && lp_r[r] != bj[r]);
+        while (m) {
+          const int src = __ffs(m) - 1;
+          m &= m - 1;
+          const int ja = __shfl_sync(0xffffffffu, lp_r[r], src), jb = __shfl_sync(0xffffffffu, bj[r], src);
+          const int64_t row = idx[r] - lane + src;
+          if (lane < D) {
+            const double x = (double)P[row * D + lane];
+            atomicAdd(&S[(int64_t)jb * D + lane], x);
+            atomicAdd(&S[(int64_t)ja * D + lane], -x);
+          }
+        }
+      }
+    }
   }
   if (acc) {
     __syncthreads();
@@ -618,7 +646,7 @@ assign_rowcst(const float* __restrict__ P, const float* __restrict__ pnorm, int6
 template <int D>
 static int launch_rowcst(const float* P, const float* pnorm, int64_t n, const float* C, const float* cnorm, int k,
                          const int32_t* lp, int32_t* lab, float* mind, double* acc, const long long* state,
-                         cudaStream_t st) {
+                         double* S, cudaStream_t st) {
   static float* bank = nullptr;
   if (bank == nullptr) {
     void* a = nullptr;
@@ -626,9 +654,16 @@ static int launch_rowcst(const float* P, const float* pnorm, int64_t n, const fl
     if (e != cudaSuccess) return (int)e;
     bank = static_cast<float*>(a);
   }
-  cudaError_t e = cudaMemcpyAsync(bank, C, (size_t)k * D * sizeof(float), cudaMemcpyDeviceToDevice, st);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(bank + (size_t)k * D, cnorm, (size_t)k * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  // one copy when the norms follow the centroid rows in memory (the engine's
+  // layout), two otherwise
+  cudaError_t e;
+  if (cnorm == C + (size_t)k * D) {
+    e = cudaMemcpyAsync(bank, C, (size_t)k * (D + 1) * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  } else {
+    e = cudaMemcpyAsync(bank, C, (size_t)k * D * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(bank + (size_t)k * D, cnorm, (size_t)k * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  }
   if (e != cudaSuccess) return (int)e;
   const size_t smem = (size_t)8 * 4 * 32 * D * sizeof(float) +
                       ((acc != nullptr && k <= kHistMax) ? (size_t)k * sizeof(int) : 0);
@@ -641,7 +676,7 @@ static int launch_rowcst(const float* P, const float* pnorm, int64_t n, const fl
   }
   const int64_t groups = (n + 256 * 4 - 1) / (256 * 4);
   const int grid = (int)std::min<int64_t>(groups, (int64_t)persistent_grid(kern, 256, smem));
-  kern<<<grid, 256, smem, st>>>(P, pnorm, n, k, lp, lab, mind, acc, state);
+  kern<<<grid, 256, smem, st>>>(P, pnorm, n, k, lp, lab, mind, acc, state, S);
   PCB_CHECK_LAUNCH();
   return 0;
 }
@@ -700,7 +735,7 @@ static int launch_rowreg(const T* P, const T* pnorm, int64_t n, int d, const T* 
 template <typename T>
 static int assign_dispatch(const T* P, const T* pnorm, int64_t n, int d, const T* C, const T* cnorm,
                            int k, const int32_t* lp, int32_t* lab, T* mind, double* acc,
-                           const long long* state, int variant, cudaStream_t st) {
+                           const long long* state, int variant, cudaStream_t st, double* S = nullptr) {
   if (n < 1 || d < 1 || k < 1 || !P || !pnorm || !C || !cnorm || !lab) return PCB_EINVAL;
   if (variant == PCB_ASSIGN_AUTO) variant = (d <= 32) ? PCB_ASSIGN_ROWREG : PCB_ASSIGN_TILED;
   if (variant == PCB_ASSIGN_ROWREG && sizeof(T) == 4 && getenv("PCB_ROWREG_SCALAR") == nullptr) {
@@ -711,8 +746,8 @@ static int assign_dispatch(const T* P, const T* pnorm, int64_t n, int d, const T
     const float* cn = reinterpret_cast<const float*>(cnorm);
     float* md = reinterpret_cast<float*>(mind);
     if (rowcst_fits(Pf, d, k)) {
-      if (d == 8) return launch_rowcst<8>(Pf, pn, n, Cf, cn, k, lp, lab, md, acc, state, st);
-      return launch_rowcst<16>(Pf, pn, n, Cf, cn, k, lp, lab, md, acc, state, st);
+      if (d == 8) return launch_rowcst<8>(Pf, pn, n, Cf, cn, k, lp, lab, md, acc, state, S, st);
+      return launch_rowcst<16>(Pf, pn, n, Cf, cn, k, lp, lab, md, acc, state, S, st);
     }
     if (d <= 1) return launch_rowpair<1, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
     if (d <= 2) return launch_rowpair<2, 2>(Pf, pn, n, d, Cf, cn, k, lp, lab, md, acc, state, st);
@@ -754,6 +789,19 @@ extern "C" int pcb_assign_f32(const float* P, const float* pnorm, int64_t n, int
                                  (cudaStream_t)stream);
   return pcb::assign_dispatch<float>(P, pnorm, n, d, C, cnorm, k, labels_prev, labels, mind, acc,
                                      state, variant, (cudaStream_t)stream);
+}
+
+// pcb_assign_f32 whose small-d kernel also applies the changed rows to the
+// delta update's sums S when the previous iteration was a delta one (kSpec);
+// kernels without the fused path leave that to pcb_delta_update_f32.
+extern "C" int pcb_assign_spec_f32(const float* P, const float* pnorm, int64_t n, int d,
+                                   const float* C, const float* cnorm, int k,
+                                   const int32_t* labels_prev, int32_t* labels, float* mind,
+                                   double* acc, const long long* state, double* S, int variant, void* stream) {
+  if (variant == PCB_ASSIGN_TC3XTF32 || variant == PCB_ASSIGN_DELTA)
+    return pcb_assign_f32(P, pnorm, n, d, C, cnorm, k, labels_prev, labels, mind, acc, state, variant, stream);
+  return pcb::assign_dispatch<float>(P, pnorm, n, d, C, cnorm, k, labels_prev, labels, mind, acc, state, variant,
+                                     (cudaStream_t)stream, S);
 }
 
 extern "C" int pcb_assign_f64(const double* P, const double* pnorm, int64_t n, int d,

@@ -375,8 +375,11 @@ class LloydEngine(ShardSequence):
             n, d, kk = self.n, self.d, self.k
             dev, td = self.dev, self.tdtype
             self.pnorm = torch.empty(n, dtype=td, device=dev)
-            self.C = torch.zeros((kk, d), dtype=td, device=dev)
-            self.cnorm = torch.empty(kk, dtype=td, device=dev)
+            # centroids and their norms in one allocation (C rows, then cnorm):
+            # the small-d kernel copies both into the constant bank in one copy
+            self._cbuf = torch.zeros(kk * d + kk, dtype=td, device=dev)
+            self.C = self._cbuf[: kk * d].view(kk, d)
+            self.cnorm = self._cbuf[kk * d:]
             self.labels = [torch.zeros(n, dtype=torch.int32, device=dev) for _ in range(2)]
             self.mind = torch.empty(n, dtype=td, device=dev)
             self.acc_size = kk * d + kk + 2
@@ -673,9 +676,15 @@ class LloydEngine(ShardSequence):
                    self.d, _p(self.C_hi), _p(self.C_lo), _p(self.cnorm), self.k, _p(prev), _p(new),
                    _p(self.mind), _p(acc), _p(state), _stream())
         else:
-            L.call(f"pcb_assign_{self.sfx}", _p(self.P), _p(self.pnorm), self.n, self.d, _p(self.C),
-                   _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
-                   self.vcode, _stream())
+            if self.delta_frac >= 0 and self.dtype == _F32 and acc is not None:
+                # the small-d kernel applies the changed rows to S itself (update mode 3)
+                L.call("pcb_assign_spec_f32", _p(self.P), _p(self.pnorm), self.n, self.d, _p(self.C),
+                       _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
+                       _p(self.S), self.vcode, _stream())
+            else:
+                L.call(f"pcb_assign_{self.sfx}", _p(self.P), _p(self.pnorm), self.n, self.d, _p(self.C),
+                       _p(self.cnorm), self.k, _p(prev), _p(new), _p(self.mind), _p(acc), _p(state),
+                       self.vcode, _stream())
         self._kmark(1)
 
     def _count_labels(self, new, prev, acc, state) -> None:
