@@ -647,16 +647,22 @@ template <int D>
 static int launch_rowcst(const float* P, const float* pnorm, int64_t n, const float* C, const float* cnorm, int k,
                          const int32_t* lp, int32_t* lab, float* mind, double* acc, const long long* state,
                          double* S, cudaStream_t st) {
-  static float* bank = nullptr;
-  if (bank == nullptr) {
+  // the bank's device address and the smem opt-in are per device
+  static float* banks[64] = {nullptr};
+  static bool attrs[64] = {false};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  if (dev < 0 || dev >= 64) return PCB_EUNSUP;
+  if (banks[dev] == nullptr) {
     void* a = nullptr;
-    cudaError_t e = cudaGetSymbolAddress(&a, c_cst);
+    e = cudaGetSymbolAddress(&a, c_cst);
     if (e != cudaSuccess) return (int)e;
-    bank = static_cast<float*>(a);
+    banks[dev] = static_cast<float*>(a);
   }
+  float* bank = banks[dev];
   // one copy when the norms follow the centroid rows in memory (the engine's
   // layout), two otherwise
-  cudaError_t e;
   if (cnorm == C + (size_t)k * D) {
     e = cudaMemcpyAsync(bank, C, (size_t)k * (D + 1) * sizeof(float), cudaMemcpyDeviceToDevice, st);
   } else {
@@ -668,11 +674,10 @@ static int launch_rowcst(const float* P, const float* pnorm, int64_t n, const fl
   const size_t smem = (size_t)8 * 4 * 32 * D * sizeof(float) +
                       ((acc != nullptr && k <= kHistMax) ? (size_t)k * sizeof(int) : 0);
   auto kern = assign_rowcst<D>;
-  static bool attr = false;
-  if (!attr) {
+  if (!attrs[dev]) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024 + kHistMax * 4);
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attrs[dev] = true;
   }
   const int64_t groups = (n + 256 * 4 - 1) / (256 * 4);
   const int grid = (int)std::min<int64_t>(groups, (int64_t)persistent_grid(kern, 256, smem));
