@@ -449,8 +449,9 @@ assign_rowpair(const float* __restrict__ P, const float* __restrict__ pnorm, int
 // into uniform registers and FFMA2 takes each as a broadcast scalar operand
 // (`FFMA2 R, R.F32x2, UR.F32, R`), so no vector register or shared-memory
 // wavefront is spent on centroids and the loads hoist freely.  The centroids
-// and their norms are copied into the bank (two D2D copies on the launching
-// stream, graph-capturable) before each launch; the bank is one per process
+// and their norms are copied into the bank (one D2D copy on the launching
+// stream when the norms follow the centroid rows in memory, as the engine lays
+// them out; graph-capturable) before each launch; the bank is one per process
 // and device, so launches that use it must be ordered (one stream), as every
 // launch of an engine is.
 // ---------------------------------------------------------------------------
@@ -538,7 +539,8 @@ __device__ __forceinline__ void rc_prefetch(const float* __restrict__ P, int64_t
 // Persistent loop over 1024-row groups; each warp's next group streams into its
 // stage (cp.async) while it computes the current one, so the per-group load
 // (every warp of the GPU loading at once, ~19 MB per wave at c2) no longer
-// idles the FMA pipe.
+// idles the FMA pipe.  (Measured: 58.3 -> 57.5 us at c2; most of the gain over
+// the shared-memory kernel is the constant bank.)
 template <int D>
 __global__ void __launch_bounds__(256, 2)
 assign_rowcst(const float* __restrict__ P, const float* __restrict__ pnorm, int64_t n, int k,
