@@ -258,13 +258,15 @@ def test_rowpair_bit_identical_to_rowreg(d, k, monkeypatch):
     np.testing.assert_array_equal(outs[0]["mind"].view(np.uint32), outs[1]["mind"].view(np.uint32))
 
 
-@pytest.mark.parametrize("d,k", [(2, 10), (16, 64), (16, 7), (8, 40), (5, 33)])
+@pytest.mark.parametrize("d,k", [(2, 10), (16, 64), (16, 7), (8, 40), (5, 33),
+                                 (16, 120), (16, 121), (8, 227), (8, 228)])
 @pytest.mark.parametrize("n", [400_003, 1_000_000])
 def test_small_d_full_size_bit_identical_to_rowreg(n, d, k, monkeypatch):
     """The default small-d kernel at c2's size (several rounds per block, a
-    ragged last round; assign_rowcst for d in {2, 16}, the ragged k = 7 / 33
-    tails of its centroid blocks, assign_rowpair for d = 5): labels and own
-    distances bit-identical to the scalar kernel."""
+    ragged last round; assign_rowcst for d in {8, 16}, the ragged k = 7 / 33
+    tails of its centroid blocks, the constant bank's capacity edge k (d + 1)
+    = 2048 / 2049 -> assign_rowpair, assign_rowpair for d = 2, 5): labels and
+    own distances bit-identical to the scalar kernel."""
     from paper_2501_05587_b200.engine import LloydEngine
     P = oracle.make_blobs(n, d, min(k, 50), seed=n % 97 + d)
     lab = oracle.init_assignments(n, k, 1)
